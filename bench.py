@@ -1,0 +1,513 @@
+#!/usr/bin/env python3
+"""Benchmark of the NNVISR frame<->tensor hot path on B200.
+
+One step = one pass of the whole hot path over the workload's clip (shard):
+halo exchange (N > 1), tuple plan (A1-A2), frames->tensor for every tuple
+(A3-A7) and tensor->frames for every tuple's network output (B1-B4).  The
+network itself is not part of the build (north_star); t2f reads a ring of
+seeded network-output tensors.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
+  python bench.py --impl reference ...      # the CPU oracle, timed (reference arm)
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/s per direction at 1080p/4K, 1/2/4/8 B200; HBM GB/s vs peak"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--chunk", type=int, default=0, help="tuples per launch (0 = auto)")
+    p.add_argument("--f2t-mode", default="materialize", choices=["materialize", "store"])
+    p.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=0, help="tuples in the oracle sample (0 = auto)")
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def load_traffic(kernel: str, workload: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture (profiles/traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d.get(workload, {}).get(kernel)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle
+def oracle_sample(w, count: int, threads: int):
+    """Time the CPU oracle (as it stands) on `count` tuples of workload w:
+    each unit = the tuple's frames->tensor plus its output tensor->frames.
+    Returns (units/s, seconds, threads used)."""
+    from oracle import oracle as O
+    from paper_2308_03121_b200 import synth
+    from paper_2308_03121_b200.frames import FrameLayout
+
+    cfg = w.cfg
+    lay = FrameLayout(cfg.width, cfg.height, cfg.family, cfg.bits)
+    olay = w.out_layout()
+    N, M = cfg.input_count, cfg.output_count
+    align = cfg.align
+    Hp, Wp = -(-cfg.height // align) * align, -(-cfg.width // align) * align
+    lo, hi = w.luma_range
+    frames = [synth.random_planes(lay, w.seed + i, lo, hi) for i in range(N + count)]
+    rs = np.random.default_rng(w.seed)
+    dt = np.float16 if cfg.dtype == 1 else np.float32
+    outs = [rs.uniform(-0.05, 1.05, (1, 3 * M, olay.height, olay.width)).astype(dt) for _ in range(min(count, 2))]
+    jobs = [("f2t", i) for i in range(count)] + [("t2f", i) for i in range(count)]
+
+    def run(job):
+        kind, i = job
+        if kind == "f2t":
+            O.f2t(frames[i:i + N], cfg.width, cfg.height, cfg.family, cfg.bits, cfg.matrix, cfg.range, Hp, Wp,
+                  O.F16 if cfg.dtype == 1 else O.F32)
+        else:
+            O.t2f(outs[i % len(outs)], M, olay.width, olay.height, cfg.family, cfg.bits, cfg.matrix, cfg.range)
+
+    threads = max(1, min(threads, len(jobs)))
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(run, jobs))
+    dt_s = time.perf_counter() - t0
+    return count / dt_s, dt_s, threads
+
+
+def default_cpu_sample(w):
+    px = w.cfg.width * w.cfg.height
+    return max(2, min(16, int(8 * (1920 * 1080) / px))) if px > 1e5 else 64
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the box's host cores, per step a
+    bounded sample of the workload (rank 0 only under torchrun)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2308_03121_b200 import synth
+    w = synth.WORKLOADS[args.workload]
+    cores = os.cpu_count() or 1
+    sample = args.cpu_sample or default_cpu_sample(w)
+    for _ in range(args.warmup):
+        oracle_sample(w, max(1, sample // 4), cores)
+    times = []
+    for _ in range(args.steps):
+        _, s, used = oracle_sample(w, sample, cores)
+        times.append(s)
+    ms = 1000.0 * float(np.mean(times))
+    value = sample / (ms / 1000.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "description": w.description, "sample_tuples": sample},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": used, "kind": "oracle",
+                         "sample": f"{sample} tuples of {args.workload} (frames->tensor + tensor->frames each), "
+                                   f"{used} host threads"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- GPU
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_03121_b200 import nnvisr as nv
+    from paper_2308_03121_b200 import shard as sh
+    from paper_2308_03121_b200 import synth
+    from paper_2308_03121_b200.frames import FrameBuffer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    w = synth.WORKLOADS[args.workload]
+    cfg = w.cfg
+    scaling = args.scaling if args.scaling != "auto" else ("strong" if args.workload == "c5" else "weak")
+    total = w.frames * (world if scaling == "weak" else 1)
+    h = nv.open(cfg)
+    N, M = h.N, h.M
+    L = 0 if cfg.flags else ((N - 1) // 2 if cfg.left_context == -1 else cfg.left_context)
+    R = N - 1 - L
+    s = sh.shard_of(total, world, rank, L, R)
+    cut_all = synth.cut_flags(w, total)  # each rank only uses its own flags + what the halo brings
+
+    # window buffer: [left halo | owned frames | right halo]
+    lay = w.layout()
+    win = FrameBuffer(lay, s.window_count, device=dev)
+    own = synth.generate_clip(w, device=dev, frames=s.owned, first=s.begin, total_frames=total)
+    win.data[s.left:s.left + s.owned].copy_(own.data)
+    del own
+    cut_win = torch.zeros(s.window_count, dtype=torch.uint8, device=dev)
+    cut_win[s.left:s.left + s.owned] = torch.from_numpy(cut_all[s.begin:s.end]).to(dev)
+    h.bind_frames(win.descriptors(), base=s.window_first)
+
+    # buffers (rings larger than L2 so no step re-reads L2-resident data)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    in_shape, out_shape = h.in_shape, h.out_shape
+    tdt = torch.float16 if cfg.dtype == nv.F16 else torch.float32
+    esz = 2 if cfg.dtype == nv.F16 else 4
+    in_elems = int(np.prod(in_shape))
+    out_elems = int(np.prod(out_shape))
+    Ho, Wo = out_shape[2], out_shape[3]
+    olay = w.out_layout()
+    t2f_bytes = out_elems * esz + M * olay.payload_bytes()
+    chunk = args.chunk or max(1, min(64, int(2.5e9 // max(t2f_bytes, in_elems * esz))))
+    n_in = chunk
+    n_out = max(chunk, -(-4 * l2 // (out_elems * esz)))
+    tens_in = torch.empty((n_in, in_elems), dtype=tdt, device=dev)
+    tens_out = synth.random_tensor((n_out, out_elems), cfg.dtype, w.seed + 99, device=dev)
+    ofb = FrameBuffer(olay, chunk * M, device=dev)
+    ofb_desc = ofb.descriptors()
+    store = None
+    if args.f2t_mode == "store":
+        store = torch.empty((s.window_count, 3 * in_shape[2] * in_shape[3]), dtype=tdt, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    frame_payload = lay.payload_bytes()
+
+    def plan_local():
+        cw = cut_win.cpu().numpy()
+        return h.plan_range(total, s.window_first, cw, s.begin, s.end)
+
+    ev_pairs = {"f2t": [], "t2f": []}
+
+    def step(record: bool):
+        if world > 1:
+            with torch.cuda.stream(stream):
+                sh.halo_exchange(s, win.data, cut_win)
+        runs, _ = plan_local()
+        if args.f2t_mode == "store":
+            with torch.cuda.stream(stream):
+                a = torch.cuda.Event(enable_timing=True) if record else None
+                if a:
+                    a.record(stream)
+                h.frames_to_store(s.window_first, s.window_count, store.data_ptr(), stream)
+                dup = [r for r in range(len(runs)) if np.any(np.diff(runs[r]) != 1)]
+                for c0 in range(0, len(dup), chunk):
+                    sel = runs[dup[c0:c0 + chunk]]
+                    h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream)
+                if a:
+                    b = torch.cuda.Event(enable_timing=True)
+                    b.record(stream)
+                    ev_pairs["f2t"].append((a, b, s.window_count, None))
+        for c0 in range(0, len(runs), chunk):
+            sel = runs[c0:c0 + chunk]
+            nb = len(sel)
+            with torch.cuda.stream(stream):
+                if args.f2t_mode == "materialize":
+                    a = torch.cuda.Event(enable_timing=True) if record else None
+                    if a:
+                        a.record(stream)
+                    h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream)
+                    if a:
+                        b = torch.cuda.Event(enable_timing=True)
+                        b.record(stream)
+                        ev_pairs["f2t"].append((a, b, nb, len(np.unique(sel))))
+                a = torch.cuda.Event(enable_timing=True) if record else None
+                if a:
+                    a.record(stream)
+                o0 = (c0 // chunk * chunk) % n_out
+                if o0 + nb > n_out:
+                    o0 = 0
+                h.tensor_to_frames_batch(tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo, ofb_desc[:nb * M], nb,
+                                         stream)
+                if a:
+                    b = torch.cuda.Event(enable_timing=True)
+                    b.record(stream)
+                    ev_pairs["t2f"].append((a, b, nb, None))
+        return len(runs)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # warm-up
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+
+    # ---- timed region: K steps, device time via CUDA events on `stream`
+    launches0 = nv.launch_count()
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        tuples = 0
+        for _ in range(args.steps):
+            tuples += step(True)
+        t_end.record(stream)
+        barrier()
+    launches = nv.launch_count() - launches0
+    ms_total = t_start.elapsed_time(t_end)
+    ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_total = float(ms_t.item())
+    ms_step = ms_total / args.steps
+    frames_all = s.owned * world if scaling == "weak" else total  # every rank owns a contiguous share
+    if scaling == "strong":
+        frames_all = total
+    value = frames_all * args.steps / (ms_total / 1000.0)
+
+    # per-kernel durations and algorithmic bytes
+    def kstats(kind):
+        ev = ev_pairs[kind]
+        if not ev:
+            return None
+        durs = np.array([a.elapsed_time(b) for a, b, _, _ in ev]) / 1000.0
+        units = np.array([u for _, _, u, _ in ev], dtype=np.float64)
+        if kind == "f2t" and args.f2t_mode == "materialize":
+            uniq = np.array([q for _, _, _, q in ev], dtype=np.float64)
+            bytes_ = uniq * frame_payload + units * in_elems * esz
+        elif kind == "f2t":
+            bytes_ = units * (frame_payload + 3 * in_shape[2] * in_shape[3] * esz)
+        else:
+            bytes_ = units * t2f_bytes
+        return {"launches": len(ev), "seconds": float(durs.sum()), "units": float(units.sum()),
+                "bytes": float(bytes_.sum()), "avg_launch_s": float(durs.mean()),
+                "avg_launch_bytes": float(bytes_.mean())}
+
+    ks = {k: kstats(k) for k in ("f2t", "t2f")}
+    peak, peak_src = load_peaks()
+    per_dir = {}
+    for k, v in ks.items():
+        if v:
+            gbs = v["bytes"] / v["seconds"] / 1e9
+            per_dir[k] = {"fps": v["units"] / v["seconds"] * (world if scaling == "weak" else 1),
+                          "achieved_gbs": gbs, "frac_of_measured_peak": gbs / peak, "frac_of_8tbs": gbs / 8000.0,
+                          "launches_per_step": v["launches"] / args.steps,
+                          "bytes_per_launch": v["avg_launch_bytes"], "avg_launch_ms": 1000 * v["avg_launch_s"]}
+    dom = max((k for k in ks if ks[k]), key=lambda k: ks[k]["seconds"])
+    dv = ks[dom]
+    achieved = dv["avg_launch_bytes"] / dv["avg_launch_s"] / 1e9
+    traffic = load_traffic(dom, args.workload)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dv["avg_launch_bytes"]}
+
+    # ---- e2e: host (pinned) frames in, host frames out, through the C ABI
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, in_elems, out_elems, esz,
+                      stream, dev, world, plan_local, scaling, frames_all)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = args.cpu_sample or default_cpu_sample(w)
+        v, secs, used = oracle_sample(w, sample, os.cpu_count() or 1)
+        cpu = {"value": v, "unit": "frames/s", "cores": used, "kind": "oracle",
+               "sample": f"{sample} tuples of {args.workload} (frames->tensor + tensor->frames each) in "
+                         f"{secs:.1f} s on {used} host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64" if cfg.bits == 16 else "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "description": w.description, "frames_per_step": frames_all,
+                       "clip_frames_per_rank": s.owned, "input_tensor": list(in_shape),
+                       "output_tensor": list(out_shape), "tensor_dtype": "f16" if cfg.dtype == nv.F16 else "f32",
+                       "tuples_per_launch": chunk, "f2t_mode": args.f2t_mode,
+                       "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB, t2f input ring "
+                                    f"{n_out} x {out_elems * esz / 1e6:.0f} MB >= 4 x L2 ({l2 / 1e6:.0f} MB)",
+                       "parallelism": f"frame-range shards x{world}, halo P2P"},
+            "unit_definition": "1 frame = one tuple through frames->tensor plus its network output through "
+                               "tensor->frames (n = 1: one tuple per clip frame)",
+            "per_direction": per_dir,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "seed": w.seed,
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, in_elems, out_elems, esz, stream,
+            dev, world, plan_local, scaling, frames_all):
+    """Same metric with the frames in pinned HOST memory: every step copies the
+    shard's frames host->device, runs f2t + t2f through the C ABI, and copies
+    every output frame device->host.  Copies run on their own streams and
+    overlap the kernels chunk by chunk."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_03121_b200.frames import FrameBuffer
+
+    host_in = win.data[s.left:s.left + s.owned].cpu().pin_memory()
+    M = h.M
+    Ho, Wo = h.out_shape[2], h.out_shape[3]
+    ring = 2
+    dev_out = [FrameBuffer(ofb.layout, chunk * M, device=dev) for _ in range(ring)]
+    dev_out_desc = [b.descriptors() for b in dev_out]
+    host_out = [torch.empty((chunk * M, ofb.layout.frame_bytes), dtype=torch.uint8).pin_memory() for _ in range(ring)]
+    s_in = torch.cuda.Stream(device=dev)
+    s_out = torch.cuda.Stream(device=dev)
+    runs, _ = plan_local()
+    R = s.right
+
+    def e2e_step():
+        n_done = 0
+        ev_out = [None] * ring
+        for ci, c0 in enumerate(range(0, len(runs), chunk)):
+            sel = runs[c0:c0 + chunk]
+            nb = len(sel)
+            # frames this chunk needs that have not been uploaded yet
+            hi = min(s.owned, c0 + nb + R)
+            if hi > n_done:
+                with torch.cuda.stream(s_in):
+                    win.data[s.left + n_done:s.left + hi].copy_(host_in[n_done:hi], non_blocking=True)
+                n_done = hi
+            ready = torch.cuda.Event()
+            ready.record(s_in)
+            stream.wait_event(ready)
+            k = ci % ring
+            if ev_out[k] is not None:
+                stream.wait_event(ev_out[k])  # the D2H of this ring slot finished
+            with torch.cuda.stream(stream):
+                h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream)
+                o0 = (c0 // chunk * chunk) % n_out
+                if o0 + nb > n_out:
+                    o0 = 0
+                h.tensor_to_frames_batch(tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo, dev_out_desc[k][:nb * M],
+                                         nb, stream)
+            done = torch.cuda.Event()
+            done.record(stream)
+            s_out.wait_event(done)
+            with torch.cuda.stream(s_out):
+                host_out[k][:nb * M].copy_(dev_out[k].data[:nb * M], non_blocking=True)
+            ev_out[k] = torch.cuda.Event()
+            ev_out[k].record(s_out)
+        return len(runs)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    steps = max(1, min(args.steps, 5))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    s_in.wait_event(t0)
+    for _ in range(steps):
+        e2e_step()
+    s_out_done = torch.cuda.Event()
+    s_out_done.record(s_out)
+    stream.wait_event(s_out_done)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    h2d = s.owned * win.layout.frame_bytes
+    d2h = len(runs) * M * ofb.layout.frame_bytes
+    return {"value": frames_all * steps / (ms / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms / steps, "steps": steps,
+            "path": "pinned host frames -> nnvisr_frames_to_tensor_batch -> nnvisr_tensor_to_frames_batch -> "
+                    "pinned host frames (copies on side streams, overlapped per chunk)"}
+
+
+if __name__ == "__main__":
+    main()

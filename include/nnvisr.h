@@ -1,0 +1,217 @@
+/*
+ * nnvisr.h -- C ABI of the B200-native NNVISR frame<->tensor hot path.
+ *
+ * What it computes (arXiv 2308.03121, /root/reference/PAPER.md):
+ *   - frames -> tensor: assemble the tuple of N consecutive planar integer
+ *     frames a network consumes ("a tuple of images", §1; "n ... the
+ *     number of frames being consumed by the network for each inference run",
+ *     §3.1) into one NCHW RGB tensor, converting pixel format and
+ *     colourspace (§3.1);
+ *   - tensor -> frames: convert the network's RGB output tensor back to
+ *     integer planar frames of the clip's format at the scaled size (§3.2
+ *     P:313-328);
+ *   - the tuple plan: which frames form each tuple, never crossing a scene
+ *     change (§3.2, §3.3).
+ * Where the paper is silent the readings A1..A16 of DESIGN.md §3 apply
+ * (centre chroma siting, replicate padding, round-half-even, ...).
+ *
+ * Conventions shared by every call:
+ *   - Every function returns nnvisr_status; NNVISR_OK (0) is success.  On
+ *     failure nothing was enqueued and nnvisr_last_error() (thread-local)
+ *     names the violated requirement.
+ *   - Ownership: the caller owns every frame, tensor, stream and host array it
+ *     passes; the library never frees or retains caller memory beyond the
+ *     call (device work enqueued by a call reads caller device memory when it
+ *     runs).  The library owns the handle and the small device/pinned scratch
+ *     buffers behind it; nnvisr_close() frees them.
+ *   - Device work is enqueued on the caller's CUDA stream (`stream` is a
+ *     cudaStream_t passed as void*; NULL = legacy default stream) and the call
+ *     returns after enqueueing.  Asynchronous faults surface at the caller's
+ *     synchronisation, or as NNVISR_ERR_CUDA from a later call.
+ *   - A handle is bound to the CUDA device that is current at its first
+ *     device call; it is used by one host thread at a time.  nnvisr_open,
+ *     nnvisr_tensor_shapes, nnvisr_plan*, nnvisr_close and nnvisr_last_error
+ *     do not touch the GPU (they work on machines without one).
+ *   - Frames: planar, plane order (Y, U, V) or (R, G, B); 8-bit samples are
+ *     uint8, 10/16-bit samples are uint16 holding the value in the low bits.
+ *     4:2:0 chroma planes are (width/2) x (height/2).  `pitch` is the byte
+ *     distance between rows.  Frames and tensors are in device memory unless
+ *     a parameter says "host".
+ *   - Tensors: NCHW, batch 1, fp32 or fp16, rows contiguous.  Input tensor
+ *     [1, 3N, Hp, Wp]: tuple slot t -> channels 3t, 3t+1, 3t+2 = R', G', B'
+ *     (reading A7), Hp/Wp = height/width rounded up to `align`, padding
+ *     replicates the last row/column (reading A6).  Output tensor
+ *     [1, 3M, t_h, t_w] with t_h >= H*sy, t_w >= W*sx; output slot o ->
+ *     channels 3o..3o+2, the top-left (H*sy) x (W*sx) window is converted.
+ *   - Vector fast paths need 16-byte aligned plane/tensor pointers and
+ *     pitches that are multiples of 16 bytes; anything else is still
+ *     converted correctly by a scalar path.
+ */
+#ifndef NNVISR_H
+#define NNVISR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NNVISR_OK = 0,
+    NNVISR_ERR_INVALID_CONFIG = 1,  /* nnvisr_open: format/network violates an invariant */
+    NNVISR_ERR_INVALID_ARG = 2,     /* null/misaligned pointer, bad size, index out of range */
+    NNVISR_ERR_UNSUPPORTED = 3,     /* valid request this build does not implement */
+    NNVISR_ERR_OUT_OF_MEMORY = 4,   /* scratch allocation failed */
+    NNVISR_ERR_CUDA = 5,            /* a CUDA runtime call or kernel launch failed */
+    NNVISR_ERR_CAPACITY = 7         /* caller's output array too small */
+} nnvisr_status;
+
+/* pixel family */
+enum { NNVISR_YUV420 = 0, NNVISR_YUV444 = 1, NNVISR_RGB = 2 };
+/* colour matrix (reading A1: ITU Kr, Kb; BT.2020 non-constant luminance) */
+enum { NNVISR_BT601 = 0, NNVISR_BT709 = 1, NNVISR_BT2020 = 2 };
+/* quantisation range (reading A2) */
+enum { NNVISR_LIMITED = 0, NNVISR_FULL = 1 };
+/* 4:2:0 chroma siting (reading A5); only CENTER is implemented */
+enum { NNVISR_CHROMA_CENTER = 0, NNVISR_CHROMA_LEFT = 1 };
+/* tensor element type */
+enum { NNVISR_F32 = 0, NNVISR_F16 = 1 };
+/* network flags, §3.1 */
+enum {
+    NNVISR_INTERPOLATION = 1u, /* "Interpolation": output at doubled frame rate */
+    NNVISR_EXTRA_FRAME = 2u,   /* "Extra frame": the network takes n+1 frames */
+    NNVISR_DOUBLE_FRAME = 4u   /* "Double frame": 2n outputs per run */
+};
+
+/* The clip being processed (§3.1: RGB/YUV input, the
+ * colourspace the network was trained for). */
+typedef struct {
+    int32_t width, height;  /* luma samples; even for 4:2:0 */
+    int32_t family;         /* NNVISR_YUV420 | NNVISR_YUV444 | NNVISR_RGB */
+    int32_t bits;           /* 8 | 10 | 16 */
+    int32_t matrix;         /* NNVISR_BT601 | _BT709 | _BT2020 (ignored for RGB) */
+    int32_t range;          /* NNVISR_LIMITED | NNVISR_FULL */
+    int32_t chroma_loc;     /* NNVISR_CHROMA_CENTER */
+} nnvisr_clip_format;
+
+/* The network's tuple contract (§3.1, §3.2).
+ * Accepted shapes (anything else is NNVISR_ERR_INVALID_CONFIG):
+ *   paper grouping: left_context = 0 (or -1), input_count = n + (EXTRA ? 1 : 0),
+ *                   output_count in {n, 2n, 2n+1};
+ *   sliding window: flags = 0, n = 1, output_count = 1, any input_count >= 1,
+ *                   left_context L in [0, N) (-1 = (N-1)/2, reading A8).
+ * DOUBLE_FRAME requires INTERPOLATION; INTERPOLATION without DOUBLE_FRAME
+ * requires scale 1 (SPEC.md model-desc invariants). */
+typedef struct {
+    int32_t input_count;   /* N, 1..16 */
+    int32_t output_count;  /* M, 1..16 */
+    int32_t n;             /* frames consumed per run, >= 1 */
+    int32_t left_context;  /* L; -1 = default */
+    uint32_t flags;        /* NNVISR_INTERPOLATION | _EXTRA_FRAME | _DOUBLE_FRAME */
+    int32_t sx_num, sx_den, sy_num, sy_den;  /* rational scale factor; W*sx, H*sy integral */
+    int32_t align;         /* input tensor H/W multiple: power of two in [1, 256] */
+    int32_t dtype;         /* NNVISR_F32 | NNVISR_F16 (both tensors) */
+} nnvisr_network;
+
+/* One frame: three plane pointers and their pitches in bytes. */
+typedef struct {
+    void *plane[3];
+    int64_t pitch[3];
+} nnvisr_frame;
+
+typedef struct nnvisr_handle nnvisr_handle;
+
+/* Validate the clip format and network contract and create a handle.
+ * *out is set only on success.  Does not touch the GPU. */
+nnvisr_status nnvisr_open(const nnvisr_clip_format *format, const nnvisr_network *network,
+                          nnvisr_handle **out);
+
+/* Free the handle and its scratch buffers.  nnvisr_close(NULL) is OK.  The
+ * caller must make sure no enqueued work of this handle is still pending. */
+nnvisr_status nnvisr_close(nnvisr_handle *h);
+
+/* Text of the last failure on this thread ("" if none). */
+const char *nnvisr_last_error(void);
+
+/* Input tensor shape [1, 3N, Hp, Wp] and minimum output tensor shape
+ * [1, 3M, H*sy, W*sx]; also the output frame size (W*sx, H*sy). */
+nnvisr_status nnvisr_tensor_shapes(const nnvisr_handle *h, int64_t in_nchw[4], int64_t out_nchw[4]);
+
+/* Tuple plan of a whole clip (steps A1-A2; §3.3).
+ * cut: host [num_frames]; cut[k] != 0 means a scene change between frames
+ * k-1 and k (cut[0] ignored; reading A9).  Writes run r's input frame indices
+ * to run_inputs[r*N .. r*N+N-1] and its half-open fresh interval to
+ * run_fresh[2r], run_fresh[2r+1] (host arrays, capacity `cap` runs);
+ * *num_runs = number of runs.  NNVISR_ERR_CAPACITY if cap is too small
+ * (*num_runs then holds the required count). */
+nnvisr_status nnvisr_plan(const nnvisr_handle *h, int64_t num_frames, const uint8_t *cut,
+                          int64_t *run_inputs, int64_t *run_fresh, int64_t cap, int64_t *num_runs);
+
+/* Plan of the runs whose fresh frames lie in [fresh_begin, fresh_end) of a
+ * clip of num_frames frames, knowing only the cut flags of the window
+ * [first, first+count) (a shard plus its halo).  cut: host
+ * [count], cut[i] is the flag of frame first+i.  Requires the window to
+ * cover [max(0, fresh_begin-L), min(num_frames, fresh_end+N-1-L)).  For the
+ * paper's n > 1 grouping the window must be the whole clip (otherwise
+ * NNVISR_ERR_UNSUPPORTED).  The result equals nnvisr_plan of the whole clip
+ * restricted to those runs. */
+nnvisr_status nnvisr_plan_range(const nnvisr_handle *h, int64_t num_frames, int64_t first,
+                                int64_t count, const uint8_t *cut, int64_t fresh_begin,
+                                int64_t fresh_end, int64_t *run_inputs, int64_t *run_fresh,
+                                int64_t cap, int64_t *num_runs);
+
+/* Bind the device-resident frames that batched calls refer to: frames[i]
+ * (host array of descriptors) is frame number base+i.  The descriptors are
+ * copied to a handle-owned device table (synchronously); the pixel data is
+ * not copied and must stay valid while batched work referring to it runs.
+ * Re-binding replaces the table (after the handle's pending batched work). */
+nnvisr_status nnvisr_bind_frames(nnvisr_handle *h, int64_t base, const nnvisr_frame *frames,
+                                 int64_t count);
+
+/* frames -> tensor for one tuple (steps A3-A7).  in: host array [N] of frame
+ * descriptors (the same frame may appear several times); tensor: device
+ * [1, 3N, Hp, Wp] of the handle's dtype, 16-byte aligned. */
+nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, void *tensor,
+                                      void *stream);
+
+/* frames -> tensor for num_runs tuples in one launch.  run_inputs: host
+ * [num_runs * N] absolute frame indices (e.g. from nnvisr_plan), each within
+ * the bound table; tuple r is written to tensors + r*tensor_stride_bytes
+ * (stride >= the tensor size, multiple of 16). */
+nnvisr_status nnvisr_frames_to_tensor_batch(nnvisr_handle *h, const int64_t *run_inputs,
+                                            int64_t num_runs, void *tensors,
+                                            int64_t tensor_stride_bytes, void *stream);
+
+/* Store mode (SURVEY.md §8(d) "S"; §3.3 P:373-379 at batch 1):
+ * convert bound frames first .. first+count-1 once each into a frame-major
+ * store of slots [3][Hp][Wp]; slot k = frame first+k at store + k*3*Hp*Wp*elem.
+ * A run whose inputs are consecutive indices a, a+1, ..., a+N-1 is then the
+ * valid [1, 3N, Hp, Wp] tensor starting at slot (a - first). */
+nnvisr_status nnvisr_frames_to_store(nnvisr_handle *h, int64_t first, int64_t count, void *store,
+                                     void *stream);
+
+/* tensor -> frames for one tuple's network output (steps B1-B4).  tensor:
+ * device [1, 3M, t_h, t_w]; out: host array [M] of output frame descriptors
+ * (frames of the clip's family/bits/matrix/range at W*sx x H*sy). */
+nnvisr_status nnvisr_tensor_to_frames(nnvisr_handle *h, const void *tensor, int64_t t_h,
+                                      int64_t t_w, const nnvisr_frame *out, void *stream);
+
+/* tensor -> frames for `count` output tensors in one launch: tensor c at
+ * tensors + c*tensor_stride_bytes; its output slot o goes to out[c*M + o]
+ * (host array [count*M] of descriptors). */
+nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensors,
+                                            int64_t tensor_stride_bytes, int64_t t_h,
+                                            int64_t t_w, const nnvisr_frame *out, int64_t count,
+                                            void *stream);
+
+/* Number of CUDA kernels this library has launched in this process. */
+int64_t nnvisr_launch_count(void);
+
+/* Library version string. */
+const char *nnvisr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NNVISR_H */

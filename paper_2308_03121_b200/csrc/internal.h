@@ -1,0 +1,78 @@
+// internal.h -- types shared by the C ABI layer (nnvisr.cpp) and the sm_100a
+// kernels (kernels.cu).  Not part of the public ABI (include/nnvisr.h).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nnvisr {
+
+constexpr int kYUV420 = 0, kYUV444 = 1, kRGB = 2;
+constexpr int kF32 = 0, kF16 = 1;
+constexpr int kPx = 8;           // luma columns per thread (one 16-byte fp16 store)
+constexpr int kThreads = 256;    // CTA size of the conversion kernels
+constexpr int kMaxGridY = 65535; // jobs per launch (grid.y)
+
+// Device copy of one frame descriptor (same layout as nnvisr_frame).
+struct DevFrame {
+    const void *plane[3];
+    int64_t pitch[3];
+};
+
+// frames -> tensor colour constants (steps A5-A6), fp32.
+//   luma / RGB channel : v = (16*code - y_off) * y_scale
+//   chroma             : P = (s - c_off) * c_scale, s = 16 x the (upsampled) code
+//   R = Y + r_pr*Pr ;  B = Y + b_pb*Pb ;  G = Y - g_pb*Pb - g_pr*Pr
+struct F2TColour {
+    int32_t y_off, c_off;
+    float y_scale, c_scale;
+    float r_pr, b_pb, g_pb, g_pr;
+};
+
+// tensor -> frames colour constants (steps B2, B4), in fp32 and fp64.
+//   Y' = G + kr(R-G) + kb(B-G);  Pb = (B-Y')/db;  Pr = (R-Y')/dr
+//   code = clamp(rne(Y'*ys + yo)), clamp(rne(P*cs + co)) to [0, maxc]
+struct T2FColour {
+    double kr, kb, db, dr, ys, yo, cs, co;
+    float fkr, fkb, fdb, fdr, fys, fyo, fcs, fco;
+    uint32_t maxc;
+};
+
+struct F2TArgs {
+    const DevFrame *frames;   // bound frame table (device)
+    const int32_t *job_frame; // per job: index into `frames` (device)
+    char *dst;                // tensor base of job 0's run
+    int64_t run_stride;       // bytes between consecutive runs' tensors
+    int64_t slot_bytes;       // bytes of one slot (3*Hp*Wp*elem)
+    int32_t jobs_per_run;     // N (or 1 in store mode)
+    int32_t job_base;         // first job of this launch
+    int32_t W, H, Hp, Wp;     // clip size and padded tensor size
+    int32_t units, col_units; // threads per job and column groups per row unit
+    int32_t vec_in;           // 1: all bound planes/pitches 16-byte aligned
+    int32_t vec_out;          // 1: tensor rows allow 16-byte stores
+    F2TColour col;
+};
+
+struct T2FArgs {
+    const char *src;          // tensor of job 0's tuple
+    int64_t tensor_stride;    // bytes between tuples' tensors
+    const DevFrame *out;      // output frame descriptors [count*M] (device)
+    int32_t M;                // output slots per tensor
+    int32_t job_base;
+    int32_t Wo, Ho;           // output frame size
+    int64_t th, tw;           // tensor spatial size
+    int32_t units, col_units;
+    int32_t vec_in;           // tensor rows allow 16-byte loads
+    int32_t vec_out;          // output planes allow vector stores
+    T2FColour col;
+};
+
+// Launchers (kernels.cu).  Return the CUDA error of the launch.
+cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, int num_jobs,
+                       cudaStream_t s);
+cudaError_t launch_t2f(int family, int bits, int dtype, const T2FArgs &a, int num_jobs,
+                       cudaStream_t s);
+
+void count_launch();
+
+}  // namespace nnvisr

@@ -1,0 +1,674 @@
+// nnvisr.cpp -- the C ABI (include/nnvisr.h): validation, the host tuple
+// planner, scratch management and kernel dispatch.
+//
+// Citations: PAPER.md = /root/reference/PAPER.md (arXiv 2308.03121); readings
+// A1..A16 are listed in DESIGN.md §3.
+#include "nnvisr.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace nnvisr;
+
+namespace {
+
+thread_local std::string g_error;
+std::atomic<int64_t> g_launches{0};
+
+nnvisr_status fail(nnvisr_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+nnvisr_status fail(nnvisr_status s, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_error = buf;
+    return s;
+}
+
+nnvisr_status cuda_fail(cudaError_t e, const char *what)
+{
+    return fail(NNVISR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// A1: ITU matrix coefficients (Kr, Kb).
+void kr_kb(int matrix, double &kr, double &kb)
+{
+    switch (matrix) {
+    case NNVISR_BT601: kr = 0.299; kb = 0.114; break;
+    case NNVISR_BT709: kr = 0.2126; kb = 0.0722; break;
+    default: kr = 0.2627; kb = 0.0593; break;
+    }
+}
+
+// A pinned-host + device upload slot.  Tables a launch reads (job -> frame
+// index, output frame descriptors) are copied host->pinned->device on the
+// caller's stream; the slot's event, recorded after the consuming kernels,
+// guards reuse.
+struct UploadSlot {
+    void *host = nullptr;
+    void *dev = nullptr;
+    cudaEvent_t done = nullptr;
+    bool pending = false;
+};
+constexpr size_t kSlotBytes = size_t(1) << 20;
+constexpr int kSlots = 8;
+
+}  // namespace
+
+void nnvisr::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct nnvisr_handle {
+    nnvisr_clip_format fmt{};
+    nnvisr_network net{};
+    int N = 0, M = 0, n = 0, L = 0;
+    bool paper = false;  // paper grouping (vs sliding window)
+    int64_t Hp = 0, Wp = 0, Wo = 0, Ho = 0;
+    int elem = 4;
+    F2TColour f2c{};
+    T2FColour t2c{};
+    // device state (created on the first device call)
+    int device = -1;
+    UploadSlot slots[kSlots];
+    int next_slot = 0;
+    DevFrame *frames = nullptr;
+    int64_t frames_cap = 0, frames_base = 0, frames_count = 0;
+    bool frames_vec = false;
+};
+
+namespace {
+
+// --------------------------------------------------------------- planning
+// Steps A1-A2 (§3.3; readings A8, A9).  One closed form
+// covers both tuple shapes: per scene [s, e) with m = e - s frames, runs
+// k = 0 .. ceil(m/n)-1 have
+//   base  = min(s + k n, max(s, e - n))          (recycle the last group)
+//   in[j] = clamp(base - L + j, s, e - 1)         (duplicate at scene edges)
+//   fresh = [s + k n, min(s + (k+1) n, e))
+struct PlanSink {
+    int64_t *inputs, *fresh;
+    int64_t cap, count = 0;
+    int N;
+    void emit(const int64_t *in, int64_t lo, int64_t hi)
+    {
+        if (count < cap) {
+            std::memcpy(inputs + count * N, in, sizeof(int64_t) * N);
+            fresh[2 * count] = lo;
+            fresh[2 * count + 1] = hi;
+        }
+        ++count;
+    }
+};
+
+void plan_scene(const nnvisr_handle *h, int64_t s, int64_t e, int64_t fresh_begin,
+                int64_t fresh_end, PlanSink &out)
+{
+    const int64_t n = h->n, m = e - s, K = (m + n - 1) / n;
+    int64_t in[16];
+    for (int64_t k = 0; k < K; ++k) {
+        const int64_t lo = s + k * n, hi = std::min(s + (k + 1) * n, e);
+        if (lo < fresh_begin || lo >= fresh_end) continue;
+        const int64_t base = std::min(s + k * n, std::max(s, e - n));
+        for (int j = 0; j < h->N; ++j) in[j] = std::min(std::max(base - h->L + j, s), e - 1);
+        out.emit(in, lo, hi);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *nnvisr_last_error(void) { return g_error.c_str(); }
+const char *nnvisr_version(void) { return "nnvisr-b200 0.1 (sm_100a)"; }
+int64_t nnvisr_launch_count(void) { return g_launches.load(); }
+
+nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *net, nnvisr_handle **out)
+{
+    g_error.clear();
+    if (!fmt || !net || !out) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    const nnvisr_clip_format f = *fmt;
+    const nnvisr_network w = *net;
+    if (f.width < 1 || f.height < 1 || f.width > 32768 || f.height > 32768)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "frame size %dx%d outside [1, 32768]", f.width, f.height);
+    if (f.family != NNVISR_YUV420 && f.family != NNVISR_YUV444 && f.family != NNVISR_RGB)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "unknown pixel family %d", f.family);
+    if (f.bits != 8 && f.bits != 10 && f.bits != 16)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "bits must be 8, 10 or 16 (got %d)", f.bits);
+    if (f.family != NNVISR_RGB && (f.matrix < NNVISR_BT601 || f.matrix > NNVISR_BT2020))
+        return fail(NNVISR_ERR_INVALID_CONFIG, "unknown colour matrix %d", f.matrix);
+    if (f.range != NNVISR_LIMITED && f.range != NNVISR_FULL)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "unknown range %d", f.range);
+    if (f.chroma_loc == NNVISR_CHROMA_LEFT)
+        return fail(NNVISR_ERR_UNSUPPORTED, "LEFT (MPEG-2) chroma siting is not implemented");
+    if (f.chroma_loc != NNVISR_CHROMA_CENTER)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "unknown chroma siting %d", f.chroma_loc);
+    if (f.family == NNVISR_YUV420 && ((f.width | f.height) & 1))
+        return fail(NNVISR_ERR_INVALID_CONFIG, "4:2:0 needs even width and height (got %dx%d)", f.width, f.height);
+
+    if (w.input_count < 1 || w.input_count > 16)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "input_count must be in [1, 16] (got %d)", w.input_count);
+    if (w.output_count < 1 || w.output_count > 16)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "output_count must be in [1, 16] (got %d)", w.output_count);
+    if (w.n < 1) return fail(NNVISR_ERR_INVALID_CONFIG, "n must be >= 1 (got %d)", w.n);
+    if (w.flags & ~7u) return fail(NNVISR_ERR_INVALID_CONFIG, "unknown flag bits 0x%x", w.flags);
+    const bool interp = w.flags & NNVISR_INTERPOLATION, extra = w.flags & NNVISR_EXTRA_FRAME,
+               dbl = w.flags & NNVISR_DOUBLE_FRAME;
+    if (dbl && !interp) return fail(NNVISR_ERR_INVALID_CONFIG, "DOUBLE_FRAME requires INTERPOLATION");
+    if (w.sx_num < 1 || w.sx_den < 1 || w.sy_num < 1 || w.sy_den < 1)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "scale factor terms must be positive");
+    if (interp && !dbl && (w.sx_num != w.sx_den || w.sy_num != w.sy_den))
+        return fail(NNVISR_ERR_INVALID_CONFIG, "INTERPOLATION without DOUBLE_FRAME passes input frames through: scale must be 1");
+    if ((int64_t)f.width * w.sx_num % w.sx_den || (int64_t)f.height * w.sy_num % w.sy_den)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "output size W*sx x H*sy is not integral");
+    const int64_t Wo = (int64_t)f.width * w.sx_num / w.sx_den, Ho = (int64_t)f.height * w.sy_num / w.sy_den;
+    if (Wo > 65536 || Ho > 65536) return fail(NNVISR_ERR_INVALID_CONFIG, "output size too large");
+    if (f.family == NNVISR_YUV420 && ((Wo | Ho) & 1))
+        return fail(NNVISR_ERR_INVALID_CONFIG, "4:2:0 output size must be even");
+    if (!is_pow2(w.align) || w.align > 256)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "align must be a power of two in [1, 256] (got %d)", w.align);
+    if (w.dtype != NNVISR_F32 && w.dtype != NNVISR_F16)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "unknown tensor dtype %d", w.dtype);
+
+    // tuple shape: paper grouping or sliding window (reading A8)
+    const int N = w.input_count, M = w.output_count, n = w.n;
+    bool paper = false;
+    int L = 0;
+    if ((w.left_context == 0 || w.left_context == -1) && N == n + (extra ? 1 : 0)) {
+        const bool m_ok = dbl ? (M == 2 * n || M == 2 * n + 1) : (M == n);
+        if (!m_ok)
+            return fail(NNVISR_ERR_INVALID_CONFIG, "paper grouping: output_count must be %s (got %d)",
+                        dbl ? "2n or 2n+1" : "n", M);
+        paper = true;
+        L = 0;
+    } else if (w.flags == 0 && n == 1 && M == 1) {
+        L = w.left_context == -1 ? (N - 1) / 2 : w.left_context;
+        if (L < 0 || L >= N)
+            return fail(NNVISR_ERR_INVALID_CONFIG, "left_context must be in [0, input_count) (got %d)", L);
+    } else {
+        return fail(NNVISR_ERR_INVALID_CONFIG,
+                    "tuple shape: need input_count = n + EXTRA (paper grouping) or flags = 0, n = 1, "
+                    "output_count = 1 (sliding window)");
+    }
+
+    nnvisr_handle *h = new (std::nothrow) nnvisr_handle();
+    if (!h) return fail(NNVISR_ERR_OUT_OF_MEMORY, "handle allocation failed");
+    h->fmt = f;
+    h->net = w;
+    h->N = N; h->M = M; h->n = n; h->L = L; h->paper = paper;
+    h->Hp = round_up(f.height, w.align);
+    h->Wp = round_up(f.width, w.align);
+    h->Wo = Wo; h->Ho = Ho;
+    h->elem = w.dtype == NNVISR_F16 ? 2 : 4;
+
+    // A5 dequantisation on 16x codes: luma v = (16c - y_off) * y_scale,
+    // chroma P = (s - c_off) * c_scale with s = 16 x (upsampled) code.
+    const double k = std::ldexp(1.0, f.bits - 8), full = std::ldexp(1.0, f.bits) - 1.0;
+    if (f.range == NNVISR_LIMITED) {
+        h->f2c.y_off = (int32_t)(256 * k);
+        h->f2c.y_scale = (float)(1.0 / (16.0 * 219.0 * k));
+        h->f2c.c_off = (int32_t)(2048 * k);
+        h->f2c.c_scale = (float)(1.0 / (16.0 * 224.0 * k));
+    } else {
+        h->f2c.y_off = 0;
+        h->f2c.y_scale = (float)(1.0 / (16.0 * full));
+        h->f2c.c_off = (int32_t)(16 * std::ldexp(1.0, f.bits - 1));
+        h->f2c.c_scale = (float)(1.0 / (16.0 * full));
+    }
+    // A6 inverse matrix; G in difference form (gray axis exact, reading A16)
+    double kr = 0, kb = 0;
+    kr_kb(f.matrix, kr, kb);
+    const double kg = 1.0 - kr - kb;
+    h->f2c.r_pr = (float)(2.0 * (1.0 - kr));
+    h->f2c.b_pb = (float)(2.0 * (1.0 - kb));
+    h->f2c.g_pb = (float)(kb * 2.0 * (1.0 - kb) / kg);
+    h->f2c.g_pr = (float)(kr * 2.0 * (1.0 - kr) / kg);
+    // B2/B4 constants
+    T2FColour &c = h->t2c;
+    c.kr = kr; c.kb = kb; c.db = 2.0 * (1.0 - kb); c.dr = 2.0 * (1.0 - kr);
+    if (f.range == NNVISR_LIMITED) { c.ys = 219.0 * k; c.yo = 16.0 * k; c.cs = 224.0 * k; c.co = 128.0 * k; }
+    else { c.ys = full; c.yo = 0.0; c.cs = full; c.co = std::ldexp(1.0, f.bits - 1); }
+    c.fkr = (float)c.kr; c.fkb = (float)c.kb; c.fdb = (float)c.db; c.fdr = (float)c.dr;
+    c.fys = (float)c.ys; c.fyo = (float)c.yo; c.fcs = (float)c.cs; c.fco = (float)c.co;
+    c.maxc = (uint32_t)full;
+    *out = h;
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_close(nnvisr_handle *h)
+{
+    g_error.clear();
+    if (!h) return NNVISR_OK;
+    if (h->device >= 0) {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        if (prev != h->device) cudaSetDevice(h->device);
+        for (auto &s : h->slots) {
+            if (s.done) { cudaEventSynchronize(s.done); cudaEventDestroy(s.done); }
+            if (s.host) cudaFreeHost(s.host);
+            if (s.dev) cudaFree(s.dev);
+        }
+        if (h->frames) cudaFree(h->frames);
+        if (prev >= 0 && prev != h->device) cudaSetDevice(prev);
+    }
+    delete h;
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_tensor_shapes(const nnvisr_handle *h, int64_t in_nchw[4], int64_t out_nchw[4])
+{
+    g_error.clear();
+    if (!h) return fail(NNVISR_ERR_INVALID_ARG, "null handle");
+    if (in_nchw) { in_nchw[0] = 1; in_nchw[1] = 3 * h->N; in_nchw[2] = h->Hp; in_nchw[3] = h->Wp; }
+    if (out_nchw) { out_nchw[0] = 1; out_nchw[1] = 3 * h->M; out_nchw[2] = h->Ho; out_nchw[3] = h->Wo; }
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_plan(const nnvisr_handle *h, int64_t num_frames, const uint8_t *cut,
+                          int64_t *run_inputs, int64_t *run_fresh, int64_t cap, int64_t *num_runs)
+{
+    g_error.clear();
+    if (!h || !num_runs) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (num_frames < 0) return fail(NNVISR_ERR_INVALID_ARG, "num_frames < 0");
+    if (num_frames > 0 && !cut) return fail(NNVISR_ERR_INVALID_ARG, "null cut array");
+    if (cap > 0 && (!run_inputs || !run_fresh)) return fail(NNVISR_ERR_INVALID_ARG, "null output arrays");
+    PlanSink sink{run_inputs, run_fresh, std::max<int64_t>(cap, 0), 0, h->N};
+    int64_t s = 0;
+    for (int64_t k = 1; k <= num_frames; ++k) {
+        if (k == num_frames || cut[k]) {
+            plan_scene(h, s, k, 0, num_frames, sink);
+            s = k;
+        }
+    }
+    *num_runs = sink.count;
+    if (sink.count > cap) return fail(NNVISR_ERR_CAPACITY, "plan needs %lld runs, capacity %lld",
+                                      (long long)sink.count, (long long)cap);
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_plan_range(const nnvisr_handle *h, int64_t num_frames, int64_t first, int64_t count,
+                                const uint8_t *cut, int64_t fresh_begin, int64_t fresh_end,
+                                int64_t *run_inputs, int64_t *run_fresh, int64_t cap, int64_t *num_runs)
+{
+    g_error.clear();
+    if (!h || !num_runs) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (num_frames < 0 || first < 0 || count < 0 || first + count > num_frames)
+        return fail(NNVISR_ERR_INVALID_ARG, "window [%lld, %lld) outside the clip of %lld frames",
+                    (long long)first, (long long)(first + count), (long long)num_frames);
+    if (fresh_begin < 0 || fresh_end > num_frames || fresh_begin > fresh_end)
+        return fail(NNVISR_ERR_INVALID_ARG, "bad fresh range [%lld, %lld)", (long long)fresh_begin,
+                    (long long)fresh_end);
+    if (count > 0 && !cut) return fail(NNVISR_ERR_INVALID_ARG, "null cut array");
+    if (cap > 0 && (!run_inputs || !run_fresh)) return fail(NNVISR_ERR_INVALID_ARG, "null output arrays");
+    PlanSink sink{run_inputs, run_fresh, std::max<int64_t>(cap, 0), 0, h->N};
+    if (fresh_begin == fresh_end) { *num_runs = 0; return NNVISR_OK; }
+    if (h->paper && h->n > 1) {
+        // a run's phase depends on its scene start, possibly far outside a
+        // shard window (SURVEY.md §8(e) "Limitation")
+        if (first != 0 || count != num_frames)
+            return fail(NNVISR_ERR_UNSUPPORTED, "n > 1 grouping needs the whole clip's cut flags");
+        int64_t s = 0;
+        for (int64_t k = 1; k <= num_frames; ++k)
+            if (k == num_frames || cut[k]) { plan_scene(h, s, k, fresh_begin, fresh_end, sink); s = k; }
+    } else {
+        const int64_t need_lo = std::max<int64_t>(0, fresh_begin - h->L);
+        const int64_t need_hi = std::min<int64_t>(num_frames, fresh_end + h->N - 1 - h->L);
+        if (first > need_lo || first + count < need_hi)
+            return fail(NNVISR_ERR_INVALID_ARG, "window [%lld, %lld) does not cover [%lld, %lld)",
+                        (long long)first, (long long)(first + count), (long long)need_lo, (long long)need_hi);
+        // Scene bounds seen from inside the window.  Bounds beyond the window
+        // never bind: every clamp argument lies inside the covered range.
+        const int64_t end = first + count;
+        std::vector<int64_t> scene_end(count);  // first cut after each frame
+        int64_t e = end;
+        for (int64_t k = end - 1; k >= first; --k) {
+            scene_end[k - first] = e;
+            if (cut[k - first] && k > 0) e = k;
+        }
+        int64_t s = first;
+        for (int64_t k = first; k < end; ++k) {
+            if (k > first && cut[k - first]) s = k;
+            if (k < fresh_begin || k >= fresh_end) continue;
+            const int64_t ek = scene_end[k - first];
+            int64_t in[16];
+            for (int j = 0; j < h->N; ++j) in[j] = std::min(std::max(k - h->L + j, s), ek - 1);
+            sink.emit(in, k, k + 1);
+        }
+    }
+    *num_runs = sink.count;
+    if (sink.count > cap) return fail(NNVISR_ERR_CAPACITY, "plan needs %lld runs, capacity %lld",
+                                      (long long)sink.count, (long long)cap);
+    return NNVISR_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ device side
+namespace {
+
+nnvisr_status ensure_device(nnvisr_handle *h)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (h->device < 0) {
+        h->device = dev;
+        for (auto &s : h->slots) {
+            if ((e = cudaHostAlloc(&s.host, kSlotBytes, cudaHostAllocDefault)) != cudaSuccess)
+                return cuda_fail(e, "cudaHostAlloc (upload slot)");
+            if ((e = cudaMalloc(&s.dev, kSlotBytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (upload slot)");
+            if ((e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "cudaEventCreate");
+        }
+    } else if (dev != h->device) {
+        return fail(NNVISR_ERR_INVALID_ARG, "handle is bound to device %d but device %d is current",
+                    h->device, dev);
+    }
+    return NNVISR_OK;
+}
+
+// Take the next upload slot, waiting for its previous consumer if needed.
+nnvisr_status acquire_slot(nnvisr_handle *h, UploadSlot **out)
+{
+    UploadSlot &s = h->slots[h->next_slot];
+    h->next_slot = (h->next_slot + 1) % kSlots;
+    if (s.pending) {
+        cudaError_t e = cudaEventSynchronize(s.done);
+        if (e != cudaSuccess) return cuda_fail(e, "waiting for an upload slot");
+        s.pending = false;
+    }
+    *out = &s;
+    return NNVISR_OK;
+}
+
+nnvisr_status upload(UploadSlot *s, size_t bytes, cudaStream_t st)
+{
+    cudaError_t e = cudaMemcpyAsync(s->dev, s->host, bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync (upload)");
+    return NNVISR_OK;
+}
+
+nnvisr_status release_slot(UploadSlot *s, cudaStream_t st)
+{
+    cudaError_t e = cudaEventRecord(s->done, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    s->pending = true;
+    return NNVISR_OK;
+}
+
+nnvisr_status check_frame(const nnvisr_handle *h, const nnvisr_frame &fr, int64_t w, int64_t hgt,
+                          const char *what, int64_t idx, bool *vec)
+{
+    const int bytes = h->fmt.bits == 8 ? 1 : 2;
+    for (int p = 0; p < 3; ++p) {
+        const bool sub = h->fmt.family == NNVISR_YUV420 && p > 0;
+        const int64_t pw = sub ? w / 2 : w;
+        (void)hgt;
+        if (!fr.plane[p]) return fail(NNVISR_ERR_INVALID_ARG, "%s %lld: plane %d is null", what, (long long)idx, p);
+        if (fr.pitch[p] < pw * bytes || fr.pitch[p] % bytes)
+            return fail(NNVISR_ERR_INVALID_ARG, "%s %lld: plane %d pitch %lld invalid (row is %lld bytes)", what,
+                        (long long)idx, p, (long long)fr.pitch[p], (long long)(pw * bytes));
+        if (reinterpret_cast<uintptr_t>(fr.plane[p]) % bytes)
+            return fail(NNVISR_ERR_INVALID_ARG, "%s %lld: plane %d not sample aligned", what, (long long)idx, p);
+        if (!aligned16(fr.plane[p]) || fr.pitch[p] % 16) *vec = false;
+    }
+    return NNVISR_OK;
+}
+
+F2TArgs f2t_args(const nnvisr_handle *h)
+{
+    F2TArgs a{};
+    const int rows = h->fmt.family == NNVISR_YUV420 ? 2 : 1;
+    a.W = h->fmt.width; a.H = h->fmt.height; a.Hp = (int32_t)h->Hp; a.Wp = (int32_t)h->Wp;
+    a.col_units = (int32_t)((h->Wp + kPx - 1) / kPx);
+    a.units = (int32_t)(h->Hp / rows) * a.col_units;
+    a.slot_bytes = 3 * h->Hp * h->Wp * h->elem;
+    a.vec_out = (h->Wp * h->elem) % 16 == 0;
+    a.col = h->f2c;
+    return a;
+}
+
+nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, cudaStream_t st)
+{
+    for (int64_t j0 = 0; j0 < jobs; j0 += kMaxGridY) {
+        a.job_base = (int32_t)j0;
+        const int n = (int)std::min<int64_t>(kMaxGridY, jobs - j0);
+        cudaError_t e = launch_f2t(h->fmt.family, h->fmt.bits, h->net.dtype, a, n, st);
+        if (e != cudaSuccess) return cuda_fail(e, "f2t kernel launch");
+    }
+    return NNVISR_OK;
+}
+
+T2FArgs t2f_args(const nnvisr_handle *h, int64_t t_h, int64_t t_w)
+{
+    T2FArgs a{};
+    const int rows = h->fmt.family == NNVISR_YUV420 ? 2 : 1;
+    a.M = h->M; a.Wo = (int32_t)h->Wo; a.Ho = (int32_t)h->Ho; a.th = t_h; a.tw = t_w;
+    a.col_units = (int32_t)((h->Wo + kPx - 1) / kPx);
+    a.units = (int32_t)(h->Ho / rows) * a.col_units;
+    a.vec_in = (t_w * h->elem) % 16 == 0;
+    a.col = h->t2c;
+    return a;
+}
+
+nnvisr_status run_t2f(nnvisr_handle *h, T2FArgs a, int64_t jobs, cudaStream_t st)
+{
+    for (int64_t j0 = 0; j0 < jobs; j0 += kMaxGridY) {
+        a.job_base = (int32_t)j0;
+        const int n = (int)std::min<int64_t>(kMaxGridY, jobs - j0);
+        cudaError_t e = launch_t2f(h->fmt.family, h->fmt.bits, h->net.dtype, a, n, st);
+        if (e != cudaSuccess) return cuda_fail(e, "t2f kernel launch");
+    }
+    return NNVISR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+nnvisr_status nnvisr_bind_frames(nnvisr_handle *h, int64_t base, const nnvisr_frame *frames, int64_t count)
+{
+    g_error.clear();
+    if (!h) return fail(NNVISR_ERR_INVALID_ARG, "null handle");
+    if (count < 0 || (count > 0 && !frames)) return fail(NNVISR_ERR_INVALID_ARG, "bad frame array");
+    if (count > INT32_MAX) return fail(NNVISR_ERR_INVALID_ARG, "too many frames");
+    bool vec = true;
+    for (int64_t i = 0; i < count; ++i) {
+        nnvisr_status s = check_frame(h, frames[i], h->fmt.width, h->fmt.height, "frame", base + i, &vec);
+        if (s) return s;
+    }
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    cudaError_t e;
+    // previous batched work may still read the old table
+    for (auto &sl : h->slots)
+        if (sl.pending && (e = cudaEventSynchronize(sl.done)) != cudaSuccess) return cuda_fail(e, "sync");
+    if (count > h->frames_cap) {
+        if (h->frames) cudaFree(h->frames);
+        h->frames = nullptr;
+        h->frames_cap = 0;
+        if ((e = cudaMalloc(&h->frames, sizeof(DevFrame) * count)) != cudaSuccess)
+            return cuda_fail(e, "cudaMalloc (frame table)");
+        h->frames_cap = count;
+    }
+    static_assert(sizeof(DevFrame) == sizeof(nnvisr_frame), "descriptor layout");
+    if (count && (e = cudaMemcpy(h->frames, frames, sizeof(DevFrame) * count, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpy (frame table)");
+    h->frames_base = base;
+    h->frames_count = count;
+    h->frames_vec = vec;
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, void *tensor, void *stream)
+{
+    g_error.clear();
+    if (!h || !in || !tensor) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (!aligned16(tensor)) return fail(NNVISR_ERR_INVALID_ARG, "tensor pointer not 16-byte aligned");
+    bool vec = true;
+    for (int t = 0; t < h->N; ++t) {
+        nnvisr_status s = check_frame(h, in[t], h->fmt.width, h->fmt.height, "input slot", t, &vec);
+        if (s) return s;
+    }
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    UploadSlot *slot = nullptr;
+    if ((s = acquire_slot(h, &slot))) return s;
+    // [DevFrame x N][int32 x N]
+    std::memcpy(slot->host, in, sizeof(DevFrame) * h->N);
+    int32_t *idx = reinterpret_cast<int32_t *>(static_cast<char *>(slot->host) + sizeof(DevFrame) * h->N);
+    for (int t = 0; t < h->N; ++t) idx[t] = t;
+    if ((s = upload(slot, sizeof(DevFrame) * h->N + sizeof(int32_t) * h->N, st))) return s;
+    F2TArgs a = f2t_args(h);
+    a.frames = static_cast<const DevFrame *>(slot->dev);
+    a.job_frame = reinterpret_cast<const int32_t *>(static_cast<char *>(slot->dev) + sizeof(DevFrame) * h->N);
+    a.dst = static_cast<char *>(tensor);
+    a.run_stride = 0;
+    a.jobs_per_run = h->N;
+    a.vec_in = vec;
+    s = run_f2t(h, a, h->N, st);
+    nnvisr_status s2 = release_slot(slot, st);
+    return s ? s : s2;
+}
+
+static nnvisr_status f2t_indexed(nnvisr_handle *h, const int64_t *frame_idx, int64_t jobs, int jobs_per_run,
+                                 void *dst, int64_t run_stride, cudaStream_t st)
+{
+    if (!h->frames) return fail(NNVISR_ERR_INVALID_ARG, "no frames bound (nnvisr_bind_frames)");
+    const int64_t per_slot = (int64_t)(kSlotBytes / sizeof(int32_t)) / jobs_per_run * jobs_per_run;
+    F2TArgs a = f2t_args(h);
+    a.frames = h->frames;
+    a.jobs_per_run = jobs_per_run;
+    a.run_stride = run_stride;
+    a.vec_in = h->frames_vec;
+    for (int64_t j0 = 0; j0 < jobs; j0 += per_slot) {
+        const int64_t nj = std::min(per_slot, jobs - j0);
+        UploadSlot *slot = nullptr;
+        nnvisr_status s = acquire_slot(h, &slot);
+        if (s) return s;
+        int32_t *idx = static_cast<int32_t *>(slot->host);
+        for (int64_t j = 0; j < nj; ++j) idx[j] = (int32_t)(frame_idx[j0 + j] - h->frames_base);
+        if ((s = upload(slot, sizeof(int32_t) * nj, st))) return s;
+        a.job_frame = static_cast<const int32_t *>(slot->dev);
+        a.dst = static_cast<char *>(dst) + (j0 / jobs_per_run) * run_stride;
+        s = run_f2t(h, a, nj, st);
+        nnvisr_status s2 = release_slot(slot, st);
+        if (s) return s;
+        if (s2) return s2;
+    }
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_frames_to_tensor_batch(nnvisr_handle *h, const int64_t *run_inputs, int64_t num_runs,
+                                            void *tensors, int64_t tensor_stride_bytes, void *stream)
+{
+    g_error.clear();
+    if (!h || (num_runs > 0 && (!run_inputs || !tensors))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (num_runs < 0) return fail(NNVISR_ERR_INVALID_ARG, "num_runs < 0");
+    if (num_runs == 0) return NNVISR_OK;
+    const int64_t tbytes = 3 * h->N * h->Hp * h->Wp * h->elem;
+    if (!aligned16(tensors) || tensor_stride_bytes % 16)
+        return fail(NNVISR_ERR_INVALID_ARG, "tensors / stride not 16-byte aligned");
+    if (num_runs > 1 && tensor_stride_bytes < tbytes)
+        return fail(NNVISR_ERR_INVALID_ARG, "tensor stride %lld < tensor size %lld", (long long)tensor_stride_bytes,
+                    (long long)tbytes);
+    const int64_t jobs = num_runs * h->N;
+    for (int64_t j = 0; j < jobs; ++j) {
+        const int64_t f = run_inputs[j];
+        if (f < h->frames_base || f >= h->frames_base + h->frames_count)
+            return fail(NNVISR_ERR_INVALID_ARG, "run %lld slot %lld: frame %lld not bound (bound [%lld, %lld))",
+                        (long long)(j / h->N), (long long)(j % h->N), (long long)f, (long long)h->frames_base,
+                        (long long)(h->frames_base + h->frames_count));
+    }
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    return f2t_indexed(h, run_inputs, jobs, h->N, tensors, tensor_stride_bytes, static_cast<cudaStream_t>(stream));
+}
+
+nnvisr_status nnvisr_frames_to_store(nnvisr_handle *h, int64_t first, int64_t count, void *store, void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && !store)) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
+    if (count == 0) return NNVISR_OK;
+    if (!aligned16(store)) return fail(NNVISR_ERR_INVALID_ARG, "store not 16-byte aligned");
+    if (first < h->frames_base || first + count > h->frames_base + h->frames_count)
+        return fail(NNVISR_ERR_INVALID_ARG, "frames [%lld, %lld) not bound", (long long)first, (long long)(first + count));
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    std::vector<int64_t> idx(count);
+    for (int64_t i = 0; i < count; ++i) idx[i] = first + i;
+    const int64_t slot_bytes = 3 * h->Hp * h->Wp * h->elem;
+    return f2t_indexed(h, idx.data(), count, 1, store, slot_bytes, static_cast<cudaStream_t>(stream));
+}
+
+static nnvisr_status t2f_common(nnvisr_handle *h, const void *tensors, int64_t stride, int64_t t_h, int64_t t_w,
+                                const nnvisr_frame *out, int64_t count, cudaStream_t st)
+{
+    if (t_h < h->Ho || t_w < h->Wo)
+        return fail(NNVISR_ERR_INVALID_ARG, "tensor %lldx%lld smaller than the output frame %lldx%lld",
+                    (long long)t_w, (long long)t_h, (long long)h->Wo, (long long)h->Ho);
+    if (!aligned16(tensors) || stride % 16) return fail(NNVISR_ERR_INVALID_ARG, "tensor / stride not 16-byte aligned");
+    const int64_t tbytes = 3 * h->M * t_h * t_w * h->elem;
+    if (count > 1 && stride < tbytes) return fail(NNVISR_ERR_INVALID_ARG, "tensor stride smaller than the tensor");
+    const int64_t jobs = count * h->M;
+    bool vec = true;
+    for (int64_t j = 0; j < jobs; ++j) {
+        nnvisr_status s = check_frame(h, out[j], h->Wo, h->Ho, "output frame", j, &vec);
+        if (s) return s;
+    }
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    T2FArgs a = t2f_args(h, t_h, t_w);
+    a.tensor_stride = stride;
+    a.vec_out = vec;
+    const int64_t per_slot = (int64_t)(kSlotBytes / sizeof(DevFrame)) / h->M * h->M;
+    for (int64_t j0 = 0; j0 < jobs; j0 += per_slot) {
+        const int64_t nj = std::min(per_slot, jobs - j0);
+        UploadSlot *slot = nullptr;
+        if ((s = acquire_slot(h, &slot))) return s;
+        std::memcpy(slot->host, out + j0, sizeof(DevFrame) * nj);
+        if ((s = upload(slot, sizeof(DevFrame) * nj, st))) return s;
+        a.out = static_cast<const DevFrame *>(slot->dev);
+        a.src = static_cast<const char *>(tensors) + (j0 / h->M) * stride;
+        s = run_t2f(h, a, nj, st);
+        nnvisr_status s2 = release_slot(slot, st);
+        if (s) return s;
+        if (s2) return s2;
+    }
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_tensor_to_frames(nnvisr_handle *h, const void *tensor, int64_t t_h, int64_t t_w,
+                                      const nnvisr_frame *out, void *stream)
+{
+    g_error.clear();
+    if (!h || !tensor || !out) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    return t2f_common(h, tensor, 0, t_h, t_w, out, 1, static_cast<cudaStream_t>(stream));
+}
+
+nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensors, int64_t tensor_stride_bytes,
+                                            int64_t t_h, int64_t t_w, const nnvisr_frame *out, int64_t count,
+                                            void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && (!tensors || !out))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
+    if (count == 0) return NNVISR_OK;
+    return t2f_common(h, tensors, tensor_stride_bytes, t_h, t_w, out, count, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

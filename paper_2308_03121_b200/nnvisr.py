@@ -1,0 +1,202 @@
+"""Thin ctypes binding of ``libnnvisr.so`` (include/nnvisr.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+sm_100a kernels.  Names follow the C ABI (``nnvisr_open`` -> :func:`open`,
+``nnvisr_frames_to_tensor`` -> :meth:`Handle.frames_to_tensor`, ...).
+PyTorch is used only to hold device memory and to name CUDA streams.
+
+There is no fallback: if the shared library is missing, importing this module
+raises, and every device call goes through the library or fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Sequence
+
+import numpy as np
+
+from .config import (BT601, BT709, BT2020, CHROMA_CENTER, CHROMA_LEFT, DOUBLE_FRAME, EXTRA_FRAME, F16,  # noqa: F401
+                     F32, FULL, INTERPOLATION, LIMITED, RGB, STATUS, YUV420, YUV444, ClipFormat, Config, Frame,
+                     Network)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnnvisr.so")
+
+
+class NnvisrError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"nnvisr {STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    st = C.c_int
+    H = C.c_void_p
+    i64 = C.c_int64
+    i64p = C.POINTER(C.c_int64)
+    sig = {
+        "nnvisr_open": (st, [C.POINTER(ClipFormat), C.POINTER(Network), C.POINTER(H)]),
+        "nnvisr_close": (st, [H]),
+        "nnvisr_last_error": (C.c_char_p, []),
+        "nnvisr_version": (C.c_char_p, []),
+        "nnvisr_launch_count": (i64, []),
+        "nnvisr_tensor_shapes": (st, [H, i64p, i64p]),
+        "nnvisr_plan": (st, [H, i64, C.c_void_p, i64p, i64p, i64, i64p]),
+        "nnvisr_plan_range": (st, [H, i64, i64, i64, C.c_void_p, i64, i64, i64p, i64p, i64, i64p]),
+        "nnvisr_bind_frames": (st, [H, i64, C.POINTER(Frame), i64]),
+        "nnvisr_frames_to_tensor": (st, [H, C.POINTER(Frame), C.c_void_p, C.c_void_p]),
+        "nnvisr_frames_to_tensor_batch": (st, [H, i64p, i64, C.c_void_p, i64, C.c_void_p]),
+        "nnvisr_frames_to_store": (st, [H, i64, i64, C.c_void_p, C.c_void_p]),
+        "nnvisr_tensor_to_frames": (st, [H, C.c_void_p, i64, i64, C.POINTER(Frame), C.c_void_p]),
+        "nnvisr_tensor_to_frames_batch": (st, [H, C.c_void_p, i64, i64, i64, C.POINTER(Frame), i64, C.c_void_p]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+_lib = _load()
+EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version", "nnvisr_launch_count",
+            "nnvisr_tensor_shapes", "nnvisr_plan", "nnvisr_plan_range", "nnvisr_bind_frames",
+            "nnvisr_frames_to_tensor", "nnvisr_frames_to_tensor_batch", "nnvisr_frames_to_store",
+            "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch")
+
+
+def lib():
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise NnvisrError(status, _lib.nnvisr_last_error().decode())
+
+
+def launch_count() -> int:
+    return int(_lib.nnvisr_launch_count())
+
+
+def version() -> str:
+    return _lib.nnvisr_version().decode()
+
+
+def _i64p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def _stream_ptr(stream) -> int | None:
+    """A torch.cuda.Stream, a raw cudaStream_t integer, or None (legacy default)."""
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def frame_array(frames: Sequence[Frame]):
+    arr = (Frame * len(frames))()
+    for i, f in enumerate(frames):
+        arr[i] = f
+    return arr
+
+
+class Handle:
+    """An open nnvisr handle (nnvisr_open ... nnvisr_close)."""
+
+    def __init__(self, cfg: Config):
+        f, n = cfg.structs()
+        h = C.c_void_p()
+        _check(_lib.nnvisr_open(C.byref(f), C.byref(n), C.byref(h)))
+        self._h = h
+        self.cfg = cfg
+        i = np.zeros(4, np.int64)
+        o = np.zeros(4, np.int64)
+        _check(_lib.nnvisr_tensor_shapes(self._h, _i64p(i), _i64p(o)))
+        self.in_shape = tuple(int(v) for v in i)
+        self.out_shape = tuple(int(v) for v in o)  # minimum; also (Ho, Wo) of output frames
+
+    # -- lifetime
+    def close(self):
+        if self._h:
+            _check(_lib.nnvisr_close(self._h))
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def N(self):
+        return self.in_shape[1] // 3
+
+    @property
+    def M(self):
+        return self.out_shape[1] // 3
+
+    # -- planning (host)
+    def plan(self, cut):
+        cut = np.ascontiguousarray(np.asarray(cut, dtype=np.uint8))
+        F = cut.shape[0]
+        cap = max(F, 1)
+        ins = np.zeros((cap, self.N), np.int64)
+        fresh = np.zeros((cap, 2), np.int64)
+        nr = C.c_int64()
+        _check(_lib.nnvisr_plan(self._h, F, cut.ctypes.data if F else None, _i64p(ins), _i64p(fresh), cap,
+                                C.byref(nr)))
+        return ins[:nr.value].copy(), fresh[:nr.value].copy()
+
+    def plan_range(self, num_frames, first, cut_window, fresh_begin, fresh_end):
+        cut = np.ascontiguousarray(np.asarray(cut_window, dtype=np.uint8))
+        cap = max(fresh_end - fresh_begin, 1)
+        ins = np.zeros((cap, self.N), np.int64)
+        fresh = np.zeros((cap, 2), np.int64)
+        nr = C.c_int64()
+        _check(_lib.nnvisr_plan_range(self._h, num_frames, first, cut.shape[0],
+                                      cut.ctypes.data if cut.shape[0] else None, fresh_begin, fresh_end,
+                                      _i64p(ins), _i64p(fresh), cap, C.byref(nr)))
+        return ins[:nr.value].copy(), fresh[:nr.value].copy()
+
+    # -- device work
+    def bind_frames(self, frames: Sequence[Frame], base: int = 0):
+        arr = frame_array(frames)
+        _check(_lib.nnvisr_bind_frames(self._h, base, arr, len(frames)))
+
+    def frames_to_tensor(self, frames: Sequence[Frame], tensor_ptr: int, stream=None):
+        arr = frame_array(frames)
+        _check(_lib.nnvisr_frames_to_tensor(self._h, arr, tensor_ptr, _stream_ptr(stream)))
+
+    def frames_to_tensor_batch(self, run_inputs: np.ndarray, tensors_ptr: int, stride: int, stream=None):
+        ri = np.ascontiguousarray(run_inputs, dtype=np.int64)
+        nr = ri.shape[0] if ri.ndim == 2 else ri.size // self.N
+        _check(_lib.nnvisr_frames_to_tensor_batch(self._h, _i64p(ri), nr, tensors_ptr, stride, _stream_ptr(stream)))
+
+    def frames_to_store(self, first: int, count: int, store_ptr: int, stream=None):
+        _check(_lib.nnvisr_frames_to_store(self._h, first, count, store_ptr, _stream_ptr(stream)))
+
+    def tensor_to_frames(self, tensor_ptr: int, t_h: int, t_w: int, out: Sequence[Frame], stream=None):
+        arr = frame_array(out)
+        _check(_lib.nnvisr_tensor_to_frames(self._h, tensor_ptr, t_h, t_w, arr, _stream_ptr(stream)))
+
+    def tensor_to_frames_batch(self, tensors_ptr: int, stride: int, t_h: int, t_w: int, out: Sequence[Frame],
+                               count: int, stream=None):
+        arr = frame_array(out)
+        _check(_lib.nnvisr_tensor_to_frames_batch(self._h, tensors_ptr, stride, t_h, t_w, arr, count,
+                                                  _stream_ptr(stream)))
+
+
+def open(cfg: Config) -> Handle:  # noqa: A001 - mirrors nnvisr_open
+    return Handle(cfg)

@@ -1,0 +1,181 @@
+"""CPU tests of the C ABI (include/nnvisr.h): the library loads and exports
+every declared symbol, nnvisr_open validates the configuration (SPEC.md
+model-desc invariants; SURVEY.md §8(b) "Validation at open"), and the host
+planner (steps A1-A2) equals the oracle bit-exactly."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2308_03121_b200 import nnvisr as nv
+from paper_2308_03121_b200 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "nnvisr.h")).read()
+    declared = set(re.findall(r"\b(nnvisr_[a-z_]+)\s*\(", hdr))
+    assert len(declared) >= 14
+    lib = nv.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(nv.EXPORTED) == declared
+    assert "sm_100a" in nv.version()
+
+
+def _cfg(**kw):
+    base = dict(width=64, height=64, family=nv.YUV420, bits=8, matrix=nv.BT709, range=nv.LIMITED,
+                input_count=2, output_count=1, n=1, left_context=-1, flags=0, align=1, dtype=nv.F32)
+    base.update(kw)
+    return nv.Config(**base)
+
+
+@pytest.mark.parametrize("kw,status,needle", [
+    (dict(width=63), 1, "even"),
+    (dict(height=65), 1, "even"),
+    (dict(bits=12), 1, "bits"),
+    (dict(matrix=7), 1, "matrix"),
+    (dict(range=3), 1, "range"),
+    (dict(family=9), 1, "family"),
+    (dict(chroma_loc=nv.CHROMA_LEFT), 3, "LEFT"),
+    (dict(input_count=0), 1, "input_count"),
+    (dict(input_count=17), 1, "input_count"),
+    (dict(output_count=0), 1, "output_count"),
+    (dict(flags=nv.DOUBLE_FRAME), 1, "DOUBLE_FRAME"),
+    (dict(flags=nv.INTERPOLATION | nv.EXTRA_FRAME, sx=(2, 1), sy=(2, 1)), 1, "scale must be 1"),
+    (dict(width=66, sx=(3, 4)), 1, "integral"),
+    (dict(width=66, sx=(3, 2)), 1, "even"),
+    (dict(align=3), 1, "align"),
+    (dict(align=512), 1, "align"),
+    (dict(dtype=5), 1, "dtype"),
+    (dict(input_count=5, left_context=5), 1, "left_context"),
+    (dict(n=2, input_count=5), 1, "tuple shape"),
+    (dict(flags=nv.INTERPOLATION | nv.EXTRA_FRAME, input_count=2, output_count=2), 1, "output_count"),
+])
+def test_open_rejects(kw, status, needle):
+    with pytest.raises(nv.NnvisrError) as e:
+        nv.open(_cfg(**kw))
+    assert e.value.status == status
+    assert needle in e.value.message
+
+
+def test_open_accepts_and_shapes():
+    for w in synth.WORKLOADS.values():
+        with nv.open(w.cfg) as h:
+            c = w.cfg
+            hp = -(-c.height // c.align) * c.align
+            wp = -(-c.width // c.align) * c.align
+            assert h.in_shape == (1, 3 * c.input_count, hp, wp)
+            assert h.out_shape == (1, 3 * c.output_count, c.height * c.sy[0] // c.sy[1],
+                                   c.width * c.sx[0] // c.sx[1])
+    assert nv.open(synth.WORKLOADS["c2"].cfg).in_shape == (1, 15, 1088, 1920)
+
+
+def _oracle_plan(cut, n, N, L):
+    return O.plan(cut, n, N, L)
+
+
+def test_plan_equals_oracle_grid():
+    rng = np.random.default_rng(42)
+    for n in range(1, 7):
+        for extra in (0, 1):
+            flags = (nv.INTERPOLATION | nv.EXTRA_FRAME) if extra else 0
+            cfg = _cfg(n=n, input_count=n + extra, output_count=n, left_context=0, flags=flags)
+            with nv.open(cfg) as h:
+                for m in range(1, 41):
+                    cut = np.zeros(m, np.uint8)
+                    a, b = h.plan(cut)
+                    oa, ob = _oracle_plan(cut, n, n + extra, 0)
+                    assert np.array_equal(a, oa) and np.array_equal(b, ob)
+                for _ in range(40):
+                    F = int(rng.integers(0, 70))
+                    cut = (rng.random(F) < 0.12).astype(np.uint8)
+                    a, b = h.plan(cut)
+                    oa, ob = _oracle_plan(cut, n, n + extra, 0)
+                    assert np.array_equal(a, oa) and np.array_equal(b, ob)
+    for N in range(1, 8):
+        for L in range(N):
+            with nv.open(_cfg(input_count=N, left_context=L)) as h:
+                for _ in range(25):
+                    F = int(rng.integers(1, 60))
+                    cut = (rng.random(F) < 0.15).astype(np.uint8)
+                    a, b = h.plan(cut)
+                    oa, ob = O.plan_window(cut, N, L)
+                    assert np.array_equal(a, oa) and np.array_equal(b, ob)
+
+
+def test_plan_workloads_match_oracle():
+    for w in synth.WORKLOADS.values():
+        cut = synth.cut_flags(w)
+        with nv.open(w.cfg) as h:
+            a, b = h.plan(cut)
+        c = w.cfg
+        L = 0 if c.left_context == -1 and c.flags else (c.input_count - 1) // 2 if c.left_context == -1 else c.left_context
+        oa, ob = O.plan(cut, c.n, c.input_count, L)
+        assert np.array_equal(a, oa) and np.array_equal(b, ob)
+        assert len(a) == w.frames  # n = 1: one tuple per frame
+
+
+def test_plan_capacity_error():
+    with nv.open(_cfg()) as h:
+        import ctypes as C
+        cut = np.zeros(10, np.uint8)
+        ins = np.zeros((4, 2), np.int64)
+        fr = np.zeros((4, 2), np.int64)
+        nr = C.c_int64()
+        st = nv.lib().nnvisr_plan(h._h, 10, cut.ctypes.data, nv._i64p(ins), nv._i64p(fr), 4, C.byref(nr))
+        assert st == 7 and nr.value == 10
+
+
+def _shard_bounds(F, W):
+    return [(r * F // W, (r + 1) * F // W) for r in range(W)]
+
+
+@pytest.mark.parametrize("N,L", [(2, 0), (3, 1), (4, 1), (5, 2), (7, 3), (1, 0)])
+def test_plan_range_equals_global_plan(N, L):
+    """Shard planner: local plan from the shard's flags plus
+    its halo flags == the global plan restricted to the shard, including cuts
+    exactly at, one before and one after every shard boundary."""
+    rng = np.random.default_rng(N * 10 + L)
+    with nv.open(_cfg(input_count=N, left_context=L)) as h:
+        for W in (1, 2, 3, 4, 8):
+            for trial in range(12):
+                F = int(rng.integers(W, 90))
+                cut = (rng.random(F) < 0.08).astype(np.uint8)
+                bounds = _shard_bounds(F, W)
+                if trial % 3 == 1:
+                    for a, _ in bounds[1:]:
+                        for d in (-1, 0, 1):
+                            if 0 < a + d < F:
+                                cut[a + d] = 1
+                ga, gb = h.plan(cut)
+                for a, b in bounds:
+                    lo = max(0, a - L)
+                    hi = min(F, b + N - 1 - L)
+                    la, lb = h.plan_range(F, lo, cut[lo:hi], a, b)
+                    assert np.array_equal(la, ga[a:b]) and np.array_equal(lb, gb[a:b])
+
+
+def test_plan_range_rejects_short_window():
+    with nv.open(_cfg(input_count=5, left_context=2)) as h:
+        cut = np.zeros(20, np.uint8)
+        with pytest.raises(nv.NnvisrError):
+            h.plan_range(20, 6, cut[6:12], 5, 10)
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    """No CPU fallback: without a GPU the device calls raise NNVISR_ERR_CUDA."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with nv.open(_cfg()) as h:
+        f = nv.Frame()
+        for p in range(3):
+            f.plane[p] = 4096
+            f.pitch[p] = 64
+        with pytest.raises(nv.NnvisrError) as e:
+            h.frames_to_tensor([f, f], 4096)
+        assert e.value.status == 5
