@@ -23,10 +23,13 @@ struct DevFrame {
 //   luma / RGB channel : v = (16*code - y_off) * y_scale
 //   chroma             : P = (s - c_off) * c_scale, s = 16 x the (upsampled) code
 //   R = Y + r_pr*Pr ;  B = Y + b_pb*Pb ;  G = Y - g_pb*Pb - g_pr*Pr
+//   fp16 tensors: values with |v| < 2^-9 (where an fp16 ULP is finer than the
+//   fp32 rounding error) are recomputed in fp64 with the *_d constants.
 struct F2TColour {
     int32_t y_off, c_off;
     float y_scale, c_scale;
     float r_pr, b_pb, g_pb, g_pr;
+    double y_scale_d, c_scale_d, r_pr_d, b_pb_d, g_pb_d, g_pr_d;
 };
 
 // tensor -> frames colour constants (steps B2, B4), in fp32 and fp64.

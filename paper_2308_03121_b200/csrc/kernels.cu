@@ -159,6 +159,36 @@ __device__ __forceinline__ void f2t_colour(const F2TColour &c, int ys, int us, i
     }
 }
 
+// fp16 tensors near zero: a difference of O(1) terms rounded in fp32 can be
+// off by more than one fp16 ULP once |v| < 2^-9 (the ULP there is < 2^-19).
+// Those (rare) pixels are recomputed in fp64 and rounded once to fp16; the
+// returned float is that fp16 value exactly, so the RNE store reproduces it.
+__device__ __forceinline__ float3 f2t_colour_precise(const F2TColour &c, int ys, int us, int vs)
+{
+    const double Y = static_cast<double>(ys - c.y_off) * c.y_scale_d;
+    const double Pb = static_cast<double>(us - c.c_off) * c.c_scale_d;
+    const double Pr = static_cast<double>(vs - c.c_off) * c.c_scale_d;
+    return make_float3(__half2float(__double2half(Y + c.r_pr_d * Pr)),
+                       __half2float(__double2half(Y - c.g_pb_d * Pb - c.g_pr_d * Pr)),
+                       __half2float(__double2half(Y + c.b_pb_d * Pb)));
+}
+
+template <int FAMILY, typename OUT>
+__device__ __forceinline__ void f2t_pixel(const F2TColour &c, int ys, int us, int vs, float &R, float &G,
+                                          float &B)
+{
+    f2t_colour<FAMILY>(c, ys, us, vs, R, G, B);
+    if (FAMILY != kRGB && sizeof(OUT) == 2) {
+        constexpr float kTiny = 1.0f / 512.0f;
+        if (fabsf(R) < kTiny || fabsf(G) < kTiny || fabsf(B) < kTiny) {
+            const float3 p = f2t_colour_precise(c, ys, us, vs);
+            R = p.x;
+            G = p.y;
+            B = p.z;
+        }
+    }
+}
+
 // Scalar path: sample codes of pixel (x, y) with every coordinate clamped
 // (padding replicates the last row/column, reading A6; chroma taps clamp to
 // the plane, reading A5).  Values are 16 x code.
@@ -277,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) f2t_kernel(const F2TArgs a)
     for (int r = 0; r < ROWS; ++r) {
         float R[kPx], G[kPx], B[kPx];
 #pragma unroll
-        for (int k = 0; k < kPx; ++k) f2t_colour<FAMILY>(a.col, ys[r][k], us[r][k], vs[r][k], R[k], G[k], B[k]);
+        for (int k = 0; k < kPx; ++k) f2t_pixel<FAMILY, OUT>(a.col, ys[r][k], us[r][k], vs[r][k], R[k], G[k], B[k]);
         OUT *o = dst + static_cast<int64_t>(y0 + r) * a.Wp + x0;
         if (vec_store) {
             store8(o, R);

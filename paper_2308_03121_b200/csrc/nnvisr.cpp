@@ -235,6 +235,12 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
     h->f2c.b_pb = (float)(2.0 * (1.0 - kb));
     h->f2c.g_pb = (float)(kb * 2.0 * (1.0 - kb) / kg);
     h->f2c.g_pr = (float)(kr * 2.0 * (1.0 - kr) / kg);
+    h->f2c.y_scale_d = f.range == NNVISR_LIMITED ? 1.0 / (16.0 * 219.0 * k) : 1.0 / (16.0 * full);
+    h->f2c.c_scale_d = f.range == NNVISR_LIMITED ? 1.0 / (16.0 * 224.0 * k) : 1.0 / (16.0 * full);
+    h->f2c.r_pr_d = 2.0 * (1.0 - kr);
+    h->f2c.b_pb_d = 2.0 * (1.0 - kb);
+    h->f2c.g_pb_d = kb * 2.0 * (1.0 - kb) / kg;
+    h->f2c.g_pr_d = kr * 2.0 * (1.0 - kr) / kg;
     // B2/B4 constants
     T2FColour &c = h->t2c;
     c.kr = kr; c.kb = kb; c.db = 2.0 * (1.0 - kb); c.dr = 2.0 * (1.0 - kr);

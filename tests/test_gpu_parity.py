@@ -11,7 +11,7 @@ from paper_2308_03121_b200 import nnvisr as nv
 from paper_2308_03121_b200 import synth
 from paper_2308_03121_b200.frames import FrameBuffer, FrameLayout
 
-from .helpers import assert_codes_close, assert_tensor_close, oracle_f2t, oracle_t2f, parallel
+from .helpers import CodeStats, assert_codes_close, assert_tensor_close, oracle_f2t, oracle_t2f, parallel
 
 pytestmark = pytest.mark.gpu
 
@@ -64,6 +64,7 @@ def test_f2t_small_parity(family, bits, dtype, geom):
 @pytest.mark.parametrize("family,bits,dtype", CASES)
 def test_t2f_small_parity(family, bits, dtype):
     rs = np.random.default_rng(100 + bits + 7 * family + dtype)
+    stats = CodeStats()
     for (W, H, sx) in ((34, 18, (2, 1)), (64, 32, (1, 1))):
         for matrix, rng_ in ((nv.BT709, nv.LIMITED), (nv.BT2020, nv.FULL), (nv.BT601, nv.FULL)):
             cfg = _small_cfg(family, bits, dtype, matrix, rng_, W, H, M=3, sx=sx)
@@ -77,7 +78,8 @@ def test_t2f_small_parity(family, bits, dtype):
                 torch.cuda.synchronize()
                 ref = oracle_t2f(_tensor_np(t), h.M, olay, cfg)
                 for o in range(h.M):
-                    assert_codes_close(out.host_planes(o), ref[o], f"t2f {cfg} slot {o}")
+                    stats.add(out.host_planes(o), ref[o], f"t2f {cfg} slot {o}")
+    stats.check(f"t2f family {family} bits {bits} dtype {dtype}")
 
 
 def test_t2f_special_values():
@@ -97,9 +99,11 @@ def test_t2f_special_values():
         torch.cuda.synchronize()
         g = out.host_planes(0)
     ref = O.t2f(t.cpu().numpy(), 1, 8, 2, O.YUV444, 10, O.BT709, O.FULL)[0]
-    assert g[0][0, 0] == 0 and g[1][0, 0] == ref[1][0, 0] and g[2][0, 0] == ref[2][0, 0]
-    assert g[0][0, 1] == 1023
-    assert_codes_close(g, ref, "specials")
+    assert g[0][0, 0] == 0 and g[1][0, 0] == 0 and g[2][0, 0] == 0            # NaN -> 0
+    assert g[0][0, 1] == ref[0][0, 1] == 0                                     # inf - inf = NaN luma
+    assert g[1][1, 0] == ref[1][1, 0] == 0                                     # exact 0.5 tie -> even
+    for p in range(3):
+        assert np.array_equal(g[p], ref[p]), p
 
 
 def test_unaligned_scalar_path():
@@ -118,11 +122,18 @@ def test_unaligned_scalar_path():
             h.frames_to_tensor(buf.descriptors(), t.data_ptr())
             torch.cuda.synchronize()
             assert_tensor_close(_tensor_np(t), oracle_f2t(lay, host, H, W, cfg), "unaligned f2t")
+            # luma survives f2t -> t2f exactly (Y' = G + Kr(R-G) + Kb(B-G))
             out = FrameBuffer(lay, 1, device=DEV)
             h.tensor_to_frames(t.data_ptr(), H, W, out.descriptors())
             torch.cuda.synchronize()
-            ref = oracle_t2f(_tensor_np(t)[:, :3], 1, lay, cfg)
-            assert_codes_close(out.host_planes(0), ref[0], "unaligned t2f")
+            assert np.array_equal(out.host_planes(0)[0], host[0][0])
+            # t2f of a random tensor through the scalar path
+            rt = synth.random_tensor((1, 3, H, W), dtype, 77 + dtype, device=DEV)
+            h.tensor_to_frames(rt.data_ptr(), H, W, out.descriptors())
+            torch.cuda.synchronize()
+            st = CodeStats()
+            st.add(out.host_planes(0), oracle_t2f(_tensor_np(rt), 1, lay, cfg)[0], "unaligned t2f")
+            assert st.exact >= st.total - 2
 
 
 # ------------------------------------------------------------ workloads
