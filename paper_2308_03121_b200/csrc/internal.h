@@ -32,23 +32,31 @@ struct F2TColour {
     double y_scale_d, c_scale_d, r_pr_d, b_pb_d, g_pb_d, g_pr_d;
 };
 
-// tensor -> frames colour constants (steps B2, B4), in fp32 and fp64.
-//   Y' = G + kr(R-G) + kb(B-G);  Pb = (B-Y')/db;  Pr = (R-Y')/dr
-//   code = clamp(rne(Y'*ys + yo)), clamp(rne(P*cs + co)) to [0, maxc]
+// tensor -> frames colour constants (steps B2-B4), in fp32 and fp64.
+//   Y' = G + kr(R-G) + kb(B-G)                      (exact on the gray axis)
+//   luma code   = rne(clamp(Y' * ys + yo, 0, maxc))
+//   chroma: S = sum over the k pixels of the chroma sample (k = 4 for 4:2:0,
+//   1 for 4:4:4) of (B - Y') [or (R - Y')];  P = S / (k * db) by a reciprocal
+//   and one FMA correction (correctly rounded, so the primaries' exact 0.5
+//   ties stay exact);  chroma code = rne(clamp(P * cs + co, 0, maxc)).
 struct T2FColour {
-    double kr, kb, db, dr, ys, yo, cs, co;
-    float fkr, fkb, fdb, fdr, fys, fyo, fcs, fco;
-    uint32_t maxc;
+    double kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
+    float fkr, fkb, fdb, fdr, fidb, fidr, fys, fyo, fcs, fco, fmaxc;
 };
 
+// frames -> tensor work list of one launch: job j converts the distinct frame
+// frames[job_frame[j]] once and stores it to every (run, slot) that uses it:
+// dst_code[job_dst[j] .. job_dst[j+1]) = run * 32 + slot, written at
+// dst + run * run_stride + slot * slot_bytes.
 struct F2TArgs {
     const DevFrame *frames;   // bound frame table (device)
-    const int32_t *job_frame; // per job: index into `frames` (device)
-    char *dst;                // tensor base of job 0's run
+    const int32_t *job_frame; // [jobs] index into `frames`
+    const int32_t *job_dst;   // [jobs + 1] CSR offsets into dst_code
+    const int32_t *dst_code;  // run * 32 + slot
+    char *dst;                // tensor of run 0 of this launch
     int64_t run_stride;       // bytes between consecutive runs' tensors
     int64_t slot_bytes;       // bytes of one slot (3*Hp*Wp*elem)
-    int32_t jobs_per_run;     // N (or 1 in store mode)
-    int32_t job_base;         // first job of this launch
+    int32_t job_base;         // first job of this launch (grid.y offset)
     int32_t W, H, Hp, Wp;     // clip size and padded tensor size
     int32_t units, col_units; // threads per job and column groups per row unit
     int32_t vec_in;           // 1: all bound planes/pitches 16-byte aligned

@@ -101,20 +101,6 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b)
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t *>(&h);
 }
-__device__ __forceinline__ void store8(__half *p, const float (&v)[kPx])
-{
-    uint4 q = make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]),
-                         pack_half2(v[4], v[5]), pack_half2(v[6], v[7]));
-    *reinterpret_cast<uint4 *>(p) = q;
-}
-__device__ __forceinline__ void store8(float *p, const float (&v)[kPx])
-{
-    reinterpret_cast<float4 *>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
-    reinterpret_cast<float4 *>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
-}
-__device__ __forceinline__ void store1(__half *p, float v) { *p = __float2half_rn(v); }
-__device__ __forceinline__ void store1(float *p, float v) { *p = v; }
-
 // ------------------------------------------------------------- tensor load
 __device__ __forceinline__ void tload8(const __half *p, float (&v)[kPx])
 {
@@ -232,6 +218,46 @@ __device__ __forceinline__ void chroma_row6(const IN *row, int i0, int cw, int (
     c[5] = load1(row + min(i0 + 4, cw - 1));
 }
 
+// Packed tensor values of one row of 8 pixels and one channel.
+template <typename OUT> struct Row8;
+template <> struct Row8<__half> {
+    uint4 v;
+    __device__ __forceinline__ void set(const float (&x)[kPx])
+    {
+        v = make_uint4(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]), pack_half2(x[4], x[5]),
+                       pack_half2(x[6], x[7]));
+    }
+    __device__ __forceinline__ void store(__half *p) const { *reinterpret_cast<uint4 *>(p) = v; }
+    __device__ __forceinline__ void store_n(__half *p, int n) const
+    {
+        const __half *h = reinterpret_cast<const __half *>(&v);
+        for (int k = 0; k < n; ++k) p[k] = h[k];
+    }
+};
+template <> struct Row8<float> {
+    float4 a, b;
+    __device__ __forceinline__ void set(const float (&x)[kPx])
+    {
+        a = make_float4(x[0], x[1], x[2], x[3]);
+        b = make_float4(x[4], x[5], x[6], x[7]);
+    }
+    __device__ __forceinline__ void store(float *p) const
+    {
+        reinterpret_cast<float4 *>(p)[0] = a;
+        reinterpret_cast<float4 *>(p)[1] = b;
+    }
+    __device__ __forceinline__ void store_n(float *p, int n) const
+    {
+        const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        for (int k = 0; k < n; ++k) p[k] = x[k];
+    }
+};
+
+// One thread: ROWS rows x 8 columns of one distinct frame, converted once and
+// stored to every (run, slot) of the launch that holds this frame (a frame
+// shared by N overlapping windows, or repeated inside a tuple at a scene cut,
+// is read and converted once: PAPER.md §3.3 P:373-377's point that a batch
+// only has b*n+1 distinct frames).
 template <int FAMILY, typename IN, typename OUT>
 __global__ void __launch_bounds__(kThreads) f2t_kernel(const F2TArgs a)
 {
@@ -243,9 +269,6 @@ __global__ void __launch_bounds__(kThreads) f2t_kernel(const F2TArgs a)
     const int x0 = (unit - ru * a.col_units) * kPx;
     const int y0 = ru * ROWS;
     const DevFrame f = a.frames[a.job_frame[job]];
-    const int run = job / a.jobs_per_run, slot = job - run * a.jobs_per_run;
-    OUT *dst = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(run) * a.run_stride +
-                                       static_cast<int64_t>(slot) * a.slot_bytes);
 
     int ys[ROWS][kPx], us[ROWS][kPx], vs[ROWS][kPx];
     int yc[ROWS];
@@ -261,7 +284,7 @@ __global__ void __launch_bounds__(kThreads) f2t_kernel(const F2TArgs a)
         }
         if (FAMILY == kYUV420) {
             const int cw = a.W >> 1, ch = a.H >> 1, i0 = x0 >> 1;
-            // near row is shared by both luma rows; far rows differ
+            // the near chroma row is shared by both luma rows; far rows differ
             const int jn = yc[0] >> 1;
             int jf[ROWS];
 #pragma unroll
@@ -279,8 +302,8 @@ __global__ void __launch_bounds__(kThreads) f2t_kernel(const F2TArgs a)
                     hup(cf, hf);
 #pragma unroll
                     for (int k = 0; k < kPx; ++k) {
-                        const int s = 3 * hn[k] + hf[k];
-                        if (p == 1) us[r][k] = s; else vs[r][k] = s;
+                        const int sm = 3 * hn[k] + hf[k];
+                        if (p == 1) us[r][k] = sm; else vs[r][k] = sm;
                     }
                 }
             }
@@ -301,23 +324,32 @@ __global__ void __launch_bounds__(kThreads) f2t_kernel(const F2TArgs a)
                 f2t_codes_scalar<FAMILY, IN>(f, a.W, a.H, x0 + k, y0 + r, ys[r][k], us[r][k], vs[r][k]);
     }
 
-    const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
-    const bool vec_store = a.vec_out && (x0 + kPx <= a.Wp);
+    Row8<OUT> out[ROWS][3];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
         float R[kPx], G[kPx], B[kPx];
 #pragma unroll
         for (int k = 0; k < kPx; ++k) f2t_pixel<FAMILY, OUT>(a.col, ys[r][k], us[r][k], vs[r][k], R[k], G[k], B[k]);
-        OUT *o = dst + static_cast<int64_t>(y0 + r) * a.Wp + x0;
-        if (vec_store) {
-            store8(o, R);
-            store8(o + plane, G);
-            store8(o + 2 * plane, B);
-        } else {
-            for (int k = 0; k < kPx && x0 + k < a.Wp; ++k) {
-                store1(o + k, R[k]);
-                store1(o + plane + k, G[k]);
-                store1(o + 2 * plane + k, B[k]);
+        out[r][0].set(R);
+        out[r][1].set(G);
+        out[r][2].set(B);
+    }
+
+    const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
+    const int64_t off = static_cast<int64_t>(y0) * a.Wp + x0;
+    const bool vec_store = a.vec_out && (x0 + kPx <= a.Wp);
+    const int d1 = a.job_dst[job + 1];
+    for (int d = a.job_dst[job]; d < d1; ++d) {
+        const int code = a.dst_code[d];
+        OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(code >> 5) * a.run_stride +
+                                         static_cast<int64_t>(code & 31) * a.slot_bytes) + off;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                OUT *q = o + c * plane + static_cast<int64_t>(r) * a.Wp;
+                if (vec_store) out[r][c].store(q);
+                else out[r][c].store_n(q, min(kPx, a.Wp - x0));
             }
         }
     }
@@ -326,38 +358,67 @@ __global__ void __launch_bounds__(kThreads) f2t_kernel(const F2TArgs a)
 // ------------------------------------------------------------ t2f colour
 template <typename T> struct T2FConst;
 template <> struct T2FConst<float> {
-    float kr, kb, db, dr, ys, yo, cs, co;
+    float kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
     __device__ explicit T2FConst(const T2FColour &c)
-        : kr(c.fkr), kb(c.fkb), db(c.fdb), dr(c.fdr), ys(c.fys), yo(c.fyo), cs(c.fcs), co(c.fco) {}
+        : kr(c.fkr), kb(c.fkb), db(c.fdb), dr(c.fdr), idb(c.fidb), idr(c.fidr), ys(c.fys), yo(c.fyo),
+          cs(c.fcs), co(c.fco), maxc(c.fmaxc) {}
 };
 template <> struct T2FConst<double> {
-    double kr, kb, db, dr, ys, yo, cs, co;
+    double kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
     __device__ explicit T2FConst(const T2FColour &c)
-        : kr(c.kr), kb(c.kb), db(c.db), dr(c.dr), ys(c.ys), yo(c.yo), cs(c.cs), co(c.co) {}
+        : kr(c.kr), kb(c.kb), db(c.db), dr(c.dr), idb(c.idb), idr(c.idr), ys(c.ys), yo(c.yo), cs(c.cs),
+          co(c.co), maxc(c.maxc) {}
 };
 
-// Step B4: round half to even, clamp to [0, maxc]; NaN -> 0 (cvt.rni
-// saturates to the u32 range and maps NaN to 0).
-__device__ __forceinline__ uint32_t quant(float q, uint32_t maxc) { return min(__float2uint_rn(q), maxc); }
-__device__ __forceinline__ uint32_t quant(double q, uint32_t maxc) { return min(__double2uint_rn(q), maxc); }
+__device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
+
+// Step B4: clamp to [0, maxc] (NaN -> 0: fmax returns the non-NaN operand),
+// then round half to even by adding 1.5 * 2^(p-1): the sum lies where the
+// spacing of representable values is exactly 1, so the FP add rounds the
+// value to the nearest integer, ties to even, and the integer is the low bits.
+__device__ __forceinline__ uint32_t quant(float q, float maxc)
+{
+    const float x = fminf(fmaxf(q, 0.0f), maxc);
+    return __float_as_uint(x + 12582912.0f) - 0x4B400000u;
+}
+__device__ __forceinline__ uint32_t quant(double q, double maxc)
+{
+    const double x = fmin(fmax(q, 0.0), maxc);
+    return static_cast<uint32_t>(__double2loint(x + 6755399441055744.0));
+}
+
+// S / d for a divisor d with precomputed reciprocal id: one FMA correction of
+// the reciprocal product (correctly rounded quotient; keeps exact quotients
+// such as the full-range primaries' +-0.5 exact).
+template <typename T>
+__device__ __forceinline__ T divide(T S, T d, T id)
+{
+    const T q0 = S * id;
+    const T r = fma_(-q0, d, S);
+    return fma_(r, id, q0);
+}
 
 __device__ __forceinline__ void store_samples8(uint16_t *p, const uint32_t (&v)[kPx])
 {
-    *reinterpret_cast<uint4 *>(p) =
-        make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+    *reinterpret_cast<uint4 *>(p) = make_uint4(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410),
+                                               __byte_perm(v[4], v[5], 0x5410), __byte_perm(v[6], v[7], 0x5410));
+}
+__device__ __forceinline__ uint32_t pack4_u8(uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 __device__ __forceinline__ void store_samples8(uint8_t *p, const uint32_t (&v)[kPx])
 {
-    *reinterpret_cast<uint2 *>(p) = make_uint2(v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24),
-                                               v[4] | (v[5] << 8) | (v[6] << 16) | (v[7] << 24));
+    *reinterpret_cast<uint2 *>(p) = make_uint2(pack4_u8(v[0], v[1], v[2], v[3]), pack4_u8(v[4], v[5], v[6], v[7]));
 }
 __device__ __forceinline__ void store_samples4(uint16_t *p, const uint32_t *v)
 {
-    *reinterpret_cast<uint2 *>(p) = make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16));
+    *reinterpret_cast<uint2 *>(p) = make_uint2(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410));
 }
 __device__ __forceinline__ void store_samples4(uint8_t *p, const uint32_t *v)
 {
-    *reinterpret_cast<uint32_t *>(p) = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+    *reinterpret_cast<uint32_t *>(p) = pack4_u8(v[0], v[1], v[2], v[3]);
 }
 
 template <int FAMILY, typename OS, typename TIN, typename AR>
@@ -378,6 +439,7 @@ __global__ void __launch_bounds__(kThreads) t2f_kernel(const T2FArgs a)
     const int nvalid = min(kPx, a.Wo - x0);
     const bool full = nvalid == kPx;
 
+    // Step B1: the thread's 2x8 (4:2:0) or 1x8 window of R', G', B'
     float R[ROWS][kPx], G[ROWS][kPx], B[ROWS][kPx];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
@@ -405,9 +467,9 @@ __global__ void __launch_bounds__(kThreads) t2f_kernel(const T2FArgs a)
             uint32_t q[3][kPx];
 #pragma unroll
             for (int k = 0; k < kPx; ++k) {
-                q[0][k] = quant(static_cast<AR>(R[r][k]) * c.ys + c.yo, a.col.maxc);
-                q[1][k] = quant(static_cast<AR>(G[r][k]) * c.ys + c.yo, a.col.maxc);
-                q[2][k] = quant(static_cast<AR>(B[r][k]) * c.ys + c.yo, a.col.maxc);
+                q[0][k] = quant(fma_(static_cast<AR>(R[r][k]), c.ys, c.yo), c.maxc);
+                q[1][k] = quant(fma_(static_cast<AR>(G[r][k]), c.ys, c.yo), c.maxc);
+                q[2][k] = quant(fma_(static_cast<AR>(B[r][k]), c.ys, c.yo), c.maxc);
             }
 #pragma unroll
             for (int p = 0; p < 3; ++p) {
@@ -419,18 +481,18 @@ __global__ void __launch_bounds__(kThreads) t2f_kernel(const T2FArgs a)
         return;
     }
 
-    // Step B2: Y' = G + Kr(R-G) + Kb(B-G); Pb = (B-Y')/(2(1-Kb)); Pr = (R-Y')/(2(1-Kr))
-    AR Pb[ROWS][kPx], Pr[ROWS][kPx];
+    // Step B2 (luma) + B4: Y' = G + Kr(R-G) + Kb(B-G); keep B-Y', R-Y'
+    AR BY[ROWS][kPx], RY[ROWS][kPx];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
         uint32_t qy[kPx];
 #pragma unroll
         for (int k = 0; k < kPx; ++k) {
             const AR r_ = R[r][k], g_ = G[r][k], b_ = B[r][k];
-            const AR Y = g_ + c.kr * (r_ - g_) + c.kb * (b_ - g_);
-            Pb[r][k] = (b_ - Y) / c.db;
-            Pr[r][k] = (r_ - Y) / c.dr;
-            qy[k] = quant(Y * c.ys + c.yo, a.col.maxc);
+            const AR Y = fma_(c.kb, b_ - g_, fma_(c.kr, r_ - g_, g_));
+            BY[r][k] = b_ - Y;
+            RY[r][k] = r_ - Y;
+            qy[k] = quant(fma_(Y, c.ys, c.yo), c.maxc);
         }
         OS *out = row_ptr_w<OS>(f, 0, y0 + r) + x0;
         if (vec_store) store_samples8(out, qy);
@@ -441,8 +503,8 @@ __global__ void __launch_bounds__(kThreads) t2f_kernel(const T2FArgs a)
         uint32_t qb[kPx], qr[kPx];
 #pragma unroll
         for (int k = 0; k < kPx; ++k) {
-            qb[k] = quant(Pb[0][k] * c.cs + c.co, a.col.maxc);
-            qr[k] = quant(Pr[0][k] * c.cs + c.co, a.col.maxc);
+            qb[k] = quant(fma_(divide(BY[0][k], c.db, c.idb), c.cs, c.co), c.maxc);
+            qr[k] = quant(fma_(divide(RY[0][k], c.dr, c.idr), c.cs, c.co), c.maxc);
         }
         OS *ob = row_ptr_w<OS>(f, 1, y0) + x0, *orr = row_ptr_w<OS>(f, 2, y0) + x0;
         if (vec_store) { store_samples8(ob, qb); store_samples8(orr, qr); }
@@ -450,15 +512,17 @@ __global__ void __launch_bounds__(kThreads) t2f_kernel(const T2FArgs a)
         return;
     }
 
-    // Step B3: 2x2 box mean ((a+b)+(c+d))/4 of the block the thread holds.
+    // Step B3: 2x2 box mean, ((a+b)+(c+d))/4, folded into the divisor 4*db
+    // (a power-of-two scaling, exact): Pb = S / (4 db), Pr = S / (4 dr).
+    const AR db4 = c.db * AR(4), dr4 = c.dr * AR(4), idb4 = c.idb * AR(0.25), idr4 = c.idr * AR(0.25);
     uint32_t qb[4], qr[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         const int r1 = ROWS - 1;
-        const AR mb = ((Pb[0][2 * m] + Pb[0][2 * m + 1]) + (Pb[r1][2 * m] + Pb[r1][2 * m + 1])) * AR(0.25);
-        const AR mr = ((Pr[0][2 * m] + Pr[0][2 * m + 1]) + (Pr[r1][2 * m] + Pr[r1][2 * m + 1])) * AR(0.25);
-        qb[m] = quant(mb * c.cs + c.co, a.col.maxc);
-        qr[m] = quant(mr * c.cs + c.co, a.col.maxc);
+        const AR sb = (BY[0][2 * m] + BY[0][2 * m + 1]) + (BY[r1][2 * m] + BY[r1][2 * m + 1]);
+        const AR sr = (RY[0][2 * m] + RY[0][2 * m + 1]) + (RY[r1][2 * m] + RY[r1][2 * m + 1]);
+        qb[m] = quant(fma_(divide(sb, db4, idb4), c.cs, c.co), c.maxc);
+        qr[m] = quant(fma_(divide(sr, dr4, idr4), c.cs, c.co), c.maxc);
     }
     OS *ob = row_ptr_w<OS>(f, 1, y0 >> 1) + (x0 >> 1), *orr = row_ptr_w<OS>(f, 2, y0 >> 1) + (x0 >> 1);
     if (vec_store) { store_samples4(ob, qb); store_samples4(orr, qr); }

@@ -244,11 +244,13 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
     // B2/B4 constants
     T2FColour &c = h->t2c;
     c.kr = kr; c.kb = kb; c.db = 2.0 * (1.0 - kb); c.dr = 2.0 * (1.0 - kr);
+    c.idb = 1.0 / c.db; c.idr = 1.0 / c.dr;
     if (f.range == NNVISR_LIMITED) { c.ys = 219.0 * k; c.yo = 16.0 * k; c.cs = 224.0 * k; c.co = 128.0 * k; }
     else { c.ys = full; c.yo = 0.0; c.cs = full; c.co = std::ldexp(1.0, f.bits - 1); }
+    c.maxc = full;
     c.fkr = (float)c.kr; c.fkb = (float)c.kb; c.fdb = (float)c.db; c.fdr = (float)c.dr;
-    c.fys = (float)c.ys; c.fyo = (float)c.yo; c.fcs = (float)c.cs; c.fco = (float)c.co;
-    c.maxc = (uint32_t)full;
+    c.fidb = 1.0f / c.fdb; c.fidr = 1.0f / c.fdr;
+    c.fys = (float)c.ys; c.fyo = (float)c.yo; c.fcs = (float)c.cs; c.fco = (float)c.co; c.fmaxc = (float)full;
     *out = h;
     return NNVISR_OK;
 }
@@ -457,6 +459,35 @@ nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, cudaStream_t st
     return NNVISR_OK;
 }
 
+// Work list of one f2t launch over `runs` runs of `per_run` slots whose frame
+// keys are key[r*per_run + t]: one job per distinct key, with the (run, slot)
+// destinations of that key.  Written into `buf` as
+// [job_frame: J][job_dst: J+1][dst_code: runs*per_run] (int32); returns J.
+int64_t build_f2t_jobs(const int64_t *key, int64_t runs, int per_run, int64_t key_base, int32_t *buf)
+{
+    const int64_t n = runs * per_run;
+    std::vector<std::pair<int64_t, int32_t>> items(n);
+    for (int64_t i = 0; i < n; ++i)
+        items[i] = {key[i] - key_base, (int32_t)((i / per_run) * 32 + (i % per_run))};
+    std::stable_sort(items.begin(), items.end(),
+                     [](const auto &x, const auto &y) { return x.first < y.first; });
+    int64_t J = 0;
+    for (int64_t i = 0; i < n; ++i)
+        if (i == 0 || items[i].first != items[i - 1].first) ++J;
+    int32_t *job_frame = buf, *job_dst = buf + J, *dst_code = buf + 2 * J + 1;
+    int64_t j = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        if (i == 0 || items[i].first != items[i - 1].first) {
+            ++j;
+            job_frame[j] = (int32_t)items[i].first;
+            job_dst[j] = (int32_t)i;
+        }
+        dst_code[i] = items[i].second;
+    }
+    job_dst[J] = (int32_t)n;
+    return J;
+}
+
 T2FArgs t2f_args(const nnvisr_handle *h, int64_t t_h, int64_t t_w)
 {
     T2FArgs a{};
@@ -533,44 +564,59 @@ nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     UploadSlot *slot = nullptr;
     if ((s = acquire_slot(h, &slot))) return s;
-    // [DevFrame x N][int32 x N]
+    // [DevFrame x N][job_frame, job_dst, dst_code]; identical descriptors are
+    // one job (a frame repeated in the tuple is converted once)
+    std::vector<int64_t> key(h->N);
+    for (int t = 0; t < h->N; ++t) {
+        key[t] = t;
+        for (int u = 0; u < t; ++u)
+            if (!std::memcmp(&in[u], &in[t], sizeof(nnvisr_frame))) { key[t] = u; break; }
+    }
     std::memcpy(slot->host, in, sizeof(DevFrame) * h->N);
-    int32_t *idx = reinterpret_cast<int32_t *>(static_cast<char *>(slot->host) + sizeof(DevFrame) * h->N);
-    for (int t = 0; t < h->N; ++t) idx[t] = t;
-    if ((s = upload(slot, sizeof(DevFrame) * h->N + sizeof(int32_t) * h->N, st))) return s;
+    int32_t *tab = reinterpret_cast<int32_t *>(static_cast<char *>(slot->host) + sizeof(DevFrame) * h->N);
+    const int64_t J = build_f2t_jobs(key.data(), 1, h->N, 0, tab);
+    const size_t tab_ints = 2 * J + 1 + h->N;
+    if ((s = upload(slot, sizeof(DevFrame) * h->N + sizeof(int32_t) * tab_ints, st))) return s;
     F2TArgs a = f2t_args(h);
+    const int32_t *dtab = reinterpret_cast<const int32_t *>(static_cast<char *>(slot->dev) + sizeof(DevFrame) * h->N);
     a.frames = static_cast<const DevFrame *>(slot->dev);
-    a.job_frame = reinterpret_cast<const int32_t *>(static_cast<char *>(slot->dev) + sizeof(DevFrame) * h->N);
+    a.job_frame = dtab;
+    a.job_dst = dtab + J;
+    a.dst_code = dtab + 2 * J + 1;
     a.dst = static_cast<char *>(tensor);
     a.run_stride = 0;
-    a.jobs_per_run = h->N;
     a.vec_in = vec;
-    s = run_f2t(h, a, h->N, st);
+    s = run_f2t(h, a, J, st);
     nnvisr_status s2 = release_slot(slot, st);
     return s ? s : s2;
 }
 
-static nnvisr_status f2t_indexed(nnvisr_handle *h, const int64_t *frame_idx, int64_t jobs, int jobs_per_run,
+static nnvisr_status f2t_indexed(nnvisr_handle *h, const int64_t *frame_idx, int64_t runs, int per_run,
                                  void *dst, int64_t run_stride, cudaStream_t st)
 {
     if (!h->frames) return fail(NNVISR_ERR_INVALID_ARG, "no frames bound (nnvisr_bind_frames)");
-    const int64_t per_slot = (int64_t)(kSlotBytes / sizeof(int32_t)) / jobs_per_run * jobs_per_run;
+    // an upload slot holds 3 ints per (run, slot) plus one; runs per launch
+    // are also bounded by the 5-bit slot / run encoding of dst_code
+    const int64_t max_runs = std::min<int64_t>((int64_t)(kSlotBytes / sizeof(int32_t) - 1) / (3 * per_run),
+                                               (int64_t)(INT32_MAX / 32));
     F2TArgs a = f2t_args(h);
     a.frames = h->frames;
-    a.jobs_per_run = jobs_per_run;
     a.run_stride = run_stride;
     a.vec_in = h->frames_vec;
-    for (int64_t j0 = 0; j0 < jobs; j0 += per_slot) {
-        const int64_t nj = std::min(per_slot, jobs - j0);
+    for (int64_t r0 = 0; r0 < runs; r0 += max_runs) {
+        const int64_t nr = std::min(max_runs, runs - r0);
         UploadSlot *slot = nullptr;
         nnvisr_status s = acquire_slot(h, &slot);
         if (s) return s;
-        int32_t *idx = static_cast<int32_t *>(slot->host);
-        for (int64_t j = 0; j < nj; ++j) idx[j] = (int32_t)(frame_idx[j0 + j] - h->frames_base);
-        if ((s = upload(slot, sizeof(int32_t) * nj, st))) return s;
-        a.job_frame = static_cast<const int32_t *>(slot->dev);
-        a.dst = static_cast<char *>(dst) + (j0 / jobs_per_run) * run_stride;
-        s = run_f2t(h, a, nj, st);
+        int32_t *tab = static_cast<int32_t *>(slot->host);
+        const int64_t J = build_f2t_jobs(frame_idx + r0 * per_run, nr, per_run, h->frames_base, tab);
+        if ((s = upload(slot, sizeof(int32_t) * (2 * J + 1 + nr * per_run), st))) return s;
+        const int32_t *dtab = static_cast<const int32_t *>(slot->dev);
+        a.job_frame = dtab;
+        a.job_dst = dtab + J;
+        a.dst_code = dtab + 2 * J + 1;
+        a.dst = static_cast<char *>(dst) + r0 * run_stride;
+        s = run_f2t(h, a, J, st);
         nnvisr_status s2 = release_slot(slot, st);
         if (s) return s;
         if (s2) return s2;
@@ -601,7 +647,7 @@ nnvisr_status nnvisr_frames_to_tensor_batch(nnvisr_handle *h, const int64_t *run
     }
     nnvisr_status s = ensure_device(h);
     if (s) return s;
-    return f2t_indexed(h, run_inputs, jobs, h->N, tensors, tensor_stride_bytes, static_cast<cudaStream_t>(stream));
+    return f2t_indexed(h, run_inputs, num_runs, h->N, tensors, tensor_stride_bytes, static_cast<cudaStream_t>(stream));
 }
 
 nnvisr_status nnvisr_frames_to_store(nnvisr_handle *h, int64_t first, int64_t count, void *store, void *stream)
