@@ -1,0 +1,489 @@
+// common.cuh -- device helpers shared by the generic (LDG) and the TMA
+// pipelined conversion kernels: memory access, the colour arithmetic of
+// steps A5-A6 (frames -> tensor) and B2-B4 (tensor -> frames), packing.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "internal.h"
+
+namespace nnvisr {
+namespace dev {
+
+// ------------------------------------------------------------------ memory
+__device__ __forceinline__ uint4 ld_stream_v4(const void *p)
+{
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint2 ld_stream_v2(const void *p)
+{
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint2 ld_v2(const void *p)
+{
+    uint2 r;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_v1(const void *p)
+{
+    uint32_t r;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int load1(const uint16_t *p) { return __ldg(p); }
+__device__ __forceinline__ int load1(const uint8_t *p) { return __ldg(p); }
+
+__device__ __forceinline__ DevFrame load_frame(const DevFrame *p)
+{
+    DevFrame f;
+    const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
+    const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+    const uint4 c = __ldg(reinterpret_cast<const uint4 *>(p) + 2);
+    f.plane[0] = reinterpret_cast<const void *>((uint64_t)a.x | ((uint64_t)a.y << 32));
+    f.plane[1] = reinterpret_cast<const void *>((uint64_t)a.z | ((uint64_t)a.w << 32));
+    f.plane[2] = reinterpret_cast<const void *>((uint64_t)b.x | ((uint64_t)b.y << 32));
+    f.pitch[0] = (int64_t)((uint64_t)b.z | ((uint64_t)b.w << 32));
+    f.pitch[1] = (int64_t)((uint64_t)c.x | ((uint64_t)c.y << 32));
+    f.pitch[2] = (int64_t)((uint64_t)c.z | ((uint64_t)c.w << 32));
+    return f;
+}
+
+template <typename T>
+__device__ __forceinline__ const T *row_ptr(const DevFrame &f, int p, int y)
+{
+    return reinterpret_cast<const T *>(static_cast<const char *>(f.plane[p]) + static_cast<int64_t>(y) * f.pitch[p]);
+}
+template <typename T>
+__device__ __forceinline__ T *row_ptr_w(const DevFrame &f, int p, int y)
+{
+    return reinterpret_cast<T *>(const_cast<char *>(static_cast<const char *>(f.plane[p])) +
+                                 static_cast<int64_t>(y) * f.pitch[p]);
+}
+
+// unpack 8 / 4 packed samples
+__device__ __forceinline__ void unpack8(uint4 q, int (&v)[kPx])
+{
+    v[0] = q.x & 0xffff; v[1] = q.x >> 16; v[2] = q.y & 0xffff; v[3] = q.y >> 16;
+    v[4] = q.z & 0xffff; v[5] = q.z >> 16; v[6] = q.w & 0xffff; v[7] = q.w >> 16;
+}
+__device__ __forceinline__ void unpack8(uint2 q, int (&v)[kPx])
+{
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = (q.x >> (8 * k)) & 0xff;
+        v[k + 4] = (q.y >> (8 * k)) & 0xff;
+    }
+}
+__device__ __forceinline__ void unpack4(uint2 q, int *v)
+{
+    v[0] = q.x & 0xffff; v[1] = q.x >> 16; v[2] = q.y & 0xffff; v[3] = q.y >> 16;
+}
+__device__ __forceinline__ void unpack4(uint32_t q, int *v)
+{
+    v[0] = q & 0xff; v[1] = (q >> 8) & 0xff; v[2] = (q >> 16) & 0xff; v[3] = q >> 24;
+}
+// 8 samples / 4 samples packed in one vector of the sample type
+template <typename IN> struct Pack;
+template <> struct Pack<uint16_t> { using V8 = uint4; using V4 = uint2; };
+template <> struct Pack<uint8_t> { using V8 = uint2; using V4 = uint32_t; };
+
+__device__ __forceinline__ uint32_t pack_half2(float a, float b)
+{
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+// ------------------------------------------------------------ f2t colour
+// Steps A5-A6: dequantise (exact integer offset, one fp32 rounding) and the
+// inverse matrix with no clamp (reading A4).  Inputs are 16 x code.
+template <int FAMILY>
+__device__ __forceinline__ void f2t_colour(const F2TColour &c, int ys, int us, int vs, float &R, float &G, float &B)
+{
+    if (FAMILY == kRGB) {
+        R = static_cast<float>(ys - c.y_off) * c.y_scale;
+        G = static_cast<float>(us - c.y_off) * c.y_scale;
+        B = static_cast<float>(vs - c.y_off) * c.y_scale;
+    } else {
+        const float Y = static_cast<float>(ys - c.y_off) * c.y_scale;
+        const float Pb = static_cast<float>(us - c.c_off) * c.c_scale;
+        const float Pr = static_cast<float>(vs - c.c_off) * c.c_scale;
+        R = fmaf(c.r_pr, Pr, Y);
+        B = fmaf(c.b_pb, Pb, Y);
+        G = fmaf(-c.g_pr, Pr, fmaf(-c.g_pb, Pb, Y));
+    }
+}
+
+// fp16 tensors near zero: a difference of O(1) terms rounded in fp32 can be
+// off by more than one fp16 ULP once |v| < 2^-9 (the ULP there is < 2^-19).
+// Those (rare) pixels are recomputed in fp64 and rounded once to fp16; the
+// returned float is that fp16 value exactly, so the RNE store reproduces it.
+__device__ __forceinline__ float3 f2t_colour_precise(const F2TColour &c, int ys, int us, int vs)
+{
+    const double Y = static_cast<double>(ys - c.y_off) * c.y_scale_d;
+    const double Pb = static_cast<double>(us - c.c_off) * c.c_scale_d;
+    const double Pr = static_cast<double>(vs - c.c_off) * c.c_scale_d;
+    return make_float3(__half2float(__double2half(Y + c.r_pr_d * Pr)),
+                       __half2float(__double2half(Y - c.g_pb_d * Pb - c.g_pr_d * Pr)),
+                       __half2float(__double2half(Y + c.b_pb_d * Pb)));
+}
+
+template <int FAMILY, typename OUT>
+__device__ __forceinline__ void f2t_pixel(const F2TColour &c, int ys, int us, int vs, float &R, float &G, float &B)
+{
+    f2t_colour<FAMILY>(c, ys, us, vs, R, G, B);
+    if (FAMILY != kRGB && sizeof(OUT) == 2) {
+        constexpr float kTiny = 1.0f / 512.0f;
+        if (fabsf(R) < kTiny || fabsf(G) < kTiny || fabsf(B) < kTiny) {
+            const float3 p = f2t_colour_precise(c, ys, us, vs);
+            R = p.x;
+            G = p.y;
+            B = p.z;
+        }
+    }
+}
+
+// Horizontal 2x upsample of one chroma row around an item's 8 columns:
+// c[0] = sample i0-1 (clamped), c[1..4] = i0..i0+3, c[5] = i0+4 (clamped).
+// Even luma column 2m: 3*c[m+1] + c[m];  odd 2m+1: 3*c[m+1] + c[m+2]
+// (centre siting, reading A5; the vertical pass adds 3*near + far).
+__device__ __forceinline__ void hup(const int (&c)[6], int (&h)[kPx])
+{
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        h[2 * m] = 3 * c[m + 1] + c[m];
+        h[2 * m + 1] = 3 * c[m + 1] + c[m + 2];
+    }
+}
+
+// Chroma rows of a 4:2:0 luma row y (already clamped to the frame): the near
+// row and the far row (above for even y, below for odd y), clamped.
+__device__ __forceinline__ int chroma_near(int yc) { return yc >> 1; }
+__device__ __forceinline__ int chroma_far(int yc, int ch)
+{
+    return (yc & 1) ? min((yc >> 1) + 1, ch - 1) : max((yc >> 1) - 1, 0);
+}
+
+// Scalar path: sample codes of pixel (x, y) with every coordinate clamped
+// (padding replicates the last row/column, reading A6; chroma taps clamp to
+// the plane, reading A5).  Values are 16 x code.
+template <int FAMILY, typename IN>
+__device__ __forceinline__ void f2t_codes_scalar(const DevFrame &f, int W, int H, int x, int y, int &ys, int &us,
+                                                 int &vs)
+{
+    const int xc = min(x, W - 1), yc = min(y, H - 1);
+    ys = 16 * load1(row_ptr<IN>(f, 0, yc) + xc);
+    if (FAMILY == kYUV420) {
+        const int cw = W >> 1, ch = H >> 1;
+        const int jn = chroma_near(yc), jf = chroma_far(yc, ch);
+        const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
+        const IN *u0 = row_ptr<IN>(f, 1, jn), *u1 = row_ptr<IN>(f, 1, jf);
+        const IN *v0 = row_ptr<IN>(f, 2, jn), *v1 = row_ptr<IN>(f, 2, jf);
+        us = 9 * load1(u0 + in_) + 3 * load1(u0 + if_) + 3 * load1(u1 + in_) + load1(u1 + if_);
+        vs = 9 * load1(v0 + in_) + 3 * load1(v0 + if_) + 3 * load1(v1 + in_) + load1(v1 + if_);
+    } else {
+        us = 16 * load1(row_ptr<IN>(f, 1, yc) + xc);
+        vs = 16 * load1(row_ptr<IN>(f, 2, yc) + xc);
+    }
+}
+
+// Packed tensor values of one row of 8 pixels and one channel.
+template <typename OUT> struct Row8;
+template <> struct Row8<__half> {
+    uint4 v;
+    __device__ __forceinline__ void set(const float (&x)[kPx])
+    {
+        v = make_uint4(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]), pack_half2(x[4], x[5]), pack_half2(x[6], x[7]));
+    }
+    __device__ __forceinline__ void store(__half *p) const { *reinterpret_cast<uint4 *>(p) = v; }
+    __device__ __forceinline__ void store_n(__half *p, int n) const
+    {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < kPx; ++k)
+            if (k < n) reinterpret_cast<uint16_t *>(p)[k] = static_cast<uint16_t>(w[k >> 1] >> (16 * (k & 1)));
+    }
+};
+template <> struct Row8<float> {
+    float4 a, b;
+    __device__ __forceinline__ void set(const float (&x)[kPx])
+    {
+        a = make_float4(x[0], x[1], x[2], x[3]);
+        b = make_float4(x[4], x[5], x[6], x[7]);
+    }
+    __device__ __forceinline__ void store(float *p) const
+    {
+        reinterpret_cast<float4 *>(p)[0] = a;
+        reinterpret_cast<float4 *>(p)[1] = b;
+    }
+    __device__ __forceinline__ void store_n(float *p, int n) const
+    {
+        const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < kPx; ++k)
+            if (k < n) p[k] = x[k];
+    }
+};
+
+// One row of 16x codes -> the three packed channel rows.
+template <int FAMILY, typename OUT>
+__device__ __forceinline__ void f2t_row(const F2TColour &c, const int (&ys)[kPx], const int (&us)[kPx],
+                                        const int (&vs)[kPx], Row8<OUT> (&o)[3])
+{
+    float R[kPx], G[kPx], B[kPx];
+#pragma unroll
+    for (int k = 0; k < kPx; ++k) f2t_pixel<FAMILY, OUT>(c, ys[k], us[k], vs[k], R[k], G[k], B[k]);
+    o[0].set(R);
+    o[1].set(G);
+    o[2].set(B);
+}
+
+constexpr int kDstRegs = 8;  // destinations of a job held in registers
+
+// Destinations of job j: dst_code[job_dst[j] .. job_dst[j+1]), the first
+// kDstRegs in registers.
+struct DstList {
+    int d0, nd;
+    int code[kDstRegs];
+    __device__ __forceinline__ void load(const F2TArgs &a, int job)
+    {
+        d0 = a.job_dst[job];
+        nd = a.job_dst[job + 1] - d0;
+#pragma unroll
+        for (int k = 0; k < kDstRegs; ++k) code[k] = k < nd ? a.dst_code[d0 + k] : 0;
+    }
+    __device__ __forceinline__ int get(const F2TArgs &a, int d) const
+    {
+        int cd = 0;
+#pragma unroll
+        for (int k = 0; k < kDstRegs; ++k)
+            if (d == k) cd = code[k];
+        if (d >= kDstRegs) cd = a.dst_code[d0 + d];
+        return cd;
+    }
+};
+
+// Store an item's ROWS x 3 packed rows at column x0, row y0 of every
+// destination (run, slot) of its frame.
+template <int ROWS, typename OUT>
+__device__ __forceinline__ void f2t_store(const F2TArgs &a, const DstList &dl, const Row8<OUT> (&out)[ROWS][3], int x0,
+                                          int y0)
+{
+    const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
+    const int64_t off = static_cast<int64_t>(y0) * a.Wp + x0;
+    const bool vec_store = a.vec_out && (x0 + kPx <= a.Wp);
+    const int nvalid = min(kPx, a.Wp - x0);
+    for (int d = 0; d < dl.nd; ++d) {
+        const int cd = dl.get(a, d);
+        OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
+                                         static_cast<int64_t>(cd & 31) * a.slot_bytes) + off;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                OUT *q = o + c * plane + static_cast<int64_t>(r) * a.Wp;
+                if (vec_store) out[r][c].store(q);
+                else out[r][c].store_n(q, nvalid);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ t2f colour
+template <typename T> struct T2FConst;
+template <> struct T2FConst<float> {
+    float kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
+    __device__ explicit T2FConst(const T2FColour &c)
+        : kr(c.fkr), kb(c.fkb), db(c.fdb), dr(c.fdr), idb(c.fidb), idr(c.fidr), ys(c.fys), yo(c.fyo), cs(c.fcs),
+          co(c.fco), maxc(c.fmaxc) {}
+};
+template <> struct T2FConst<double> {
+    double kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
+    __device__ explicit T2FConst(const T2FColour &c)
+        : kr(c.kr), kb(c.kb), db(c.db), dr(c.dr), idb(c.idb), idr(c.idr), ys(c.ys), yo(c.yo), cs(c.cs), co(c.co),
+          maxc(c.maxc) {}
+};
+
+__device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
+
+// Step B4: clamp to [0, maxc] (NaN -> 0: fmax returns the non-NaN operand),
+// then round half to even by adding 1.5 * 2^(p-1): the sum lies where the
+// spacing of representable values is exactly 1, so the FP add rounds the
+// value to the nearest integer, ties to even, and the integer is the low bits.
+__device__ __forceinline__ uint32_t quant(float q, float maxc)
+{
+    const float x = fminf(fmaxf(q, 0.0f), maxc);
+    return __float_as_uint(x + 12582912.0f) - 0x4B400000u;
+}
+__device__ __forceinline__ uint32_t quant(double q, double maxc)
+{
+    const double x = fmin(fmax(q, 0.0), maxc);
+    return static_cast<uint32_t>(__double2loint(x + 6755399441055744.0));
+}
+
+// S / d for a divisor d with precomputed reciprocal id: one FMA correction of
+// the reciprocal product (correctly rounded quotient; keeps exact quotients
+// such as the full-range primaries' +-0.5 exact).
+template <typename T>
+__device__ __forceinline__ T divide(T S, T d, T id)
+{
+    const T q0 = S * id;
+    const T r = fma_(-q0, d, S);
+    return fma_(r, id, q0);
+}
+
+__device__ __forceinline__ uint32_t pack4_u8(uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+__device__ __forceinline__ void store_samples8(uint16_t *p, const uint32_t (&v)[kPx])
+{
+    *reinterpret_cast<uint4 *>(p) = make_uint4(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410),
+                                               __byte_perm(v[4], v[5], 0x5410), __byte_perm(v[6], v[7], 0x5410));
+}
+__device__ __forceinline__ void store_samples8(uint8_t *p, const uint32_t (&v)[kPx])
+{
+    *reinterpret_cast<uint2 *>(p) = make_uint2(pack4_u8(v[0], v[1], v[2], v[3]), pack4_u8(v[4], v[5], v[6], v[7]));
+}
+__device__ __forceinline__ void store_samples4(uint16_t *p, const uint32_t (&v)[4])
+{
+    *reinterpret_cast<uint2 *>(p) = make_uint2(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410));
+}
+__device__ __forceinline__ void store_samples4(uint8_t *p, const uint32_t (&v)[4])
+{
+    *reinterpret_cast<uint32_t *>(p) = pack4_u8(v[0], v[1], v[2], v[3]);
+}
+template <typename OS, int N>
+__device__ __forceinline__ void store_samples_n(OS *p, const uint32_t (&v)[N], int n)
+{
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+        if (k < n) p[k] = static_cast<OS>(v[k]);
+}
+
+// Unpack 8 tensor values of one row and channel.
+__device__ __forceinline__ void tunpack8(uint4 v, float (&x)[kPx])
+{
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w[k]));
+        x[2 * k] = f.x;
+        x[2 * k + 1] = f.y;
+    }
+}
+__device__ __forceinline__ void tunpack8(uint4 a, uint4 b, float (&x)[kPx])
+{
+    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y); x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+    x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y); x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
+}
+// 8 tensor values from memory (global or shared), 16-byte aligned
+__device__ __forceinline__ void tload8(const __half *p, float (&x)[kPx]) { tunpack8(*reinterpret_cast<const uint4 *>(p), x); }
+__device__ __forceinline__ void tload8(const float *p, float (&x)[kPx])
+{
+    tunpack8(reinterpret_cast<const uint4 *>(p)[0], reinterpret_cast<const uint4 *>(p)[1], x);
+}
+__device__ __forceinline__ void tload8_stream(const __half *p, float (&x)[kPx]) { tunpack8(ld_stream_v4(p), x); }
+__device__ __forceinline__ void tload8_stream(const float *p, float (&x)[kPx])
+{
+    tunpack8(ld_stream_v4(p), ld_stream_v4(p + 4), x);
+}
+__device__ __forceinline__ float tload1(const __half *p) { return __half2float(p[0]); }
+__device__ __forceinline__ float tload1(const float *p) { return p[0]; }
+
+// One output row y (row r of the item) of R', G', B' -> luma codes (and
+// 4:4:4 chroma codes, or the 4:2:0 partial 2x2 sums of B-Y', R-Y').
+template <int FAMILY, typename OS, typename AR>
+__device__ __forceinline__ void t2f_row(const T2FConst<AR> &c, const T2FColour &cc, const DevFrame &f, int x0, int y,
+                                        int r, const float (&R)[kPx], const float (&G)[kPx], const float (&B)[kPx],
+                                        int nvalid, bool vec_store, AR (&sb)[4], AR (&sr)[4])
+{
+    (void)cc;
+    if constexpr (FAMILY == kRGB) {
+        uint32_t q[3][kPx];
+#pragma unroll
+        for (int k = 0; k < kPx; ++k) {
+            q[0][k] = quant(fma_(static_cast<AR>(R[k]), c.ys, c.yo), c.maxc);
+            q[1][k] = quant(fma_(static_cast<AR>(G[k]), c.ys, c.yo), c.maxc);
+            q[2][k] = quant(fma_(static_cast<AR>(B[k]), c.ys, c.yo), c.maxc);
+        }
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            OS *out = row_ptr_w<OS>(f, p, y) + x0;
+            if (vec_store) store_samples8(out, q[p]);
+            else store_samples_n(out, q[p], nvalid);
+        }
+    } else {
+        // Step B2 (luma) + B4: Y' = G + Kr(R-G) + Kb(B-G)
+        AR BY[kPx], RY[kPx];
+        uint32_t qy[kPx];
+#pragma unroll
+        for (int k = 0; k < kPx; ++k) {
+            const AR r_ = R[k], g_ = G[k], b_ = B[k];
+            const AR Y = fma_(c.kb, b_ - g_, fma_(c.kr, r_ - g_, g_));
+            BY[k] = b_ - Y;
+            RY[k] = r_ - Y;
+            qy[k] = quant(fma_(Y, c.ys, c.yo), c.maxc);
+        }
+        OS *out = row_ptr_w<OS>(f, 0, y) + x0;
+        if (vec_store) store_samples8(out, qy);
+        else store_samples_n(out, qy, nvalid);
+        if constexpr (FAMILY == kYUV444) {
+            uint32_t qb[kPx], qr[kPx];
+#pragma unroll
+            for (int k = 0; k < kPx; ++k) {
+                qb[k] = quant(fma_(divide(BY[k], c.db, c.idb), c.cs, c.co), c.maxc);
+                qr[k] = quant(fma_(divide(RY[k], c.dr, c.idr), c.cs, c.co), c.maxc);
+            }
+            OS *ob = row_ptr_w<OS>(f, 1, y) + x0, *orr = row_ptr_w<OS>(f, 2, y) + x0;
+            if (vec_store) {
+                store_samples8(ob, qb);
+                store_samples8(orr, qr);
+            } else {
+                store_samples_n(ob, qb, nvalid);
+                store_samples_n(orr, qr, nvalid);
+            }
+        } else {
+            // 4:2:0: accumulate ((a+b) + (c+d)) row by row
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const AR pb = BY[2 * m] + BY[2 * m + 1], pr = RY[2 * m] + RY[2 * m + 1];
+                sb[m] = r == 0 ? pb : sb[m] + pb;
+                sr[m] = r == 0 ? pr : sr[m] + pr;
+            }
+        }
+    }
+}
+
+// Step B3 + B4 for 4:2:0: 2x2 box mean ((a+b)+(c+d))/4, folded into the
+// divisor 4*db (a power-of-two scaling, exact), then quantise and store the
+// item's 4 chroma samples of each plane at chroma row y0/2.
+template <typename OS, typename AR>
+__device__ __forceinline__ void t2f_chroma420(const T2FConst<AR> &c, const DevFrame &f, int x0, int y0,
+                                              const AR (&sb)[4], const AR (&sr)[4], int nvalid, bool vec_store)
+{
+    const AR db4 = c.db * AR(4), dr4 = c.dr * AR(4), idb4 = c.idb * AR(0.25), idr4 = c.idr * AR(0.25);
+    uint32_t qb[4], qr[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        qb[m] = quant(fma_(divide(sb[m], db4, idb4), c.cs, c.co), c.maxc);
+        qr[m] = quant(fma_(divide(sr[m], dr4, idr4), c.cs, c.co), c.maxc);
+    }
+    OS *ob = row_ptr_w<OS>(f, 1, y0 >> 1) + (x0 >> 1), *orr = row_ptr_w<OS>(f, 2, y0 >> 1) + (x0 >> 1);
+    if (vec_store) {
+        store_samples4(ob, qb);
+        store_samples4(orr, qr);
+    } else {
+        store_samples_n(ob, qb, nvalid / 2);
+        store_samples_n(orr, qr, nvalid / 2);
+    }
+}
+
+}  // namespace dev
+}  // namespace nnvisr

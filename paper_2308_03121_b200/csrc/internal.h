@@ -11,7 +11,6 @@ constexpr int kYUV420 = 0, kYUV444 = 1, kRGB = 2;
 constexpr int kF32 = 0, kF16 = 1;
 constexpr int kPx = 8;           // luma columns per thread (one 16-byte fp16 store)
 constexpr int kThreads = 256;    // CTA size of the conversion kernels
-constexpr int kMaxGridY = 65535; // jobs per launch (grid.y)
 
 // Device copy of one frame descriptor (same layout as nnvisr_frame).
 struct DevFrame {
@@ -56,11 +55,14 @@ struct F2TArgs {
     char *dst;                // tensor of run 0 of this launch
     int64_t run_stride;       // bytes between consecutive runs' tensors
     int64_t slot_bytes;       // bytes of one slot (3*Hp*Wp*elem)
-    int32_t job_base;         // first job of this launch (grid.y offset)
+    int64_t items;            // jobs * units
     int32_t W, H, Hp, Wp;     // clip size and padded tensor size
-    int32_t units, col_units; // threads per job and column groups per row unit
+    int32_t units, col_units; // items per job and column groups per row unit
     int32_t vec_in;           // 1: all bound planes/pitches 16-byte aligned
     int32_t vec_out;          // 1: tensor rows allow 16-byte stores
+    // TMA-pipelined path (kernels_tma.cu): tiles = jobs * rowunits * nseg
+    int32_t tma_ok, rowunits, nseg, stages, stage_bytes;
+    int64_t tiles;
     F2TColour col;
 };
 
@@ -69,20 +71,22 @@ struct T2FArgs {
     int64_t tensor_stride;    // bytes between tuples' tensors
     const DevFrame *out;      // output frame descriptors [count*M] (device)
     int32_t M;                // output slots per tensor
-    int32_t job_base;
+    int64_t items;            // jobs * units
     int32_t Wo, Ho;           // output frame size
     int64_t th, tw;           // tensor spatial size
     int32_t units, col_units;
     int32_t vec_in;           // tensor rows allow 16-byte loads
     int32_t vec_out;          // output planes allow vector stores
+    int32_t tma_ok, rowunits, nseg, stages, stage_bytes;
+    int64_t tiles;
     T2FColour col;
 };
 
 // Launchers (kernels.cu).  Return the CUDA error of the launch.
-cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, int num_jobs,
-                       cudaStream_t s);
-cudaError_t launch_t2f(int family, int bits, int dtype, const T2FArgs &a, int num_jobs,
-                       cudaStream_t s);
+cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s);
+cudaError_t launch_t2f(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s);
+cudaError_t launch_f2t_tma(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s);
+cudaError_t launch_t2f_tma(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s);
 
 void count_launch();
 

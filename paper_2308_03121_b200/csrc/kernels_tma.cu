@@ -1,0 +1,458 @@
+// kernels_tma.cu -- TMA-pipelined conversion kernels (sm_100a).
+//
+// The hot path is a pair of streaming passes (SURVEY.md §8(a) A3-A7 and
+// B1-B4).  Both kernels here are persistent: each CTA walks a contiguous range
+// of tiles, a tile being one row unit (a 4:2:0 row pair, else one row) times
+// a segment of up to 2048 columns, i.e. 8 columns per thread.  Thread 0 keeps
+// a ring of S shared-memory stages full with TMA bulk copies
+// (cp.async.bulk.shared::cluster.global, completion counted in bytes on one
+// mbarrier per stage) -- for frames->tensor the tile's luma rows together with
+// its co-sited chroma rows and their one-sample halo (north_star: "TMA or
+// shared-memory staging of luma tiles together with their co-sited chroma
+// rows"), for tensor->frames the tile's R', G', B' rows.  All threads convert
+// from shared memory and store with 128-bit st.global, while the copies of the
+// next S-1 tiles are in flight.
+//
+// Coordinates outside the frame are clamped when shared memory is read
+// (padding replicates the last row/column, reading A6; chroma taps clamp to
+// the plane, reading A5), so no copy ever leaves the plane: the copy windows
+// are clamped to the plane and 16-byte aligned.  The host enables this path
+// only when every window is 16-byte aligned (see nnvisr.cpp, tma_ok).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace nnvisr {
+namespace {
+using namespace dev;
+
+// ---------------------------------------------------------------- TMA / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "DONE:\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy (TMA engine; SASS UBLKCP), completes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+constexpr int kSegW = kThreads * kPx;  // columns per tile segment (2048)
+constexpr int kBarBytes = 128;         // mbarrier block at the start of dynamic smem
+
+struct TileCursor {
+    int64_t t, end;
+    __device__ __forceinline__ void init(int64_t tiles)
+    {
+        t = tiles * blockIdx.x / gridDim.x;
+        end = tiles * (blockIdx.x + 1) / gridDim.x;
+    }
+};
+
+// tile -> (job, row unit, segment)
+__device__ __forceinline__ void decode_tile(int64_t t, int rowunits, int nseg, int seg_w, int &job, int &ru, int &x0)
+{
+    const int64_t per_job = static_cast<int64_t>(rowunits) * nseg;
+    job = static_cast<int>(t / per_job);
+    const int rem = static_cast<int>(t - static_cast<int64_t>(job) * per_job);
+    ru = rem / nseg;
+    x0 = (rem - ru * nseg) * seg_w;
+}
+
+// ------------------------------------------------------------------ f2t
+// Stage layout (samples of IN): 4:2:0 = luma[2][LCAP] | U[3][CCAP] | V[3][CCAP]
+// (chroma rows: near, far of row 0, far of row 1); 4:4:4/RGB = P0 | P1 | P2
+// [1][LCAP].  LCAP = seg_w, CCAP = seg_w/2 + 2 * (16 / sizeof(IN)).
+template <int FAMILY, typename IN> struct F2TStage {
+    static constexpr int G = 16 / sizeof(IN);  // samples per 16 bytes
+    static constexpr int LCAP = kSegW;
+    static constexpr int CCAP = kSegW / 2 + 2 * G;
+    static constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
+    static constexpr int BYTES = FAMILY == kYUV420 ? (2 * LCAP + 6 * CCAP) * sizeof(IN) : 3 * LCAP * sizeof(IN);
+    __device__ static IN *luma(uint8_t *st, int r) { return reinterpret_cast<IN *>(st) + r * LCAP; }
+    __device__ static IN *chroma(uint8_t *st, int p, int q)
+    {
+        return reinterpret_cast<IN *>(st) + 2 * LCAP + (p * 3 + q) * CCAP;
+    }
+    __device__ static IN *plane(uint8_t *st, int p) { return reinterpret_cast<IN *>(st) + p * LCAP; }
+};
+
+// Copy windows of a segment [x0, x1): luma [lw0, lw1), chroma [cw0, cw1).
+struct F2TWindow {
+    int lw0, lw1, cw0, cw1;
+    __device__ __forceinline__ void set(int x0, int x1, int W, int G, bool chroma420)
+    {
+        const int xr = min(x1, W);
+        if (x0 < W) {
+            lw0 = x0;
+            lw1 = xr;
+        } else {  // a segment of padding columns only: they replicate column W-1
+            lw0 = W - G;
+            lw1 = W;
+        }
+        if (chroma420) {
+            const int cw = W >> 1;
+            const int lo = (min(x0, W - 1) >> 1) - 1;
+            cw0 = max(0, (lo >= 0 ? lo : -G) / G * G);
+            cw1 = min(cw, ((xr >> 1) + 1 + G - 1) / G * G);
+        }
+    }
+};
+
+template <int FAMILY, typename IN>
+__device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *st, uint64_t *bar)
+{
+    using S = F2TStage<FAMILY, IN>;
+    int job, ru, x0;
+    decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
+    const int x1 = min(x0 + kSegW, a.Wp);
+    const DevFrame f = load_frame(a.frames + a.job_frame[job]);
+    F2TWindow w;
+    w.set(x0, x1, a.W, S::G, FAMILY == kYUV420);
+    const int y0 = ru * S::ROWS;
+    const uint32_t lbytes = (w.lw1 - w.lw0) * sizeof(IN);
+    if constexpr (FAMILY == kYUV420) {
+        const uint32_t cbytes = (w.cw1 - w.cw0) * sizeof(IN);
+        mbar_arrive_expect_tx(bar, 2 * lbytes + 6 * cbytes);
+        const int yc0 = min(y0, a.H - 1), yc1 = min(y0 + 1, a.H - 1), ch = a.H >> 1;
+        bulk_g2s(S::luma(st, 0), row_ptr<IN>(f, 0, yc0) + w.lw0, lbytes, bar);
+        bulk_g2s(S::luma(st, 1), row_ptr<IN>(f, 0, yc1) + w.lw0, lbytes, bar);
+        const int rows[3] = {chroma_near(yc0), chroma_far(yc0, ch), chroma_far(yc1, ch)};
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                bulk_g2s(S::chroma(st, p, q), row_ptr<IN>(f, p + 1, rows[q]) + w.cw0, cbytes, bar);
+    } else {
+        mbar_arrive_expect_tx(bar, 3 * lbytes);
+        const int yc = min(y0, a.H - 1);
+#pragma unroll
+        for (int p = 0; p < 3; ++p) bulk_g2s(S::plane(st, p), row_ptr<IN>(f, p, yc) + w.lw0, lbytes, bar);
+    }
+}
+
+template <int FAMILY, typename IN, typename OUT>
+__global__ void __launch_bounds__(kThreads) f2t_tma(const F2TArgs a)
+{
+    using S = F2TStage<FAMILY, IN>;
+    using V8 = typename Pack<IN>::V8;
+    using V4 = typename Pack<IN>::V4;
+    constexpr int ROWS = S::ROWS;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+    uint8_t *stages = smem + kBarBytes;
+    const int nst = a.stages;
+
+    TileCursor tc;
+    tc.init(a.tiles);
+    if (tc.t >= tc.end) return;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < nst; ++k) mbar_init(&bars[k], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int k = 0; k < nst && tc.t + k < tc.end; ++k)
+            f2t_issue<FAMILY, IN>(a, tc.t + k, stages + k * a.stage_bytes, &bars[k]);
+
+    int cj = -1;
+    DstList dl;
+    int k = 0;
+    uint32_t phase = 0;
+    for (int64_t t = tc.t; t < tc.end; ++t) {
+        int job, ru, x0;
+        decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
+        const int x1 = min(x0 + kSegW, a.Wp);
+        const int y0 = ru * ROWS;
+        const int x = x0 + kPx * threadIdx.x;
+        if (job != cj) {
+            cj = job;
+            dl.load(a, job);
+        }
+        uint8_t *st = stages + k * a.stage_bytes;
+        mbar_wait(&bars[k], phase);
+        if (x < x1) {
+            F2TWindow w;
+            w.set(x0, x1, a.W, S::G, FAMILY == kYUV420);
+            const bool fast = x + kPx <= a.W;
+            Row8<OUT> out[ROWS][3];
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+                int ys[kPx], us[kPx], vs[kPx];
+                if constexpr (FAMILY == kYUV420) {
+                    const IN *L = S::luma(st, r);
+                    const int cw = a.W >> 1;
+                    if (fast) {
+                        unpack8(*reinterpret_cast<const V8 *>(L + (x - w.lw0)), ys);
+                        const int i0 = x >> 1;
+#pragma unroll
+                        for (int p = 0; p < 2; ++p) {
+                            int h[2][kPx];
+#pragma unroll
+                            for (int q = 0; q < 2; ++q) {
+                                const IN *C = S::chroma(st, p, q == 0 ? 0 : 1 + r) - w.cw0;
+                                int c[6];
+                                unpack4(*reinterpret_cast<const V4 *>(C + i0), &c[1]);
+                                c[0] = C[max(i0 - 1, 0)];
+                                c[5] = C[min(i0 + 4, cw - 1)];
+                                hup(c, h[q]);
+                            }
+#pragma unroll
+                            for (int kk = 0; kk < kPx; ++kk) {
+                                const int s = 3 * h[0][kk] + h[1][kk];
+                                if (p == 0) us[kk] = s; else vs[kk] = s;
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < kPx; ++kk) {
+                            const int xc = min(x + kk, a.W - 1);
+                            ys[kk] = L[xc - w.lw0];
+                            const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
+                            const IN *Un = S::chroma(st, 0, 0) - w.cw0, *Uf = S::chroma(st, 0, 1 + r) - w.cw0;
+                            const IN *Vn = S::chroma(st, 1, 0) - w.cw0, *Vf = S::chroma(st, 1, 1 + r) - w.cw0;
+                            us[kk] = 9 * Un[in_] + 3 * Un[if_] + 3 * Uf[in_] + Uf[if_];
+                            vs[kk] = 9 * Vn[in_] + 3 * Vn[if_] + 3 * Vf[in_] + Vf[if_];
+                        }
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < kPx; ++kk) ys[kk] *= 16;
+                } else {
+                    const IN *P0 = S::plane(st, 0) - w.lw0, *P1 = S::plane(st, 1) - w.lw0,
+                             *P2 = S::plane(st, 2) - w.lw0;
+                    if (fast) {
+                        unpack8(*reinterpret_cast<const V8 *>(P0 + x), ys);
+                        unpack8(*reinterpret_cast<const V8 *>(P1 + x), us);
+                        unpack8(*reinterpret_cast<const V8 *>(P2 + x), vs);
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < kPx; ++kk) {
+                            const int xc = min(x + kk, a.W - 1);
+                            ys[kk] = P0[xc];
+                            us[kk] = P1[xc];
+                            vs[kk] = P2[xc];
+                        }
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < kPx; ++kk) {
+                        ys[kk] *= 16;
+                        us[kk] *= 16;
+                        vs[kk] *= 16;
+                    }
+                }
+                f2t_row<FAMILY, OUT>(a.col, ys, us, vs, out[r]);
+            }
+            f2t_store<ROWS, OUT>(a, dl, out, x, y0);
+        }
+        __syncthreads();  // every thread is done reading stage k
+        if (threadIdx.x == 0 && t + nst < tc.end) {
+            fence_proxy_async();
+            f2t_issue<FAMILY, IN>(a, t + nst, st, &bars[k]);
+        }
+        if (++k == nst) {
+            k = 0;
+            phase ^= 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ t2f
+// Stage layout (values of TIN): [ROWS][3 channels][seg_w].
+template <int FAMILY, typename TIN> struct T2FStage {
+    static constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
+    static constexpr int BYTES = ROWS * 3 * kSegW * sizeof(TIN);
+    __device__ static TIN *row(uint8_t *st, int r, int c) { return reinterpret_cast<TIN *>(st) + (r * 3 + c) * kSegW; }
+};
+
+template <int FAMILY, typename TIN>
+__device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *st, uint64_t *bar)
+{
+    using S = T2FStage<FAMILY, TIN>;
+    int job, ru, x0;
+    decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
+    const int x1 = min(x0 + kSegW, a.Wo);
+    const int tup = job / a.M, o = job - tup * a.M;
+    const int64_t plane = a.th * a.tw;
+    const TIN *src = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
+                     static_cast<int64_t>(3 * o) * plane + static_cast<int64_t>(ru * S::ROWS) * a.tw + x0;
+    const uint32_t bytes = (x1 - x0) * sizeof(TIN);
+    mbar_arrive_expect_tx(bar, S::ROWS * 3 * bytes);
+#pragma unroll
+    for (int r = 0; r < S::ROWS; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) bulk_g2s(S::row(st, r, c), src + c * plane + r * a.tw, bytes, bar);
+}
+
+template <int FAMILY, typename OS, typename TIN, typename AR>
+__global__ void __launch_bounds__(kThreads) t2f_tma(const T2FArgs a)
+{
+    using S = T2FStage<FAMILY, TIN>;
+    constexpr int ROWS = S::ROWS;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+    uint8_t *stages = smem + kBarBytes;
+    const int nst = a.stages;
+
+    TileCursor tc;
+    tc.init(a.tiles);
+    if (tc.t >= tc.end) return;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < nst; ++k) mbar_init(&bars[k], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int k = 0; k < nst && tc.t + k < tc.end; ++k)
+            t2f_issue<FAMILY, TIN>(a, tc.t + k, stages + k * a.stage_bytes, &bars[k]);
+
+    const T2FConst<AR> c(a.col);
+    int cj = -1;
+    DevFrame f;
+    int k = 0;
+    uint32_t phase = 0;
+    for (int64_t t = tc.t; t < tc.end; ++t) {
+        int job, ru, x0;
+        decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
+        const int x1 = min(x0 + kSegW, a.Wo);
+        const int y0 = ru * ROWS;
+        const int xo = kPx * threadIdx.x;  // column within the segment
+        if (job != cj) {
+            cj = job;
+            f = load_frame(a.out + job);
+        }
+        uint8_t *st = stages + k * a.stage_bytes;
+        mbar_wait(&bars[k], phase);
+        if (x0 + xo < x1) {
+            const int x = x0 + xo;
+            AR sb[4], sr[4];
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+                float R[kPx], G[kPx], B[kPx];
+                tload8(S::row(st, r, 0) + xo, R);
+                tload8(S::row(st, r, 1) + xo, G);
+                tload8(S::row(st, r, 2) + xo, B);
+                t2f_row<FAMILY, OS, AR>(c, a.col, f, x, y0 + r, r, R, G, B, kPx, a.vec_out, sb, sr);
+            }
+            if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, y0, sb, sr, kPx, a.vec_out);
+        }
+        __syncthreads();  // every thread is done reading stage k
+        if (threadIdx.x == 0 && t + nst < tc.end) {
+            fence_proxy_async();
+            t2f_issue<FAMILY, TIN>(a, t + nst, st, &bars[k]);
+        }
+        if (++k == nst) {
+            k = 0;
+            phase ^= 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ launch
+int sms()
+{
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+// Stages per CTA: as many as fit in ~100 KB (2..4), so two CTAs share an SM.
+template <typename K, typename A>
+cudaError_t launch_tma(K kernel, A a, int stage_bytes, cudaStream_t s)
+{
+    if (a.tiles <= 0) return cudaSuccess;
+    a.stage_bytes = (stage_bytes + 127) / 128 * 128;
+    a.stages = std::max(2, std::min(4, (100 * 1024) / a.stage_bytes));
+    const int smem = kBarBytes + a.stages * a.stage_bytes;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
+    kernel<<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int FAMILY>
+cudaError_t f2t_tma_dispatch(int bits, int dtype, const F2TArgs &a, cudaStream_t s)
+{
+    if (bits == 8) {
+        constexpr int B = F2TStage<FAMILY, uint8_t>::BYTES;
+        if (dtype == kF16) return launch_tma(f2t_tma<FAMILY, uint8_t, __half>, a, B, s);
+        return launch_tma(f2t_tma<FAMILY, uint8_t, float>, a, B, s);
+    }
+    constexpr int B = F2TStage<FAMILY, uint16_t>::BYTES;
+    if (dtype == kF16) return launch_tma(f2t_tma<FAMILY, uint16_t, __half>, a, B, s);
+    return launch_tma(f2t_tma<FAMILY, uint16_t, float>, a, B, s);
+}
+
+template <int FAMILY>
+cudaError_t t2f_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t s)
+{
+    constexpr int BH = T2FStage<FAMILY, __half>::BYTES, BF = T2FStage<FAMILY, float>::BYTES;
+    if (bits == 8) {
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, BH, s);
+        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, BF, s);
+    }
+    if (bits == 10) {
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, BH, s);
+        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, BF, s);
+    }
+    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, BH, s);
+    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, BF, s);
+}
+
+}  // namespace
+
+cudaError_t launch_f2t_tma(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s)
+{
+    switch (family) {
+    case kYUV420: return f2t_tma_dispatch<kYUV420>(bits, dtype, a, s);
+    case kYUV444: return f2t_tma_dispatch<kYUV444>(bits, dtype, a, s);
+    default: return f2t_tma_dispatch<kRGB>(bits, dtype, a, s);
+    }
+}
+
+cudaError_t launch_t2f_tma(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s)
+{
+    switch (family) {
+    case kYUV420: return t2f_tma_dispatch<kYUV420>(bits, dtype, a, s);
+    case kYUV444: return t2f_tma_dispatch<kYUV444>(bits, dtype, a, s);
+    default: return t2f_tma_dispatch<kRGB>(bits, dtype, a, s);
+    }
+}
+
+}  // namespace nnvisr

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -87,6 +88,7 @@ struct nnvisr_handle {
     DevFrame *frames = nullptr;
     int64_t frames_cap = 0, frames_base = 0, frames_count = 0;
     bool frames_vec = false;
+    bool force_generic = false;  // NNVISR_FORCE_GENERIC=1: never take the TMA path (tests)
 };
 
 namespace {
@@ -212,6 +214,8 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
     h->Wp = round_up(f.width, w.align);
     h->Wo = Wo; h->Ho = Ho;
     h->elem = w.dtype == NNVISR_F16 ? 2 : 4;
+    const char *fg = std::getenv("NNVISR_FORCE_GENERIC");
+    h->force_generic = fg && fg[0] == '1';
 
     // A5 dequantisation on 16x codes: luma v = (16c - y_off) * y_scale,
     // chroma P = (s - c_off) * c_scale with s = 16 x (upsampled) code.
@@ -450,12 +454,16 @@ F2TArgs f2t_args(const nnvisr_handle *h)
 
 nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, cudaStream_t st)
 {
-    for (int64_t j0 = 0; j0 < jobs; j0 += kMaxGridY) {
-        a.job_base = (int32_t)j0;
-        const int n = (int)std::min<int64_t>(kMaxGridY, jobs - j0);
-        cudaError_t e = launch_f2t(h->fmt.family, h->fmt.bits, h->net.dtype, a, n, st);
-        if (e != cudaSuccess) return cuda_fail(e, "f2t kernel launch");
-    }
+    a.items = jobs * a.units;
+    // TMA-pipelined path: every copy window 16-byte aligned (planes and
+    // pitches aligned, width a multiple of 32 samples) and 16-byte stores
+    const int rows = h->fmt.family == NNVISR_YUV420 ? 2 : 1;
+    a.rowunits = (int32_t)(h->Hp / rows);
+    a.nseg = (int32_t)((h->Wp + kThreads * kPx - 1) / (kThreads * kPx));
+    a.tiles = jobs * a.rowunits * a.nseg;
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->fmt.width % 32 == 0;
+    cudaError_t e = launch_f2t(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
+    if (e != cudaSuccess) return cuda_fail(e, "f2t kernel launch");
     return NNVISR_OK;
 }
 
@@ -502,12 +510,14 @@ T2FArgs t2f_args(const nnvisr_handle *h, int64_t t_h, int64_t t_w)
 
 nnvisr_status run_t2f(nnvisr_handle *h, T2FArgs a, int64_t jobs, cudaStream_t st)
 {
-    for (int64_t j0 = 0; j0 < jobs; j0 += kMaxGridY) {
-        a.job_base = (int32_t)j0;
-        const int n = (int)std::min<int64_t>(kMaxGridY, jobs - j0);
-        cudaError_t e = launch_t2f(h->fmt.family, h->fmt.bits, h->net.dtype, a, n, st);
-        if (e != cudaSuccess) return cuda_fail(e, "t2f kernel launch");
-    }
+    a.items = jobs * a.units;
+    const int rows = h->fmt.family == NNVISR_YUV420 ? 2 : 1;
+    a.rowunits = (int32_t)(h->Ho / rows);
+    a.nseg = (int32_t)((h->Wo + kThreads * kPx - 1) / (kThreads * kPx));
+    a.tiles = jobs * a.rowunits * a.nseg;
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wo % 32 == 0 && a.tensor_stride % 16 == 0;
+    cudaError_t e = launch_t2f(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
+    if (e != cudaSuccess) return cuda_fail(e, "t2f kernel launch");
     return NNVISR_OK;
 }
 
