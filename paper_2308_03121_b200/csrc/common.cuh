@@ -296,11 +296,12 @@ __device__ __forceinline__ void f2t_store(const F2TArgs &a, const DstList &dl, c
 
 // ------------------------------------------------------------ t2f colour
 template <typename T> struct T2FConst;
+// fp32: ys, yo, cs, co are divided by maxc (see quant)
 template <> struct T2FConst<float> {
     float kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
     __device__ explicit T2FConst(const T2FColour &c)
-        : kr(c.fkr), kb(c.fkb), db(c.fdb), dr(c.fdr), idb(c.fidb), idr(c.fidr), ys(c.fys), yo(c.fyo), cs(c.fcs),
-          co(c.fco), maxc(c.fmaxc) {}
+        : kr(c.fkr), kb(c.fkb), db(c.fdb), dr(c.fdr), idb(c.fidb), idr(c.fidr), ys(c.fys_n), yo(c.fyo_n),
+          cs(c.fcs_n), co(c.fco_n), maxc(c.fmaxc) {}
 };
 template <> struct T2FConst<double> {
     double kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
@@ -312,18 +313,20 @@ template <> struct T2FConst<double> {
 __device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
 
-// Step B4: clamp to [0, maxc] (NaN -> 0: fmax returns the non-NaN operand),
-// then round half to even by adding 1.5 * 2^(p-1): the sum lies where the
-// spacing of representable values is exactly 1, so the FP add rounds the
-// value to the nearest integer, ties to even, and the integer is the low bits.
-__device__ __forceinline__ uint32_t quant(float q, float maxc)
+// Step B4: clamp to [0, maxc] and round half to even.
+// fp32 (8/10-bit codes): q = sat(v * s/maxc + o/maxc) in [0, 1] (FFMA.SAT;
+// NaN -> 0), then one FFMA q * maxc + 1.5 * 2^23: the sum lies where the
+// spacing of floats is exactly 1, so that single rounding is RNE to an
+// integer, which sits in the low mantissa bits.  fp64 (16-bit codes): clamp,
+// then the same trick with 1.5 * 2^52.  Either way the code is the low 16 bits
+// of the returned word (the packers below take only those bits).
+__device__ __forceinline__ uint32_t quant(float v, float sn, float on, float maxc)
 {
-    const float x = fminf(fmaxf(q, 0.0f), maxc);
-    return __float_as_uint(x + 12582912.0f) - 0x4B400000u;
+    return __float_as_uint(fmaf(__saturatef(fmaf(v, sn, on)), maxc, 12582912.0f));
 }
-__device__ __forceinline__ uint32_t quant(double q, double maxc)
+__device__ __forceinline__ uint32_t quant(double v, double s, double o, double maxc)
 {
-    const double x = fmin(fmax(q, 0.0), maxc);
+    const double x = fmin(fmax(fma(v, s, o), 0.0), maxc);
     return static_cast<uint32_t>(__double2loint(x + 6755399441055744.0));
 }
 
@@ -409,9 +412,9 @@ __device__ __forceinline__ void t2f_row(const T2FConst<AR> &c, const T2FColour &
         uint32_t q[3][kPx];
 #pragma unroll
         for (int k = 0; k < kPx; ++k) {
-            q[0][k] = quant(fma_(static_cast<AR>(R[k]), c.ys, c.yo), c.maxc);
-            q[1][k] = quant(fma_(static_cast<AR>(G[k]), c.ys, c.yo), c.maxc);
-            q[2][k] = quant(fma_(static_cast<AR>(B[k]), c.ys, c.yo), c.maxc);
+            q[0][k] = quant(static_cast<AR>(R[k]), c.ys, c.yo, c.maxc);
+            q[1][k] = quant(static_cast<AR>(G[k]), c.ys, c.yo, c.maxc);
+            q[2][k] = quant(static_cast<AR>(B[k]), c.ys, c.yo, c.maxc);
         }
 #pragma unroll
         for (int p = 0; p < 3; ++p) {
@@ -429,7 +432,7 @@ __device__ __forceinline__ void t2f_row(const T2FConst<AR> &c, const T2FColour &
             const AR Y = fma_(c.kb, b_ - g_, fma_(c.kr, r_ - g_, g_));
             BY[k] = b_ - Y;
             RY[k] = r_ - Y;
-            qy[k] = quant(fma_(Y, c.ys, c.yo), c.maxc);
+            qy[k] = quant(Y, c.ys, c.yo, c.maxc);
         }
         OS *out = row_ptr_w<OS>(f, 0, y) + x0;
         if (vec_store) store_samples8(out, qy);
@@ -438,8 +441,8 @@ __device__ __forceinline__ void t2f_row(const T2FConst<AR> &c, const T2FColour &
             uint32_t qb[kPx], qr[kPx];
 #pragma unroll
             for (int k = 0; k < kPx; ++k) {
-                qb[k] = quant(fma_(divide(BY[k], c.db, c.idb), c.cs, c.co), c.maxc);
-                qr[k] = quant(fma_(divide(RY[k], c.dr, c.idr), c.cs, c.co), c.maxc);
+                qb[k] = quant(divide(BY[k], c.db, c.idb), c.cs, c.co, c.maxc);
+                qr[k] = quant(divide(RY[k], c.dr, c.idr), c.cs, c.co, c.maxc);
             }
             OS *ob = row_ptr_w<OS>(f, 1, y) + x0, *orr = row_ptr_w<OS>(f, 2, y) + x0;
             if (vec_store) {
@@ -472,8 +475,8 @@ __device__ __forceinline__ void t2f_chroma420(const T2FConst<AR> &c, const DevFr
     uint32_t qb[4], qr[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        qb[m] = quant(fma_(divide(sb[m], db4, idb4), c.cs, c.co), c.maxc);
-        qr[m] = quant(fma_(divide(sr[m], dr4, idr4), c.cs, c.co), c.maxc);
+        qb[m] = quant(divide(sb[m], db4, idb4), c.cs, c.co, c.maxc);
+        qr[m] = quant(divide(sr[m], dr4, idr4), c.cs, c.co, c.maxc);
     }
     OS *ob = row_ptr_w<OS>(f, 1, y0 >> 1) + (x0 >> 1), *orr = row_ptr_w<OS>(f, 2, y0 >> 1) + (x0 >> 1);
     if (vec_store) {

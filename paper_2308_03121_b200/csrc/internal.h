@@ -40,7 +40,7 @@ struct F2TColour {
 //   ties stay exact);  chroma code = rne(clamp(P * cs + co, 0, maxc)).
 struct T2FColour {
     double kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
-    float fkr, fkb, fdb, fdr, fidb, fidr, fys, fyo, fcs, fco, fmaxc;
+    float fkr, fkb, fdb, fdr, fidb, fidr, fys_n, fyo_n, fcs_n, fco_n, fmaxc;  // *_n = / maxc
 };
 
 // frames -> tensor work list of one launch: job j converts the distinct frame

@@ -62,18 +62,33 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// shared -> global bulk store (TMA engine), tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 constexpr int kSegW = kThreads * kPx;  // columns per tile segment (2048)
 constexpr int kBarBytes = 128;         // mbarrier block at the start of dynamic smem
 
+// CTA b takes tiles b, b + G, b + 2G, ... (G = grid size): every CTA gets the
+// same mix of frames, whatever each frame's number of destinations.
 struct TileCursor {
-    int64_t t, end;
+    int64_t count;  // tiles of this CTA
     __device__ __forceinline__ void init(int64_t tiles)
     {
-        t = tiles * blockIdx.x / gridDim.x;
-        end = tiles * (blockIdx.x + 1) / gridDim.x;
+        count = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    }
+    __device__ __forceinline__ int64_t tile(int64_t i) const
+    {
+        return blockIdx.x + i * static_cast<int64_t>(gridDim.x);
     }
 };
 
@@ -160,7 +175,7 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
 }
 
 template <int FAMILY, typename IN, typename OUT>
-__global__ void __launch_bounds__(kThreads) f2t_tma(const F2TArgs a)
+__global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
 {
     using S = F2TStage<FAMILY, IN>;
     using V8 = typename Pack<IN>::V8;
@@ -173,26 +188,32 @@ __global__ void __launch_bounds__(kThreads) f2t_tma(const F2TArgs a)
 
     TileCursor tc;
     tc.init(a.tiles);
-    if (tc.t >= tc.end) return;
+    if (tc.count == 0) return;
     if (threadIdx.x == 0) {
         for (int k = 0; k < nst; ++k) mbar_init(&bars[k], 1);
         fence_barrier_init();
     }
     __syncthreads();
     if (threadIdx.x == 0)
-        for (int k = 0; k < nst && tc.t + k < tc.end; ++k)
-            f2t_issue<FAMILY, IN>(a, tc.t + k, stages + k * a.stage_bytes, &bars[k]);
+        for (int k = 0; k < nst && k < tc.count; ++k)
+            f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &bars[k]);
 
     int cj = -1;
     DstList dl;
     int k = 0;
     uint32_t phase = 0;
-    for (int64_t t = tc.t; t < tc.end; ++t) {
+    int ob_sel = 0;
+    OUT *obuf = reinterpret_cast<OUT *>(stages + nst * a.stage_bytes);
+    constexpr int kOutElems = ROWS * 3 * kSegW;
+    for (int64_t i = 0; i < tc.count; ++i) {
+        const int64_t t = tc.tile(i);
         int job, ru, x0;
         decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
         const int x1 = min(x0 + kSegW, a.Wp);
+        const int sw = x1 - x0;
         const int y0 = ru * ROWS;
         const int x = x0 + kPx * threadIdx.x;
+        OUT *ob = obuf + ob_sel * kOutElems;
         if (job != cj) {
             cj = job;
             dl.load(a, job);
@@ -270,18 +291,46 @@ __global__ void __launch_bounds__(kThreads) f2t_tma(const F2TArgs a)
                 }
                 f2t_row<FAMILY, OUT>(a.col, ys, us, vs, out[r]);
             }
-            f2t_store<ROWS, OUT>(a, dl, out, x, y0);
+            // stage the converted rows in this tile's output buffer,
+            // layout [channel][row][sw] (rows of a channel adjacent)
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) out[r][c].store(ob + (c * ROWS + r) * sw + (x - x0));
         }
-        __syncthreads();  // every thread is done reading stage k
-        if (threadIdx.x == 0 && t + nst < tc.end) {
-            fence_proxy_async();
-            f2t_issue<FAMILY, IN>(a, t + nst, st, &bars[k]);
+        fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
+        if (threadIdx.x == 0) bulk_wait_read_all();  // the other output buffer is free again
+        __syncthreads();      // stage k fully read, output buffer complete
+        if (threadIdx.x == 0) {
+            if (i + nst < tc.count) f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), st, &bars[k]);
+            // fan the tile out to every (run, slot) holding this frame
+            const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
+            const bool whole_rows = x0 == 0 && sw == a.Wp;
+            for (int d = 0; d < dl.nd; ++d) {
+                const int cd = dl.get(a, d);
+                OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
+                                                 static_cast<int64_t>(cd & 31) * a.slot_bytes) +
+                         static_cast<int64_t>(y0) * a.Wp + x0;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (whole_rows) {
+                        bulk_s2g(o + c * plane, ob + c * ROWS * sw, ROWS * sw * sizeof(OUT));
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < ROWS; ++r)
+                            bulk_s2g(o + c * plane + r * a.Wp, ob + (c * ROWS + r) * sw, sw * sizeof(OUT));
+                    }
+                }
+            }
+            bulk_commit();
         }
+        ob_sel ^= 1;
         if (++k == nst) {
             k = 0;
             phase ^= 1;
         }
     }
+    if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------ t2f
@@ -312,7 +361,7 @@ __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *
 }
 
 template <int FAMILY, typename OS, typename TIN, typename AR>
-__global__ void __launch_bounds__(kThreads) t2f_tma(const T2FArgs a)
+__global__ void __launch_bounds__(kThreads, sizeof(AR) == 4 ? 3 : 2) t2f_tma(const T2FArgs a)
 {
     using S = T2FStage<FAMILY, TIN>;
     constexpr int ROWS = S::ROWS;
@@ -323,22 +372,23 @@ __global__ void __launch_bounds__(kThreads) t2f_tma(const T2FArgs a)
 
     TileCursor tc;
     tc.init(a.tiles);
-    if (tc.t >= tc.end) return;
+    if (tc.count == 0) return;
     if (threadIdx.x == 0) {
         for (int k = 0; k < nst; ++k) mbar_init(&bars[k], 1);
         fence_barrier_init();
     }
     __syncthreads();
     if (threadIdx.x == 0)
-        for (int k = 0; k < nst && tc.t + k < tc.end; ++k)
-            t2f_issue<FAMILY, TIN>(a, tc.t + k, stages + k * a.stage_bytes, &bars[k]);
+        for (int k = 0; k < nst && k < tc.count; ++k)
+            t2f_issue<FAMILY, TIN>(a, tc.tile(k), stages + k * a.stage_bytes, &bars[k]);
 
     const T2FConst<AR> c(a.col);
     int cj = -1;
     DevFrame f;
     int k = 0;
     uint32_t phase = 0;
-    for (int64_t t = tc.t; t < tc.end; ++t) {
+    for (int64_t i = 0; i < tc.count; ++i) {
+        const int64_t t = tc.tile(i);
         int job, ru, x0;
         decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
         const int x1 = min(x0 + kSegW, a.Wo);
@@ -364,9 +414,9 @@ __global__ void __launch_bounds__(kThreads) t2f_tma(const T2FArgs a)
             if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, y0, sb, sr, kPx, a.vec_out);
         }
         __syncthreads();  // every thread is done reading stage k
-        if (threadIdx.x == 0 && t + nst < tc.end) {
+        if (threadIdx.x == 0 && i + nst < tc.count) {
             fence_proxy_async();
-            t2f_issue<FAMILY, TIN>(a, t + nst, st, &bars[k]);
+            t2f_issue<FAMILY, TIN>(a, tc.tile(i + nst), st, &bars[k]);
         }
         if (++k == nst) {
             k = 0;
@@ -387,14 +437,15 @@ int sms()
     return n;
 }
 
-// Stages per CTA: as many as fit in ~100 KB (2..4), so two CTAs share an SM.
+// Dynamic smem = mbarriers | `stages` input stages | `extra` bytes (f2t: two
+// output staging buffers).  Stages: as many as fit in `budget` (2..4).
 template <typename K, typename A>
-cudaError_t launch_tma(K kernel, A a, int stage_bytes, cudaStream_t s)
+cudaError_t launch_tma(K kernel, A a, int stage_bytes, int extra, int budget, cudaStream_t s)
 {
     if (a.tiles <= 0) return cudaSuccess;
     a.stage_bytes = (stage_bytes + 127) / 128 * 128;
-    a.stages = std::max(2, std::min(4, (100 * 1024) / a.stage_bytes));
-    const int smem = kBarBytes + a.stages * a.stage_bytes;
+    a.stages = std::max(2, std::min(4, (budget - extra) / a.stage_bytes));
+    const int smem = kBarBytes + a.stages * a.stage_bytes + extra;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -406,17 +457,23 @@ cudaError_t launch_tma(K kernel, A a, int stage_bytes, cudaStream_t s)
     return cudaGetLastError();
 }
 
+template <int FAMILY, typename IN, typename OUT>
+cudaError_t f2t_tma_launch(const F2TArgs &a, cudaStream_t s)
+{
+    constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
+    constexpr int out_bytes = 2 * ROWS * 3 * kSegW * sizeof(OUT);
+    return launch_tma(f2t_tma<FAMILY, IN, OUT>, a, F2TStage<FAMILY, IN>::BYTES, out_bytes, 110 * 1024, s);
+}
+
 template <int FAMILY>
 cudaError_t f2t_tma_dispatch(int bits, int dtype, const F2TArgs &a, cudaStream_t s)
 {
     if (bits == 8) {
-        constexpr int B = F2TStage<FAMILY, uint8_t>::BYTES;
-        if (dtype == kF16) return launch_tma(f2t_tma<FAMILY, uint8_t, __half>, a, B, s);
-        return launch_tma(f2t_tma<FAMILY, uint8_t, float>, a, B, s);
+        if (dtype == kF16) return f2t_tma_launch<FAMILY, uint8_t, __half>(a, s);
+        return f2t_tma_launch<FAMILY, uint8_t, float>(a, s);
     }
-    constexpr int B = F2TStage<FAMILY, uint16_t>::BYTES;
-    if (dtype == kF16) return launch_tma(f2t_tma<FAMILY, uint16_t, __half>, a, B, s);
-    return launch_tma(f2t_tma<FAMILY, uint16_t, float>, a, B, s);
+    if (dtype == kF16) return f2t_tma_launch<FAMILY, uint16_t, __half>(a, s);
+    return f2t_tma_launch<FAMILY, uint16_t, float>(a, s);
 }
 
 template <int FAMILY>
@@ -424,15 +481,15 @@ cudaError_t t2f_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t
 {
     constexpr int BH = T2FStage<FAMILY, __half>::BYTES, BF = T2FStage<FAMILY, float>::BYTES;
     if (bits == 8) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, BH, s);
-        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, BF, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, BH, 0, 72 * 1024, s);
+        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, BF, 0, 72 * 1024, s);
     }
     if (bits == 10) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, BH, s);
-        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, BF, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, BH, 0, 72 * 1024, s);
+        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, BF, 0, 72 * 1024, s);
     }
-    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, BH, s);
-    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, BF, s);
+    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, BH, 0, 110 * 1024, s);
+    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, BF, 0, 110 * 1024, s);
 }
 
 }  // namespace

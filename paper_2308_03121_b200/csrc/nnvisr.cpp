@@ -254,7 +254,8 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
     c.maxc = full;
     c.fkr = (float)c.kr; c.fkb = (float)c.kb; c.fdb = (float)c.db; c.fdr = (float)c.dr;
     c.fidb = 1.0f / c.fdb; c.fidr = 1.0f / c.fdr;
-    c.fys = (float)c.ys; c.fyo = (float)c.yo; c.fcs = (float)c.cs; c.fco = (float)c.co; c.fmaxc = (float)full;
+    c.fys_n = (float)(c.ys / full); c.fyo_n = (float)(c.yo / full); c.fcs_n = (float)(c.cs / full);
+    c.fco_n = (float)(c.co / full); c.fmaxc = (float)full;
     *out = h;
     return NNVISR_OK;
 }

@@ -1,0 +1,134 @@
+// hbm_probe.cu -- HBM bandwidth of simple streaming kernels with different
+// read:write mixes on this GPU (128-bit loads/stores, grid = 4 x 148 x 256).
+// Context for the f2t (write-heavy, ~1:6) and t2f (read-heavy, ~2:1) rooflines.
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/hbm_probe.cu -o /tmp/hbm_probe
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void mix(const uint4 *__restrict__ in, uint4 *__restrict__ out, long n_in, int wmul, long n_out)
+{
+    // each thread reads in[i] (if i < n_in) and writes it to wmul destinations
+    const long stride = (long)gridDim.x * blockDim.x;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n_out / wmul; i += stride) {
+        uint4 v = i < n_in ? in[i] : make_uint4(i, i, i, i);
+        for (int k = 0; k < wmul; ++k) out[(long)k * (n_out / wmul) + i] = v;
+    }
+}
+
+__global__ void r2w1(const uint4 *__restrict__ in, uint4 *__restrict__ out, long m)
+{
+    const long stride = (long)gridDim.x * blockDim.x;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        uint4 x = in[i], y = in[i + m];
+        out[i] = make_uint4(x.x ^ y.x, x.y ^ y.y, x.z ^ y.z, x.w ^ y.w);
+    }
+}
+
+// 1 read : W writes, each CTA-iteration loads a 64 KB chunk into registers
+// and writes it to the W destinations one after another (64 KB contiguous each)
+template <int W>
+__global__ void fanout_chunked(const uint4 *__restrict__ in, uint4 *__restrict__ out, long m)
+{
+    constexpr int U = 16;
+    const long chunk = (long)blockDim.x * U;
+    for (long base = (long)blockIdx.x * chunk; base < m; base += (long)gridDim.x * chunk) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long i = base + u * blockDim.x + threadIdx.x;
+            v[u] = i < m ? in[i] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long i = base + u * blockDim.x + threadIdx.x;
+                if (i < m) out[(long)k * m + i] = v[u];
+            }
+    }
+}
+
+// same, but the CTA stages the chunk in shared memory and one thread writes it
+// to the W destinations with TMA bulk stores (cp.async.bulk.global.shared::cta)
+template <int W>
+__global__ void fanout_tma(const uint4 *__restrict__ in, uint4 *__restrict__ out, long m)
+{
+    extern __shared__ __align__(128) uint4 sm[];
+    constexpr int U = 16;
+    const long chunk = (long)blockDim.x * U;
+    for (long base = (long)blockIdx.x * chunk; base < m; base += (long)gridDim.x * chunk) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long i = base + u * blockDim.x + threadIdx.x;
+            sm[u * blockDim.x + threadIdx.x] = i < m ? in[i] : make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const long n = min(chunk, m - base);
+            for (int k = 0; k < W; ++k) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + (long)k * m + base),
+                             "r"((unsigned)__cvta_generic_to_shared(sm)), "r"((unsigned)(n * 16))
+                             : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__global__ void readonly(const uint4 *__restrict__ in, long n, unsigned *sink)
+{
+    const long stride = (long)gridDim.x * blockDim.x;
+    unsigned acc = 0;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        uint4 v = in[i];
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x12345678u) *sink = acc;
+}
+
+int main()
+{
+    const long bytes = 4l << 30;
+    const long n = bytes / 16;
+    uint4 *a, *b;
+    unsigned *sink;
+    cudaMalloc(&a, bytes);
+    cudaMalloc(&b, bytes);
+    cudaMalloc(&sink, 4);
+    cudaMemset(a, 1, bytes);
+    cudaEvent_t s, e;
+    cudaEventCreate(&s);
+    cudaEventCreate(&e);
+    const int grid = 4 * 148, block = 256;
+    auto run = [&](const char *name, auto fn, double moved) {
+        for (int i = 0; i < 3; ++i) fn();
+        float best = 1e9;
+        for (int r = 0; r < 10; ++r) {
+            cudaEventRecord(s);
+            fn();
+            cudaEventRecord(e);
+            cudaEventSynchronize(e);
+            float ms;
+            cudaEventElapsedTime(&ms, s, e);
+            if (ms < best) best = ms;
+        }
+        printf("{\"probe\": \"%s\", \"gbs\": %.1f}\n", name, moved / (best / 1000) / 1e9);
+    };
+    run("read_only", [&] { readonly<<<grid, block>>>(a, n, sink); }, (double)bytes);
+    run("write_only", [&] { mix<<<grid, block>>>(a, b, 0, 1, n); }, (double)bytes);
+    run("copy_1r_1w", [&] { mix<<<grid, block>>>(a, b, n, 1, n); }, 2.0 * bytes);
+    run("1r_2w", [&] { mix<<<grid, block>>>(a, b, n / 2, 2, n); }, 1.5 * bytes);
+    run("1r_6w", [&] { mix<<<grid, block>>>(a, b, n / 6, 6, n / 6 * 6); }, (double)bytes * 7 / 6);
+    run("2r_1w", [&] { r2w1<<<grid, block>>>(a, b, n / 2); }, 1.5 * bytes);
+    run("1r_6w_chunked", [&] { fanout_chunked<6><<<grid, block>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    cudaFuncSetAttribute(fanout_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    run("1r_6w_tma", [&] { fanout_tma<6><<<2 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    run("1r_6w_tma_3cta", [&] { fanout_tma<6><<<3 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
+    return 0;
+}
