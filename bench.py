@@ -157,9 +157,12 @@ def oracle_sample(w, count: int, threads: int):
     return count / dt_s, dt_s, threads
 
 
-def default_cpu_sample(w):
+def default_cpu_sample(w, cores=None):
+    """Tuples in the oracle sample: ~4 per host thread at 1080p (10-30 s of
+    CPU work on the GPU box), scaled by frame area."""
+    cores = cores or os.cpu_count() or 1
     px = w.cfg.width * w.cfg.height
-    return max(2, min(16, int(8 * (1920 * 1080) / px))) if px > 1e5 else 64
+    return int(max(2, min(256, round(4 * cores * (1920 * 1080) / px))))
 
 
 def run_reference(args):
@@ -246,69 +249,70 @@ def main():
     Ho, Wo = out_shape[2], out_shape[3]
     olay = w.out_layout()
     t2f_bytes = out_elems * esz + M * olay.payload_bytes()
-    chunk = args.chunk or max(1, min(64, int(2.5e9 // max(t2f_bytes, in_elems * esz))))
-    n_in = chunk
-    n_out = max(chunk, -(-4 * l2 // (out_elems * esz)))
-    tens_in = torch.empty((n_in, in_elems), dtype=tdt, device=dev)
+    frame_payload = lay.payload_bytes()
+    slot_bytes = 3 * in_shape[2] * in_shape[3] * esz
+    # tuples per launch: ~3 GB of algorithmic traffic per f2t launch, ~4 GB per
+    # t2f launch (launch ramp/tail < 2%); rings sized so nothing is re-read from L2
+    fchunk = args.chunk or max(1, min(64, int(3e9 // (frame_payload + in_elems * esz))))
+    tchunk = args.chunk or max(1, min(64, int(4e9 // t2f_bytes)))
+    n_out = max(tchunk, -(-4 * l2 // (out_elems * esz)))
+    tens_in = torch.empty((fchunk, in_elems), dtype=tdt, device=dev)
     tens_out = synth.random_tensor((n_out, out_elems), cfg.dtype, w.seed + 99, device=dev)
-    ofb = FrameBuffer(olay, chunk * M, device=dev)
+    ofb = FrameBuffer(olay, tchunk * M, device=dev)
     ofb_desc = ofb.descriptors()
     store = None
     if args.f2t_mode == "store":
-        store = torch.empty((s.window_count, 3 * in_shape[2] * in_shape[3]), dtype=tdt, device=dev)
+        store = torch.empty((s.window_count, slot_bytes // esz), dtype=tdt, device=dev)
     stream = torch.cuda.Stream(device=dev)
-    frame_payload = lay.payload_bytes()
 
     def plan_local():
         cw = cut_win.cpu().numpy()
         return h.plan_range(total, s.window_first, cw, s.begin, s.end)
 
+    # per launch: (start event, end event, units, algorithmic bytes)
     ev_pairs = {"f2t": [], "t2f": []}
+
+    def timed(kind, record, units, nbytes, fn):
+        if not record:
+            fn()
+            return
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        ev_pairs[kind].append((a, b, units, nbytes))
 
     def step(record: bool):
         if world > 1:
             with torch.cuda.stream(stream):
                 sh.halo_exchange(s, win.data, cut_win)
         runs, _ = plan_local()
-        if args.f2t_mode == "store":
-            with torch.cuda.stream(stream):
-                a = torch.cuda.Event(enable_timing=True) if record else None
-                if a:
-                    a.record(stream)
-                h.frames_to_store(s.window_first, s.window_count, store.data_ptr(), stream)
+        with torch.cuda.stream(stream):
+            if args.f2t_mode == "store":
+                # each window frame converted once into the frame-major store;
+                # tuples with consecutive indices are windows of it, the ones
+                # with duplicated indices (scene edges) are materialised
+                timed("f2t", record, s.owned, s.window_count * (frame_payload + slot_bytes),
+                      lambda: h.frames_to_store(s.window_first, s.window_count, store.data_ptr(), stream))
                 dup = [r for r in range(len(runs)) if np.any(np.diff(runs[r]) != 1)]
-                for c0 in range(0, len(dup), chunk):
-                    sel = runs[dup[c0:c0 + chunk]]
-                    h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream)
-                if a:
-                    b = torch.cuda.Event(enable_timing=True)
-                    b.record(stream)
-                    ev_pairs["f2t"].append((a, b, s.window_count, None))
-        for c0 in range(0, len(runs), chunk):
-            sel = runs[c0:c0 + chunk]
-            nb = len(sel)
-            with torch.cuda.stream(stream):
-                if args.f2t_mode == "materialize":
-                    a = torch.cuda.Event(enable_timing=True) if record else None
-                    if a:
-                        a.record(stream)
-                    h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream)
-                    if a:
-                        b = torch.cuda.Event(enable_timing=True)
-                        b.record(stream)
-                        ev_pairs["f2t"].append((a, b, nb, len(np.unique(sel))))
-                a = torch.cuda.Event(enable_timing=True) if record else None
-                if a:
-                    a.record(stream)
-                o0 = (c0 // chunk * chunk) % n_out
+                for c0 in range(0, len(dup), fchunk):
+                    sel = runs[dup[c0:c0 + fchunk]]
+                    timed("f2t", record, 0, len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz,
+                          lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
+            else:
+                for c0 in range(0, len(runs), fchunk):
+                    sel = runs[c0:c0 + fchunk]
+                    timed("f2t", record, len(sel), len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz,
+                          lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
+            for c0 in range(0, len(runs), tchunk):
+                nb = min(tchunk, len(runs) - c0)
+                o0 = (c0 // tchunk * tchunk) % n_out
                 if o0 + nb > n_out:
                     o0 = 0
-                h.tensor_to_frames_batch(tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo, ofb_desc[:nb * M], nb,
-                                         stream)
-                if a:
-                    b = torch.cuda.Event(enable_timing=True)
-                    b.record(stream)
-                    ev_pairs["t2f"].append((a, b, nb, None))
+                timed("t2f", record, nb, nb * t2f_bytes,
+                      lambda o0=o0, nb=nb: h.tensor_to_frames_batch(tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo,
+                                                                    ofb_desc[:nb * M], nb, stream))
         return len(runs)
 
     def barrier():
@@ -345,20 +349,14 @@ def main():
         frames_all = total
     value = frames_all * args.steps / (ms_total / 1000.0)
 
-    # per-kernel durations and algorithmic bytes
+    # per-kernel durations and algorithmic bytes (DESIGN.md §6)
     def kstats(kind):
         ev = ev_pairs[kind]
         if not ev:
             return None
         durs = np.array([a.elapsed_time(b) for a, b, _, _ in ev]) / 1000.0
         units = np.array([u for _, _, u, _ in ev], dtype=np.float64)
-        if kind == "f2t" and args.f2t_mode == "materialize":
-            uniq = np.array([q for _, _, _, q in ev], dtype=np.float64)
-            bytes_ = uniq * frame_payload + units * in_elems * esz
-        elif kind == "f2t":
-            bytes_ = units * (frame_payload + 3 * in_shape[2] * in_shape[3] * esz)
-        else:
-            bytes_ = units * t2f_bytes
+        bytes_ = np.array([q for _, _, _, q in ev], dtype=np.float64)
         return {"launches": len(ev), "seconds": float(durs.sum()), "units": float(units.sum()),
                 "bytes": float(bytes_.sum()), "avg_launch_s": float(durs.mean()),
                 "avg_launch_bytes": float(bytes_.mean())}
@@ -384,8 +382,8 @@ def main():
     # ---- e2e: host (pinned) frames in, host frames out, through the C ABI
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, in_elems, out_elems, esz,
-                      stream, dev, world, plan_local, scaling, frames_all)
+        e2e = run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, min(8, fchunk, tchunk), in_elems,
+                      out_elems, esz, stream, dev, world, plan_local, scaling, frames_all)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -403,7 +401,7 @@ def main():
             "config": {"workload": args.workload, "description": w.description, "frames_per_step": frames_all,
                        "clip_frames_per_rank": s.owned, "input_tensor": list(in_shape),
                        "output_tensor": list(out_shape), "tensor_dtype": "f16" if cfg.dtype == nv.F16 else "f32",
-                       "tuples_per_launch": chunk, "f2t_mode": args.f2t_mode,
+                       "tuples_per_launch": {"f2t": fchunk, "t2f": tchunk}, "f2t_mode": args.f2t_mode,
                        "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB, t2f input ring "
                                     f"{n_out} x {out_elems * esz / 1e6:.0f} MB >= 4 x L2 ({l2 / 1e6:.0f} MB)",
                        "parallelism": f"frame-range shards x{world}, halo P2P"},

@@ -62,6 +62,7 @@ struct F2TArgs {
     int32_t vec_out;          // 1: tensor rows allow 16-byte stores
     // TMA-pipelined path (kernels_tma.cu): tiles = jobs * rowunits * nseg
     int32_t tma_ok, rowunits, nseg, stages, stage_bytes;
+    int32_t lcap, nob, ob_elems;  // staged row capacity, output buffers, elements per buffer
     int64_t tiles;
     F2TColour col;
 };

@@ -19,6 +19,7 @@
 // are clamped to the plane and 16-byte aligned.  The host enables this path
 // only when every window is 16-byte aligned (see nnvisr.cpp, tma_ok).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -70,7 +71,8 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -108,16 +110,19 @@ __device__ __forceinline__ void decode_tile(int64_t t, int rowunits, int nseg, i
 // [1][LCAP].  LCAP = seg_w, CCAP = seg_w/2 + 2 * (16 / sizeof(IN)).
 template <int FAMILY, typename IN> struct F2TStage {
     static constexpr int G = 16 / sizeof(IN);  // samples per 16 bytes
-    static constexpr int LCAP = kSegW;
-    static constexpr int CCAP = kSegW / 2 + 2 * G;
     static constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
-    static constexpr int BYTES = FAMILY == kYUV420 ? (2 * LCAP + 6 * CCAP) * sizeof(IN) : 3 * LCAP * sizeof(IN);
-    __device__ static IN *luma(uint8_t *st, int r) { return reinterpret_cast<IN *>(st) + r * LCAP; }
-    __device__ static IN *chroma(uint8_t *st, int p, int q)
+    int lcap, ccap;  // samples per staged luma / chroma row (runtime: min(seg, Wp))
+    __device__ __host__ explicit F2TStage(int lc) : lcap(lc), ccap(lc / 2 + 2 * G) {}
+    __device__ __host__ int bytes() const
     {
-        return reinterpret_cast<IN *>(st) + 2 * LCAP + (p * 3 + q) * CCAP;
+        return FAMILY == kYUV420 ? (2 * lcap + 6 * ccap) * (int)sizeof(IN) : 3 * lcap * (int)sizeof(IN);
     }
-    __device__ static IN *plane(uint8_t *st, int p) { return reinterpret_cast<IN *>(st) + p * LCAP; }
+    __device__ IN *luma(uint8_t *st, int r) const { return reinterpret_cast<IN *>(st) + r * lcap; }
+    __device__ IN *chroma(uint8_t *st, int p, int q) const
+    {
+        return reinterpret_cast<IN *>(st) + 2 * lcap + (p * 3 + q) * ccap;
+    }
+    __device__ IN *plane(uint8_t *st, int p) const { return reinterpret_cast<IN *>(st) + p * lcap; }
 };
 
 // Copy windows of a segment [x0, x1): luma [lw0, lw1), chroma [cw0, cw1).
@@ -146,6 +151,7 @@ template <int FAMILY, typename IN>
 __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *st, uint64_t *bar)
 {
     using S = F2TStage<FAMILY, IN>;
+    const S sg(a.lcap);
     int job, ru, x0;
     decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
     const int x1 = min(x0 + kSegW, a.Wp);
@@ -158,19 +164,19 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
         const uint32_t cbytes = (w.cw1 - w.cw0) * sizeof(IN);
         mbar_arrive_expect_tx(bar, 2 * lbytes + 6 * cbytes);
         const int yc0 = min(y0, a.H - 1), yc1 = min(y0 + 1, a.H - 1), ch = a.H >> 1;
-        bulk_g2s(S::luma(st, 0), row_ptr<IN>(f, 0, yc0) + w.lw0, lbytes, bar);
-        bulk_g2s(S::luma(st, 1), row_ptr<IN>(f, 0, yc1) + w.lw0, lbytes, bar);
+        bulk_g2s(sg.luma(st, 0), row_ptr<IN>(f, 0, yc0) + w.lw0, lbytes, bar);
+        bulk_g2s(sg.luma(st, 1), row_ptr<IN>(f, 0, yc1) + w.lw0, lbytes, bar);
         const int rows[3] = {chroma_near(yc0), chroma_far(yc0, ch), chroma_far(yc1, ch)};
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
             for (int q = 0; q < 3; ++q)
-                bulk_g2s(S::chroma(st, p, q), row_ptr<IN>(f, p + 1, rows[q]) + w.cw0, cbytes, bar);
+                bulk_g2s(sg.chroma(st, p, q), row_ptr<IN>(f, p + 1, rows[q]) + w.cw0, cbytes, bar);
     } else {
         mbar_arrive_expect_tx(bar, 3 * lbytes);
         const int yc = min(y0, a.H - 1);
 #pragma unroll
-        for (int p = 0; p < 3; ++p) bulk_g2s(S::plane(st, p), row_ptr<IN>(f, p, yc) + w.lw0, lbytes, bar);
+        for (int p = 0; p < 3; ++p) bulk_g2s(sg.plane(st, p), row_ptr<IN>(f, p, yc) + w.lw0, lbytes, bar);
     }
 }
 
@@ -202,9 +208,10 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
     DstList dl;
     int k = 0;
     uint32_t phase = 0;
+    const S sg(a.lcap);
     int ob_sel = 0;
     OUT *obuf = reinterpret_cast<OUT *>(stages + nst * a.stage_bytes);
-    constexpr int kOutElems = ROWS * 3 * kSegW;
+    const int nob = a.nob;  // output buffers (2 or 3)
     for (int64_t i = 0; i < tc.count; ++i) {
         const int64_t t = tc.tile(i);
         int job, ru, x0;
@@ -213,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
         const int sw = x1 - x0;
         const int y0 = ru * ROWS;
         const int x = x0 + kPx * threadIdx.x;
-        OUT *ob = obuf + ob_sel * kOutElems;
+        OUT *ob = obuf + ob_sel * a.ob_elems;
         if (job != cj) {
             cj = job;
             dl.load(a, job);
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
             for (int r = 0; r < ROWS; ++r) {
                 int ys[kPx], us[kPx], vs[kPx];
                 if constexpr (FAMILY == kYUV420) {
-                    const IN *L = S::luma(st, r);
+                    const IN *L = sg.luma(st, r);
                     const int cw = a.W >> 1;
                     if (fast) {
                         unpack8(*reinterpret_cast<const V8 *>(L + (x - w.lw0)), ys);
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
                             int h[2][kPx];
 #pragma unroll
                             for (int q = 0; q < 2; ++q) {
-                                const IN *C = S::chroma(st, p, q == 0 ? 0 : 1 + r) - w.cw0;
+                                const IN *C = sg.chroma(st, p, q == 0 ? 0 : 1 + r) - w.cw0;
                                 int c[6];
                                 unpack4(*reinterpret_cast<const V4 *>(C + i0), &c[1]);
                                 c[0] = C[max(i0 - 1, 0)];
@@ -258,8 +265,8 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
                             const int xc = min(x + kk, a.W - 1);
                             ys[kk] = L[xc - w.lw0];
                             const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
-                            const IN *Un = S::chroma(st, 0, 0) - w.cw0, *Uf = S::chroma(st, 0, 1 + r) - w.cw0;
-                            const IN *Vn = S::chroma(st, 1, 0) - w.cw0, *Vf = S::chroma(st, 1, 1 + r) - w.cw0;
+                            const IN *Un = sg.chroma(st, 0, 0) - w.cw0, *Uf = sg.chroma(st, 0, 1 + r) - w.cw0;
+                            const IN *Vn = sg.chroma(st, 1, 0) - w.cw0, *Vf = sg.chroma(st, 1, 1 + r) - w.cw0;
                             us[kk] = 9 * Un[in_] + 3 * Un[if_] + 3 * Uf[in_] + Uf[if_];
                             vs[kk] = 9 * Vn[in_] + 3 * Vn[if_] + 3 * Vf[in_] + Vf[if_];
                         }
@@ -267,8 +274,8 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
 #pragma unroll
                     for (int kk = 0; kk < kPx; ++kk) ys[kk] *= 16;
                 } else {
-                    const IN *P0 = S::plane(st, 0) - w.lw0, *P1 = S::plane(st, 1) - w.lw0,
-                             *P2 = S::plane(st, 2) - w.lw0;
+                    const IN *P0 = sg.plane(st, 0) - w.lw0, *P1 = sg.plane(st, 1) - w.lw0,
+                             *P2 = sg.plane(st, 2) - w.lw0;
                     if (fast) {
                         unpack8(*reinterpret_cast<const V8 *>(P0 + x), ys);
                         unpack8(*reinterpret_cast<const V8 *>(P1 + x), us);
@@ -299,7 +306,11 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
                 for (int c = 0; c < 3; ++c) out[r][c].store(ob + (c * ROWS + r) * sw + (x - x0));
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
-        if (threadIdx.x == 0) bulk_wait_read_all();  // the other output buffer is free again
+        // the buffer of tile t+1 (used by tile t+1-nob) must have been read
+        if (threadIdx.x == 0) {
+            if (nob >= 3) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+        }
         __syncthreads();      // stage k fully read, output buffer complete
         if (threadIdx.x == 0) {
             if (i + nst < tc.count) f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), st, &bars[k]);
@@ -324,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
             }
             bulk_commit();
         }
-        ob_sel ^= 1;
+        if (++ob_sel == nob) ob_sel = 0;
         if (++k == nst) {
             k = 0;
             phase ^= 1;
@@ -457,12 +468,43 @@ cudaError_t launch_tma(K kernel, A a, int stage_bytes, int extra, int budget, cu
     return cudaGetLastError();
 }
 
-template <int FAMILY, typename IN, typename OUT>
-cudaError_t f2t_tma_launch(const F2TArgs &a, cudaStream_t s)
+int env_int(const char *name, int dflt)
 {
-    constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
-    constexpr int out_bytes = 2 * ROWS * 3 * kSegW * sizeof(OUT);
-    return launch_tma(f2t_tma<FAMILY, IN, OUT>, a, F2TStage<FAMILY, IN>::BYTES, out_bytes, 110 * 1024, s);
+    const char *v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
+// f2t smem: mbarriers | stages x input stage | nob x output buffer.  Sized at
+// run time from the segment width min(2048, Wp), to keep two CTAs per SM
+// (<= 112 KB each) with 3 output buffers where they fit (more bulk stores in
+// flight), else 2.
+template <int FAMILY, typename IN, typename OUT>
+cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
+{
+    using S = F2TStage<FAMILY, IN>;
+    constexpr int ROWS = S::ROWS;
+    if (a.tiles <= 0) return cudaSuccess;
+    const int segw = std::min(kSegW, (a.Wp + 31) / 32 * 32);
+    a.lcap = (segw + S::G - 1) / S::G * S::G;
+    a.stage_bytes = (S(a.lcap).bytes() + 127) / 128 * 128;
+    a.ob_elems = (ROWS * 3 * segw * (int)sizeof(OUT) + 127) / 128 * 128 / (int)sizeof(OUT);
+    const int ob_bytes = a.ob_elems * (int)sizeof(OUT);
+    const int budget = env_int("NNVISR_F2T_SMEM_KB", 112) * 1024 - kBarBytes;
+    a.nob = env_int("NNVISR_F2T_NOB", 0);
+    a.stages = env_int("NNVISR_F2T_STAGES", 0);
+    if (!a.nob) a.nob = 2 * a.stage_bytes + 3 * ob_bytes <= budget ? 3 : 2;
+    if (!a.stages) a.stages = std::max(2, std::min(4, (budget - a.nob * ob_bytes) / a.stage_bytes));
+    const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes;
+    auto kernel = f2t_tma<FAMILY, IN, OUT>;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
+    kernel<<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 template <int FAMILY>

@@ -50,11 +50,10 @@ __global__ void fanout_chunked(const uint4 *__restrict__ in, uint4 *__restrict__
 
 // same, but the CTA stages the chunk in shared memory and one thread writes it
 // to the W destinations with TMA bulk stores (cp.async.bulk.global.shared::cta)
-template <int W>
+template <int W, int U = 16>
 __global__ void fanout_tma(const uint4 *__restrict__ in, uint4 *__restrict__ out, long m)
 {
     extern __shared__ __align__(128) uint4 sm[];
-    constexpr int U = 16;
     const long chunk = (long)blockDim.x * U;
     for (long base = (long)blockIdx.x * chunk; base < m; base += (long)gridDim.x * chunk) {
 #pragma unroll
@@ -128,6 +127,12 @@ int main()
     cudaFuncSetAttribute(fanout_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     run("1r_6w_tma", [&] { fanout_tma<6><<<2 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
     run("1r_6w_tma_3cta", [&] { fanout_tma<6><<<3 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    cudaFuncSetAttribute(fanout_tma<6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(fanout_tma<6, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    run("1r_6w_tma_8KB_2cta", [&] { fanout_tma<6, 2><<<2 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    run("1r_6w_tma_8KB_3cta", [&] { fanout_tma<6, 2><<<3 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    run("1r_6w_tma_16KB_3cta", [&] { fanout_tma<6, 4><<<3 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    run("1r_6w_tma_8KB_6cta", [&] { fanout_tma<6, 2><<<6 * 148, block, 32 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
     return 0;
