@@ -317,17 +317,18 @@ __device__ __forceinline__ double fma_(double a, double b, double c) { return fm
 // fp32 (8/10-bit codes): q = sat(v * s/maxc + o/maxc) in [0, 1] (FFMA.SAT;
 // NaN -> 0), then one FFMA q * maxc + 1.5 * 2^23: the sum lies where the
 // spacing of floats is exactly 1, so that single rounding is RNE to an
-// integer, which sits in the low mantissa bits.  fp64 (16-bit codes): clamp,
-// then the same trick with 1.5 * 2^52.  Either way the code is the low 16 bits
-// of the returned word (the packers below take only those bits).
+// integer, which sits in the low mantissa bits (the packers below take only
+// the low 16 bits).  fp64 (16-bit codes): a saturating RNE convert to u32 and
+// an integer clamp.
 __device__ __forceinline__ uint32_t quant(float v, float sn, float on, float maxc)
 {
     return __float_as_uint(fmaf(__saturatef(fmaf(v, sn, on)), maxc, 12582912.0f));
 }
 __device__ __forceinline__ uint32_t quant(double v, double s, double o, double maxc)
 {
-    const double x = fmin(fmax(fma(v, s, o), 0.0), maxc);
-    return static_cast<uint32_t>(__double2loint(x + 6755399441055744.0));
+    // cvt.rni.u32.f64: round half to even, saturating (negative -> 0,
+    // NaN -> 0, +inf -> 2^32-1), then the integer clamp to maxc
+    return min(__double2uint_rn(fma(v, s, o)), static_cast<uint32_t>(maxc));
 }
 
 // S / d for a divisor d with precomputed reciprocal id: one FMA correction of

@@ -41,6 +41,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     asm volatile(
@@ -77,8 +81,11 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-constexpr int kSegW = kThreads * kPx;  // columns per tile segment (2048)
-constexpr int kBarBytes = 128;         // mbarrier block at the start of dynamic smem
+constexpr int kSegW = kThreads * kPx;         // columns per tile segment (2048)
+constexpr int kConsumerWarps = kThreads / 32;  // converting warps; one more warp produces
+constexpr int kMaxStages = 4;
+constexpr int kMaxOutBufs = 8;
+constexpr int kBarBytes = 8 * (2 * kMaxStages + kMaxOutBufs);  // mbarriers at the start of dynamic smem
 
 // CTA b takes tiles b, b + G, b + 2G, ... (G = grid size): every CTA gets the
 // same mix of frames, whatever each frame's number of destinations.
@@ -180,38 +187,100 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
     }
 }
 
+// Warp-specialised: warps 0..7 convert (consumers), warp 8 lane 0 is the
+// producer.  Per stage k: full[k] (TMA bytes landed), empty[k] (8 consumer
+// warps done: input stage read AND the tile's output buffer written).  Per
+// output buffer b: ofree[b] (the bulk stores that last read it are done).
+// The producer waits empty, fans the finished tile out with bulk stores,
+// refills the stage, and releases output buffers as the stores drain; no
+// consumer ever waits on a store or on a descriptor load.
 template <int FAMILY, typename IN, typename OUT>
-__global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
+__global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
 {
     using S = F2TStage<FAMILY, IN>;
     using V8 = typename Pack<IN>::V8;
     using V4 = typename Pack<IN>::V4;
     constexpr int ROWS = S::ROWS;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages, *ofree = empty + kMaxStages;
     uint8_t *stages = smem + kBarBytes;
-    const int nst = a.stages;
+    const int nst = a.stages, nob = a.nob;
+    const S sg(a.lcap);
+    OUT *obuf = reinterpret_cast<OUT *>(stages + nst * a.stage_bytes);
 
     TileCursor tc;
     tc.init(a.tiles);
     if (tc.count == 0) return;
     if (threadIdx.x == 0) {
-        for (int k = 0; k < nst; ++k) mbar_init(&bars[k], 1);
+        for (int k = 0; k < nst; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kConsumerWarps);
+        }
+        for (int b = 0; b < nob; ++b) mbar_init(&ofree[b], 1);
         fence_barrier_init();
     }
-    __syncthreads();
-    if (threadIdx.x == 0)
-        for (int k = 0; k < nst && k < tc.count; ++k)
-            f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &bars[k]);
+    __syncthreads();  // the last CTA-wide barrier: roles split below
 
-    int cj = -1;
-    DstList dl;
-    int k = 0;
-    uint32_t phase = 0;
-    const S sg(a.lcap);
-    int ob_sel = 0;
-    OUT *obuf = reinterpret_cast<OUT *>(stages + nst * a.stage_bytes);
-    const int nob = a.nob;  // output buffers (2 or 3)
+    if (threadIdx.x >= kThreads) {  // ---------------- producer warp
+        if (threadIdx.x != kThreads) return;
+        for (int k = 0; k < nst && k < tc.count; ++k)
+            f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k]);
+        int lj = -1;
+        DstList dl;
+        const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
+        for (int64_t i = 0; i < tc.count; ++i) {
+            const int k = static_cast<int>(i % nst);
+            mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
+            // fan tile i out to every (run, slot) holding its frame
+            int job, ru, x0;
+            decode_tile(tc.tile(i), a.rowunits, a.nseg, kSegW, job, ru, x0);
+            const int sw = min(x0 + kSegW, a.Wp) - x0, y0 = ru * ROWS;
+            if (job != lj) {
+                lj = job;
+                dl.load(a, job);
+            }
+            const OUT *ob = obuf + static_cast<int>(i % nob) * a.ob_elems;
+            const bool whole_rows = x0 == 0 && sw == a.Wp;
+            for (int d = 0; d < dl.nd; ++d) {
+                const int cd = dl.get(a, d);
+                OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
+                                                 static_cast<int64_t>(cd & 31) * a.slot_bytes) +
+                         static_cast<int64_t>(y0) * a.Wp + x0;
+                for (int c = 0; c < 3; ++c) {
+                    if (whole_rows) {
+                        bulk_s2g(o + c * plane, ob + c * ROWS * sw, ROWS * sw * sizeof(OUT));
+                    } else {
+                        for (int r = 0; r < ROWS; ++r)
+                            bulk_s2g(o + c * plane + r * a.Wp, ob + (c * ROWS + r) * sw, sw * sizeof(OUT));
+                    }
+                }
+            }
+            bulk_commit();
+            // refill stage k with tile i + nst
+            if (i + nst < tc.count) {
+                fence_proxy_async();
+                f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k]);
+            }
+            // buffer of tile i+2 (last read by tile i+2-nob's stores) is free
+            // once at most nob-2 store groups are still reading smem
+            if (i + 2 >= nob && i + 2 < tc.count) {
+                switch (nob) {
+                case 2: bulk_wait_read<0>(); break;
+                case 3: bulk_wait_read<1>(); break;
+                case 4: bulk_wait_read<2>(); break;
+                case 5: bulk_wait_read<3>(); break;
+                case 6: bulk_wait_read<4>(); break;
+                case 7: bulk_wait_read<5>(); break;
+                default: bulk_wait_read<6>(); break;
+                }
+                mbar_arrive(&ofree[static_cast<int>((i + 2) % nob)]);
+            }
+        }
+        bulk_wait_all();
+        return;
+    }
+
+    // ------------------------------------------------------------ consumers
     for (int64_t i = 0; i < tc.count; ++i) {
         const int64_t t = tc.tile(i);
         int job, ru, x0;
@@ -220,13 +289,12 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
         const int sw = x1 - x0;
         const int y0 = ru * ROWS;
         const int x = x0 + kPx * threadIdx.x;
-        OUT *ob = obuf + ob_sel * a.ob_elems;
-        if (job != cj) {
-            cj = job;
-            dl.load(a, job);
-        }
+        (void)y0;
+        const int k = static_cast<int>(i % nst);
         uint8_t *st = stages + k * a.stage_bytes;
-        mbar_wait(&bars[k], phase);
+        OUT *ob = obuf + static_cast<int>(i % nob) * a.ob_elems;
+        mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
+        if (i >= nob) mbar_wait(&ofree[static_cast<int>(i % nob)], static_cast<uint32_t>((i / nob - 1) & 1));
         if (x < x1) {
             F2TWindow w;
             w.set(x0, x1, a.W, S::G, FAMILY == kYUV420);
@@ -306,42 +374,9 @@ __global__ void __launch_bounds__(kThreads, 2) f2t_tma(const F2TArgs a)
                 for (int c = 0; c < 3; ++c) out[r][c].store(ob + (c * ROWS + r) * sw + (x - x0));
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
-        // the buffer of tile t+1 (used by tile t+1-nob) must have been read
-        if (threadIdx.x == 0) {
-            if (nob >= 3) bulk_wait_read<1>();
-            else bulk_wait_read<0>();
-        }
-        __syncthreads();      // stage k fully read, output buffer complete
-        if (threadIdx.x == 0) {
-            if (i + nst < tc.count) f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), st, &bars[k]);
-            // fan the tile out to every (run, slot) holding this frame
-            const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
-            const bool whole_rows = x0 == 0 && sw == a.Wp;
-            for (int d = 0; d < dl.nd; ++d) {
-                const int cd = dl.get(a, d);
-                OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
-                                                 static_cast<int64_t>(cd & 31) * a.slot_bytes) +
-                         static_cast<int64_t>(y0) * a.Wp + x0;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    if (whole_rows) {
-                        bulk_s2g(o + c * plane, ob + c * ROWS * sw, ROWS * sw * sizeof(OUT));
-                    } else {
-#pragma unroll
-                        for (int r = 0; r < ROWS; ++r)
-                            bulk_s2g(o + c * plane + r * a.Wp, ob + (c * ROWS + r) * sw, sw * sizeof(OUT));
-                    }
-                }
-            }
-            bulk_commit();
-        }
-        if (++ob_sel == nob) ob_sel = 0;
-        if (++k == nst) {
-            k = 0;
-            phase ^= 1;
-        }
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[k]);
     }
-    if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------ t2f
@@ -371,13 +406,15 @@ __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *
         for (int c = 0; c < 3; ++c) bulk_g2s(S::row(st, r, c), src + c * plane + r * a.tw, bytes, bar);
 }
 
+// Warp-specialised like f2t_tma: warps 0..7 convert and store with st.global,
+// warp 8 lane 0 keeps the stages full.
 template <int FAMILY, typename OS, typename TIN, typename AR>
-__global__ void __launch_bounds__(kThreads, sizeof(AR) == 4 ? 3 : 2) t2f_tma(const T2FArgs a)
+__global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tma(const T2FArgs a)
 {
     using S = T2FStage<FAMILY, TIN>;
     constexpr int ROWS = S::ROWS;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages;
     uint8_t *stages = smem + kBarBytes;
     const int nst = a.stages;
 
@@ -385,20 +422,33 @@ __global__ void __launch_bounds__(kThreads, sizeof(AR) == 4 ? 3 : 2) t2f_tma(con
     tc.init(a.tiles);
     if (tc.count == 0) return;
     if (threadIdx.x == 0) {
-        for (int k = 0; k < nst; ++k) mbar_init(&bars[k], 1);
+        for (int k = 0; k < nst; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kConsumerWarps);
+        }
         fence_barrier_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int k = 0; k < nst && k < tc.count; ++k)
-            t2f_issue<FAMILY, TIN>(a, tc.tile(k), stages + k * a.stage_bytes, &bars[k]);
 
+    if (threadIdx.x >= kThreads) {  // ---------------- producer warp
+        if (threadIdx.x != kThreads) return;
+        for (int k = 0; k < nst && k < tc.count; ++k)
+            t2f_issue<FAMILY, TIN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k]);
+        for (int64_t i = 0; i + nst < tc.count; ++i) {
+            const int k = static_cast<int>(i % nst);
+            mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
+            fence_proxy_async();
+            t2f_issue<FAMILY, TIN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k]);
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------ consumers
     const T2FConst<AR> c(a.col);
     int cj = -1;
     DevFrame f;
-    int k = 0;
-    uint32_t phase = 0;
     for (int64_t i = 0; i < tc.count; ++i) {
+        const int k = static_cast<int>(i % nst);
         const int64_t t = tc.tile(i);
         int job, ru, x0;
         decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
@@ -410,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(AR) == 4 ? 3 : 2) t2f_tma(con
             f = load_frame(a.out + job);
         }
         uint8_t *st = stages + k * a.stage_bytes;
-        mbar_wait(&bars[k], phase);
+        mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
         if (x0 + xo < x1) {
             const int x = x0 + xo;
             AR sb[4], sr[4];
@@ -424,15 +474,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(AR) == 4 ? 3 : 2) t2f_tma(con
             }
             if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, y0, sb, sr, kPx, a.vec_out);
         }
-        __syncthreads();  // every thread is done reading stage k
-        if (threadIdx.x == 0 && i + nst < tc.count) {
-            fence_proxy_async();
-            t2f_issue<FAMILY, TIN>(a, tc.tile(i + nst), st, &bars[k]);
-        }
-        if (++k == nst) {
-            k = 0;
-            phase ^= 1;
-        }
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[k]);
     }
 }
 
@@ -455,16 +498,16 @@ cudaError_t launch_tma(K kernel, A a, int stage_bytes, int extra, int budget, cu
 {
     if (a.tiles <= 0) return cudaSuccess;
     a.stage_bytes = (stage_bytes + 127) / 128 * 128;
-    a.stages = std::max(2, std::min(4, (budget - extra) / a.stage_bytes));
+    a.stages = std::max(2, std::min(kMaxStages, (budget - extra) / a.stage_bytes));
     const int smem = kBarBytes + a.stages * a.stage_bytes + extra;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads + 32, smem);
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
-    kernel<<<grid, kThreads, smem, s>>>(a);
+    kernel<<<grid, kThreads + 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -492,18 +535,22 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     const int budget = env_int("NNVISR_F2T_SMEM_KB", 112) * 1024 - kBarBytes;
     a.nob = env_int("NNVISR_F2T_NOB", 0);
     a.stages = env_int("NNVISR_F2T_STAGES", 0);
-    if (!a.nob) a.nob = 2 * a.stage_bytes + 3 * ob_bytes <= budget ? 3 : 2;
-    if (!a.stages) a.stages = std::max(2, std::min(4, (budget - a.nob * ob_bytes) / a.stage_bytes));
+    // two input stages suffice (inputs are a small share of f2t traffic); the
+    // rest of the budget becomes output buffers = bulk-store groups in flight
+    if (!a.stages) a.stages = 2;
+    a.stages = std::max(1, std::min(kMaxStages, a.stages));
+    if (!a.nob) a.nob = std::max(2, std::min(kMaxOutBufs, (budget - a.stages * a.stage_bytes) / ob_bytes));
+    a.nob = std::max(2, std::min(kMaxOutBufs, a.nob));
     const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes;
     auto kernel = f2t_tma<FAMILY, IN, OUT>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads + 32, smem);
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
-    kernel<<<grid, kThreads, smem, s>>>(a);
+    kernel<<<grid, kThreads + 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 
