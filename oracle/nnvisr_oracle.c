@@ -492,3 +492,50 @@ int oracle_codes_to_rgb(int matrix, int bits, int range, double cy, double cb, d
     *G = Y - (kr * (*R - Y) + kb * (*B - Y)) / (1.0 - kr - kb);
     return 0;
 }
+
+/* ---- scene-change detection (SPEC.md [MODULE] scenedetect,
+ * detect_scene_changes).
+ * The paper delegates detection to upstream filters (§3.2
+ * P:333-339); this is the SPEC's detector: frame i (i > 0) starts a scene
+ * iff the mean absolute luma difference to frame i-1, on the normalised
+ * luma scale, exceeds the threshold.  Luma = the Y plane; for RGB clips
+ * 0.299 R + 0.587 G + 0.114 B, kept exact as the integer 299R + 587G + 114B
+ * (units of 1/1000 code).  Normalisation: one code step is 1/(219*2^(d-8))
+ * (limited) or 1/(2^d-1) (full), the dequantisation of reading A2.
+ * sad[i] = sum over pixels of |luma_i - luma_{i-1}| (exact integer, in the
+ * units above); mad = sad / (pixels * scale [* 1000 for RGB]); cut = mad > t.
+ * frames[i] = 3 plane pointers + pitches of frame i; sad[0] = cut[0] = 0. */
+int oracle_scene_detect(const oracle_format *f, int count, const void *const *planes, const int64_t *pitches,
+                        double threshold, uint64_t *sad, uint8_t *cut)
+{
+    if (check_format(f) || count < 0) return -1;
+    int64_t W = f->width, H = f->height;
+    double scale = (f->range == OR_LIMITED) ? 219.0 * ldexp(1.0, f->bits - 8) : ldexp(1.0, f->bits) - 1.0;
+    if (f->family == OR_RGB) scale *= 1000.0;
+    for (int i = 0; i < count; ++i) {
+        uint64_t s = 0;
+        if (i > 0) {
+            for (int64_t y = 0; y < H; ++y) {
+                for (int64_t x = 0; x < W; ++x) {
+                    int64_t a, b;
+                    if (f->family == OR_RGB) {
+                        a = 299 * (int64_t)sample_at(planes[3 * i], pitches[3 * i], f->bits, x, y) +
+                            587 * (int64_t)sample_at(planes[3 * i + 1], pitches[3 * i + 1], f->bits, x, y) +
+                            114 * (int64_t)sample_at(planes[3 * i + 2], pitches[3 * i + 2], f->bits, x, y);
+                        b = 299 * (int64_t)sample_at(planes[3 * i - 3], pitches[3 * i - 3], f->bits, x, y) +
+                            587 * (int64_t)sample_at(planes[3 * i - 2], pitches[3 * i - 2], f->bits, x, y) +
+                            114 * (int64_t)sample_at(planes[3 * i - 1], pitches[3 * i - 1], f->bits, x, y);
+                    } else {
+                        a = (int64_t)sample_at(planes[3 * i], pitches[3 * i], f->bits, x, y);
+                        b = (int64_t)sample_at(planes[3 * i - 3], pitches[3 * i - 3], f->bits, x, y);
+                    }
+                    s += (uint64_t)(a > b ? a - b : b - a);
+                }
+            }
+        }
+        sad[i] = s;
+        double mad = (double)s / ((double)(W * H) * scale);
+        cut[i] = (uint8_t)(i > 0 && mad > threshold);
+    }
+    return 0;
+}

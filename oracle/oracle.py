@@ -65,6 +65,9 @@ def lib():
         L.oracle_t2f.restype = C.c_int
         L.oracle_t2f.argtypes = [C.POINTER(_Format), C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                  C.c_int64, C.POINTER(C.c_void_p), i64p]
+        L.oracle_scene_detect.restype = C.c_int
+        L.oracle_scene_detect.argtypes = [C.POINTER(_Format), C.c_int, C.POINTER(C.c_void_p), i64p, C.c_double,
+                                          C.POINTER(C.c_uint64), C.POINTER(C.c_uint8)]
         dp = C.POINTER(C.c_double)
         L.oracle_rgb_to_codes.restype = C.c_int
         L.oracle_rgb_to_codes.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, dp, dp, dp]
@@ -180,3 +183,26 @@ def codes_to_rgb(matrix, bits, rng, cy, cb, cr):
     if lib().oracle_codes_to_rgb(matrix, bits, rng, cy, cb, cr, C.byref(R), C.byref(G), C.byref(B)):
         raise ValueError("bad matrix")
     return R.value, G.value, B.value
+
+
+def scene_detect(frames, width, height, family, bits, matrix, rng, threshold):
+    """frames: list of 3-tuples of planes.  Returns (sad uint64 [F], cut uint8 [F])
+    (SPEC.md scenedetect.detect_scene_changes)."""
+    F = len(frames)
+    ptrs = (C.c_void_p * max(3 * F, 1))()
+    pitches = np.zeros(max(3 * F, 1), dtype=np.int64)
+    keep = []
+    for t, fr in enumerate(frames):
+        for p in range(3):
+            a = np.ascontiguousarray(fr[p])
+            keep.append(a)
+            ptrs[3 * t + p] = a.ctypes.data
+            pitches[3 * t + p] = a.strides[0]
+    sad = np.zeros(max(F, 1), np.uint64)
+    cut = np.zeros(max(F, 1), np.uint8)
+    f = _fmt(width, height, family, bits, matrix, rng)
+    rc = lib().oracle_scene_detect(C.byref(f), F, ptrs, pitches.ctypes.data_as(C.POINTER(C.c_int64)), threshold,
+                                   sad.ctypes.data_as(C.POINTER(C.c_uint64)), cut.ctypes.data_as(C.POINTER(C.c_uint8)))
+    if rc:
+        raise ValueError("oracle_scene_detect rejected the arguments")
+    return sad[:F], cut[:F]
