@@ -41,6 +41,9 @@ def parse():
     p.add_argument("--f2t-mode", default="materialize", choices=["materialize", "store"])
     p.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--detect", action="store_true",
+                   help="detect scene changes on the GPU each step (NEXT-4) and plan from those flags")
+    p.add_argument("--detect-threshold", type=float, default=0.15)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="tuples in the oracle sample (0 = auto)")
     return p.parse_args()
@@ -270,7 +273,11 @@ def main():
         return h.plan_range(total, s.window_first, cw, s.begin, s.end)
 
     # per launch: (start event, end event, units, algorithmic bytes)
-    ev_pairs = {"f2t": [], "t2f": []}
+    ev_pairs = {"f2t": [], "t2f": [], "detect": []}
+    if args.detect:
+        sad_d = torch.zeros(s.window_count, dtype=torch.int64, device=dev)
+        cut_d = torch.zeros(s.window_count, dtype=torch.uint8, device=dev)
+        luma_bytes = lay.plane_dims()[0][0] * lay.plane_dims()[0][1] * lay.sample_bytes * (3 if cfg.family == nv.RGB else 1)
 
     def timed(kind, record, units, nbytes, fn):
         if not record:
@@ -287,6 +294,13 @@ def main():
         if world > 1:
             with torch.cuda.stream(stream):
                 sh.halo_exchange(s, win.data, cut_win)
+        if args.detect:
+            # the flags the plan consumes come from the frames themselves
+            with torch.cuda.stream(stream):
+                timed("detect", record, s.window_count, s.window_count * luma_bytes,
+                      lambda: h.scene_detect(s.window_first, s.window_count, args.detect_threshold, sad_d.data_ptr(),
+                                             cut_d.data_ptr(), stream))
+                cut_win.copy_(cut_d)
         runs, _ = plan_local()
         with torch.cuda.stream(stream):
             if args.f2t_mode == "store":
@@ -361,7 +375,7 @@ def main():
                 "bytes": float(bytes_.sum()), "avg_launch_s": float(durs.mean()),
                 "avg_launch_bytes": float(bytes_.mean())}
 
-    ks = {k: kstats(k) for k in ("f2t", "t2f")}
+    ks = {k: kstats(k) for k in ("f2t", "t2f", "detect")}
     peak, peak_src = load_peaks()
     per_dir = {}
     for k, v in ks.items():
@@ -402,6 +416,8 @@ def main():
                        "clip_frames_per_rank": s.owned, "input_tensor": list(in_shape),
                        "output_tensor": list(out_shape), "tensor_dtype": "f16" if cfg.dtype == nv.F16 else "f32",
                        "tuples_per_launch": {"f2t": fchunk, "t2f": tchunk}, "f2t_mode": args.f2t_mode,
+                       "scene_flags": ("detected on the GPU each step (threshold %g)" % args.detect_threshold
+                                       if args.detect else "given (synthetic cut pattern)"),
                        "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB, t2f input ring "
                                     f"{n_out} x {out_elems * esz / 1e6:.0f} MB >= 4 x L2 ({l2 / 1e6:.0f} MB)",
                        "parallelism": f"frame-range shards x{world}, halo P2P"},

@@ -204,6 +204,20 @@ nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensor
                                             int64_t t_w, const nnvisr_frame *out, int64_t count,
                                             void *stream);
 
+/* Scene-change detection (SPEC.md [MODULE] scenedetect,
+ * detect_scene_changes, S:105-113 -- the paper leaves detection to upstream
+ * filters, §3.2).  For bound frames first+i, i in
+ * [0, count): sad[i] = sum over the W x H pixels of |luma(first+i) -
+ * luma(first+i-1)|, an exact integer (luma = the Y plane; for RGB clips
+ * 299 R + 587 G + 114 B), and cut[i] = 1 iff
+ * sad[i] / (W * H * scale) > threshold with scale = 219 * 2^(d-8) (limited)
+ * or 2^d - 1 (full), times 1000 for RGB (the normalised luma step of reading
+ * A2).  sad[0] = cut[0] = 0: frame first-1 is not compared.  sad (uint64)
+ * and cut (uint8) are device arrays [count] written on `stream`; the flags
+ * are in the form nnvisr_plan consumes (copy them to the host). */
+nnvisr_status nnvisr_scene_detect(nnvisr_handle *h, int64_t first, int64_t count, double threshold,
+                                  uint64_t *sad, uint8_t *cut, void *stream);
+
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t nnvisr_launch_count(void);
 

@@ -734,4 +734,25 @@ nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensor
     return t2f_common(h, tensors, tensor_stride_bytes, t_h, t_w, out, count, static_cast<cudaStream_t>(stream));
 }
 
+nnvisr_status nnvisr_scene_detect(nnvisr_handle *h, int64_t first, int64_t count, double threshold, uint64_t *sad,
+                                  uint8_t *cut, void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && (!sad || !cut))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (count < 0 || count > INT32_MAX) return fail(NNVISR_ERR_INVALID_ARG, "bad count");
+    if (!(threshold >= 0.0)) return fail(NNVISR_ERR_INVALID_ARG, "threshold must be >= 0");
+    if (count == 0) return NNVISR_OK;
+    if (!h->frames) return fail(NNVISR_ERR_INVALID_ARG, "no frames bound (nnvisr_bind_frames)");
+    if (first < h->frames_base || first + count > h->frames_base + h->frames_count)
+        return fail(NNVISR_ERR_INVALID_ARG, "frames [%lld, %lld) not bound", (long long)first, (long long)(first + count));
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    const int vec = h->frames_vec && h->fmt.width % kPx == 0;
+    cudaError_t e = launch_scene_detect(h->fmt.family, h->fmt.bits, h->fmt.range, h->fmt.width, h->fmt.height,
+                                        h->frames + (first - h->frames_base), (int)count, vec, threshold, sad, cut,
+                                        static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "scene detection launch");
+    return NNVISR_OK;
+}
+
 }  // extern "C"

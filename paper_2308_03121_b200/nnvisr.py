@@ -54,6 +54,7 @@ def _load():
         "nnvisr_frames_to_store": (st, [H, i64, i64, C.c_void_p, C.c_void_p]),
         "nnvisr_tensor_to_frames": (st, [H, C.c_void_p, i64, i64, C.POINTER(Frame), C.c_void_p]),
         "nnvisr_tensor_to_frames_batch": (st, [H, C.c_void_p, i64, i64, i64, C.POINTER(Frame), i64, C.c_void_p]),
+        "nnvisr_scene_detect": (st, [H, i64, i64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -66,7 +67,7 @@ _lib = _load()
 EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version", "nnvisr_launch_count",
             "nnvisr_tensor_shapes", "nnvisr_plan", "nnvisr_plan_range", "nnvisr_bind_frames",
             "nnvisr_frames_to_tensor", "nnvisr_frames_to_tensor_batch", "nnvisr_frames_to_store",
-            "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch")
+            "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch", "nnvisr_scene_detect")
 
 
 def lib():
@@ -190,6 +191,10 @@ class Handle:
     def tensor_to_frames(self, tensor_ptr: int, t_h: int, t_w: int, out: Sequence[Frame], stream=None):
         arr = frame_array(out)
         _check(_lib.nnvisr_tensor_to_frames(self._h, tensor_ptr, t_h, t_w, arr, _stream_ptr(stream)))
+
+    def scene_detect(self, first: int, count: int, threshold: float, sad_ptr: int, cut_ptr: int, stream=None):
+        """nnvisr_scene_detect: sad (uint64) and cut (uint8) device arrays [count]."""
+        _check(_lib.nnvisr_scene_detect(self._h, first, count, threshold, sad_ptr, cut_ptr, _stream_ptr(stream)))
 
     def tensor_to_frames_batch(self, tensors_ptr: int, stride: int, t_h: int, t_w: int, out: Sequence[Frame],
                                count: int, stream=None):
