@@ -235,9 +235,7 @@ def main():
     # window buffer: [left halo | owned frames | right halo]
     lay = w.layout()
     win = FrameBuffer(lay, s.window_count, device=dev)
-    own = synth.generate_clip(w, device=dev, frames=s.owned, first=s.begin, total_frames=total)
-    win.data[s.left:s.left + s.owned].copy_(own.data)
-    del own
+    synth.generate_clip(w, device=dev, frames=s.owned, first=s.begin, total_frames=total, out=win, out_offset=s.left)
     cut_win = torch.zeros(s.window_count, dtype=torch.uint8, device=dev)
     cut_win[s.left:s.left + s.owned] = torch.from_numpy(cut_all[s.begin:s.end]).to(dev)
     h.bind_frames(win.descriptors(), base=s.window_first)
@@ -448,7 +446,10 @@ def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, i
 
     from paper_2308_03121_b200.frames import FrameBuffer
 
-    host_in = win.data[s.left:s.left + s.owned].cpu().pin_memory()
+    # pinned host copy of the shard's frames, capped at 256 frames (a 4K clip
+    # would not fit in host RAM): frame i is uploaded from host slot i mod pool
+    pool = min(s.owned, 256)
+    host_in = win.data[s.left:s.left + pool].cpu().pin_memory()
     M = h.M
     Ho, Wo = h.out_shape[2], h.out_shape[3]
     ring = 2
@@ -470,8 +471,11 @@ def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, i
             hi = min(s.owned, c0 + nb + R)
             if hi > n_done:
                 with torch.cuda.stream(s_in):
-                    win.data[s.left + n_done:s.left + hi].copy_(host_in[n_done:hi], non_blocking=True)
-                n_done = hi
+                    while n_done < hi:  # contiguous host runs of the pool
+                        a0 = n_done % pool
+                        n = min(hi - n_done, pool - a0)
+                        win.data[s.left + n_done:s.left + n_done + n].copy_(host_in[a0:a0 + n], non_blocking=True)
+                        n_done += n
             ready = torch.cuda.Event()
             ready.record(s_in)
             stream.wait_event(ready)

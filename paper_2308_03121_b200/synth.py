@@ -156,13 +156,14 @@ def scene_ids(cut: np.ndarray) -> np.ndarray:
 
 
 def generate_clip(w: Workload, device="cuda", frames: int | None = None, first: int = 0,
-                  total_frames: int | None = None) -> FrameBuffer:
+                  total_frames: int | None = None, out: FrameBuffer | None = None, out_offset: int = 0) -> FrameBuffer:
     """Frames [first, first+frames) of workload w's synthetic clip (total
-    length total_frames, default w.frames) into a new FrameBuffer."""
+    length total_frames, default w.frames) into a new FrameBuffer, or into
+    rows out_offset.. of `out`."""
     F = w.frames if total_frames is None else total_frames
     count = (F - first) if frames is None else frames
     layout = w.layout()
-    buf = FrameBuffer(layout, count, device=device)
+    buf = out if out is not None else FrameBuffer(layout, count, device=device)
     cut = cut_flags(w, F)
     sid = scene_ids(cut)
     dims = layout.plane_dims()
@@ -192,7 +193,7 @@ def generate_clip(w: Workload, device="cuda", frames: int | None = None, first: 
                 if p > 0 and w.cfg.family == nv.YUV420:
                     dx, dy = dx // 2, dy // 2
                 plane = torch.roll(tex, shifts=(dy, dx), dims=(0, 1))
-            _write_plane(buf, i, p, plane)
+            _write_plane(buf, out_offset + i, p, plane)
     return buf
 
 
