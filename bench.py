@@ -38,7 +38,10 @@ def parse():
     p.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--chunk", type=int, default=0, help="tuples per launch (0 = auto)")
-    p.add_argument("--f2t-mode", default="materialize", choices=["materialize", "store"])
+    p.add_argument("--f2t-mode", default="materialize", choices=["materialize", "store", "batch"],
+                   help="materialize every tuple; store: frame-major store (sliding windows); batch: the paper's "
+                        "Fig. 1 batched shared store (paper grouping, --batch lanes)")
+    p.add_argument("--batch", type=int, default=8, help="lanes per batch for --f2t-mode batch")
     p.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--detect", action="store_true",
@@ -264,6 +267,13 @@ def main():
     store = None
     if args.f2t_mode == "store":
         store = torch.empty((s.window_count, slot_bytes // esz), dtype=tdt, device=dev)
+    if args.f2t_mode == "batch":
+        # Fig. 1 batches (§3.3): each batch's slots (b*n+1 shared, or
+        # b*N plain) in its own region of a chunk store; a launch converts the
+        # slots of ~fchunk runs' batches, every distinct frame once
+        bmax = args.batch * N
+        per_launch = max(1, fchunk // args.batch)
+        store = torch.empty((per_launch * bmax, slot_bytes // esz), dtype=tdt, device=dev)
     stream = torch.cuda.Stream(device=dev)
 
     def plan_local():
@@ -312,6 +322,18 @@ def main():
                     sel = runs[dup[c0:c0 + fchunk]]
                     timed("f2t", record, 0, len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz,
                           lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
+            elif args.f2t_mode == "batch":
+                batches = h.plan_batches(cut_win.cpu().numpy(), args.batch)
+                for c0 in range(0, len(batches), per_launch):
+                    grp = batches[c0:c0 + per_launch]
+                    sf = np.full(len(grp) * bmax, -1, np.int64)
+                    for i, x in enumerate(grp):
+                        sf[i * bmax:i * bmax + len(x["slots"])] = x["slots"]
+                    nslots = int((sf >= 0).sum())
+                    nruns = sum(sum(x["emit"]) for x in grp)
+                    nbytes = len(np.unique(sf[sf >= 0])) * frame_payload + nslots * slot_bytes
+                    timed("f2t", record, nruns, nbytes,
+                          lambda sf=sf: h.frames_to_slots(sf, store.data_ptr(), stream))
             else:
                 for c0 in range(0, len(runs), fchunk):
                     sel = runs[c0:c0 + fchunk]

@@ -204,6 +204,43 @@ nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensor
                                             int64_t t_w, const nnvisr_frame *out, int64_t count,
                                             void *stream);
 
+/* ---- Batched shared frame store (§3.3 P:360-382 and Fig. 1;
+ * SURVEY.md §8(f) NEXT-2).  A batch of b interpolation runs of n+1 frames
+ * needs only b*n + 1 distinct frames; the store keeps each input slot's b
+ * lanes contiguous (the batched network input of slot k is the [b, 3, Hp, Wp]
+ * tensor starting at offset(k, 0)) and the next batch needs one slot copy. */
+
+/* Offset of input slot k (0..n) of lane j (0..b-1) in region r of the shared
+ * layout (SPEC.md framestore.shared_slot_offset): base = r*n*b; slot 0 ->
+ * base + j; slot n -> base + 1 + j; slot k in 1..n-1 -> base + 1 + b +
+ * (k-1)*b + j.  Frame f0 + j*n + k sits there.  Returns -1 for bad arguments. */
+int64_t nnvisr_shared_slot_offset(int32_t n, int32_t b, int32_t region, int32_t k, int32_t j);
+
+/* Batches of b runs (SPEC.md grouper.plan_batches), paper grouping only
+ * (NNVISR_ERR_UNSUPPORTED for sliding windows): each scene's runs in order,
+ * b per batch, never mixing scenes; a short last batch repeats its last run
+ * in the remaining lanes with emit = 0.  A batch is shared (Fig. 1 layout,
+ * b*n + 1 slots) when the network takes the extra frame and all b lanes are
+ * runs over consecutive frames f, f+1, ..., f+n stepping by n; else plain
+ * (b*N slots, slot k of lane j at offset k*b + j).  Per batch i (host arrays,
+ * capacity `cap` batches): shared[i]; lanes[i*b + j] = run index (as in
+ * nnvisr_plan); emit[i*b + j]; slot_frames[i*b*N + o] = frame at offset o
+ * (-1 past the batch's slot count).  NNVISR_ERR_CAPACITY if cap is short. */
+nnvisr_status nnvisr_plan_batches(const nnvisr_handle *h, int64_t num_frames, const uint8_t *cut, int32_t b,
+                                  uint8_t *shared, int64_t *lanes, uint8_t *emit, int64_t *slot_frames,
+                                  int64_t cap, int64_t *num_batches);
+
+/* frames -> slots of a frame-major store: slot i (3*Hp*Wp elements at
+ * store + i*3*Hp*Wp*elem) receives bound frame slot_frames[i] (host array
+ * [count]; -1 leaves the slot untouched).  A frame listed at several slots
+ * is read and converted once. */
+nnvisr_status nnvisr_frames_to_slots(nnvisr_handle *h, const int64_t *slot_frames, int64_t count, void *store,
+                                     void *stream);
+
+/* The single-frame advance ("6 to 5 in the figure"):
+ * copy store slot src to slot dst on `stream`. */
+nnvisr_status nnvisr_copy_slot(nnvisr_handle *h, void *store, int64_t src, int64_t dst, void *stream);
+
 /* Scene-change detection (SPEC.md [MODULE] scenedetect,
  * detect_scene_changes, S:105-113 -- the paper leaves detection to upstream
  * filters, §3.2).  For bound frames first+i, i in

@@ -471,19 +471,22 @@ nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, cudaStream_t st
 // Work list of one f2t launch over `runs` runs of `per_run` slots whose frame
 // keys are key[r*per_run + t]: one job per distinct key, with the (run, slot)
 // destinations of that key.  Written into `buf` as
-// [job_frame: J][job_dst: J+1][dst_code: runs*per_run] (int32); returns J.
+// [job_frame: J][job_dst: J+1][dst_code: <= runs*per_run] (int32); returns J.
+// Keys < 0 have no destination (nnvisr_frames_to_slots' "leave untouched").
 int64_t build_f2t_jobs(const int64_t *key, int64_t runs, int per_run, int64_t key_base, int32_t *buf)
 {
-    const int64_t n = runs * per_run;
-    std::vector<std::pair<int64_t, int32_t>> items(n);
-    for (int64_t i = 0; i < n; ++i)
-        items[i] = {key[i] - key_base, (int32_t)((i / per_run) * 32 + (i % per_run))};
+    std::vector<std::pair<int64_t, int32_t>> items;
+    items.reserve(runs * per_run);
+    for (int64_t i = 0; i < runs * per_run; ++i)  // key < 0: no destination
+        if (key[i] >= 0) items.push_back({key[i] - key_base, (int32_t)((i / per_run) * 32 + (i % per_run))});
+    const int64_t n = (int64_t)items.size();
     std::stable_sort(items.begin(), items.end(),
                      [](const auto &x, const auto &y) { return x.first < y.first; });
     int64_t J = 0;
     for (int64_t i = 0; i < n; ++i)
         if (i == 0 || items[i].first != items[i - 1].first) ++J;
     int32_t *job_frame = buf, *job_dst = buf + J, *dst_code = buf + 2 * J + 1;
+    if (J == 0) return 0;
     int64_t j = -1;
     for (int64_t i = 0; i < n; ++i) {
         if (i == 0 || items[i].first != items[i - 1].first) {
@@ -621,6 +624,10 @@ static nnvisr_status f2t_indexed(nnvisr_handle *h, const int64_t *frame_idx, int
         if (s) return s;
         int32_t *tab = static_cast<int32_t *>(slot->host);
         const int64_t J = build_f2t_jobs(frame_idx + r0 * per_run, nr, per_run, h->frames_base, tab);
+        if (J == 0) {
+            release_slot(slot, st);
+            continue;
+        }
         if ((s = upload(slot, sizeof(int32_t) * (2 * J + 1 + nr * per_run), st))) return s;
         const int32_t *dtab = static_cast<const int32_t *>(slot->dev);
         a.job_frame = dtab;
@@ -752,6 +759,118 @@ nnvisr_status nnvisr_scene_detect(nnvisr_handle *h, int64_t first, int64_t count
                                         h->frames + (first - h->frames_base), (int)count, vec, threshold, sad, cut,
                                         static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "scene detection launch");
+    return NNVISR_OK;
+}
+
+int64_t nnvisr_shared_slot_offset(int32_t n, int32_t b, int32_t region, int32_t k, int32_t j)
+{
+    if (n < 1 || b < 1 || region < 0 || k < 0 || k > n || j < 0 || j >= b) return -1;
+    const int64_t base = (int64_t)region * n * b;
+    if (k == 0) return base + j;
+    if (k == n) return base + 1 + j;
+    return base + 1 + b + (int64_t)(k - 1) * b + j;
+}
+
+nnvisr_status nnvisr_plan_batches(const nnvisr_handle *h, int64_t num_frames, const uint8_t *cut, int32_t b,
+                                  uint8_t *shared, int64_t *lanes, uint8_t *emit, int64_t *slot_frames, int64_t cap,
+                                  int64_t *num_batches)
+{
+    g_error.clear();
+    if (!h || !num_batches) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (!h->paper) return fail(NNVISR_ERR_UNSUPPORTED, "batches are planned for the paper's grouping only");
+    if (b < 1 || b > 1024) return fail(NNVISR_ERR_INVALID_ARG, "batch size b must be in [1, 1024]");
+    if (num_frames < 0 || (num_frames > 0 && !cut)) return fail(NNVISR_ERR_INVALID_ARG, "bad cut array");
+    if (cap > 0 && (!shared || !lanes || !emit || !slot_frames))
+        return fail(NNVISR_ERR_INVALID_ARG, "null output arrays");
+    // the runs of the whole clip, and each scene's run range
+    const int N = h->N, n = h->n;
+    std::vector<int64_t> ins(std::max<int64_t>(num_frames, 1) * N), fr(std::max<int64_t>(num_frames, 1) * 2);
+    PlanSink sink{ins.data(), fr.data(), std::max<int64_t>(num_frames, 1), 0, N};
+    std::vector<std::pair<int64_t, int64_t>> scene_runs;  // [first run, end run)
+    int64_t s0 = 0;
+    for (int64_t k = 1; k <= num_frames; ++k) {
+        if (k == num_frames || cut[k]) {
+            const int64_t r0 = sink.count;
+            plan_scene(h, s0, k, 0, num_frames, sink);
+            scene_runs.push_back({r0, sink.count});
+            s0 = k;
+        }
+    }
+    const bool extra = h->net.flags & NNVISR_EXTRA_FRAME;
+    auto consecutive = [&](int64_t r) {
+        for (int k2 = 1; k2 < N; ++k2)
+            if (ins[r * N + k2] != ins[r * N] + k2) return false;
+        return true;
+    };
+    int64_t nb = 0;
+    for (auto [ra, rb] : scene_runs) {
+        for (int64_t c = ra; c < rb; c += b) {
+            if (nb < cap) {
+                bool all_aligned = true, full = true;
+                for (int j = 0; j < b; ++j) {
+                    const bool real = c + j < rb;
+                    const int64_t r = real ? c + j : rb - 1;
+                    lanes[nb * b + j] = r;
+                    emit[nb * b + j] = real;
+                    full = full && real;
+                    all_aligned = all_aligned && consecutive(r) && (j == 0 || ins[r * N] == ins[(r - 1) * N] + n);
+                }
+                const bool sh = extra && full && all_aligned;
+                shared[nb] = sh;
+                int64_t *sf = slot_frames + nb * (int64_t)b * N;
+                for (int64_t o = 0; o < (int64_t)b * N; ++o) sf[o] = -1;
+                if (sh) {
+                    const int64_t f0 = ins[c * N];
+                    for (int j = 0; j < b; ++j)
+                        for (int k2 = 0; k2 <= n; ++k2)
+                            sf[nnvisr_shared_slot_offset(n, b, 0, k2, j)] = f0 + (int64_t)j * n + k2;
+                } else {
+                    for (int k2 = 0; k2 < N; ++k2)
+                        for (int j = 0; j < b; ++j) sf[(int64_t)k2 * b + j] = ins[lanes[nb * b + j] * N + k2];
+                }
+            }
+            ++nb;
+        }
+    }
+    *num_batches = nb;
+    if (nb > cap) return fail(NNVISR_ERR_CAPACITY, "plan needs %lld batches, capacity %lld", (long long)nb,
+                              (long long)cap);
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_frames_to_slots(nnvisr_handle *h, const int64_t *slot_frames, int64_t count, void *store,
+                                     void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && (!slot_frames || !store))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
+    if (count == 0) return NNVISR_OK;
+    if (!aligned16(store)) return fail(NNVISR_ERR_INVALID_ARG, "store not 16-byte aligned");
+    for (int64_t i = 0; i < count; ++i) {
+        const int64_t f = slot_frames[i];
+        if (f < 0) continue;
+        if (f < h->frames_base || f >= h->frames_base + h->frames_count)
+            return fail(NNVISR_ERR_INVALID_ARG, "slot %lld: frame %lld not bound", (long long)i, (long long)f);
+    }
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    const int64_t slot_bytes = 3 * h->Hp * h->Wp * h->elem;
+    return f2t_indexed(h, slot_frames, count, 1, store, slot_bytes, static_cast<cudaStream_t>(stream));
+}
+
+nnvisr_status nnvisr_copy_slot(nnvisr_handle *h, void *store, int64_t src, int64_t dst, void *stream)
+{
+    g_error.clear();
+    if (!h || !store) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (src < 0 || dst < 0) return fail(NNVISR_ERR_INVALID_ARG, "negative slot");
+    if (src == dst) return NNVISR_OK;
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    const int64_t slot_bytes = 3 * h->Hp * h->Wp * h->elem;
+    char *base = static_cast<char *>(store);
+    cudaError_t e = cudaMemcpyAsync(base + dst * slot_bytes, base + src * slot_bytes, slot_bytes,
+                                    cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync (slot copy)");
     return NNVISR_OK;
 }
 

@@ -55,6 +55,10 @@ def _load():
         "nnvisr_tensor_to_frames": (st, [H, C.c_void_p, i64, i64, C.POINTER(Frame), C.c_void_p]),
         "nnvisr_tensor_to_frames_batch": (st, [H, C.c_void_p, i64, i64, i64, C.POINTER(Frame), i64, C.c_void_p]),
         "nnvisr_scene_detect": (st, [H, i64, i64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
+        "nnvisr_shared_slot_offset": (i64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+        "nnvisr_plan_batches": (st, [H, i64, C.c_void_p, C.c_int32, C.c_void_p, i64p, C.c_void_p, i64p, i64, i64p]),
+        "nnvisr_frames_to_slots": (st, [H, i64p, i64, C.c_void_p, C.c_void_p]),
+        "nnvisr_copy_slot": (st, [H, C.c_void_p, i64, i64, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -67,7 +71,8 @@ _lib = _load()
 EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version", "nnvisr_launch_count",
             "nnvisr_tensor_shapes", "nnvisr_plan", "nnvisr_plan_range", "nnvisr_bind_frames",
             "nnvisr_frames_to_tensor", "nnvisr_frames_to_tensor_batch", "nnvisr_frames_to_store",
-            "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch", "nnvisr_scene_detect")
+            "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch", "nnvisr_scene_detect",
+            "nnvisr_shared_slot_offset", "nnvisr_plan_batches", "nnvisr_frames_to_slots", "nnvisr_copy_slot")
 
 
 def lib():
@@ -192,6 +197,32 @@ class Handle:
         arr = frame_array(out)
         _check(_lib.nnvisr_tensor_to_frames(self._h, tensor_ptr, t_h, t_w, arr, _stream_ptr(stream)))
 
+    def plan_batches(self, cut, b: int):
+        """nnvisr_plan_batches: list of dicts (shared, lanes, emit, slots)."""
+        cut = np.ascontiguousarray(np.asarray(cut, dtype=np.uint8))
+        F = cut.shape[0]
+        cap = max(F, 1)
+        sh = np.zeros(cap, np.uint8)
+        lanes = np.zeros(cap * b, np.int64)
+        emit = np.zeros(cap * b, np.uint8)
+        slots = np.zeros(cap * b * self.N, np.int64)
+        nb = C.c_int64()
+        _check(_lib.nnvisr_plan_batches(self._h, F, cut.ctypes.data if F else None, b, sh.ctypes.data, _i64p(lanes),
+                                        emit.ctypes.data, _i64p(slots), cap, C.byref(nb)))
+        out = []
+        for i in range(nb.value):
+            sl = slots[i * b * self.N:(i + 1) * b * self.N]
+            out.append(dict(shared=bool(sh[i]), lanes=lanes[i * b:(i + 1) * b].tolist(),
+                            emit=[bool(e) for e in emit[i * b:(i + 1) * b]], slots=[int(v) for v in sl if v >= 0]))
+        return out
+
+    def frames_to_slots(self, slot_frames, store_ptr: int, stream=None):
+        sf = np.ascontiguousarray(slot_frames, dtype=np.int64)
+        _check(_lib.nnvisr_frames_to_slots(self._h, _i64p(sf), sf.size, store_ptr, _stream_ptr(stream)))
+
+    def copy_slot(self, store_ptr: int, src: int, dst: int, stream=None):
+        _check(_lib.nnvisr_copy_slot(self._h, store_ptr, src, dst, _stream_ptr(stream)))
+
     def scene_detect(self, first: int, count: int, threshold: float, sad_ptr: int, cut_ptr: int, stream=None):
         """nnvisr_scene_detect: sad (uint64) and cut (uint8) device arrays [count]."""
         _check(_lib.nnvisr_scene_detect(self._h, first, count, threshold, sad_ptr, cut_ptr, _stream_ptr(stream)))
@@ -201,6 +232,10 @@ class Handle:
         arr = frame_array(out)
         _check(_lib.nnvisr_tensor_to_frames_batch(self._h, tensors_ptr, stride, t_h, t_w, arr, count,
                                                   _stream_ptr(stream)))
+
+
+def shared_slot_offset(n: int, b: int, region: int, k: int, j: int) -> int:
+    return int(_lib.nnvisr_shared_slot_offset(n, b, region, k, j))
 
 
 def open(cfg: Config) -> Handle:  # noqa: A001 - mirrors nnvisr_open

@@ -179,3 +179,34 @@ def test_device_calls_fail_loudly_without_gpu():
         with pytest.raises(nv.NnvisrError) as e:
             h.frames_to_tensor([f, f], 4096)
         assert e.value.status == 5
+
+
+def test_shared_offsets_and_plan_batches_match_oracle():
+    """NEXT-2 host side (§3.3 Fig. 1; SPEC plan_batches) equals the oracle."""
+    from oracle import batch_store as B
+    for n in range(1, 6):
+        for b in range(1, 6):
+            for r in range(3):
+                for k in range(n + 1):
+                    for j in range(b):
+                        assert nv.shared_slot_offset(n, b, r, k, j) == B.shared_slot_offset(k, j, n, b, r)
+    assert nv.shared_slot_offset(3, 2, 0, 4, 0) == -1
+    rng = np.random.default_rng(11)
+    for trial in range(60):
+        n = int(rng.integers(1, 5))
+        extra = bool(trial % 3)
+        b = int(rng.integers(1, 5))
+        flags = (nv.INTERPOLATION | nv.EXTRA_FRAME) if extra else 0
+        F = int(rng.integers(1, 45))
+        cut = (rng.random(F) < 0.12).astype(np.uint8)
+        with nv.open(_cfg(n=n, input_count=n + extra, output_count=n, left_context=0, flags=flags)) as h:
+            got = h.plan_batches(cut, b)
+        want = B.plan_batches(cut, n, extra, b)
+        assert len(got) == len(want)
+        for g, w in zip(got, want):
+            assert g["shared"] == w["shared"] and g["lanes"] == w["lanes"] and g["emit"] == w["emit"]
+            assert g["slots"] == w["slots"]
+    with nv.open(_cfg(input_count=5, left_context=2)) as h:
+        with pytest.raises(nv.NnvisrError) as e:
+            h.plan_batches(np.zeros(8, np.uint8), 2)
+        assert e.value.status == 3
