@@ -62,7 +62,9 @@ struct F2TArgs {
     int32_t vec_out;          // 1: tensor rows allow 16-byte stores
     // TMA-pipelined path (kernels_tma.cu): tiles = jobs * rowunits * nseg
     int32_t tma_ok, rowunits, nseg, stages, stage_bytes;
-    int32_t lcap, nob, ob_elems;  // staged row capacity, output buffers, elements per buffer
+    int32_t nob, ob_elems;        // output buffers, elements per buffer
+    int32_t band, ls, cs, whole;  // band height (row units), staged row strides, whole-row copies
+    int64_t pitch_y, pitch_c;     // uniform plane pitches of the bound frames (0 = not uniform)
     int64_t tiles;
     F2TColour col;
 };

@@ -112,24 +112,30 @@ __device__ __forceinline__ void decode_tile(int64_t t, int rowunits, int nseg, i
 }
 
 // ------------------------------------------------------------------ f2t
-// Stage layout (samples of IN): 4:2:0 = luma[2][LCAP] | U[3][CCAP] | V[3][CCAP]
-// (chroma rows: near, far of row 0, far of row 1); 4:4:4/RGB = P0 | P1 | P2
-// [1][LCAP].  LCAP = seg_w, CCAP = seg_w/2 + 2 * (16 / sizeof(IN)).
+// A tile is a band of B row units (4:2:0 row pairs, else rows) of one column
+// segment of one distinct frame.  Stage layout (samples of IN):
+//   4:2:0     luma rows [2B][ls] | U rows [B+2][cs] | V rows [B+2][cs]
+//   4:4:4/RGB plane p rows [B][ls], p = 0, 1, 2
+// holding the band's rows clamped to the frame (padding rows replicate row
+// H-1): luma rows ly0..ly1 and chroma rows cy0..cy1, the near and far chroma
+// rows of every luma row of the band.  With a single segment whose staged row
+// stride equals the plane pitch (a.whole) each plane's band rows arrive in ONE
+// bulk copy; otherwise one copy per row of the segment's window.
 template <int FAMILY, typename IN> struct F2TStage {
     static constexpr int G = 16 / sizeof(IN);  // samples per 16 bytes
     static constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
-    int lcap, ccap;  // samples per staged luma / chroma row (runtime: min(seg, Wp))
-    __device__ __host__ explicit F2TStage(int lc) : lcap(lc), ccap(lc / 2 + 2 * G) {}
+    int ls, cs, B;  // luma / chroma staged row strides (samples), band height
+    __device__ __host__ F2TStage(int ls_, int cs_, int B_) : ls(ls_), cs(cs_), B(B_) {}
     __device__ __host__ int bytes() const
     {
-        return FAMILY == kYUV420 ? (2 * lcap + 6 * ccap) * (int)sizeof(IN) : 3 * lcap * (int)sizeof(IN);
+        return FAMILY == kYUV420 ? (2 * B * ls + 2 * (B + 2) * cs) * (int)sizeof(IN) : 3 * B * ls * (int)sizeof(IN);
     }
-    __device__ IN *luma(uint8_t *st, int r) const { return reinterpret_cast<IN *>(st) + r * lcap; }
-    __device__ IN *chroma(uint8_t *st, int p, int q) const
+    __device__ IN *luma(uint8_t *st, int row) const { return reinterpret_cast<IN *>(st) + row * ls; }
+    __device__ IN *chroma(uint8_t *st, int p, int row) const
     {
-        return reinterpret_cast<IN *>(st) + 2 * lcap + (p * 3 + q) * ccap;
+        return reinterpret_cast<IN *>(st) + 2 * B * ls + (p * (B + 2) + row) * cs;
     }
-    __device__ IN *plane(uint8_t *st, int p) const { return reinterpret_cast<IN *>(st) + p * lcap; }
+    __device__ IN *plane(uint8_t *st, int p, int row) const { return reinterpret_cast<IN *>(st) + (p * B + row) * ls; }
 };
 
 // Copy windows of a segment [x0, x1): luma [lw0, lw1), chroma [cw0, cw1).
@@ -154,36 +160,64 @@ struct F2TWindow {
     }
 };
 
+// tile -> (job, band, segment start); band = row units [band*B, min(band*B + B, rowunits))
+struct F2TTile {
+    int job, u0, nu, x0, x1, ly0, ly1, cy0, cy1;
+    __device__ __forceinline__ void set(const F2TArgs &a, int64_t t, int ROWS)
+    {
+        const int bands = (a.rowunits + a.band - 1) / a.band;
+        int band;
+        decode_tile(t, bands, a.nseg, kSegW, job, band, x0);
+        x1 = min(x0 + kSegW, a.Wp);
+        u0 = band * a.band;
+        nu = min(a.band, a.rowunits - u0);
+        ly0 = min(u0 * ROWS, a.H - 1);
+        ly1 = min((u0 + nu) * ROWS - 1, a.H - 1);
+        const int ch = a.H >> 1;
+        cy0 = (ly0 & 1) ? (ly0 >> 1) : max((ly0 >> 1) - 1, 0);
+        cy1 = (ly1 & 1) ? min((ly1 >> 1) + 1, ch - 1) : (ly1 >> 1);
+    }
+};
+
 template <int FAMILY, typename IN>
 __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *st, uint64_t *bar)
 {
     using S = F2TStage<FAMILY, IN>;
-    const S sg(a.lcap);
-    int job, ru, x0;
-    decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
-    const int x1 = min(x0 + kSegW, a.Wp);
-    const DevFrame f = load_frame(a.frames + a.job_frame[job]);
+    const S sg(a.ls, a.cs, a.band);
+    F2TTile tl;
+    tl.set(a, t, S::ROWS);
+    const DevFrame f = load_frame(a.frames + a.job_frame[tl.job]);
     F2TWindow w;
-    w.set(x0, x1, a.W, S::G, FAMILY == kYUV420);
-    const int y0 = ru * S::ROWS;
-    const uint32_t lbytes = (w.lw1 - w.lw0) * sizeof(IN);
+    w.set(tl.x0, tl.x1, a.W, S::G, FAMILY == kYUV420);
+    const int nl = tl.ly1 - tl.ly0 + 1;
     if constexpr (FAMILY == kYUV420) {
-        const uint32_t cbytes = (w.cw1 - w.cw0) * sizeof(IN);
-        mbar_arrive_expect_tx(bar, 2 * lbytes + 6 * cbytes);
-        const int yc0 = min(y0, a.H - 1), yc1 = min(y0 + 1, a.H - 1), ch = a.H >> 1;
-        bulk_g2s(sg.luma(st, 0), row_ptr<IN>(f, 0, yc0) + w.lw0, lbytes, bar);
-        bulk_g2s(sg.luma(st, 1), row_ptr<IN>(f, 0, yc1) + w.lw0, lbytes, bar);
-        const int rows[3] = {chroma_near(yc0), chroma_far(yc0, ch), chroma_far(yc1, ch)};
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int q = 0; q < 3; ++q)
-                bulk_g2s(sg.chroma(st, p, q), row_ptr<IN>(f, p + 1, rows[q]) + w.cw0, cbytes, bar);
+        const int nc = tl.cy1 - tl.cy0 + 1;
+        if (a.whole) {
+            const uint32_t lb = nl * a.ls * sizeof(IN), cb = nc * a.cs * sizeof(IN);
+            mbar_arrive_expect_tx(bar, lb + 2 * cb);
+            bulk_g2s(sg.luma(st, 0), row_ptr<IN>(f, 0, tl.ly0), lb, bar);
+            bulk_g2s(sg.chroma(st, 0, 0), row_ptr<IN>(f, 1, tl.cy0), cb, bar);
+            bulk_g2s(sg.chroma(st, 1, 0), row_ptr<IN>(f, 2, tl.cy0), cb, bar);
+        } else {
+            const uint32_t lb = (w.lw1 - w.lw0) * sizeof(IN), cb = (w.cw1 - w.cw0) * sizeof(IN);
+            mbar_arrive_expect_tx(bar, nl * lb + 2 * nc * cb);
+            for (int r = 0; r < nl; ++r) bulk_g2s(sg.luma(st, r), row_ptr<IN>(f, 0, tl.ly0 + r) + w.lw0, lb, bar);
+            for (int p = 0; p < 2; ++p)
+                for (int r = 0; r < nc; ++r)
+                    bulk_g2s(sg.chroma(st, p, r), row_ptr<IN>(f, p + 1, tl.cy0 + r) + w.cw0, cb, bar);
+        }
     } else {
-        mbar_arrive_expect_tx(bar, 3 * lbytes);
-        const int yc = min(y0, a.H - 1);
-#pragma unroll
-        for (int p = 0; p < 3; ++p) bulk_g2s(sg.plane(st, p), row_ptr<IN>(f, p, yc) + w.lw0, lbytes, bar);
+        if (a.whole) {
+            const uint32_t lb = nl * a.ls * sizeof(IN);
+            mbar_arrive_expect_tx(bar, 3 * lb);
+            for (int p = 0; p < 3; ++p) bulk_g2s(sg.plane(st, p, 0), row_ptr<IN>(f, p, tl.ly0), lb, bar);
+        } else {
+            const uint32_t lb = (w.lw1 - w.lw0) * sizeof(IN);
+            mbar_arrive_expect_tx(bar, 3 * nl * lb);
+            for (int p = 0; p < 3; ++p)
+                for (int r = 0; r < nl; ++r)
+                    bulk_g2s(sg.plane(st, p, r), row_ptr<IN>(f, p, tl.ly0 + r) + w.lw0, lb, bar);
+        }
     }
 }
 
@@ -194,6 +228,8 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
 // The producer waits empty, fans the finished tile out with bulk stores,
 // refills the stage, and releases output buffers as the stores drain; no
 // consumer ever waits on a store or on a descriptor load.
+// Output buffer layout: [channel][B*ROWS rows][sw]: with a single segment a
+// channel's band rows are contiguous in the tensor too, one bulk store each.
 template <int FAMILY, typename IN, typename OUT>
 __global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
 {
@@ -204,8 +240,8 @@ __global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages, *ofree = empty + kMaxStages;
     uint8_t *stages = smem + kBarBytes;
-    const int nst = a.stages, nob = a.nob;
-    const S sg(a.lcap);
+    const int nst = a.stages, nob = a.nob, brows = a.band * ROWS;
+    const S sg(a.ls, a.cs, a.band);
     OUT *obuf = reinterpret_cast<OUT *>(stages + nst * a.stage_bytes);
 
     TileCursor tc;
@@ -232,26 +268,27 @@ __global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
             const int k = static_cast<int>(i % nst);
             mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
             // fan tile i out to every (run, slot) holding its frame
-            int job, ru, x0;
-            decode_tile(tc.tile(i), a.rowunits, a.nseg, kSegW, job, ru, x0);
-            const int sw = min(x0 + kSegW, a.Wp) - x0, y0 = ru * ROWS;
-            if (job != lj) {
-                lj = job;
-                dl.load(a, job);
+            F2TTile tl;
+            tl.set(a, tc.tile(i), ROWS);
+            const int sw = tl.x1 - tl.x0, rows = tl.nu * ROWS;
+            if (tl.job != lj) {
+                lj = tl.job;
+                dl.load(a, tl.job);
             }
             const OUT *ob = obuf + static_cast<int>(i % nob) * a.ob_elems;
-            const bool whole_rows = x0 == 0 && sw == a.Wp;
+            const bool whole_rows = tl.x0 == 0 && sw == a.Wp;
             for (int d = 0; d < dl.nd; ++d) {
                 const int cd = dl.get(a, d);
                 OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
                                                  static_cast<int64_t>(cd & 31) * a.slot_bytes) +
-                         static_cast<int64_t>(y0) * a.Wp + x0;
+                         static_cast<int64_t>(tl.u0 * ROWS) * a.Wp + tl.x0;
                 for (int c = 0; c < 3; ++c) {
                     if (whole_rows) {
-                        bulk_s2g(o + c * plane, ob + c * ROWS * sw, ROWS * sw * sizeof(OUT));
+                        bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
                     } else {
-                        for (int r = 0; r < ROWS; ++r)
-                            bulk_s2g(o + c * plane + r * a.Wp, ob + (c * ROWS + r) * sw, sw * sizeof(OUT));
+                        for (int r = 0; r < rows; ++r)
+                            bulk_s2g(o + c * plane + static_cast<int64_t>(r) * a.Wp, ob + (c * brows + r) * sw,
+                                     sw * sizeof(OUT));
                     }
                 }
             }
@@ -281,97 +318,99 @@ __global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
     }
 
     // ------------------------------------------------------------ consumers
+    const int cw = a.W >> 1, ch = a.H >> 1;
     for (int64_t i = 0; i < tc.count; ++i) {
-        const int64_t t = tc.tile(i);
-        int job, ru, x0;
-        decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
-        const int x1 = min(x0 + kSegW, a.Wp);
-        const int sw = x1 - x0;
-        const int y0 = ru * ROWS;
-        const int x = x0 + kPx * threadIdx.x;
-        (void)y0;
+        F2TTile tl;
+        tl.set(a, tc.tile(i), ROWS);
+        const int sw = tl.x1 - tl.x0;
+        const int x = tl.x0 + kPx * threadIdx.x;
         const int k = static_cast<int>(i % nst);
         uint8_t *st = stages + k * a.stage_bytes;
         OUT *ob = obuf + static_cast<int>(i % nob) * a.ob_elems;
+        F2TWindow w;
+        w.set(tl.x0, tl.x1, a.W, S::G, FAMILY == kYUV420);
+        if (a.whole) {  // whole rows staged: window = the full row
+            w.lw0 = 0;
+            w.cw0 = 0;
+        }
+        const bool fast = x + kPx <= a.W;
         mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
         if (i >= nob) mbar_wait(&ofree[static_cast<int>(i % nob)], static_cast<uint32_t>((i / nob - 1) & 1));
-        if (x < x1) {
-            F2TWindow w;
-            w.set(x0, x1, a.W, S::G, FAMILY == kYUV420);
-            const bool fast = x + kPx <= a.W;
-            Row8<OUT> out[ROWS][3];
+        if (x < tl.x1) {
+            for (int u = 0; u < tl.nu; ++u) {
 #pragma unroll
-            for (int r = 0; r < ROWS; ++r) {
-                int ys[kPx], us[kPx], vs[kPx];
-                if constexpr (FAMILY == kYUV420) {
-                    const IN *L = sg.luma(st, r);
-                    const int cw = a.W >> 1;
-                    if (fast) {
-                        unpack8(*reinterpret_cast<const V8 *>(L + (x - w.lw0)), ys);
-                        const int i0 = x >> 1;
+                for (int r = 0; r < ROWS; ++r) {
+                    const int yc = min((tl.u0 + u) * ROWS + r, a.H - 1);
+                    int ys[kPx], us[kPx], vs[kPx];
+                    if constexpr (FAMILY == kYUV420) {
+                        const IN *L = sg.luma(st, yc - tl.ly0) - w.lw0;
+                        const IN *Cn[2] = {sg.chroma(st, 0, chroma_near(yc) - tl.cy0) - w.cw0,
+                                           sg.chroma(st, 1, chroma_near(yc) - tl.cy0) - w.cw0};
+                        const IN *Cf[2] = {sg.chroma(st, 0, chroma_far(yc, ch) - tl.cy0) - w.cw0,
+                                           sg.chroma(st, 1, chroma_far(yc, ch) - tl.cy0) - w.cw0};
+                        if (fast) {
+                            unpack8(*reinterpret_cast<const V8 *>(L + x), ys);
+                            const int i0 = x >> 1;
 #pragma unroll
-                        for (int p = 0; p < 2; ++p) {
-                            int h[2][kPx];
+                            for (int p = 0; p < 2; ++p) {
+                                int h[2][kPx];
 #pragma unroll
-                            for (int q = 0; q < 2; ++q) {
-                                const IN *C = sg.chroma(st, p, q == 0 ? 0 : 1 + r) - w.cw0;
-                                int c[6];
-                                unpack4(*reinterpret_cast<const V4 *>(C + i0), &c[1]);
-                                c[0] = C[max(i0 - 1, 0)];
-                                c[5] = C[min(i0 + 4, cw - 1)];
-                                hup(c, h[q]);
+                                for (int q = 0; q < 2; ++q) {
+                                    const IN *C = q == 0 ? Cn[p] : Cf[p];
+                                    int c[6];
+                                    unpack4(*reinterpret_cast<const V4 *>(C + i0), &c[1]);
+                                    c[0] = C[max(i0 - 1, 0)];
+                                    c[5] = C[min(i0 + 4, cw - 1)];
+                                    hup(c, h[q]);
+                                }
+#pragma unroll
+                                for (int kk = 0; kk < kPx; ++kk) {
+                                    const int s2 = 3 * h[0][kk] + h[1][kk];
+                                    if (p == 0) us[kk] = s2; else vs[kk] = s2;
+                                }
                             }
+                        } else {
 #pragma unroll
                             for (int kk = 0; kk < kPx; ++kk) {
-                                const int s = 3 * h[0][kk] + h[1][kk];
-                                if (p == 0) us[kk] = s; else vs[kk] = s;
+                                const int xc = min(x + kk, a.W - 1);
+                                ys[kk] = L[xc];
+                                const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
+                                us[kk] = 9 * Cn[0][in_] + 3 * Cn[0][if_] + 3 * Cf[0][in_] + Cf[0][if_];
+                                vs[kk] = 9 * Cn[1][in_] + 3 * Cn[1][if_] + 3 * Cf[1][in_] + Cf[1][if_];
                             }
                         }
+#pragma unroll
+                        for (int kk = 0; kk < kPx; ++kk) ys[kk] *= 16;
                     } else {
+                        const IN *P0 = sg.plane(st, 0, yc - tl.ly0) - w.lw0,
+                                 *P1 = sg.plane(st, 1, yc - tl.ly0) - w.lw0,
+                                 *P2 = sg.plane(st, 2, yc - tl.ly0) - w.lw0;
+                        if (fast) {
+                            unpack8(*reinterpret_cast<const V8 *>(P0 + x), ys);
+                            unpack8(*reinterpret_cast<const V8 *>(P1 + x), us);
+                            unpack8(*reinterpret_cast<const V8 *>(P2 + x), vs);
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < kPx; ++kk) {
+                                const int xc = min(x + kk, a.W - 1);
+                                ys[kk] = P0[xc];
+                                us[kk] = P1[xc];
+                                vs[kk] = P2[xc];
+                            }
+                        }
 #pragma unroll
                         for (int kk = 0; kk < kPx; ++kk) {
-                            const int xc = min(x + kk, a.W - 1);
-                            ys[kk] = L[xc - w.lw0];
-                            const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
-                            const IN *Un = sg.chroma(st, 0, 0) - w.cw0, *Uf = sg.chroma(st, 0, 1 + r) - w.cw0;
-                            const IN *Vn = sg.chroma(st, 1, 0) - w.cw0, *Vf = sg.chroma(st, 1, 1 + r) - w.cw0;
-                            us[kk] = 9 * Un[in_] + 3 * Un[if_] + 3 * Uf[in_] + Uf[if_];
-                            vs[kk] = 9 * Vn[in_] + 3 * Vn[if_] + 3 * Vf[in_] + Vf[if_];
+                            ys[kk] *= 16;
+                            us[kk] *= 16;
+                            vs[kk] *= 16;
                         }
                     }
+                    Row8<OUT> o3[3];
+                    f2t_row<FAMILY, OUT>(a.col, ys, us, vs, o3);
 #pragma unroll
-                    for (int kk = 0; kk < kPx; ++kk) ys[kk] *= 16;
-                } else {
-                    const IN *P0 = sg.plane(st, 0) - w.lw0, *P1 = sg.plane(st, 1) - w.lw0,
-                             *P2 = sg.plane(st, 2) - w.lw0;
-                    if (fast) {
-                        unpack8(*reinterpret_cast<const V8 *>(P0 + x), ys);
-                        unpack8(*reinterpret_cast<const V8 *>(P1 + x), us);
-                        unpack8(*reinterpret_cast<const V8 *>(P2 + x), vs);
-                    } else {
-#pragma unroll
-                        for (int kk = 0; kk < kPx; ++kk) {
-                            const int xc = min(x + kk, a.W - 1);
-                            ys[kk] = P0[xc];
-                            us[kk] = P1[xc];
-                            vs[kk] = P2[xc];
-                        }
-                    }
-#pragma unroll
-                    for (int kk = 0; kk < kPx; ++kk) {
-                        ys[kk] *= 16;
-                        us[kk] *= 16;
-                        vs[kk] *= 16;
-                    }
+                    for (int c = 0; c < 3; ++c) o3[c].store(ob + (c * brows + u * ROWS + r) * sw + (x - tl.x0));
                 }
-                f2t_row<FAMILY, OUT>(a.col, ys, us, vs, out[r]);
             }
-            // stage the converted rows in this tile's output buffer,
-            // layout [channel][row][sw] (rows of a channel adjacent)
-#pragma unroll
-            for (int r = 0; r < ROWS; ++r)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) out[r][c].store(ob + (c * ROWS + r) * sw + (x - x0));
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
         __syncwarp();
@@ -528,20 +567,47 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     constexpr int ROWS = S::ROWS;
     if (a.tiles <= 0) return cudaSuccess;
     const int segw = std::min(kSegW, (a.Wp + 31) / 32 * 32);
-    a.lcap = (segw + S::G - 1) / S::G * S::G;
-    a.stage_bytes = (S(a.lcap).bytes() + 127) / 128 * 128;
-    a.ob_elems = (ROWS * 3 * segw * (int)sizeof(OUT) + 127) / 128 * 128 / (int)sizeof(OUT);
-    const int ob_bytes = a.ob_elems * (int)sizeof(OUT);
-    const int budget = env_int("NNVISR_F2T_SMEM_KB", 112) * 1024 - kBarBytes;
+    const int lcap = (segw + 2 * S::G - 1) / (2 * S::G) * (2 * S::G);  // ccap*sizeof(IN) stays 16-byte aligned
+    const int ccap = lcap / 2 + 2 * S::G;
+    // whole rows: one segment, and every bound frame's pitches are the staged strides
+    const int sb = sizeof(IN);
+    const bool whole = a.nseg == 1 && a.pitch_y > 0 && a.pitch_y % 16 == 0 && a.pitch_y / sb <= 4 * lcap &&
+                       (FAMILY != kYUV420 || (a.pitch_c > 0 && a.pitch_c % 16 == 0));
+    a.whole = whole;
+    a.ls = whole ? a.pitch_y / sb : lcap;
+    a.cs = whole ? (FAMILY == kYUV420 ? a.pitch_c / sb : a.ls) : ccap;
+    auto stage_bytes = [&](int B) { return (S(a.ls, a.cs, B).bytes() + 127) / 128 * 128; };
+    auto ob_bytes = [&](int B) { return (ROWS * B * 3 * segw * (int)sizeof(OUT) + 127) / 128 * 128; };
+    // band height and buffering, from the tools/sweep_f2t.sh sweep on B200
+    // (profiles/r01/f2t_sweep.txt): bands of 2 row units with 3 output buffers
+    // for whole-row frames and 4:4:4; single row units for 4:2:0 frames wider
+    // than one 2048-column segment (per-row copies, chroma halo rows)
+    int B = env_int("NNVISR_F2T_BAND", 0);
+    if (B <= 0) B = (FAMILY == kYUV420 && a.nseg > 1) ? 1 : 2;
+    a.band = std::max(1, std::min(B, a.rowunits));
+    const int bands = (a.rowunits + a.band - 1) / a.band;
+    a.tiles = a.tiles / ((int64_t)a.rowunits * a.nseg) * bands * a.nseg;  // jobs * bands * nseg
+    a.stage_bytes = stage_bytes(a.band);
+    a.ob_elems = ob_bytes(a.band) / (int)sizeof(OUT);
     a.nob = env_int("NNVISR_F2T_NOB", 0);
     a.stages = env_int("NNVISR_F2T_STAGES", 0);
-    // two input stages suffice (inputs are a small share of f2t traffic); the
-    // rest of the budget becomes output buffers = bulk-store groups in flight
     if (!a.stages) a.stages = 2;
     a.stages = std::max(1, std::min(kMaxStages, a.stages));
-    if (!a.nob) a.nob = std::max(2, std::min(kMaxOutBufs, (budget - a.stages * a.stage_bytes) / ob_bytes));
+    if (!a.nob) a.nob = 3;
     a.nob = std::max(2, std::min(kMaxOutBufs, a.nob));
-    const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes;
+    // never exceed the 227 KB a CTA may use: shed output buffers, then band rows
+    constexpr int kMaxSmem = 227 * 1024;
+    while (kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band) > kMaxSmem) {
+        if (a.nob > 2) --a.nob;
+        else if (a.stages > 1) --a.stages;
+        else if (a.band > 1) {
+            --a.band;
+            a.stage_bytes = stage_bytes(a.band);
+            a.ob_elems = ob_bytes(a.band) / (int)sizeof(OUT);
+        } else break;
+    }
+    a.tiles = a.tiles / bands * ((a.rowunits + a.band - 1) / a.band);
+    const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band);
     auto kernel = f2t_tma<FAMILY, IN, OUT>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

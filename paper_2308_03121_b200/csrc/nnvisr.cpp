@@ -88,6 +88,7 @@ struct nnvisr_handle {
     DevFrame *frames = nullptr;
     int64_t frames_cap = 0, frames_base = 0, frames_count = 0;
     bool frames_vec = false;
+    int64_t frames_pitch_y = 0, frames_pitch_c = 0;  // uniform pitches of the bound frames, 0 if they differ
     bool force_generic = false;  // NNVISR_FORCE_GENERIC=1: never take the TMA path (tests)
 };
 
@@ -440,6 +441,19 @@ nnvisr_status check_frame(const nnvisr_handle *h, const nnvisr_frame &fr, int64_
     return NNVISR_OK;
 }
 
+// Uniform plane pitches of a frame list: luma (plane 0) and chroma (planes 1
+// and 2, which must agree; for 4:4:4 / RGB also with plane 0), else 0.
+void uniform_pitches(const nnvisr_handle *h, const nnvisr_frame *fr, int64_t count, int64_t &py, int64_t &pc)
+{
+    py = count ? fr[0].pitch[0] : 0;
+    pc = count ? fr[0].pitch[1] : 0;
+    for (int64_t i = 0; i < count; ++i) {
+        if (fr[i].pitch[0] != py) py = 0;
+        if (fr[i].pitch[1] != pc || fr[i].pitch[2] != pc) pc = 0;
+    }
+    if (h->fmt.family != NNVISR_YUV420 && pc != py) py = pc = 0;
+}
+
 F2TArgs f2t_args(const nnvisr_handle *h)
 {
     F2TArgs a{};
@@ -560,6 +574,7 @@ nnvisr_status nnvisr_bind_frames(nnvisr_handle *h, int64_t base, const nnvisr_fr
     h->frames_base = base;
     h->frames_count = count;
     h->frames_vec = vec;
+    uniform_pitches(h, frames, count, h->frames_pitch_y, h->frames_pitch_c);
     return NNVISR_OK;
 }
 
@@ -600,6 +615,7 @@ nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, 
     a.dst = static_cast<char *>(tensor);
     a.run_stride = 0;
     a.vec_in = vec;
+    uniform_pitches(h, in, h->N, a.pitch_y, a.pitch_c);
     s = run_f2t(h, a, J, st);
     nnvisr_status s2 = release_slot(slot, st);
     return s ? s : s2;
@@ -617,6 +633,8 @@ static nnvisr_status f2t_indexed(nnvisr_handle *h, const int64_t *frame_idx, int
     a.frames = h->frames;
     a.run_stride = run_stride;
     a.vec_in = h->frames_vec;
+    a.pitch_y = h->frames_pitch_y;
+    a.pitch_c = h->frames_pitch_c;
     for (int64_t r0 = 0; r0 < runs; r0 += max_runs) {
         const int64_t nr = std::min(max_runs, runs - r0);
         UploadSlot *slot = nullptr;
