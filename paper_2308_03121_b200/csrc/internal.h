@@ -80,7 +80,7 @@ struct T2FArgs {
     int32_t units, col_units;
     int32_t vec_in;           // tensor rows allow 16-byte loads
     int32_t vec_out;          // output planes allow vector stores
-    int32_t tma_ok, rowunits, nseg, stages, stage_bytes;
+    int32_t tma_ok, rowunits, nseg, stages, stage_bytes, segw;
     int64_t tiles;
     T2FColour col;
 };

@@ -83,7 +83,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 constexpr int kSegW = kThreads * kPx;         // columns per tile segment (2048)
 constexpr int kConsumerWarps = kThreads / 32;  // converting warps; one more warp produces
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int kMaxOutBufs = 8;
 constexpr int kBarBytes = 8 * (2 * kMaxStages + kMaxOutBufs);  // mbarriers at the start of dynamic smem
 
@@ -431,8 +431,8 @@ __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *
 {
     using S = T2FStage<FAMILY, TIN>;
     int job, ru, x0;
-    decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
-    const int x1 = min(x0 + kSegW, a.Wo);
+    decode_tile(t, a.rowunits, a.nseg, a.segw, job, ru, x0);
+    const int x1 = min(x0 + a.segw, a.Wo);
     const int tup = job / a.M, o = job - tup * a.M;
     const int64_t plane = a.th * a.tw;
     const TIN *src = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
@@ -490,8 +490,8 @@ __global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tm
         const int k = static_cast<int>(i % nst);
         const int64_t t = tc.tile(i);
         int job, ru, x0;
-        decode_tile(t, a.rowunits, a.nseg, kSegW, job, ru, x0);
-        const int x1 = min(x0 + kSegW, a.Wo);
+        decode_tile(t, a.rowunits, a.nseg, a.segw, job, ru, x0);
+        const int x1 = min(x0 + a.segw, a.Wo);
         const int y0 = ru * ROWS;
         const int xo = kPx * threadIdx.x;  // column within the segment
         if (job != cj) {
@@ -530,14 +530,26 @@ int sms()
     return n;
 }
 
+int env_int(const char *name, int dflt)
+{
+    const char *v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
 // Dynamic smem = mbarriers | `stages` input stages | `extra` bytes (f2t: two
-// output staging buffers).  Stages: as many as fit in `budget` (2..4).
+// output staging buffers).  Stages: `default_stages` (tools/sweep_t2f.sh on
+// B200, profiles/r01/t2f_sweep.txt), else as many as fit in `budget`.
 template <typename K, typename A>
-cudaError_t launch_tma(K kernel, A a, int stage_bytes, int extra, int budget, cudaStream_t s)
+cudaError_t launch_tma(K kernel, A a, int stage_bytes, int extra, int budget, int default_stages, cudaStream_t s)
 {
     if (a.tiles <= 0) return cudaSuccess;
     a.stage_bytes = (stage_bytes + 127) / 128 * 128;
-    a.stages = std::max(2, std::min(kMaxStages, (budget - extra) / a.stage_bytes));
+    // equal segments of a multiple of 32 columns (<= 2048): no thin tail tile
+    a.segw = std::min(kSegW, ((a.Wo + a.nseg - 1) / a.nseg + 31) / 32 * 32);
+    budget = env_int("NNVISR_T2F_SMEM_KB", budget / 1024) * 1024;
+    a.stages = env_int("NNVISR_T2F_STAGES", default_stages);
+    if (a.stages <= 0) a.stages = (budget - extra) / a.stage_bytes;
+    a.stages = std::max(2, std::min(kMaxStages, a.stages));
     const int smem = kBarBytes + a.stages * a.stage_bytes + extra;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -548,12 +560,6 @@ cudaError_t launch_tma(K kernel, A a, int stage_bytes, int extra, int budget, cu
         1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
     kernel<<<grid, kThreads + 32, smem, s>>>(a);
     return cudaGetLastError();
-}
-
-int env_int(const char *name, int dflt)
-{
-    const char *v = std::getenv(name);
-    return v && *v ? std::atoi(v) : dflt;
 }
 
 // f2t smem: mbarriers | stages x input stage | nob x output buffer.  Sized at
@@ -636,15 +642,15 @@ cudaError_t t2f_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t
 {
     constexpr int BH = T2FStage<FAMILY, __half>::BYTES, BF = T2FStage<FAMILY, float>::BYTES;
     if (bits == 8) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, BH, 0, 72 * 1024, s);
-        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, BF, 0, 72 * 1024, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, BH, 0, 72 * 1024, 2, s);
+        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, BF, 0, 72 * 1024, 2, s);
     }
     if (bits == 10) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, BH, 0, 72 * 1024, s);
-        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, BF, 0, 72 * 1024, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, BH, 0, 72 * 1024, 2, s);
+        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, BF, 0, 72 * 1024, 2, s);
     }
-    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, BH, 0, 110 * 1024, s);
-    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, BF, 0, 110 * 1024, s);
+    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, BH, 0, 72 * 1024, 3, s);
+    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, BF, 0, 72 * 1024, 3, s);
 }
 
 }  // namespace
