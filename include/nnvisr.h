@@ -204,6 +204,30 @@ nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensor
                                             int64_t t_w, const nnvisr_frame *out, int64_t count,
                                             void *stream);
 
+/* ---- Output emission (§3.1 P:251-261:
+ * "Interpolation ... produce output video in doubled framerate"; without
+ * "Double frame", "input frames are also used as output frames as is, and
+ * network outputs are all treated as intermediate frames"; SPEC.md
+ * grouper.schedule_outputs).  For run r of nnvisr_plan, entries
+ * e in [run_first[r], run_first[r+1]) say which outputs are presented:
+ * source[e] >= 0: network output slot; source[e] < 0: pass-through of input
+ * slot -source[e]-1; present[e]: presentation index (frame index, or 2t and
+ * 2t+1 under INTERPOLATION).  Only fresh frames are emitted (the recycled
+ * prefix of a scene's last run is dropped; with M = 2n+1 the trailing
+ * enhanced lookahead is dropped).  Every presentation index 0 .. F-1 (2F-1)
+ * appears once.  Host arrays; capacities cap_entries, cap_runs+1. */
+nnvisr_status nnvisr_schedule_outputs(const nnvisr_handle *h, int64_t num_frames, const uint8_t *cut,
+                                      int32_t *source, int64_t *present, int64_t *run_first, int64_t cap_entries,
+                                      int64_t cap_runs, int64_t *num_entries, int64_t *num_runs);
+
+/* Pass-through frames: copy bound frames src_frames[i] (host array of frame
+ * indices) verbatim into out[i] (host array of device frame descriptors of
+ * the clip's size and format), i < count, on `stream`.
+ * nnvisr_tensor_to_frames[_batch] skip outputs whose descriptor has
+ * plane[0] == NULL, so a dropped network output costs no traffic. */
+nnvisr_status nnvisr_copy_frames(nnvisr_handle *h, const int64_t *src_frames, const nnvisr_frame *out, int64_t count,
+                                 void *stream);
+
 /* ---- Batched shared frame store (§3.3 P:360-382 and Fig. 1;
  * SURVEY.md §8(f) NEXT-2).  A batch of b interpolation runs of n+1 frames
  * needs only b*n + 1 distinct frames; the store keeps each input slot's b

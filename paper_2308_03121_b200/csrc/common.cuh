@@ -294,6 +294,20 @@ __device__ __forceinline__ void f2t_store(const F2TArgs &a, const DstList &dl, c
     }
 }
 
+// t2f job -> (tuple, output slot): dense (job = tuple * M + slot) unless the
+// launch skips outputs (NEXT-1 emission), then an explicit code table.
+__device__ __forceinline__ void t2f_job(const T2FArgs &a, int job, int &tup, int &o)
+{
+    if (a.job_code) {
+        const int c = a.job_code[job];
+        tup = c >> 5;
+        o = c & 31;
+    } else {
+        tup = job / a.M;
+        o = job - tup * a.M;
+    }
+}
+
 // ------------------------------------------------------------ t2f colour
 template <typename T> struct T2FConst;
 // fp32: ys, yo, cs, co are divided by maxc (see quant)

@@ -70,6 +70,7 @@ struct F2TArgs {
 };
 
 struct T2FArgs {
+    const int32_t *job_code;  // optional [jobs]: tuple * 32 + slot (skipped outputs removed); null = dense
     const char *src;          // tensor of job 0's tuple
     int64_t tensor_stride;    // bytes between tuples' tensors
     const DevFrame *out;      // output frame descriptors [count*M] (device)

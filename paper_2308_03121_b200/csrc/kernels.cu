@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(kThreads) t2f_generic(const T2FArgs a)
         const int ru = unit / a.col_units;
         const int x0 = (unit - ru * a.col_units) * kPx;
         const int y0 = ru * ROWS;
-        const int tup = job / a.M, o = job - tup * a.M;
+        int tup, o;
+        t2f_job(a, job, tup, o);
         const TIN *src = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
                          static_cast<int64_t>(3 * o) * plane + static_cast<int64_t>(y0) * a.tw + x0;
         const int nvalid = min(kPx, a.Wo - x0);

@@ -433,7 +433,8 @@ __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *
     int job, ru, x0;
     decode_tile(t, a.rowunits, a.nseg, a.segw, job, ru, x0);
     const int x1 = min(x0 + a.segw, a.Wo);
-    const int tup = job / a.M, o = job - tup * a.M;
+    int tup, o;
+    t2f_job(a, job, tup, o);
     const int64_t plane = a.th * a.tw;
     const TIN *src = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
                      static_cast<int64_t>(3 * o) * plane + static_cast<int64_t>(ru * S::ROWS) * a.tw + x0;

@@ -89,6 +89,7 @@ struct nnvisr_handle {
     int64_t frames_cap = 0, frames_base = 0, frames_count = 0;
     bool frames_vec = false;
     int64_t frames_pitch_y = 0, frames_pitch_c = 0;  // uniform pitches of the bound frames, 0 if they differ
+    std::vector<nnvisr_frame> frames_host;            // host copy of the bound descriptors
     bool force_generic = false;  // NNVISR_FORCE_GENERIC=1: never take the TMA path (tests)
 };
 
@@ -575,6 +576,7 @@ nnvisr_status nnvisr_bind_frames(nnvisr_handle *h, int64_t base, const nnvisr_fr
     h->frames_count = count;
     h->frames_vec = vec;
     uniform_pitches(h, frames, count, h->frames_pitch_y, h->frames_pitch_c);
+    h->frames_host.assign(frames, frames + count);
     return NNVISR_OK;
 }
 
@@ -712,26 +714,53 @@ static nnvisr_status t2f_common(nnvisr_handle *h, const void *tensors, int64_t s
     if (!aligned16(tensors) || stride % 16) return fail(NNVISR_ERR_INVALID_ARG, "tensor / stride not 16-byte aligned");
     const int64_t tbytes = 3 * h->M * t_h * t_w * h->elem;
     if (count > 1 && stride < tbytes) return fail(NNVISR_ERR_INVALID_ARG, "tensor stride smaller than the tensor");
-    const int64_t jobs = count * h->M;
-    bool vec = true;
-    for (int64_t j = 0; j < jobs; ++j) {
+    // outputs whose descriptor has plane[0] == NULL are not converted (an
+    // output the emission schedule drops, NEXT-1)
+    const int64_t all_jobs = count * h->M;
+    std::vector<int32_t> codes;
+    std::vector<nnvisr_frame> kept;
+    bool vec = true, skipped = false;
+    for (int64_t j = 0; j < all_jobs; ++j) {
+        if (!out[j].plane[0]) {
+            skipped = true;
+            continue;
+        }
         nnvisr_status s = check_frame(h, out[j], h->Wo, h->Ho, "output frame", j, &vec);
         if (s) return s;
     }
+    if (skipped) {
+        if (count > (INT32_MAX >> 5)) return fail(NNVISR_ERR_INVALID_ARG, "too many tuples");
+        for (int64_t j = 0; j < all_jobs; ++j)
+            if (out[j].plane[0]) {
+                codes.push_back((int32_t)((j / h->M) * 32 + j % h->M));
+                kept.push_back(out[j]);
+            }
+    }
+    const int64_t jobs = skipped ? (int64_t)kept.size() : all_jobs;
+    const nnvisr_frame *desc = skipped ? kept.data() : out;
+    if (jobs == 0) return NNVISR_OK;
     nnvisr_status s = ensure_device(h);
     if (s) return s;
     T2FArgs a = t2f_args(h, t_h, t_w);
     a.tensor_stride = stride;
     a.vec_out = vec;
-    const int64_t per_slot = (int64_t)(kSlotBytes / sizeof(DevFrame)) / h->M * h->M;
+    const size_t per_job = sizeof(DevFrame) + (skipped ? sizeof(int32_t) : 0);
+    const int64_t per_slot = skipped ? (int64_t)(kSlotBytes / per_job) : (int64_t)(kSlotBytes / sizeof(DevFrame)) / h->M * h->M;
     for (int64_t j0 = 0; j0 < jobs; j0 += per_slot) {
         const int64_t nj = std::min(per_slot, jobs - j0);
         UploadSlot *slot = nullptr;
         if ((s = acquire_slot(h, &slot))) return s;
-        std::memcpy(slot->host, out + j0, sizeof(DevFrame) * nj);
-        if ((s = upload(slot, sizeof(DevFrame) * nj, st))) return s;
+        std::memcpy(slot->host, desc + j0, sizeof(DevFrame) * nj);
+        if (skipped) std::memcpy(static_cast<char *>(slot->host) + sizeof(DevFrame) * nj, codes.data() + j0, sizeof(int32_t) * nj);
+        if ((s = upload(slot, per_job * nj, st))) return s;
         a.out = static_cast<const DevFrame *>(slot->dev);
-        a.src = static_cast<const char *>(tensors) + (j0 / h->M) * stride;
+        if (skipped) {
+            a.job_code = reinterpret_cast<const int32_t *>(static_cast<char *>(slot->dev) + sizeof(DevFrame) * nj);
+            a.src = static_cast<const char *>(tensors);  // codes carry absolute tuple indices
+        } else {
+            a.job_code = nullptr;
+            a.src = static_cast<const char *>(tensors) + (j0 / h->M) * stride;
+        }
         s = run_t2f(h, a, nj, st);
         nnvisr_status s2 = release_slot(slot, st);
         if (s) return s;
@@ -889,6 +918,92 @@ nnvisr_status nnvisr_copy_slot(nnvisr_handle *h, void *store, int64_t src, int64
     cudaError_t e = cudaMemcpyAsync(base + dst * slot_bytes, base + src * slot_bytes, slot_bytes,
                                     cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync (slot copy)");
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_schedule_outputs(const nnvisr_handle *h, int64_t num_frames, const uint8_t *cut,
+                                      int32_t *source, int64_t *present, int64_t *run_first, int64_t cap_entries,
+                                      int64_t cap_runs, int64_t *num_entries, int64_t *num_runs)
+{
+    g_error.clear();
+    if (!h || !num_entries || !num_runs) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (num_frames < 0 || (num_frames > 0 && !cut)) return fail(NNVISR_ERR_INVALID_ARG, "bad cut array");
+    if ((cap_entries > 0 && (!source || !present)) || (cap_runs >= 0 && !run_first))
+        return fail(NNVISR_ERR_INVALID_ARG, "null output arrays");
+    const int N = h->N, n = h->n;
+    const int64_t R = std::max<int64_t>(num_frames, 1);
+    std::vector<int64_t> ins(R * N), fr(R * 2);
+    PlanSink sink{ins.data(), fr.data(), R, 0, N};
+    int64_t s0 = 0;
+    for (int64_t k = 1; k <= num_frames; ++k)
+        if (k == num_frames || cut[k]) {
+            plan_scene(h, s0, k, 0, num_frames, sink);
+            s0 = k;
+        }
+    const bool interp = h->net.flags & NNVISR_INTERPOLATION, dbl = h->net.flags & NNVISR_DOUBLE_FRAME;
+    int64_t e = 0;
+    for (int64_t r = 0; r < sink.count; ++r) {
+        if (r <= cap_runs) run_first[r] = e;
+        for (int64_t p = fr[2 * r]; p < fr[2 * r + 1]; ++p) {
+            int q = 0;  // consumed position of fresh frame p (sliding windows: the single output)
+            if (h->paper)
+                while (q < n - 1 && ins[r * N + q] != p) ++q;
+            auto put = [&](int32_t src, int64_t pres) {
+                if (e < cap_entries) {
+                    source[e] = src;
+                    present[e] = pres;
+                }
+                ++e;
+            };
+            if (!interp) {
+                put(h->paper ? q : 0, p);
+            } else if (!dbl) {
+                put(-(q + 1), 2 * p);
+                put(q, 2 * p + 1);
+            } else {
+                put(2 * q, 2 * p);
+                put(2 * q + 1, 2 * p + 1);
+            }
+        }
+    }
+    if (sink.count <= cap_runs) run_first[sink.count] = e;
+    *num_entries = e;
+    *num_runs = sink.count;
+    if (e > cap_entries || sink.count > cap_runs)
+        return fail(NNVISR_ERR_CAPACITY, "schedule needs %lld entries / %lld runs", (long long)e, (long long)sink.count);
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_copy_frames(nnvisr_handle *h, const int64_t *src_frames, const nnvisr_frame *out, int64_t count,
+                                 void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && (!src_frames || !out))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (count <= 0) return count < 0 ? fail(NNVISR_ERR_INVALID_ARG, "count < 0") : NNVISR_OK;
+    if (!h->frames) return fail(NNVISR_ERR_INVALID_ARG, "no frames bound (nnvisr_bind_frames)");
+    bool vec = true;
+    for (int64_t i = 0; i < count; ++i) {
+        const int64_t f = src_frames[i];
+        if (f < h->frames_base || f >= h->frames_base + h->frames_count)
+            return fail(NNVISR_ERR_INVALID_ARG, "copy %lld: frame %lld not bound", (long long)i, (long long)f);
+        nnvisr_status s = check_frame(h, out[i], h->fmt.width, h->fmt.height, "pass-through frame", i, &vec);
+        if (s) return s;
+    }
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    std::vector<nnvisr_frame> src(count);
+    for (int64_t i = 0; i < count; ++i) src[i] = h->frames_host[src_frames[i] - h->frames_base];
+    const int sb = h->fmt.bits == 8 ? 1 : 2;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int64_t i = 0; i < count; ++i) {
+        for (int p = 0; p < 3; ++p) {
+            const bool sub = h->fmt.family == NNVISR_YUV420 && p > 0;
+            const int64_t w = (sub ? h->fmt.width / 2 : h->fmt.width) * sb, rows = sub ? h->fmt.height / 2 : h->fmt.height;
+            cudaError_t e = cudaMemcpy2DAsync(out[i].plane[p], out[i].pitch[p], src[i].plane[p], src[i].pitch[p], w,
+                                              rows, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync (pass-through)");
+        }
+    }
     return NNVISR_OK;
 }
 

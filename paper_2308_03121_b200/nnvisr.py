@@ -59,6 +59,8 @@ def _load():
         "nnvisr_plan_batches": (st, [H, i64, C.c_void_p, C.c_int32, C.c_void_p, i64p, C.c_void_p, i64p, i64, i64p]),
         "nnvisr_frames_to_slots": (st, [H, i64p, i64, C.c_void_p, C.c_void_p]),
         "nnvisr_copy_slot": (st, [H, C.c_void_p, i64, i64, C.c_void_p]),
+        "nnvisr_schedule_outputs": (st, [H, i64, C.c_void_p, C.c_void_p, i64p, i64p, i64, i64, i64p, i64p]),
+        "nnvisr_copy_frames": (st, [H, i64p, C.POINTER(Frame), i64, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -72,7 +74,8 @@ EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version"
             "nnvisr_tensor_shapes", "nnvisr_plan", "nnvisr_plan_range", "nnvisr_bind_frames",
             "nnvisr_frames_to_tensor", "nnvisr_frames_to_tensor_batch", "nnvisr_frames_to_store",
             "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch", "nnvisr_scene_detect",
-            "nnvisr_shared_slot_offset", "nnvisr_plan_batches", "nnvisr_frames_to_slots", "nnvisr_copy_slot")
+            "nnvisr_shared_slot_offset", "nnvisr_plan_batches", "nnvisr_frames_to_slots", "nnvisr_copy_slot",
+            "nnvisr_schedule_outputs", "nnvisr_copy_frames")
 
 
 def lib():
@@ -215,6 +218,24 @@ class Handle:
             out.append(dict(shared=bool(sh[i]), lanes=lanes[i * b:(i + 1) * b].tolist(),
                             emit=[bool(e) for e in emit[i * b:(i + 1) * b]], slots=[int(v) for v in sl if v >= 0]))
         return out
+
+    def schedule_outputs(self, cut):
+        """nnvisr_schedule_outputs: per run a list of (source, presentation index)."""
+        cut = np.ascontiguousarray(np.asarray(cut, dtype=np.uint8))
+        F = cut.shape[0]
+        cap_e, cap_r = max(2 * F, 1), max(F, 1)
+        src = np.zeros(cap_e, np.int32)
+        pres = np.zeros(cap_e, np.int64)
+        first = np.zeros(cap_r + 1, np.int64)
+        ne, nr = C.c_int64(), C.c_int64()
+        _check(_lib.nnvisr_schedule_outputs(self._h, F, cut.ctypes.data if F else None, src.ctypes.data, _i64p(pres),
+                                            _i64p(first), cap_e, cap_r, C.byref(ne), C.byref(nr)))
+        return [[(int(src[e]), int(pres[e])) for e in range(first[r], first[r + 1])] for r in range(nr.value)]
+
+    def copy_frames(self, src_frames, out: Sequence[Frame], stream=None):
+        sf = np.ascontiguousarray(src_frames, dtype=np.int64)
+        arr = frame_array(out)
+        _check(_lib.nnvisr_copy_frames(self._h, _i64p(sf), arr, sf.size, _stream_ptr(stream)))
 
     def frames_to_slots(self, slot_frames, store_ptr: int, stream=None):
         sf = np.ascontiguousarray(slot_frames, dtype=np.int64)

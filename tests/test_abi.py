@@ -210,3 +210,26 @@ def test_shared_offsets_and_plan_batches_match_oracle():
         with pytest.raises(nv.NnvisrError) as e:
             h.plan_batches(np.zeros(8, np.uint8), 2)
         assert e.value.status == 3
+
+
+def test_schedule_outputs_matches_oracle():
+    """NEXT-1 host schedule (§3.1) equals the oracle's."""
+    from oracle import emission as E
+    rng = np.random.default_rng(12)
+    for trial in range(80):
+        n = int(rng.integers(1, 5))
+        interp = bool(trial % 2)
+        double = interp and bool(trial % 4 == 1)
+        extra = interp or bool(rng.integers(0, 2))
+        M = (2 * n + int(rng.integers(0, 2))) if double else n
+        flags = (nv.INTERPOLATION if interp else 0) | (nv.EXTRA_FRAME if extra else 0) | (nv.DOUBLE_FRAME if double else 0)
+        F = int(rng.integers(1, 50))
+        cut = (rng.random(F) < 0.12).astype(np.uint8)
+        with nv.open(_cfg(n=n, input_count=n + extra, output_count=M, left_context=0, flags=flags)) as h:
+            got = h.schedule_outputs(cut)
+        assert got == E.schedule_outputs(cut, n, n + extra, M, interp, double), (n, interp, double, extra, M)
+    # sliding windows: the single output is the fresh frame
+    with nv.open(_cfg(input_count=5, left_context=2)) as h:
+        cut = np.zeros(9, np.uint8)
+        cut[4] = 1
+        assert h.schedule_outputs(cut) == [[(0, t)] for t in range(9)]
