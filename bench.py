@@ -42,6 +42,9 @@ def parse():
                    help="materialize every tuple; store: frame-major store (sliding windows); batch: the paper's "
                         "Fig. 1 batched shared store (paper grouping, --batch lanes)")
     p.add_argument("--batch", type=int, default=8, help="lanes per batch for --f2t-mode batch")
+    p.add_argument("--emit", action="store_true",
+                   help="t2f converts only the outputs the emission schedule presents (NEXT-1; drops e.g. the "
+                        "trailing enhanced lookahead of M = 2n+1 networks), pass-through frames are copied")
     p.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--detect", action="store_true",
@@ -339,14 +342,29 @@ def main():
                     sel = runs[c0:c0 + fchunk]
                     timed("f2t", record, len(sel), len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz,
                           lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
+            sched = h.schedule_outputs(cut_win.cpu().numpy())[s.begin - s.window_first:] if args.emit else None
             for c0 in range(0, len(runs), tchunk):
                 nb = min(tchunk, len(runs) - c0)
                 o0 = (c0 // tchunk * tchunk) % n_out
                 if o0 + nb > n_out:
                     o0 = 0
-                timed("t2f", record, nb, nb * t2f_bytes,
-                      lambda o0=o0, nb=nb: h.tensor_to_frames_batch(tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo,
-                                                                    ofb_desc[:nb * M], nb, stream))
+                desc, nconv, copies = ofb_desc[:nb * M], nb * M, []
+                if args.emit:
+                    # presented outputs only; pass-through frames copied
+                    desc, nconv = [nv.Frame() for _ in range(nb * M)], 0
+                    for j in range(nb):
+                        for src, pres in sched[c0 + j]:
+                            if src >= 0:
+                                desc[j * M + src] = ofb_desc[j * M + src]
+                                nconv += 1
+                            else:
+                                copies.append((int(runs[c0 + j][-src - 1]), ofb_desc[j * M]))
+                nbytes = nconv * (out_elems // M * esz + olay.payload_bytes())
+                timed("t2f", record, nb, nbytes,
+                      lambda o0=o0, nb=nb, desc=desc: h.tensor_to_frames_batch(tens_out[o0].data_ptr(), out_elems * esz,
+                                                                              Ho, Wo, desc, nb, stream))
+                if copies:
+                    h.copy_frames([c[0] for c in copies], [c[1] for c in copies], stream)
         return len(runs)
 
     def barrier():
@@ -436,6 +454,7 @@ def main():
                        "clip_frames_per_rank": s.owned, "input_tensor": list(in_shape),
                        "output_tensor": list(out_shape), "tensor_dtype": "f16" if cfg.dtype == nv.F16 else "f32",
                        "tuples_per_launch": {"f2t": fchunk, "t2f": tchunk}, "f2t_mode": args.f2t_mode,
+                       "t2f_outputs": "emitted only (NEXT-1 schedule)" if args.emit else "all M slots per tuple",
                        "scene_flags": ("detected on the GPU each step (threshold %g)" % args.detect_threshold
                                        if args.detect else "given (synthetic cut pattern)"),
                        "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB, t2f input ring "
