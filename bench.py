@@ -478,10 +478,13 @@ def main():
 
 def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, in_elems, out_elems, esz, stream,
             dev, world, plan_local, scaling, frames_all):
-    """Same metric with the frames in pinned HOST memory: every step copies the
-    shard's frames host->device, runs f2t + t2f through the C ABI, and copies
-    every output frame device->host.  Copies run on their own streams and
-    overlap the kernels chunk by chunk."""
+    """Same metric with the frames in pinned HOST memory, through the C ABI's
+    host-buffer calls: nnvisr_frames_to_tensor_batch_host uploads each
+    chunk's frames (library staging + copy stream) and converts them,
+    nnvisr_tensor_to_frames_batch_host converts the network outputs and
+    downloads every output frame to pinned host memory; uploads, kernels and
+    downloads of consecutive chunks overlap.  Timed with CUDA events on the
+    working stream after nnvisr_host_fence (the downloads are complete)."""
     import torch
     import torch.distributed as dist
 
@@ -489,55 +492,35 @@ def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, i
 
     # pinned host copy of the shard's frames, capped at 256 frames (a 4K clip
     # would not fit in host RAM): frame i is uploaded from host slot i mod pool
-    pool = min(s.owned, 256)
-    host_in = win.data[s.left:s.left + pool].cpu().pin_memory()
+    pool = min(s.window_count, 256)
+    host_in = FrameBuffer(win.layout, pool, device="cpu", pin=True)
+    host_in.data.copy_(win.data[:pool].cpu())
+    host_desc = host_in.descriptors()
     M = h.M
     Ho, Wo = h.out_shape[2], h.out_shape[3]
-    ring = 2
-    dev_out = [FrameBuffer(ofb.layout, chunk * M, device=dev) for _ in range(ring)]
-    dev_out_desc = [b.descriptors() for b in dev_out]
-    host_out = [torch.empty((chunk * M, ofb.layout.frame_bytes), dtype=torch.uint8).pin_memory() for _ in range(ring)]
-    s_in = torch.cuda.Stream(device=dev)
-    s_out = torch.cuda.Stream(device=dev)
+    host_out = [FrameBuffer(ofb.layout, chunk * M, device="cpu", pin=True) for _ in range(2)]
+    host_out_desc = [b.descriptors() for b in host_out]
     runs, _ = plan_local()
-    R = s.right
+    frame_payload = win.layout.payload_bytes()
+    out_payload = ofb.layout.payload_bytes()
 
     def e2e_step():
-        n_done = 0
-        ev_out = [None] * ring
+        h2d = d2h = 0
         for ci, c0 in enumerate(range(0, len(runs), chunk)):
             sel = runs[c0:c0 + chunk]
             nb = len(sel)
-            # frames this chunk needs that have not been uploaded yet
-            hi = min(s.owned, c0 + nb + R)
-            if hi > n_done:
-                with torch.cuda.stream(s_in):
-                    while n_done < hi:  # contiguous host runs of the pool
-                        a0 = n_done % pool
-                        n = min(hi - n_done, pool - a0)
-                        win.data[s.left + n_done:s.left + n_done + n].copy_(host_in[a0:a0 + n], non_blocking=True)
-                        n_done += n
-            ready = torch.cuda.Event()
-            ready.record(s_in)
-            stream.wait_event(ready)
-            k = ci % ring
-            if ev_out[k] is not None:
-                stream.wait_event(ev_out[k])  # the D2H of this ring slot finished
-            with torch.cuda.stream(stream):
-                h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream)
-                o0 = (c0 // chunk * chunk) % n_out
-                if o0 + nb > n_out:
-                    o0 = 0
-                h.tensor_to_frames_batch(tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo, dev_out_desc[k][:nb * M],
-                                         nb, stream)
-            done = torch.cuda.Event()
-            done.record(stream)
-            s_out.wait_event(done)
-            with torch.cuda.stream(s_out):
-                host_out[k][:nb * M].copy_(dev_out[k].data[:nb * M], non_blocking=True)
-            ev_out[k] = torch.cuda.Event()
-            ev_out[k].record(s_out)
-        return len(runs)
+            lo, hi = int(sel.min()), int(sel.max()) + 1
+            frames = [host_desc[(f - s.window_first) % pool] for f in range(lo, hi)]
+            h.frames_to_tensor_batch_host(frames, lo, sel, tens_in.data_ptr(), in_elems * esz, stream)
+            o0 = (c0 // chunk * chunk) % n_out
+            if o0 + nb > n_out:
+                o0 = 0
+            h.tensor_to_frames_batch_host(tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo,
+                                          host_out_desc[ci % 2][:nb * M], nb, stream)
+            h2d += (hi - lo) * frame_payload
+            d2h += nb * M * out_payload
+        h.host_fence(stream)
+        return h2d, d2h
 
     for _ in range(2):
         e2e_step()
@@ -548,24 +531,19 @@ def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, i
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    s_in.wait_event(t0)
     for _ in range(steps):
-        e2e_step()
-    s_out_done = torch.cuda.Event()
-    s_out_done.record(s_out)
-    stream.wait_event(s_out_done)
+        h2d, d2h = e2e_step()
     t1.record(stream)
     torch.cuda.synchronize(dev)
     ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    h2d = s.owned * win.layout.frame_bytes
-    d2h = len(runs) * M * ofb.layout.frame_bytes
     return {"value": frames_all * steps / (ms / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": ms / steps, "steps": steps,
-            "path": "pinned host frames -> nnvisr_frames_to_tensor_batch -> nnvisr_tensor_to_frames_batch -> "
-                    "pinned host frames (copies on side streams, overlapped per chunk)"}
+            "path": "pinned host frames -> nnvisr_frames_to_tensor_batch_host -> network-output tensors -> "
+                    "nnvisr_tensor_to_frames_batch_host -> pinned host frames (library staging + copy streams, "
+                    "uploads/kernels/downloads of consecutive chunks overlapped)"}
 
 
 if __name__ == "__main__":

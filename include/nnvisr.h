@@ -204,6 +204,33 @@ nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensor
                                             int64_t t_w, const nnvisr_frame *out, int64_t count,
                                             void *stream);
 
+/* ---- Host-buffer calls: the frames live in (pinned) host memory.  The
+ * library stages them through two device staging slots per direction and
+ * two internal copy streams, so the uploads of call i+1 and the downloads of
+ * call i-1 overlap the kernels of call i on `stream`. */
+
+/* frames -> tensor from host frames: host_frames[i] (host plane pointers,
+ * pinned memory for asynchronous copies) is frame base+i, i < count; every
+ * frame index in run_inputs [num_runs*N] must lie in [base, base+count).
+ * The frames are copied to the device, then converted as by
+ * nnvisr_frames_to_tensor_batch into the device tensors on `stream`.  The
+ * host frames must stay valid until that work has run. */
+nnvisr_status nnvisr_frames_to_tensor_batch_host(nnvisr_handle *h, const nnvisr_frame *host_frames, int64_t base,
+                                                 int64_t count, const int64_t *run_inputs, int64_t num_runs,
+                                                 void *tensors, int64_t tensor_stride_bytes, void *stream);
+
+/* tensor -> frames into host frames: as nnvisr_tensor_to_frames_batch, the
+ * output of tensor c slot o landing in host_out[c*M + o] (host plane
+ * pointers; plane[0] == NULL = not presented, not converted).  The download
+ * runs on an internal stream: call nnvisr_host_fence before synchronising
+ * `stream` to read the host frames. */
+nnvisr_status nnvisr_tensor_to_frames_batch_host(nnvisr_handle *h, const void *tensors, int64_t tensor_stride_bytes,
+                                                 int64_t t_h, int64_t t_w, const nnvisr_frame *host_out, int64_t count,
+                                                 void *stream);
+
+/* Make `stream` wait until every host download enqueued so far is complete. */
+nnvisr_status nnvisr_host_fence(nnvisr_handle *h, void *stream);
+
 /* ---- Output emission (§3.1 P:251-261:
  * "Interpolation ... produce output video in doubled framerate"; without
  * "Double frame", "input frames are also used as output frames as is, and

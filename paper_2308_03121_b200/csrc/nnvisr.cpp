@@ -90,6 +90,20 @@ struct nnvisr_handle {
     bool frames_vec = false;
     int64_t frames_pitch_y = 0, frames_pitch_c = 0;  // uniform pitches of the bound frames, 0 if they differ
     std::vector<nnvisr_frame> frames_host;            // host copy of the bound descriptors
+    // host-buffer calls (nnvisr_*_host): device staging rings and copy streams
+    struct Stage {
+        void *data = nullptr;       // packed frames
+        DevFrame *table = nullptr;  // device descriptors of the staged frames
+        std::vector<nnvisr_frame> desc;
+        int64_t cap = 0;
+        cudaEvent_t free_ev = nullptr, ready_ev = nullptr;
+        bool used = false;
+    };
+    Stage in_stage[2], out_stage[2];
+    int in_next = 0, out_next = 0;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t d2h_last = nullptr;
+    bool d2h_any = false;
     bool force_generic = false;  // NNVISR_FORCE_GENERIC=1: never take the TMA path (tests)
 };
 
@@ -276,6 +290,19 @@ nnvisr_status nnvisr_close(nnvisr_handle *h)
             if (s.dev) cudaFree(s.dev);
         }
         if (h->frames) cudaFree(h->frames);
+        if (h->h2d) cudaStreamSynchronize(h->h2d);
+        if (h->d2h) cudaStreamSynchronize(h->d2h);
+        for (auto *ring : {h->in_stage, h->out_stage})
+            for (int i = 0; i < 2; ++i) {
+                auto &g = ring[i];
+                if (g.data) cudaFree(g.data);
+                if (g.table) cudaFree(g.table);
+                if (g.free_ev) cudaEventDestroy(g.free_ev);
+                if (g.ready_ev) cudaEventDestroy(g.ready_ev);
+            }
+        if (h->h2d) cudaStreamDestroy(h->h2d);
+        if (h->d2h) cudaStreamDestroy(h->d2h);
+        if (h->d2h_last) cudaEventDestroy(h->d2h_last);
         if (prev >= 0 && prev != h->device) cudaSetDevice(prev);
     }
     delete h;
@@ -623,27 +650,45 @@ nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, 
     return s ? s : s2;
 }
 
+// The frames a batched f2t reads: the bound table, or a host-call staging ring.
+struct FrameTable {
+    const DevFrame *dev;
+    int64_t base;
+    bool vec;
+    int64_t pitch_y, pitch_c;
+};
+
+static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, const int64_t *frame_idx,
+                                       int64_t runs, int per_run, void *dst, int64_t run_stride, cudaStream_t st);
+
 static nnvisr_status f2t_indexed(nnvisr_handle *h, const int64_t *frame_idx, int64_t runs, int per_run,
                                  void *dst, int64_t run_stride, cudaStream_t st)
 {
     if (!h->frames) return fail(NNVISR_ERR_INVALID_ARG, "no frames bound (nnvisr_bind_frames)");
+    const FrameTable tab{h->frames, h->frames_base, h->frames_vec, h->frames_pitch_y, h->frames_pitch_c};
+    return f2t_indexed_table(h, tab, frame_idx, runs, per_run, dst, run_stride, st);
+}
+
+static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, const int64_t *frame_idx,
+                                       int64_t runs, int per_run, void *dst, int64_t run_stride, cudaStream_t st)
+{
     // an upload slot holds 3 ints per (run, slot) plus one; runs per launch
     // are also bounded by the 5-bit slot / run encoding of dst_code
     const int64_t max_runs = std::min<int64_t>((int64_t)(kSlotBytes / sizeof(int32_t) - 1) / (3 * per_run),
                                                (int64_t)(INT32_MAX / 32));
     F2TArgs a = f2t_args(h);
-    a.frames = h->frames;
+    a.frames = tab.dev;
     a.run_stride = run_stride;
-    a.vec_in = h->frames_vec;
-    a.pitch_y = h->frames_pitch_y;
-    a.pitch_c = h->frames_pitch_c;
+    a.vec_in = tab.vec;
+    a.pitch_y = tab.pitch_y;
+    a.pitch_c = tab.pitch_c;
     for (int64_t r0 = 0; r0 < runs; r0 += max_runs) {
         const int64_t nr = std::min(max_runs, runs - r0);
         UploadSlot *slot = nullptr;
         nnvisr_status s = acquire_slot(h, &slot);
         if (s) return s;
-        int32_t *tab = static_cast<int32_t *>(slot->host);
-        const int64_t J = build_f2t_jobs(frame_idx + r0 * per_run, nr, per_run, h->frames_base, tab);
+        int32_t *tbl = static_cast<int32_t *>(slot->host);
+        const int64_t J = build_f2t_jobs(frame_idx + r0 * per_run, nr, per_run, tab.base, tbl);
         if (J == 0) {
             release_slot(slot, st);
             continue;
@@ -1004,6 +1049,180 @@ nnvisr_status nnvisr_copy_frames(nnvisr_handle *h, const int64_t *src_frames, co
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync (pass-through)");
         }
     }
+    return NNVISR_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------- host-buffer calls
+namespace {
+
+// Packed staging layout of one frame (w x hgt, the clip's family and depth):
+// planes at 16-byte aligned offsets with 16-byte aligned pitches.
+struct PackedLayout {
+    int64_t off[3], pitch[3], rows[3], row_bytes[3], frame_bytes;
+    PackedLayout(const nnvisr_handle *h, int64_t w, int64_t hgt)
+    {
+        const int sb = h->fmt.bits == 8 ? 1 : 2;
+        int64_t o = 0;
+        for (int p = 0; p < 3; ++p) {
+            const bool sub = h->fmt.family == NNVISR_YUV420 && p > 0;
+            row_bytes[p] = (sub ? w / 2 : w) * sb;
+            rows[p] = sub ? hgt / 2 : hgt;
+            pitch[p] = round_up(row_bytes[p], 16);
+            off[p] = o;
+            o = round_up(o + pitch[p] * rows[p], 16);
+        }
+        frame_bytes = round_up(o, 256);
+    }
+};
+
+nnvisr_status ensure_streams(nnvisr_handle *h)
+{
+    cudaError_t e;
+    if (!h->h2d && (e = cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(e, "cudaStreamCreate (h2d)");
+    if (!h->d2h && (e = cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(e, "cudaStreamCreate (d2h)");
+    if (!h->d2h_last && (e = cudaEventCreateWithFlags(&h->d2h_last, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "cudaEventCreate");
+    return NNVISR_OK;
+}
+
+// Grow a staging slot to `count` frames of layout L (device memory + device
+// descriptor table); growing waits for the device to drain.
+nnvisr_status ensure_stage(nnvisr_handle::Stage &g, int64_t count, const PackedLayout &L)
+{
+    cudaError_t e;
+    if (!g.free_ev) {
+        if ((e = cudaEventCreateWithFlags(&g.free_ev, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&g.ready_ev, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "cudaEventCreate (stage)");
+    }
+    if (count > g.cap || (count && g.desc.size() && g.desc[0].pitch[0] != L.pitch[0])) {
+        if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_fail(e, "staging resize");
+        if (g.data) cudaFree(g.data);
+        if (g.table) cudaFree(g.table);
+        g.data = nullptr;
+        g.table = nullptr;
+        g.cap = 0;
+        if ((e = cudaMalloc(&g.data, L.frame_bytes * count)) != cudaSuccess) return cuda_fail(e, "cudaMalloc (staging)");
+        if ((e = cudaMalloc(&g.table, sizeof(DevFrame) * count)) != cudaSuccess)
+            return cuda_fail(e, "cudaMalloc (staging table)");
+        g.desc.resize(count);
+        for (int64_t i = 0; i < count; ++i)
+            for (int p = 0; p < 3; ++p) {
+                g.desc[i].plane[p] = static_cast<char *>(g.data) + i * L.frame_bytes + L.off[p];
+                g.desc[i].pitch[p] = L.pitch[p];
+            }
+        if ((e = cudaMemcpy(g.table, g.desc.data(), sizeof(DevFrame) * count, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return cuda_fail(e, "cudaMemcpy (staging table)");
+        g.cap = count;
+    }
+    return NNVISR_OK;
+}
+
+nnvisr_status copy_frame_planes(const nnvisr_frame &dst, const nnvisr_frame &src, const PackedLayout &L,
+                                cudaMemcpyKind kind, cudaStream_t st)
+{
+    for (int p = 0; p < 3; ++p) {
+        cudaError_t e = cudaMemcpy2DAsync(dst.plane[p], dst.pitch[p], src.plane[p], src.pitch[p], L.row_bytes[p],
+                                          L.rows[p], kind, st);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy2DAsync (host frames)");
+    }
+    return NNVISR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+nnvisr_status nnvisr_frames_to_tensor_batch_host(nnvisr_handle *h, const nnvisr_frame *host_frames, int64_t base,
+                                                 int64_t count, const int64_t *run_inputs, int64_t num_runs,
+                                                 void *tensors, int64_t tensor_stride_bytes, void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && !host_frames) || (num_runs > 0 && (!run_inputs || !tensors)))
+        return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (count < 0 || num_runs < 0) return fail(NNVISR_ERR_INVALID_ARG, "negative count");
+    if (num_runs == 0) return NNVISR_OK;
+    if (!aligned16(tensors) || tensor_stride_bytes % 16)
+        return fail(NNVISR_ERR_INVALID_ARG, "tensors / stride not 16-byte aligned");
+    const int64_t tbytes = 3 * h->N * h->Hp * h->Wp * h->elem;
+    if (num_runs > 1 && tensor_stride_bytes < tbytes) return fail(NNVISR_ERR_INVALID_ARG, "tensor stride too small");
+    for (int64_t j = 0; j < num_runs * h->N; ++j)
+        if (run_inputs[j] < base || run_inputs[j] >= base + count)
+            return fail(NNVISR_ERR_INVALID_ARG, "run %lld: frame %lld not among the host frames [%lld, %lld)",
+                        (long long)(j / h->N), (long long)run_inputs[j], (long long)base, (long long)(base + count));
+    for (int64_t i = 0; i < count; ++i)
+        for (int p = 0; p < 3; ++p)
+            if (!host_frames[i].plane[p]) return fail(NNVISR_ERR_INVALID_ARG, "host frame %lld: null plane", (long long)i);
+    nnvisr_status s = ensure_device(h);
+    if (s || (s = ensure_streams(h))) return s;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const PackedLayout L(h, h->fmt.width, h->fmt.height);
+    auto &g = h->in_stage[h->in_next];
+    h->in_next ^= 1;
+    if ((s = ensure_stage(g, count, L))) return s;
+    cudaError_t e;
+    // the kernels that last read this staging slot must be done before the upload
+    if (g.used && (e = cudaStreamWaitEvent(h->h2d, g.free_ev, 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    for (int64_t i = 0; i < count; ++i)
+        if ((s = copy_frame_planes(g.desc[i], host_frames[i], L, cudaMemcpyHostToDevice, h->h2d))) return s;
+    if ((e = cudaEventRecord(g.ready_ev, h->h2d)) != cudaSuccess || (e = cudaStreamWaitEvent(st, g.ready_ev, 0)) != cudaSuccess)
+        return cuda_fail(e, "upload event");
+    const FrameTable tab{g.table, base, true, L.pitch[0], L.pitch[1]};
+    s = f2t_indexed_table(h, tab, run_inputs, num_runs, h->N, tensors, tensor_stride_bytes, st);
+    if (s) return s;
+    if ((e = cudaEventRecord(g.free_ev, st)) != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    g.used = true;
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_tensor_to_frames_batch_host(nnvisr_handle *h, const void *tensors, int64_t tensor_stride_bytes,
+                                                 int64_t t_h, int64_t t_w, const nnvisr_frame *host_out, int64_t count,
+                                                 void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && (!tensors || !host_out))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
+    if (count == 0) return NNVISR_OK;
+    nnvisr_status s = ensure_device(h);
+    if (s || (s = ensure_streams(h))) return s;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t jobs = count * h->M;
+    const PackedLayout L(h, h->Wo, h->Ho);
+    auto &g = h->out_stage[h->out_next];
+    h->out_next ^= 1;
+    if ((s = ensure_stage(g, jobs, L))) return s;
+    cudaError_t e;
+    // the download that last read this staging slot must be done before t2f rewrites it
+    if (g.used && (e = cudaStreamWaitEvent(st, g.free_ev, 0)) != cudaSuccess) return cuda_fail(e, "wait");
+    std::vector<nnvisr_frame> dev_out(jobs);
+    for (int64_t j = 0; j < jobs; ++j) {
+        dev_out[j] = g.desc[j];
+        if (!host_out[j].plane[0]) dev_out[j].plane[0] = nullptr;  // output not presented
+    }
+    if ((s = t2f_common(h, tensors, tensor_stride_bytes, t_h, t_w, dev_out.data(), count, st))) return s;
+    if ((e = cudaEventRecord(g.ready_ev, st)) != cudaSuccess || (e = cudaStreamWaitEvent(h->d2h, g.ready_ev, 0)) != cudaSuccess)
+        return cuda_fail(e, "download event");
+    for (int64_t j = 0; j < jobs; ++j)
+        if (host_out[j].plane[0] && (s = copy_frame_planes(host_out[j], g.desc[j], L, cudaMemcpyDeviceToHost, h->d2h)))
+            return s;
+    if ((e = cudaEventRecord(g.free_ev, h->d2h)) != cudaSuccess || (e = cudaEventRecord(h->d2h_last, h->d2h)) != cudaSuccess)
+        return cuda_fail(e, "cudaEventRecord");
+    g.used = true;
+    h->d2h_any = true;
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_host_fence(nnvisr_handle *h, void *stream)
+{
+    g_error.clear();
+    if (!h) return fail(NNVISR_ERR_INVALID_ARG, "null handle");
+    if (!h->d2h_any) return NNVISR_OK;
+    cudaError_t e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), h->d2h_last, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamWaitEvent");
     return NNVISR_OK;
 }
 

@@ -61,6 +61,10 @@ def _load():
         "nnvisr_copy_slot": (st, [H, C.c_void_p, i64, i64, C.c_void_p]),
         "nnvisr_schedule_outputs": (st, [H, i64, C.c_void_p, C.c_void_p, i64p, i64p, i64, i64, i64p, i64p]),
         "nnvisr_copy_frames": (st, [H, i64p, C.POINTER(Frame), i64, C.c_void_p]),
+        "nnvisr_frames_to_tensor_batch_host": (st, [H, C.POINTER(Frame), i64, i64, i64p, i64, C.c_void_p, i64,
+                                                    C.c_void_p]),
+        "nnvisr_tensor_to_frames_batch_host": (st, [H, C.c_void_p, i64, i64, i64, C.POINTER(Frame), i64, C.c_void_p]),
+        "nnvisr_host_fence": (st, [H, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -75,7 +79,8 @@ EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version"
             "nnvisr_frames_to_tensor", "nnvisr_frames_to_tensor_batch", "nnvisr_frames_to_store",
             "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch", "nnvisr_scene_detect",
             "nnvisr_shared_slot_offset", "nnvisr_plan_batches", "nnvisr_frames_to_slots", "nnvisr_copy_slot",
-            "nnvisr_schedule_outputs", "nnvisr_copy_frames")
+            "nnvisr_schedule_outputs", "nnvisr_copy_frames", "nnvisr_frames_to_tensor_batch_host",
+            "nnvisr_tensor_to_frames_batch_host", "nnvisr_host_fence")
 
 
 def lib():
@@ -231,6 +236,22 @@ class Handle:
         _check(_lib.nnvisr_schedule_outputs(self._h, F, cut.ctypes.data if F else None, src.ctypes.data, _i64p(pres),
                                             _i64p(first), cap_e, cap_r, C.byref(ne), C.byref(nr)))
         return [[(int(src[e]), int(pres[e])) for e in range(first[r], first[r + 1])] for r in range(nr.value)]
+
+    def frames_to_tensor_batch_host(self, host_frames: Sequence[Frame], base: int, run_inputs, tensors_ptr: int,
+                                    stride: int, stream=None):
+        ri = np.ascontiguousarray(run_inputs, dtype=np.int64)
+        arr = frame_array(host_frames)
+        _check(_lib.nnvisr_frames_to_tensor_batch_host(self._h, arr, base, len(host_frames), _i64p(ri),
+                                                       ri.size // self.N, tensors_ptr, stride, _stream_ptr(stream)))
+
+    def tensor_to_frames_batch_host(self, tensors_ptr: int, stride: int, t_h: int, t_w: int,
+                                    host_out: Sequence[Frame], count: int, stream=None):
+        arr = frame_array(host_out)
+        _check(_lib.nnvisr_tensor_to_frames_batch_host(self._h, tensors_ptr, stride, t_h, t_w, arr, count,
+                                                       _stream_ptr(stream)))
+
+    def host_fence(self, stream=None):
+        _check(_lib.nnvisr_host_fence(self._h, _stream_ptr(stream)))
 
     def copy_frames(self, src_frames, out: Sequence[Frame], stream=None):
         sf = np.ascontiguousarray(src_frames, dtype=np.int64)
