@@ -20,6 +20,10 @@
  *   oracle_f2t             pinned (textbook matrices, round trip, chroma ramp)
  *   oracle_t2f             pinned (colour-bar code table, gray axis, round trip)
  *   oracle_half_from_double pinned (numpy float16 RNE conversion)
+ *   oracle_f2t_sited / oracle_t2f_sited (LEFT siting) pinned (co-sited linear
+ *                          fields, LEFT == 4:4:4 path, down/up identity)
+ *   oracle_f2t_yuv / oracle_t2f_yuv pinned (range endpoints, affine shape,
+ *                          gray vs RGB path, exact round trip, B4 specials)
  *   chroma siting / padding / channel order / even-N centring: conventions,
  *   "parity unpinned" beyond internal consistency (readings A5-A8).
  */
@@ -237,16 +241,20 @@ static int64_t clampi(int64_t v, int64_t lo, int64_t hi)
     return v < lo ? lo : (v > hi ? hi : v);
 }
 
-/* ---- A4/A5-reading: centre-sited bilinear 4:2:0 -> 4:4:4 upsample --------
- * Chroma sample i sits at luma coordinate 2i + 1/2 on each axis (centre
- * siting, reading A5).  Luma sample x sees chroma coordinate u = (x - 1/2)/2;
- * linear interpolation between floor(u) and floor(u)+1 with indices clamped
- * to the plane (edge replication).  Weights are 1/4 and 3/4, dyadic, so every
- * product and sum below is exact in double. */
-static double chroma_up(const void *plane, int64_t pitch, int bits,
+/* ---- reading A5: 4:2:0 -> 4:4:4 bilinear upsample with edge clamp --------
+ * CENTER siting: chroma sample i sits at luma coordinate 2i + 1/2 on each
+ * axis, so luma sample x sees chroma coordinate u = (x - 1/2)/2.
+ * LEFT (MPEG-2) siting: horizontally co-sited with luma column 2i (u = x/2),
+ * vertically centred like CENTER (SPEC.md chroma_up_420).
+ * Linear interpolation between floor(u) and floor(u)+1 with indices clamped
+ * to the plane (edge replication).  The weights (0, 1/4, 1/2, 3/4) are
+ * dyadic, so every product and sum below is exact in double. */
+enum { OR_CHROMA_CENTER = 0, OR_CHROMA_LEFT = 1 };
+
+static double chroma_up(const void *plane, int64_t pitch, int bits, int siting,
                         int64_t cw, int64_t ch, int64_t x, int64_t y)
 {
-    double u = (x - 0.5) / 2.0, v = (y - 0.5) / 2.0;
+    double u = (siting == OR_CHROMA_LEFT) ? x / 2.0 : (x - 0.5) / 2.0, v = (y - 0.5) / 2.0;
     int64_t i0 = (int64_t)floor(u), j0 = (int64_t)floor(v);
     double fu = u - (double)i0, fv = v - (double)j0;
     double top = (1.0 - fu) * sample_at(plane, pitch, bits, clampi(i0, 0, cw - 1), clampi(j0, 0, ch - 1))
@@ -339,9 +347,10 @@ static int check_format(const oracle_format *f)
  * channels 3t, 3t+1, 3t+2 = R', G', B' (reading A7).  Pixels outside W x H
  * (the alignment padding, reading A6) take the values of the clamped
  * position, i.e. they replicate the last row / column. */
-int oracle_f2t(const oracle_format *f, int N, const void *const *planes,
-               const int64_t *pitches, int64_t Hp, int64_t Wp, int dtype, void *out)
+int oracle_f2t_sited(const oracle_format *f, int siting, int N, const void *const *planes,
+                     const int64_t *pitches, int64_t Hp, int64_t Wp, int dtype, void *out)
 {
+    if (siting != OR_CHROMA_CENTER && siting != OR_CHROMA_LEFT) return -1;
     if (check_format(f) || N < 1 || Hp < f->height || Wp < f->width) return -1;
     if (dtype != OR_F32 && dtype != OR_F16) return -1;
     double kr = 0, kb = 0;
@@ -363,8 +372,8 @@ int oracle_f2t(const oracle_format *f, int N, const void *const *planes,
                 } else {
                     double cy = sample_at(p0, s0, f->bits, xc, yc), cu, cv;
                     if (f->family == OR_YUV420) {
-                        cu = chroma_up(p1, s1, f->bits, cw, ch, xc, yc);
-                        cv = chroma_up(p2, s2, f->bits, cw, ch, xc, yc);
+                        cu = chroma_up(p1, s1, f->bits, siting, cw, ch, xc, yc);
+                        cv = chroma_up(p2, s2, f->bits, siting, cw, ch, xc, yc);
                     } else {
                         cu = sample_at(p1, s1, f->bits, xc, yc);
                         cv = sample_at(p2, s2, f->bits, xc, yc);
@@ -393,6 +402,20 @@ int oracle_f2t(const oracle_format *f, int N, const void *const *planes,
     return 0;
 }
 
+/* Pb, Pr of tensor pixel (x, y) of the output slot whose channels start at
+ * cbase: Y' = G + Kr (R - G) + Kb (B - G), Pb = (B - Y')/(2(1 - Kb)),
+ * Pr = (R - Y')/(2(1 - Kr)). */
+static void pixel_pbpr(const void *tensor, int dtype, int64_t cbase, int64_t plane_elems, int64_t tw,
+                       int64_t x, int64_t y, double kr, double kb, double *pb, double *pr)
+{
+    double R = load_tensor(tensor, dtype, cbase + y * tw + x);
+    double G = load_tensor(tensor, dtype, cbase + plane_elems + y * tw + x);
+    double B = load_tensor(tensor, dtype, cbase + 2 * plane_elems + y * tw + x);
+    double Y = G + kr * (R - G) + kb * (B - G);
+    *pb = (B - Y) / (2.0 * (1.0 - kb));
+    *pr = (R - Y) / (2.0 * (1.0 - kr));
+}
+
 /* ---- tensor -> frames (north_star "tensor->frames": "RGB->YUV matrix,
  * chroma downsampling, scale, round-half-even and clamp").
  *
@@ -404,9 +427,10 @@ int oracle_f2t(const oracle_format *f, int N, const void *const *planes,
  *   4:2:0: Pb, Pr of the 2x2 block {(2i,2j),(2i+1,2j),(2i,2j+1),(2i+1,2j+1)}
  *          averaged as ((a + b) + (c + d)) / 4  (reading A5 centre siting, A13)
  *   quantise (limited/full, readings A2/A3/A4). */
-int oracle_t2f(const oracle_format *fo, int M, const void *tensor, int dtype,
-               int64_t th, int64_t tw, void *const *planes, const int64_t *pitches)
+int oracle_t2f_sited(const oracle_format *fo, int siting, int M, const void *tensor, int dtype,
+                     int64_t th, int64_t tw, void *const *planes, const int64_t *pitches)
 {
+    if (siting != OR_CHROMA_CENTER && siting != OR_CHROMA_LEFT) return -1;
     if (check_format(fo) || M < 1 || th < fo->height || tw < fo->width) return -1;
     if (dtype != OR_F32 && dtype != OR_F16) return -1;
     double kr = 0, kb = 0;
@@ -443,22 +467,121 @@ int oracle_t2f(const oracle_format *fo, int M, const void *tensor, int dtype,
         if (fo->family != OR_YUV420) continue;
         for (int64_t j = 0; j < Ho / 2; ++j) {
             for (int64_t i = 0; i < Wo / 2; ++i) {
-                double pb[4], pr[4];
-                for (int k = 0; k < 4; ++k) {
-                    int64_t x = 2 * i + (k & 1), y = 2 * j + (k >> 1);
-                    double R = load_tensor(tensor, dtype, cbase + y * tw + x);
-                    double G = load_tensor(tensor, dtype, cbase + plane_elems + y * tw + x);
-                    double B = load_tensor(tensor, dtype, cbase + 2 * plane_elems + y * tw + x);
-                    double Y = G + kr * (R - G) + kb * (B - G);
-                    pb[k] = (B - Y) / (2.0 * (1.0 - kb));
-                    pr[k] = (R - Y) / (2.0 * (1.0 - kr));
+                double mb, mr;
+                if (siting == OR_CHROMA_CENTER) {
+                    double pb[4], pr[4];
+                    for (int k = 0; k < 4; ++k) {
+                        int64_t x = 2 * i + (k & 1), y = 2 * j + (k >> 1);
+                        pixel_pbpr(tensor, dtype, cbase, plane_elems, tw, x, y, kr, kb, &pb[k], &pr[k]);
+                    }
+                    mb = ((pb[0] + pb[1]) + (pb[2] + pb[3])) / 4.0;
+                    mr = ((pr[0] + pr[1]) + (pr[2] + pr[3])) / 4.0;
+                } else {
+                    /* LEFT (MPEG-2): chroma i sits on luma column 2i and
+                     * between rows 2j and 2j+1: per row the [1,2,1]/4
+                     * low-pass at column 2i (column 2i-1 clamped to 0),
+                     * then the mean of the two rows (reading A5). */
+                    double hb[2], hr[2];
+                    for (int r = 0; r < 2; ++r) {
+                        double b3[3], r3[3];
+                        for (int k = 0; k < 3; ++k) {
+                            int64_t x = clampi(2 * i - 1 + k, 0, Wo - 1);
+                            pixel_pbpr(tensor, dtype, cbase, plane_elems, tw, x, 2 * j + r, kr, kb, &b3[k], &r3[k]);
+                        }
+                        hb[r] = (b3[0] + 2.0 * b3[1]) + b3[2];
+                        hr[r] = (r3[0] + 2.0 * r3[1]) + r3[2];
+                    }
+                    mb = (hb[0] + hb[1]) / 8.0;
+                    mr = (hr[0] + hr[1]) / 8.0;
                 }
-                double mb = ((pb[0] + pb[1]) + (pb[2] + pb[3])) / 4.0;
-                double mr = ((pr[0] + pr[1]) + (pr[2] + pr[3])) / 4.0;
                 store_sample(p1, s1, bits, i, j, quant_chroma(mb, bits, range));
                 store_sample(p2, s2, bits, i, j, quant_chroma(mr, bits, range));
             }
         }
+    }
+    fesetround(old_round);
+    return 0;
+}
+
+int oracle_f2t(const oracle_format *f, int N, const void *const *planes,
+               const int64_t *pitches, int64_t Hp, int64_t Wp, int dtype, void *out)
+{
+    return oracle_f2t_sited(f, OR_CHROMA_CENTER, N, planes, pitches, Hp, Wp, dtype, out);
+}
+
+int oracle_t2f(const oracle_format *fo, int M, const void *tensor, int dtype,
+               int64_t th, int64_t tw, void *const *planes, const int64_t *pitches)
+{
+    return oracle_t2f_sited(fo, OR_CHROMA_CENTER, M, tensor, dtype, th, tw, planes, pitches);
+}
+
+/* ---- YUV-native network tensors (§3.1: "NNVISR supports
+ * input and output in both RGB and YUV pixel format ... YUV420 halves the
+ * spatial dimension of 2 in 3 of its channels").
+ * No matrix and no resampling: the network sees the clip's own planes,
+ * dequantised.  Reading A22: Y' in [0, 1] and U = Pb + 1/2, V = Pr + 1/2 in
+ * [0, 1] (SPEC.md VideoFrame float planes, "(Y,U,V) = (1,0.5,0.5) -> white",
+ * S:336-337).
+ *
+ * Tensors: luma [N, Hp, Wp] (slot t = channel t) and chroma [2N, Hc, Wc]
+ * (slot t = channels 2t (U), 2t+1 (V)); Hc, Wc = Hp/2, Wp/2 for 4:2:0, else
+ * Hp, Wp.  Padding replicates the last row / column of each plane (reading
+ * A6 applied per plane).  RGB clips are rejected. */
+int oracle_f2t_yuv(const oracle_format *f, int N, const void *const *planes, const int64_t *pitches,
+                   int64_t Hp, int64_t Wp, int dtype, void *luma, void *chroma)
+{
+    if (check_format(f) || f->family == OR_RGB || N < 1 || Hp < f->height || Wp < f->width) return -1;
+    if (dtype != OR_F32 && dtype != OR_F16) return -1;
+    int sub = f->family == OR_YUV420;
+    if (sub && ((Hp | Wp) & 1)) return -1;
+    int64_t W = f->width, H = f->height, cw = sub ? W / 2 : W, ch = sub ? H / 2 : H;
+    int64_t Hc = sub ? Hp / 2 : Hp, Wc = sub ? Wp / 2 : Wp;
+    for (int t = 0; t < N; ++t) {
+        for (int64_t y = 0; y < Hp; ++y)
+            for (int64_t x = 0; x < Wp; ++x) {
+                double c = sample_at(planes[3 * t], pitches[3 * t], f->bits, x < W ? x : W - 1, y < H ? y : H - 1);
+                store_tensor(luma, dtype, ((int64_t)t * Hp + y) * Wp + x, deq_luma(c, f->bits, f->range));
+            }
+        for (int k = 0; k < 2; ++k)
+            for (int64_t y = 0; y < Hc; ++y)
+                for (int64_t x = 0; x < Wc; ++x) {
+                    double c = sample_at(planes[3 * t + 1 + k], pitches[3 * t + 1 + k], f->bits,
+                                         x < cw ? x : cw - 1, y < ch ? y : ch - 1);
+                    store_tensor(chroma, dtype, ((int64_t)(2 * t + k) * Hc + y) * Wc + x,
+                                 deq_chroma(c, f->bits, f->range) + 0.5);
+                }
+    }
+    return 0;
+}
+
+/* Inverse: luma [M, th, tw], chroma [2M, thc, twc] (thc, twc = th/2, tw/2
+ * for 4:2:0, else th, tw); output slot o reads the top-left window of its
+ * planes.  Y code = quantise(Y'), chroma code = quantise(U - 1/2) (readings
+ * A2-A4, A22). */
+int oracle_t2f_yuv(const oracle_format *fo, int M, const void *luma, const void *chroma, int dtype,
+                   int64_t th, int64_t tw, void *const *planes, const int64_t *pitches)
+{
+    if (check_format(fo) || fo->family == OR_RGB || M < 1 || th < fo->height || tw < fo->width) return -1;
+    if (dtype != OR_F32 && dtype != OR_F16) return -1;
+    int sub = fo->family == OR_YUV420;
+    if (sub && ((th | tw) & 1)) return -1;
+    int64_t Wo = fo->width, Ho = fo->height, cw = sub ? Wo / 2 : Wo, ch = sub ? Ho / 2 : Ho;
+    int64_t thc = sub ? th / 2 : th, twc = sub ? tw / 2 : tw;
+    int old_round = fegetround();
+    fesetround(FE_TONEAREST);
+    for (int o = 0; o < M; ++o) {
+        for (int64_t y = 0; y < Ho; ++y)
+            for (int64_t x = 0; x < Wo; ++x) {
+                double v = load_tensor(luma, dtype, ((int64_t)o * th + y) * tw + x);
+                store_sample(planes[3 * o], pitches[3 * o], fo->bits, x, y, quant_luma(v, fo->bits, fo->range));
+            }
+        for (int k = 0; k < 2; ++k)
+            for (int64_t y = 0; y < ch; ++y)
+                for (int64_t x = 0; x < cw; ++x) {
+                    double v = load_tensor(chroma, dtype, ((int64_t)(2 * o + k) * thc + y) * twc + x);
+                    store_sample(planes[3 * o + 1 + k], pitches[3 * o + 1 + k], fo->bits, x, y,
+                                 quant_chroma(v - 0.5, fo->bits, fo->range));
+                }
     }
     fesetround(old_round);
     return 0;

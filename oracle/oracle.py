@@ -26,6 +26,7 @@ YUV420, YUV444, RGB = 0, 1, 2
 BT601, BT709, BT2020 = 0, 1, 2
 LIMITED, FULL = 0, 1
 F32, F16 = 0, 1
+CHROMA_CENTER, CHROMA_LEFT = 0, 1
 
 
 class _Format(C.Structure):
@@ -65,6 +66,18 @@ def lib():
         L.oracle_t2f.restype = C.c_int
         L.oracle_t2f.argtypes = [C.POINTER(_Format), C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                  C.c_int64, C.POINTER(C.c_void_p), i64p]
+        L.oracle_f2t_sited.restype = C.c_int
+        L.oracle_f2t_sited.argtypes = [C.POINTER(_Format), C.c_int, C.c_int, C.POINTER(C.c_void_p), i64p,
+                                       C.c_int64, C.c_int64, C.c_int, C.c_void_p]
+        L.oracle_t2f_sited.restype = C.c_int
+        L.oracle_t2f_sited.argtypes = [C.POINTER(_Format), C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int64,
+                                       C.c_int64, C.POINTER(C.c_void_p), i64p]
+        L.oracle_f2t_yuv.restype = C.c_int
+        L.oracle_f2t_yuv.argtypes = [C.POINTER(_Format), C.c_int, C.POINTER(C.c_void_p), i64p,
+                                     C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]
+        L.oracle_t2f_yuv.restype = C.c_int
+        L.oracle_t2f_yuv.argtypes = [C.POINTER(_Format), C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int64,
+                                     C.c_int64, C.POINTER(C.c_void_p), i64p]
         L.oracle_scene_detect.restype = C.c_int
         L.oracle_scene_detect.argtypes = [C.POINTER(_Format), C.c_int, C.POINTER(C.c_void_p), i64p, C.c_double,
                                           C.POINTER(C.c_uint64), C.POINTER(C.c_uint8)]
@@ -126,12 +139,10 @@ def half_bits_from_double(v: float) -> int:
 
 
 # ------------------------------------------------------------ conversions
-def f2t(frames, width, height, family, bits, matrix, rng, Hp, Wp, dtype):
-    """frames: list (length N) of 3-tuples of 2-D numpy planes (u8/u16).
-    Returns the NCHW [1, 3N, Hp, Wp] tensor as float32 or float16 numpy."""
-    N = len(frames)
-    ptrs = (C.c_void_p * (3 * N))()
-    pitches = np.zeros(3 * N, dtype=np.int64)
+def _frame_ptrs(frames):
+    n = len(frames)
+    ptrs = (C.c_void_p * max(3 * n, 1))()
+    pitches = np.zeros(max(3 * n, 1), dtype=np.int64)
     keep = []
     for t, fr in enumerate(frames):
         for p in range(3):
@@ -139,21 +150,10 @@ def f2t(frames, width, height, family, bits, matrix, rng, Hp, Wp, dtype):
             keep.append(a)
             ptrs[3 * t + p] = a.ctypes.data
             pitches[3 * t + p] = a.strides[0]
-    out = np.zeros((1, 3 * N, Hp, Wp), dtype=np.float32 if dtype == F32 else np.float16)
-    f = _fmt(width, height, family, bits, matrix, rng)
-    rc = lib().oracle_f2t(C.byref(f), N, ptrs, pitches.ctypes.data_as(C.POINTER(C.c_int64)),
-                          Hp, Wp, dtype, out.ctypes.data)
-    if rc:
-        raise ValueError("oracle_f2t rejected the arguments")
-    return out
+    return ptrs, pitches, keep
 
 
-def t2f(tensor, M, width, height, family, bits, matrix, rng):
-    """tensor: numpy [1, 3M, th, tw] float32/float16.  Returns a list of M
-    3-tuples of planes (output frame size width x height)."""
-    tensor = np.ascontiguousarray(tensor)
-    dtype = F32 if tensor.dtype == np.float32 else F16
-    th, tw = tensor.shape[2], tensor.shape[3]
+def _out_frames(M, width, height, family, bits):
     sd = sample_dtype(bits)
     shapes = plane_shapes(width, height, family)
     outs = [tuple(np.zeros(s, dtype=sd) for s in shapes) for _ in range(M)]
@@ -163,11 +163,72 @@ def t2f(tensor, M, width, height, family, bits, matrix, rng):
         for p in range(3):
             ptrs[3 * o + p] = outs[o][p].ctypes.data
             pitches[3 * o + p] = outs[o][p].strides[0]
+    return outs, ptrs, pitches
+
+
+def f2t(frames, width, height, family, bits, matrix, rng, Hp, Wp, dtype, siting=CHROMA_CENTER):
+    """frames: list (length N) of 3-tuples of 2-D numpy planes (u8/u16).
+    Returns the NCHW [1, 3N, Hp, Wp] tensor as float32 or float16 numpy."""
+    N = len(frames)
+    ptrs, pitches, keep = _frame_ptrs(frames)
+    out = np.zeros((1, 3 * N, Hp, Wp), dtype=np.float32 if dtype == F32 else np.float16)
     f = _fmt(width, height, family, bits, matrix, rng)
-    rc = lib().oracle_t2f(C.byref(f), M, tensor.ctypes.data, dtype, th, tw, ptrs,
-                          pitches.ctypes.data_as(C.POINTER(C.c_int64)))
+    rc = lib().oracle_f2t_sited(C.byref(f), siting, N, ptrs, pitches.ctypes.data_as(C.POINTER(C.c_int64)),
+                                Hp, Wp, dtype, out.ctypes.data)
+    if rc:
+        raise ValueError("oracle_f2t rejected the arguments")
+    return out
+
+
+def t2f(tensor, M, width, height, family, bits, matrix, rng, siting=CHROMA_CENTER):
+    """tensor: numpy [1, 3M, th, tw] float32/float16.  Returns a list of M
+    3-tuples of planes (output frame size width x height)."""
+    tensor = np.ascontiguousarray(tensor)
+    dtype = F32 if tensor.dtype == np.float32 else F16
+    th, tw = tensor.shape[2], tensor.shape[3]
+    outs, ptrs, pitches = _out_frames(M, width, height, family, bits)
+    f = _fmt(width, height, family, bits, matrix, rng)
+    rc = lib().oracle_t2f_sited(C.byref(f), siting, M, tensor.ctypes.data, dtype, th, tw, ptrs,
+                                pitches.ctypes.data_as(C.POINTER(C.c_int64)))
     if rc:
         raise ValueError("oracle_t2f rejected the arguments")
+    return outs
+
+
+def chroma_dims(h, w, family):
+    return (h // 2, w // 2) if family == YUV420 else (h, w)
+
+
+def f2t_yuv(frames, width, height, family, bits, matrix, rng, Hp, Wp, dtype):
+    """YUV-native input tensors: (luma [1, N, Hp, Wp], chroma [1, 2N, Hc, Wc])."""
+    N = len(frames)
+    ptrs, pitches, keep = _frame_ptrs(frames)
+    nd = np.float32 if dtype == F32 else np.float16
+    Hc, Wc = chroma_dims(Hp, Wp, family)
+    luma = np.zeros((1, N, Hp, Wp), dtype=nd)
+    chroma = np.zeros((1, 2 * N, Hc, Wc), dtype=nd)
+    f = _fmt(width, height, family, bits, matrix, rng)
+    rc = lib().oracle_f2t_yuv(C.byref(f), N, ptrs, pitches.ctypes.data_as(C.POINTER(C.c_int64)), Hp, Wp, dtype,
+                              luma.ctypes.data, chroma.ctypes.data)
+    if rc:
+        raise ValueError("oracle_f2t_yuv rejected the arguments")
+    return luma, chroma
+
+
+def t2f_yuv(luma, chroma, M, width, height, family, bits, matrix, rng):
+    """luma [1, M, th, tw], chroma [1, 2M, thc, twc] -> M 3-tuples of planes."""
+    luma = np.ascontiguousarray(luma)
+    chroma = np.ascontiguousarray(chroma)
+    dtype = F32 if luma.dtype == np.float32 else F16
+    assert chroma.dtype == luma.dtype
+    th, tw = luma.shape[2], luma.shape[3]
+    assert chroma.shape[2:] == chroma_dims(th, tw, family)
+    outs, ptrs, pitches = _out_frames(M, width, height, family, bits)
+    f = _fmt(width, height, family, bits, matrix, rng)
+    rc = lib().oracle_t2f_yuv(C.byref(f), M, luma.ctypes.data, chroma.ctypes.data, dtype, th, tw, ptrs,
+                              pitches.ctypes.data_as(C.POINTER(C.c_int64)))
+    if rc:
+        raise ValueError("oracle_t2f_yuv rejected the arguments")
     return outs
 
 
