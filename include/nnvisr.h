@@ -72,7 +72,11 @@ enum { NNVISR_YUV420 = 0, NNVISR_YUV444 = 1, NNVISR_RGB = 2 };
 enum { NNVISR_BT601 = 0, NNVISR_BT709 = 1, NNVISR_BT2020 = 2 };
 /* quantisation range (reading A2) */
 enum { NNVISR_LIMITED = 0, NNVISR_FULL = 1 };
-/* 4:2:0 chroma siting (reading A5); only CENTER is implemented */
+/* 4:2:0 chroma siting (reading A5): CENTER = chroma between the 2x2 luma
+ * block (bilinear 3/4,1/4 up; 2x2 box mean down); LEFT = MPEG-2, horizontally
+ * co-sited with even luma columns, vertically centred (up: 1 | 1/2,1/2
+ * horizontally; down: [1,2,1]/4 horizontally, 1/2,1/2 vertically; SPEC.md
+ * S:339-347).  LEFT runs on the generic (non-TMA) kernels. */
 enum { NNVISR_CHROMA_CENTER = 0, NNVISR_CHROMA_LEFT = 1 };
 /* tensor element type */
 enum { NNVISR_F32 = 0, NNVISR_F16 = 1 };
@@ -80,7 +84,16 @@ enum { NNVISR_F32 = 0, NNVISR_F16 = 1 };
 enum {
     NNVISR_INTERPOLATION = 1u, /* "Interpolation": output at doubled frame rate */
     NNVISR_EXTRA_FRAME = 2u,   /* "Extra frame": the network takes n+1 frames */
-    NNVISR_DOUBLE_FRAME = 4u   /* "Double frame": 2n outputs per run */
+    NNVISR_DOUBLE_FRAME = 4u,  /* "Double frame": 2n outputs per run */
+    /* YUV network tensors (§3.1, "NNVISR supports input
+     * and output in both RGB and YUV pixel format"; SURVEY.md §8(f) NEXT-3;
+     * reading A22).  YUV clips only.  No matrix, no chroma resampling: a
+     * YUV tensor pair is a luma tensor [1, K, h, w] (channel k = Y' of slot
+     * k, in [0, 1]) and a chroma tensor [1, 2K, hc, wc] (channels 2k, 2k+1 =
+     * U = Pb + 1/2, V = Pr + 1/2 of slot k), hc, wc = h/2, w/2 for 4:2:0,
+     * else h, w.  Padding replicates the last row / column of each plane. */
+    NNVISR_YUV_INPUT = 8u,     /* the network consumes YUV tensors */
+    NNVISR_YUV_OUTPUT = 16u    /* the network produces YUV tensors */
 };
 
 /* The clip being processed (§3.1: RGB/YUV input, the
@@ -98,7 +111,7 @@ typedef struct {
  * Accepted shapes (anything else is NNVISR_ERR_INVALID_CONFIG):
  *   paper grouping: left_context = 0 (or -1), input_count = n + (EXTRA ? 1 : 0),
  *                   output_count in {n, 2n, 2n+1};
- *   sliding window: flags = 0, n = 1, output_count = 1, any input_count >= 1,
+ *   sliding window: no INTERPOLATION / EXTRA / DOUBLE flag, n = 1, output_count = 1, any input_count >= 1,
  *                   left_context L in [0, N) (-1 = (N-1)/2, reading A8).
  * DOUBLE_FRAME requires INTERPOLATION; INTERPOLATION without DOUBLE_FRAME
  * requires scale 1 (SPEC.md model-desc invariants). */
@@ -134,8 +147,22 @@ nnvisr_status nnvisr_close(nnvisr_handle *h);
 const char *nnvisr_last_error(void);
 
 /* Input tensor shape [1, 3N, Hp, Wp] and minimum output tensor shape
- * [1, 3M, H*sy, W*sx]; also the output frame size (W*sx, H*sy). */
+ * [1, 3M, H*sy, W*sx]; also the output frame size (W*sx, H*sy).  For a YUV
+ * side (NNVISR_YUV_INPUT / _OUTPUT) the luma tensor: [1, N, Hp, Wp] /
+ * [1, M, H*sy, W*sx]. */
 nnvisr_status nnvisr_tensor_shapes(const nnvisr_handle *h, int64_t in_nchw[4], int64_t out_nchw[4]);
+
+/* Chroma tensor shapes of the YUV sides: in [1, 2N, Hc, Wc], out
+ * [1, 2M, hc, wc] at the minimum output tensor size; all zeros for an RGB
+ * side.
+ *
+ * Packed layout: every call that takes ONE tensor pointer per tuple (or one
+ * store) uses, for a YUV side, the luma planes followed directly by the
+ * chroma planes: tuple = [K luma planes][2K chroma planes] (K = N or M), and
+ * a store slot (nnvisr_frames_to_store / _to_slots / nnvisr_copy_slot) =
+ * [Y][U][V] = Hp*Wp + 2*Hc*Wc elements.  The *_yuv_batch calls take the two
+ * tensors separately. */
+nnvisr_status nnvisr_chroma_shapes(const nnvisr_handle *h, int64_t in_nchw[4], int64_t out_nchw[4]);
 
 /* Tuple plan of a whole clip (steps A1-A2; §3.3).
  * cut: host [num_frames]; cut[k] != 0 means a scene change between frames
@@ -203,6 +230,25 @@ nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensor
                                             int64_t tensor_stride_bytes, int64_t t_h,
                                             int64_t t_w, const nnvisr_frame *out, int64_t count,
                                             void *stream);
+
+/* YUV input network (NNVISR_YUV_INPUT): frames -> separate luma and chroma
+ * tensors.  Run r's luma [N, Hp, Wp] at luma + r*luma_stride_bytes (16-byte
+ * aligned, stride a multiple of 16), its chroma [2N, Hc, Wc] at
+ * chroma + r*chroma_stride_bytes (element aligned).  Otherwise as
+ * nnvisr_frames_to_tensor_batch.  NNVISR_ERR_INVALID_ARG for an RGB-input
+ * handle. */
+nnvisr_status nnvisr_frames_to_tensor_yuv_batch(nnvisr_handle *h, const int64_t *run_inputs, int64_t num_runs,
+                                                void *luma, int64_t luma_stride_bytes, void *chroma,
+                                                int64_t chroma_stride_bytes, void *stream);
+
+/* YUV output network (NNVISR_YUV_OUTPUT): tuple c's luma [M, t_h, t_w] at
+ * luma + c*luma_stride_bytes, its chroma [2M, t_h/2, t_w/2] (4:2:0; 4:4:4:
+ * [2M, t_h, t_w]) at chroma + c*chroma_stride_bytes; t_h, t_w even for 4:2:0.
+ * Output slot o -> out[c*M + o] as nnvisr_tensor_to_frames_batch (plane[0]
+ * == NULL: not converted).  NNVISR_ERR_INVALID_ARG for an RGB-output handle. */
+nnvisr_status nnvisr_tensor_to_frames_yuv_batch(nnvisr_handle *h, const void *luma, int64_t luma_stride_bytes,
+                                                const void *chroma, int64_t chroma_stride_bytes, int64_t t_h,
+                                                int64_t t_w, const nnvisr_frame *out, int64_t count, void *stream);
 
 /* ---- Host-buffer calls: the frames live in (pinned) host memory.  The
  * library stages them through two device staging slots per direction and

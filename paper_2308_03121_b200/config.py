@@ -13,6 +13,7 @@ LIMITED, FULL = 0, 1
 CHROMA_CENTER, CHROMA_LEFT = 0, 1
 F32, F16 = 0, 1
 INTERPOLATION, EXTRA_FRAME, DOUBLE_FRAME = 1, 2, 4
+YUV_INPUT, YUV_OUTPUT = 8, 16  # YUV-native network tensors (NEXT-3)
 
 STATUS = {0: "OK", 1: "INVALID_CONFIG", 2: "INVALID_ARG", 3: "UNSUPPORTED", 4: "OUT_OF_MEMORY",
           5: "CUDA", 7: "CAPACITY"}

@@ -161,6 +161,18 @@ __device__ __forceinline__ void hup(const int (&c)[6], int (&h)[kPx])
     }
 }
 
+// LEFT (MPEG-2) siting: chroma i is co-sited with luma column 2i, so even
+// column 2m takes 4*c[m+1] and odd 2m+1 takes 2*(c[m+1] + c[m+2]) (weights
+// 1 and 1/2,1/2 scaled to the same sum 4 as hup; reading A5).
+__device__ __forceinline__ void hup_left(const int (&c)[6], int (&h)[kPx])
+{
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        h[2 * m] = 4 * c[m + 1];
+        h[2 * m + 1] = 2 * (c[m + 1] + c[m + 2]);
+    }
+}
+
 // Chroma rows of a 4:2:0 luma row y (already clamped to the frame): the near
 // row and the far row (above for even y, below for odd y), clamped.
 __device__ __forceinline__ int chroma_near(int yc) { return yc >> 1; }
@@ -174,7 +186,7 @@ __device__ __forceinline__ int chroma_far(int yc, int ch)
 // the plane, reading A5).  Values are 16 x code.
 template <int FAMILY, typename IN>
 __device__ __forceinline__ void f2t_codes_scalar(const DevFrame &f, int W, int H, int x, int y, int &ys, int &us,
-                                                 int &vs)
+                                                 int &vs, int left = 0)
 {
     const int xc = min(x, W - 1), yc = min(y, H - 1);
     ys = 16 * load1(row_ptr<IN>(f, 0, yc) + xc);
@@ -184,8 +196,15 @@ __device__ __forceinline__ void f2t_codes_scalar(const DevFrame &f, int W, int H
         const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
         const IN *u0 = row_ptr<IN>(f, 1, jn), *u1 = row_ptr<IN>(f, 1, jf);
         const IN *v0 = row_ptr<IN>(f, 2, jn), *v1 = row_ptr<IN>(f, 2, jf);
-        us = 9 * load1(u0 + in_) + 3 * load1(u0 + if_) + 3 * load1(u1 + in_) + load1(u1 + if_);
-        vs = 9 * load1(v0 + in_) + 3 * load1(v0 + if_) + 3 * load1(v1 + in_) + load1(v1 + if_);
+        if (left) {
+            // co-sited column xc/2 (even xc) or the mean of xc/2 and xc/2+1
+            const int i1 = (xc & 1) ? min(in_ + 1, cw - 1) : in_;
+            us = 2 * (3 * (load1(u0 + in_) + load1(u0 + i1)) + load1(u1 + in_) + load1(u1 + i1));
+            vs = 2 * (3 * (load1(v0 + in_) + load1(v0 + i1)) + load1(v1 + in_) + load1(v1 + i1));
+        } else {
+            us = 9 * load1(u0 + in_) + 3 * load1(u0 + if_) + 3 * load1(u1 + in_) + load1(u1 + if_);
+            vs = 9 * load1(v0 + in_) + 3 * load1(v0 + if_) + 3 * load1(v1 + in_) + load1(v1 + if_);
+        }
     } else {
         us = 16 * load1(row_ptr<IN>(f, 1, yc) + xc);
         vs = 16 * load1(row_ptr<IN>(f, 2, yc) + xc);
@@ -311,17 +330,19 @@ __device__ __forceinline__ void t2f_job(const T2FArgs &a, int job, int &tup, int
 // ------------------------------------------------------------ t2f colour
 template <typename T> struct T2FConst;
 // fp32: ys, yo, cs, co are divided by maxc (see quant)
+// yd, yod, csd, co2d: the unnormalised scale / offsets of quant_direct.
 template <> struct T2FConst<float> {
-    float kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
+    float kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc, yd, yod, csd, co2d;
     __device__ explicit T2FConst(const T2FColour &c)
         : kr(c.fkr), kb(c.fkb), db(c.fdb), dr(c.fdr), idb(c.fidb), idr(c.fidr), ys(c.fys_n), yo(c.fyo_n),
-          cs(c.fcs_n), co(c.fco_n), maxc(c.fmaxc) {}
+          cs(c.fcs_n), co(c.fco_n), maxc(c.fmaxc), yd(static_cast<float>(c.ys)), yod(static_cast<float>(c.yo)),
+          csd(static_cast<float>(c.cs)), co2d(static_cast<float>(c.co2)) {}
 };
 template <> struct T2FConst<double> {
-    double kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
+    double kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc, yd, yod, csd, co2d;
     __device__ explicit T2FConst(const T2FColour &c)
         : kr(c.kr), kb(c.kb), db(c.db), dr(c.dr), idb(c.idb), idr(c.idr), ys(c.ys), yo(c.yo), cs(c.cs), co(c.co),
-          maxc(c.maxc) {}
+          maxc(c.maxc), yd(c.ys), yod(c.yo), csd(c.cs), co2d(c.co2) {}
 };
 
 __device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
@@ -343,6 +364,22 @@ __device__ __forceinline__ uint32_t quant(double v, double s, double o, double m
     // cvt.rni.u32.f64: round half to even, saturating (negative -> 0,
     // NaN -> 0, +inf -> 2^32-1), then the integer clamp to maxc
     return min(__double2uint_rn(fma(v, s, o)), static_cast<uint32_t>(maxc));
+}
+
+// Step B4 for tensor values quantised directly (RGB clips, YUV-native
+// tensors): q = v * s + o with the unnormalised integer scale / offset in ONE
+// FMA.  An fp16 value times s (<= 2^16 - 1) is exact in fp32, so the exact
+// .5 ties that fp16 tensors hit often (v on a 2^-11 grid times 219) stay
+// ties and round to even as in the oracle; then clamp (fmaxf turns NaN into
+// 0) and the magic-add RNE.
+__device__ __forceinline__ uint32_t quant_direct(float v, float s, float o, float maxc)
+{
+    const float q = fminf(fmaxf(fmaf(v, s, o), 0.0f), maxc);
+    return __float_as_uint(q + 12582912.0f);
+}
+__device__ __forceinline__ uint32_t quant_direct(double v, double s, double o, double maxc)
+{
+    return quant(v, s, o, maxc);
 }
 
 // S / d for a divisor d with precomputed reciprocal id: one FMA correction of
@@ -417,19 +454,22 @@ __device__ __forceinline__ float tload1(const float *p) { return p[0]; }
 
 // One output row y (row r of the item) of R', G', B' -> luma codes (and
 // 4:4:4 chroma codes, or the 4:2:0 partial 2x2 sums of B-Y', R-Y').
-template <int FAMILY, typename OS, typename AR>
+// LEFT (4:2:0 only): the partial sums are the per-row [1,2,1] taps
+// (BY[2m-1] + 2 BY[2m]) + BY[2m+1] with BY[-1] = lb (column x0-1, clamped).
+template <int FAMILY, typename OS, typename AR, bool LEFT = false>
 __device__ __forceinline__ void t2f_row(const T2FConst<AR> &c, const T2FColour &cc, const DevFrame &f, int x0, int y,
                                         int r, const float (&R)[kPx], const float (&G)[kPx], const float (&B)[kPx],
-                                        int nvalid, bool vec_store, AR (&sb)[4], AR (&sr)[4])
+                                        int nvalid, bool vec_store, AR (&sb)[4], AR (&sr)[4], AR lb = AR(0),
+                                        AR lr = AR(0))
 {
     (void)cc;
     if constexpr (FAMILY == kRGB) {
         uint32_t q[3][kPx];
 #pragma unroll
         for (int k = 0; k < kPx; ++k) {
-            q[0][k] = quant(static_cast<AR>(R[k]), c.ys, c.yo, c.maxc);
-            q[1][k] = quant(static_cast<AR>(G[k]), c.ys, c.yo, c.maxc);
-            q[2][k] = quant(static_cast<AR>(B[k]), c.ys, c.yo, c.maxc);
+            q[0][k] = quant_direct(static_cast<AR>(R[k]), c.yd, c.yod, c.maxc);
+            q[1][k] = quant_direct(static_cast<AR>(G[k]), c.yd, c.yod, c.maxc);
+            q[2][k] = quant_direct(static_cast<AR>(B[k]), c.yd, c.yod, c.maxc);
         }
 #pragma unroll
         for (int p = 0; p < 3; ++p) {
@@ -471,7 +511,15 @@ __device__ __forceinline__ void t2f_row(const T2FConst<AR> &c, const T2FColour &
             // 4:2:0: accumulate ((a+b) + (c+d)) row by row
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-                const AR pb = BY[2 * m] + BY[2 * m + 1], pr = RY[2 * m] + RY[2 * m + 1];
+                AR pb, pr;
+                if constexpr (LEFT) {
+                    const AR b0 = m ? BY[2 * m - 1] : lb, r0 = m ? RY[2 * m - 1] : lr;
+                    pb = (b0 + AR(2) * BY[2 * m]) + BY[2 * m + 1];
+                    pr = (r0 + AR(2) * RY[2 * m]) + RY[2 * m + 1];
+                } else {
+                    pb = BY[2 * m] + BY[2 * m + 1];
+                    pr = RY[2 * m] + RY[2 * m + 1];
+                }
                 sb[m] = r == 0 ? pb : sb[m] + pb;
                 sr[m] = r == 0 ? pr : sr[m] + pr;
             }
@@ -482,11 +530,13 @@ __device__ __forceinline__ void t2f_row(const T2FConst<AR> &c, const T2FColour &
 // Step B3 + B4 for 4:2:0: 2x2 box mean ((a+b)+(c+d))/4, folded into the
 // divisor 4*db (a power-of-two scaling, exact), then quantise and store the
 // item's 4 chroma samples of each plane at chroma row y0/2.
-template <typename OS, typename AR>
+// LEFT: the sums carry weight 8 ([1,2,1] per row, two rows): divisor 8*db.
+template <typename OS, typename AR, bool LEFT = false>
 __device__ __forceinline__ void t2f_chroma420(const T2FConst<AR> &c, const DevFrame &f, int x0, int y0,
                                               const AR (&sb)[4], const AR (&sr)[4], int nvalid, bool vec_store)
 {
-    const AR db4 = c.db * AR(4), dr4 = c.dr * AR(4), idb4 = c.idb * AR(0.25), idr4 = c.idr * AR(0.25);
+    constexpr float kW = LEFT ? 8.0f : 4.0f;
+    const AR db4 = c.db * AR(kW), dr4 = c.dr * AR(kW), idb4 = c.idb * AR(1.0f / kW), idr4 = c.idr * AR(1.0f / kW);
     uint32_t qb[4], qr[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {

@@ -26,6 +26,7 @@ struct DevFrame {
 //   fp32 rounding error) are recomputed in fp64 with the *_d constants.
 struct F2TColour {
     int32_t y_off, c_off;
+    int32_t u_off;  // YUV-native chroma U = P + 1/2 = (16*code - u_off) * c_scale (reading A22)
     float y_scale, c_scale;
     float r_pr, b_pb, g_pb, g_pr;
     double y_scale_d, c_scale_d, r_pr_d, b_pb_d, g_pb_d, g_pr_d;
@@ -41,6 +42,9 @@ struct F2TColour {
 struct T2FColour {
     double kr, kb, db, dr, idb, idr, ys, yo, cs, co, maxc;
     float fkr, fkb, fdb, fdr, fidb, fidr, fys_n, fyo_n, fcs_n, fco_n, fmaxc;  // *_n = / maxc
+    // YUV-native chroma (reading A22): code = rne(clamp(U * cs + co2)) with
+    // co2 = co - cs/2, i.e. P = U - 1/2 folded into the offset (exact)
+    double co2;
 };
 
 // frames -> tensor work list of one launch: job j converts the distinct frame
@@ -67,6 +71,15 @@ struct F2TArgs {
     int64_t pitch_y, pitch_c;     // uniform plane pitches of the bound frames (0 = not uniform)
     int64_t tiles;
     F2TColour col;
+    // 4:2:0 chroma siting of this launch: 0 centre, 1 LEFT (generic kernels only)
+    int32_t left;
+    // YUV-native tensors (NEXT-3, kernels_yuv.cu): the luma of (run, slot) at
+    // dst + run*run_stride + slot*slot_bytes ([Hp][Wp]); its chroma planes U,
+    // V at dst2 + run*run_stride2 + slot*slot_bytes2 (+ cplane_bytes for V),
+    // each [Hc][Wc]
+    int32_t yuv, Hc, Wc, vec_out_c;
+    char *dst2;
+    int64_t run_stride2, slot_bytes2, cplane_bytes;
 };
 
 struct T2FArgs {
@@ -84,6 +97,13 @@ struct T2FArgs {
     int32_t tma_ok, rowunits, nseg, stages, stage_bytes, segw;
     int64_t tiles;
     T2FColour col;
+    int32_t left;  // 4:2:0 chroma siting: 0 centre, 1 LEFT (generic kernels only)
+    // YUV-native tensors (NEXT-3): output slot o of tuple c reads luma plane o
+    // of src + c*tensor_stride ([th][tw]) and chroma planes 2o, 2o+1 of
+    // src2 + c*tensor_stride2 ([thc][twc])
+    int32_t yuv, vec_in_c;
+    const char *src2;
+    int64_t tensor_stride2, thc, twc;
 };
 
 // Launchers (kernels.cu).  Return the CUDA error of the launch.
@@ -91,6 +111,8 @@ cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, cudaSt
 cudaError_t launch_t2f(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s);
 cudaError_t launch_f2t_tma(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s);
 cudaError_t launch_t2f_tma(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s);
+cudaError_t launch_f2t_yuv(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s);
+cudaError_t launch_t2f_yuv(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s);
 
 cudaError_t launch_scene_detect(int family, int bits, int range, int W, int H, const DevFrame *frames, int count,
                                 int vec, double threshold, uint64_t *sad, uint8_t *cut, cudaStream_t s);

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kThreads) f2t_generic(const F2TArgs a)
                             unpack4(*reinterpret_cast<const V4 *>(row + i0), &c[1]);
                             c[0] = load1(row + max(i0 - 1, 0));
                             c[5] = load1(row + min(i0 + 4, cw - 1));
-                            hup(c, h[q]);
+                            if (a.left) hup_left(c, h[q]);
+                            else hup(c, h[q]);
                         }
 #pragma unroll
                         for (int k = 0; k < kPx; ++k) {
@@ -85,12 +86,56 @@ __global__ void __launch_bounds__(kThreads) f2t_generic(const F2TArgs a)
             } else {
 #pragma unroll
                 for (int k = 0; k < kPx; ++k)
-                    f2t_codes_scalar<FAMILY, IN>(f, a.W, a.H, x0 + k, y0 + r, ys[k], us[k], vs[k]);
+                    f2t_codes_scalar<FAMILY, IN>(f, a.W, a.H, x0 + k, y0 + r, ys[k], us[k], vs[k], a.left);
             }
             f2t_row<FAMILY, OUT>(a.col, ys, us, vs, out[r]);
         }
         f2t_store<ROWS, OUT>(a, dl, out, x0, y0);
     }
+}
+
+// Left neighbour (column max(x0-1, 0)) of a row for LEFT siting: B-Y', R-Y'.
+template <typename TIN, typename AR>
+__device__ __forceinline__ void t2f_left_tap(const T2FConst<AR> &c, const TIN *row, int64_t plane, int x0, AR &lb,
+                                             AR &lr)
+{
+    const int xl = max(x0 - 1, 0);
+    const AR r_ = tload1(row + xl), g_ = tload1(row + plane + xl), b_ = tload1(row + 2 * plane + xl);
+    const AR Y = fma_(c.kb, b_ - g_, fma_(c.kr, r_ - g_, g_));
+    lb = b_ - Y;
+    lr = r_ - Y;
+}
+
+template <int FAMILY, typename OS, typename TIN, typename AR, bool LEFT>
+__device__ __forceinline__ void t2f_item(const T2FArgs &a, const T2FConst<AR> &c, const DevFrame &f, const TIN *src,
+                                         int64_t plane, int x0, int y0)
+{
+    constexpr int ROWS = (FAMILY == kYUV420) ? 2 : 1;
+    const int nvalid = min(kPx, a.Wo - x0);
+    const bool vec_store = a.vec_out && nvalid == kPx;
+    AR sb[4], sr[4];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+        float R[kPx], G[kPx], B[kPx];
+        const TIN *row = src + static_cast<int64_t>(r) * a.tw;
+        if (a.vec_in && nvalid == kPx) {
+            tload8_stream(row, R);
+            tload8_stream(row + plane, G);
+            tload8_stream(row + 2 * plane, B);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPx; ++k) {
+                const bool in = k < nvalid;
+                R[k] = in ? tload1(row + k) : 0.f;
+                G[k] = in ? tload1(row + plane + k) : 0.f;
+                B[k] = in ? tload1(row + 2 * plane + k) : 0.f;
+            }
+        }
+        AR lb = AR(0), lr = AR(0);
+        if constexpr (LEFT) t2f_left_tap<TIN, AR>(c, row - x0, plane, x0, lb, lr);
+        t2f_row<FAMILY, OS, AR, LEFT>(c, a.col, f, x0, y0 + r, r, R, G, B, nvalid, vec_store, sb, sr, lb, lr);
+    }
+    if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR, LEFT>(c, f, x0, y0, sb, sr, nvalid, vec_store);
 }
 
 template <int FAMILY, typename OS, typename TIN, typename AR>
@@ -116,29 +161,8 @@ __global__ void __launch_bounds__(kThreads) t2f_generic(const T2FArgs a)
         t2f_job(a, job, tup, o);
         const TIN *src = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
                          static_cast<int64_t>(3 * o) * plane + static_cast<int64_t>(y0) * a.tw + x0;
-        const int nvalid = min(kPx, a.Wo - x0);
-        const bool vec_store = a.vec_out && nvalid == kPx;
-        AR sb[4], sr[4];
-#pragma unroll
-        for (int r = 0; r < ROWS; ++r) {
-            float R[kPx], G[kPx], B[kPx];
-            const TIN *row = src + static_cast<int64_t>(r) * a.tw;
-            if (a.vec_in && nvalid == kPx) {
-                tload8_stream(row, R);
-                tload8_stream(row + plane, G);
-                tload8_stream(row + 2 * plane, B);
-            } else {
-#pragma unroll
-                for (int k = 0; k < kPx; ++k) {
-                    const bool in = k < nvalid;
-                    R[k] = in ? tload1(row + k) : 0.f;
-                    G[k] = in ? tload1(row + plane + k) : 0.f;
-                    B[k] = in ? tload1(row + 2 * plane + k) : 0.f;
-                }
-            }
-            t2f_row<FAMILY, OS, AR>(c, a.col, f, x0, y0 + r, r, R, G, B, nvalid, vec_store, sb, sr);
-        }
-        if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x0, y0, sb, sr, nvalid, vec_store);
+        if (FAMILY == kYUV420 && a.left) t2f_item<FAMILY, OS, TIN, AR, true>(a, c, f, src, plane, x0, y0);
+        else t2f_item<FAMILY, OS, TIN, AR, false>(a, c, f, src, plane, x0, y0);
     }
 }
 
@@ -196,6 +220,7 @@ cudaError_t t2f_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t s)
 cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s)
 {
     count_launch();
+    if (a.yuv) return launch_f2t_yuv(family, bits, dtype, a, s);
     if (a.tma_ok) return launch_f2t_tma(family, bits, dtype, a, s);
     switch (family) {
     case kYUV420: return f2t_dispatch<kYUV420>(bits, dtype, a, s);
@@ -207,6 +232,7 @@ cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, cudaSt
 cudaError_t launch_t2f(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s)
 {
     count_launch();
+    if (a.yuv) return launch_t2f_yuv(family, bits, dtype, a, s);
     if (a.tma_ok) return launch_t2f_tma(family, bits, dtype, a, s);
     switch (family) {
     case kYUV420: return t2f_dispatch<kYUV420>(bits, dtype, a, s);

@@ -77,7 +77,10 @@ struct nnvisr_handle {
     nnvisr_network net{};
     int N = 0, M = 0, n = 0, L = 0;
     bool paper = false;  // paper grouping (vs sliding window)
+    bool yuv_in = false, yuv_out = false;  // YUV-native network tensors (NEXT-3)
+    bool left = false;                      // LEFT (MPEG-2) 4:2:0 siting
     int64_t Hp = 0, Wp = 0, Wo = 0, Ho = 0;
+    int64_t Hc = 0, Wc = 0;                 // input chroma tensor plane (YUV input)
     int elem = 4;
     F2TColour f2c{};
     T2FColour t2c{};
@@ -169,9 +172,7 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
         return fail(NNVISR_ERR_INVALID_CONFIG, "unknown colour matrix %d", f.matrix);
     if (f.range != NNVISR_LIMITED && f.range != NNVISR_FULL)
         return fail(NNVISR_ERR_INVALID_CONFIG, "unknown range %d", f.range);
-    if (f.chroma_loc == NNVISR_CHROMA_LEFT)
-        return fail(NNVISR_ERR_UNSUPPORTED, "LEFT (MPEG-2) chroma siting is not implemented");
-    if (f.chroma_loc != NNVISR_CHROMA_CENTER)
+    if (f.chroma_loc != NNVISR_CHROMA_CENTER && f.chroma_loc != NNVISR_CHROMA_LEFT)
         return fail(NNVISR_ERR_INVALID_CONFIG, "unknown chroma siting %d", f.chroma_loc);
     if (f.family == NNVISR_YUV420 && ((f.width | f.height) & 1))
         return fail(NNVISR_ERR_INVALID_CONFIG, "4:2:0 needs even width and height (got %dx%d)", f.width, f.height);
@@ -181,7 +182,9 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
     if (w.output_count < 1 || w.output_count > 16)
         return fail(NNVISR_ERR_INVALID_CONFIG, "output_count must be in [1, 16] (got %d)", w.output_count);
     if (w.n < 1) return fail(NNVISR_ERR_INVALID_CONFIG, "n must be >= 1 (got %d)", w.n);
-    if (w.flags & ~7u) return fail(NNVISR_ERR_INVALID_CONFIG, "unknown flag bits 0x%x", w.flags);
+    if (w.flags & ~31u) return fail(NNVISR_ERR_INVALID_CONFIG, "unknown flag bits 0x%x", w.flags);
+    if ((w.flags & (NNVISR_YUV_INPUT | NNVISR_YUV_OUTPUT)) && f.family == NNVISR_RGB)
+        return fail(NNVISR_ERR_INVALID_CONFIG, "YUV network tensors need a YUV clip");
     const bool interp = w.flags & NNVISR_INTERPOLATION, extra = w.flags & NNVISR_EXTRA_FRAME,
                dbl = w.flags & NNVISR_DOUBLE_FRAME;
     if (dbl && !interp) return fail(NNVISR_ERR_INVALID_CONFIG, "DOUBLE_FRAME requires INTERPOLATION");
@@ -211,7 +214,7 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
                         dbl ? "2n or 2n+1" : "n", M);
         paper = true;
         L = 0;
-    } else if (w.flags == 0 && n == 1 && M == 1) {
+    } else if ((w.flags & 7u) == 0 && n == 1 && M == 1) {
         L = w.left_context == -1 ? (N - 1) / 2 : w.left_context;
         if (L < 0 || L >= N)
             return fail(NNVISR_ERR_INVALID_CONFIG, "left_context must be in [0, input_count) (got %d)", L);
@@ -230,6 +233,11 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
     h->Wp = round_up(f.width, w.align);
     h->Wo = Wo; h->Ho = Ho;
     h->elem = w.dtype == NNVISR_F16 ? 2 : 4;
+    h->yuv_in = w.flags & NNVISR_YUV_INPUT;
+    h->yuv_out = w.flags & NNVISR_YUV_OUTPUT;
+    h->left = f.chroma_loc == NNVISR_CHROMA_LEFT;
+    h->Hc = f.family == NNVISR_YUV420 ? h->Hp / 2 : h->Hp;
+    h->Wc = f.family == NNVISR_YUV420 ? h->Wp / 2 : h->Wp;
     const char *fg = std::getenv("NNVISR_FORCE_GENERIC");
     h->force_generic = fg && fg[0] == '1';
 
@@ -241,11 +249,13 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
         h->f2c.y_scale = (float)(1.0 / (16.0 * 219.0 * k));
         h->f2c.c_off = (int32_t)(2048 * k);
         h->f2c.c_scale = (float)(1.0 / (16.0 * 224.0 * k));
+        h->f2c.u_off = (int32_t)(256 * k);  // c_off - 16*224k/2
     } else {
         h->f2c.y_off = 0;
         h->f2c.y_scale = (float)(1.0 / (16.0 * full));
         h->f2c.c_off = (int32_t)(16 * std::ldexp(1.0, f.bits - 1));
         h->f2c.c_scale = (float)(1.0 / (16.0 * full));
+        h->f2c.u_off = 8;  // 16*2^(d-1) - 16*(2^d-1)/2
     }
     // A6 inverse matrix; G in difference form (gray axis exact, reading A16)
     double kr = 0, kb = 0;
@@ -272,6 +282,7 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
     c.fidb = 1.0f / c.fdb; c.fidr = 1.0f / c.fdr;
     c.fys_n = (float)(c.ys / full); c.fyo_n = (float)(c.yo / full); c.fcs_n = (float)(c.cs / full);
     c.fco_n = (float)(c.co / full); c.fmaxc = (float)full;
+    c.co2 = c.co - 0.5 * c.cs;
     *out = h;
     return NNVISR_OK;
 }
@@ -313,8 +324,25 @@ nnvisr_status nnvisr_tensor_shapes(const nnvisr_handle *h, int64_t in_nchw[4], i
 {
     g_error.clear();
     if (!h) return fail(NNVISR_ERR_INVALID_ARG, "null handle");
-    if (in_nchw) { in_nchw[0] = 1; in_nchw[1] = 3 * h->N; in_nchw[2] = h->Hp; in_nchw[3] = h->Wp; }
-    if (out_nchw) { out_nchw[0] = 1; out_nchw[1] = 3 * h->M; out_nchw[2] = h->Ho; out_nchw[3] = h->Wo; }
+    if (in_nchw) { in_nchw[0] = 1; in_nchw[1] = (h->yuv_in ? 1 : 3) * h->N; in_nchw[2] = h->Hp; in_nchw[3] = h->Wp; }
+    if (out_nchw) { out_nchw[0] = 1; out_nchw[1] = (h->yuv_out ? 1 : 3) * h->M; out_nchw[2] = h->Ho; out_nchw[3] = h->Wo; }
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_chroma_shapes(const nnvisr_handle *h, int64_t in_nchw[4], int64_t out_nchw[4])
+{
+    g_error.clear();
+    if (!h) return fail(NNVISR_ERR_INVALID_ARG, "null handle");
+    const bool sub = h->fmt.family == NNVISR_YUV420;
+    if (in_nchw) {
+        in_nchw[0] = h->yuv_in; in_nchw[1] = h->yuv_in ? 2 * h->N : 0;
+        in_nchw[2] = h->yuv_in ? h->Hc : 0; in_nchw[3] = h->yuv_in ? h->Wc : 0;
+    }
+    if (out_nchw) {
+        out_nchw[0] = h->yuv_out; out_nchw[1] = h->yuv_out ? 2 * h->M : 0;
+        out_nchw[2] = h->yuv_out ? (sub ? h->Ho / 2 : h->Ho) : 0;
+        out_nchw[3] = h->yuv_out ? (sub ? h->Wo / 2 : h->Wo) : 0;
+    }
     return NNVISR_OK;
 }
 
@@ -492,7 +520,46 @@ F2TArgs f2t_args(const nnvisr_handle *h)
     a.slot_bytes = 3 * h->Hp * h->Wp * h->elem;
     a.vec_out = (h->Wp * h->elem) % 16 == 0;
     a.col = h->f2c;
+    a.left = h->left && h->fmt.family == NNVISR_YUV420;
+    if (h->yuv_in) {
+        a.yuv = 1;
+        a.Hc = (int32_t)h->Hc;
+        a.Wc = (int32_t)h->Wc;
+        a.slot_bytes = h->Hp * h->Wp * h->elem;
+        a.slot_bytes2 = 2 * h->Hc * h->Wc * h->elem;
+        a.cplane_bytes = h->Hc * h->Wc * h->elem;
+    }
     return a;
+}
+
+// Destination of an f2t launch.  RGB: dst only.  YUV input: luma at dst, the
+// chroma at dst2 (nullptr: the packed tuple layout, chroma right after the
+// per_run luma planes of each run), with run strides run_stride / run_stride2.
+void set_f2t_dst(const nnvisr_handle *h, F2TArgs &a, char *dst, int64_t run_stride, char *dst2, int64_t run_stride2,
+                 int per_run)
+{
+    a.dst = dst;
+    a.run_stride = run_stride;
+    if (!h->yuv_in) return;
+    if (!dst2) {
+        dst2 = dst + per_run * h->Hp * h->Wp * h->elem;
+        run_stride2 = run_stride;
+    }
+    a.dst2 = dst2;
+    a.run_stride2 = run_stride2;
+    const int64_t al = h->fmt.family == NNVISR_YUV420 ? 4 * h->elem : 16;
+    a.vec_out_c = reinterpret_cast<uintptr_t>(dst2) % al == 0 && run_stride2 % al == 0 && a.slot_bytes2 % al == 0 &&
+                  a.cplane_bytes % al == 0 && (h->Wc * h->elem) % al == 0;
+}
+
+// Bytes of one network input tuple, one store slot, one output tuple.
+int64_t in_tuple_bytes(const nnvisr_handle *h)
+{
+    return h->yuv_in ? h->N * (h->Hp * h->Wp + 2 * h->Hc * h->Wc) * h->elem : 3 * h->N * h->Hp * h->Wp * h->elem;
+}
+int64_t store_slot_bytes(const nnvisr_handle *h)
+{
+    return h->yuv_in ? (h->Hp * h->Wp + 2 * h->Hc * h->Wc) * h->elem : 3 * h->Hp * h->Wp * h->elem;
 }
 
 nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, cudaStream_t st)
@@ -504,7 +571,7 @@ nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, cudaStream_t st
     a.rowunits = (int32_t)(h->Hp / rows);
     a.nseg = (int32_t)((h->Wp + kThreads * kPx - 1) / (kThreads * kPx));
     a.tiles = jobs * a.rowunits * a.nseg;
-    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->fmt.width % 32 == 0;
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->fmt.width % 32 == 0 && !a.yuv && !a.left;
     cudaError_t e = launch_f2t(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "f2t kernel launch");
     return NNVISR_OK;
@@ -551,6 +618,13 @@ T2FArgs t2f_args(const nnvisr_handle *h, int64_t t_h, int64_t t_w)
     a.units = (int32_t)(h->Ho / rows) * a.col_units;
     a.vec_in = (t_w * h->elem) % 16 == 0;
     a.col = h->t2c;
+    a.left = h->left && h->fmt.family == NNVISR_YUV420;
+    if (h->yuv_out) {
+        const bool sub = h->fmt.family == NNVISR_YUV420;
+        a.yuv = 1;
+        a.thc = sub ? t_h / 2 : t_h;
+        a.twc = sub ? t_w / 2 : t_w;
+    }
     return a;
 }
 
@@ -561,7 +635,8 @@ nnvisr_status run_t2f(nnvisr_handle *h, T2FArgs a, int64_t jobs, cudaStream_t st
     a.rowunits = (int32_t)(h->Ho / rows);
     a.nseg = (int32_t)((h->Wo + kThreads * kPx - 1) / (kThreads * kPx));
     a.tiles = jobs * a.rowunits * a.nseg;
-    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wo % 32 == 0 && a.tensor_stride % 16 == 0;
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wo % 32 == 0 && a.tensor_stride % 16 == 0 &&
+               !a.yuv && !a.left;
     cudaError_t e = launch_t2f(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "t2f kernel launch");
     return NNVISR_OK;
@@ -641,8 +716,7 @@ nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, 
     a.job_frame = dtab;
     a.job_dst = dtab + J;
     a.dst_code = dtab + 2 * J + 1;
-    a.dst = static_cast<char *>(tensor);
-    a.run_stride = 0;
+    set_f2t_dst(h, a, static_cast<char *>(tensor), 0, nullptr, 0, h->N);
     a.vec_in = vec;
     uniform_pitches(h, in, h->N, a.pitch_y, a.pitch_c);
     s = run_f2t(h, a, J, st);
@@ -658,19 +732,24 @@ struct FrameTable {
     int64_t pitch_y, pitch_c;
 };
 
+// dst2 / run_stride2: the chroma tensors of a YUV-input network (nullptr:
+// packed after the luma of each run, see set_f2t_dst).
 static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, const int64_t *frame_idx,
-                                       int64_t runs, int per_run, void *dst, int64_t run_stride, cudaStream_t st);
+                                       int64_t runs, int per_run, void *dst, int64_t run_stride, cudaStream_t st,
+                                       void *dst2 = nullptr, int64_t run_stride2 = 0);
 
 static nnvisr_status f2t_indexed(nnvisr_handle *h, const int64_t *frame_idx, int64_t runs, int per_run,
-                                 void *dst, int64_t run_stride, cudaStream_t st)
+                                 void *dst, int64_t run_stride, cudaStream_t st, void *dst2 = nullptr,
+                                 int64_t run_stride2 = 0)
 {
     if (!h->frames) return fail(NNVISR_ERR_INVALID_ARG, "no frames bound (nnvisr_bind_frames)");
     const FrameTable tab{h->frames, h->frames_base, h->frames_vec, h->frames_pitch_y, h->frames_pitch_c};
-    return f2t_indexed_table(h, tab, frame_idx, runs, per_run, dst, run_stride, st);
+    return f2t_indexed_table(h, tab, frame_idx, runs, per_run, dst, run_stride, st, dst2, run_stride2);
 }
 
 static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, const int64_t *frame_idx,
-                                       int64_t runs, int per_run, void *dst, int64_t run_stride, cudaStream_t st)
+                                       int64_t runs, int per_run, void *dst, int64_t run_stride, cudaStream_t st,
+                                       void *dst2, int64_t run_stride2)
 {
     // an upload slot holds 3 ints per (run, slot) plus one; runs per launch
     // are also bounded by the 5-bit slot / run encoding of dst_code
@@ -678,7 +757,6 @@ static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, 
                                                (int64_t)(INT32_MAX / 32));
     F2TArgs a = f2t_args(h);
     a.frames = tab.dev;
-    a.run_stride = run_stride;
     a.vec_in = tab.vec;
     a.pitch_y = tab.pitch_y;
     a.pitch_c = tab.pitch_c;
@@ -698,7 +776,8 @@ static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, 
         a.job_frame = dtab;
         a.job_dst = dtab + J;
         a.dst_code = dtab + 2 * J + 1;
-        a.dst = static_cast<char *>(dst) + r0 * run_stride;
+        set_f2t_dst(h, a, static_cast<char *>(dst) + r0 * run_stride, run_stride,
+                    dst2 ? static_cast<char *>(dst2) + r0 * run_stride2 : nullptr, run_stride2, per_run);
         s = run_f2t(h, a, J, st);
         nnvisr_status s2 = release_slot(slot, st);
         if (s) return s;
@@ -714,7 +793,7 @@ nnvisr_status nnvisr_frames_to_tensor_batch(nnvisr_handle *h, const int64_t *run
     if (!h || (num_runs > 0 && (!run_inputs || !tensors))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (num_runs < 0) return fail(NNVISR_ERR_INVALID_ARG, "num_runs < 0");
     if (num_runs == 0) return NNVISR_OK;
-    const int64_t tbytes = 3 * h->N * h->Hp * h->Wp * h->elem;
+    const int64_t tbytes = in_tuple_bytes(h);
     if (!aligned16(tensors) || tensor_stride_bytes % 16)
         return fail(NNVISR_ERR_INVALID_ARG, "tensors / stride not 16-byte aligned");
     if (num_runs > 1 && tensor_stride_bytes < tbytes)
@@ -746,19 +825,34 @@ nnvisr_status nnvisr_frames_to_store(nnvisr_handle *h, int64_t first, int64_t co
     if (s) return s;
     std::vector<int64_t> idx(count);
     for (int64_t i = 0; i < count; ++i) idx[i] = first + i;
-    const int64_t slot_bytes = 3 * h->Hp * h->Wp * h->elem;
-    return f2t_indexed(h, idx.data(), count, 1, store, slot_bytes, static_cast<cudaStream_t>(stream));
+    return f2t_indexed(h, idx.data(), count, 1, store, store_slot_bytes(h), static_cast<cudaStream_t>(stream));
 }
 
+// chroma / stride2: the chroma tensors of a YUV-output network (nullptr: packed
+// after the M luma planes of each tuple).
 static nnvisr_status t2f_common(nnvisr_handle *h, const void *tensors, int64_t stride, int64_t t_h, int64_t t_w,
-                                const nnvisr_frame *out, int64_t count, cudaStream_t st)
+                                const nnvisr_frame *out, int64_t count, cudaStream_t st, const void *chroma = nullptr,
+                                int64_t stride2 = 0)
 {
     if (t_h < h->Ho || t_w < h->Wo)
         return fail(NNVISR_ERR_INVALID_ARG, "tensor %lldx%lld smaller than the output frame %lldx%lld",
                     (long long)t_w, (long long)t_h, (long long)h->Wo, (long long)h->Ho);
     if (!aligned16(tensors) || stride % 16) return fail(NNVISR_ERR_INVALID_ARG, "tensor / stride not 16-byte aligned");
-    const int64_t tbytes = 3 * h->M * t_h * t_w * h->elem;
+    const bool sub = h->fmt.family == NNVISR_YUV420;
+    if (h->yuv_out && sub && ((t_h | t_w) & 1))
+        return fail(NNVISR_ERR_INVALID_ARG, "4:2:0 YUV tensors need an even tensor size (got %lldx%lld)",
+                    (long long)t_w, (long long)t_h);
+    const int64_t lbytes = (h->yuv_out ? 1 : 3) * h->M * t_h * t_w * h->elem;
+    const int64_t cplane = h->yuv_out ? (sub ? (t_h / 2) * (t_w / 2) : t_h * t_w) * h->elem : 0;
+    const bool packed = h->yuv_out && !chroma;
+    if (packed) {
+        chroma = static_cast<const char *>(tensors) + lbytes;
+        stride2 = stride;
+    }
+    const int64_t tbytes = packed ? lbytes + 2 * h->M * cplane : lbytes;
     if (count > 1 && stride < tbytes) return fail(NNVISR_ERR_INVALID_ARG, "tensor stride smaller than the tensor");
+    if (h->yuv_out && !packed && count > 1 && stride2 < 2 * h->M * cplane)
+        return fail(NNVISR_ERR_INVALID_ARG, "chroma stride smaller than the chroma tensor");
     // outputs whose descriptor has plane[0] == NULL are not converted (an
     // output the emission schedule drops, NEXT-1)
     const int64_t all_jobs = count * h->M;
@@ -789,6 +883,12 @@ static nnvisr_status t2f_common(nnvisr_handle *h, const void *tensors, int64_t s
     T2FArgs a = t2f_args(h, t_h, t_w);
     a.tensor_stride = stride;
     a.vec_out = vec;
+    if (h->yuv_out) {
+        const int64_t al = sub ? 4 * h->elem : 16;
+        a.tensor_stride2 = stride2;
+        a.vec_in_c = reinterpret_cast<uintptr_t>(chroma) % al == 0 && stride2 % al == 0 && cplane % al == 0 &&
+                     (a.twc * h->elem) % al == 0;
+    }
     const size_t per_job = sizeof(DevFrame) + (skipped ? sizeof(int32_t) : 0);
     const int64_t per_slot = skipped ? (int64_t)(kSlotBytes / per_job) : (int64_t)(kSlotBytes / sizeof(DevFrame)) / h->M * h->M;
     for (int64_t j0 = 0; j0 < jobs; j0 += per_slot) {
@@ -802,9 +902,11 @@ static nnvisr_status t2f_common(nnvisr_handle *h, const void *tensors, int64_t s
         if (skipped) {
             a.job_code = reinterpret_cast<const int32_t *>(static_cast<char *>(slot->dev) + sizeof(DevFrame) * nj);
             a.src = static_cast<const char *>(tensors);  // codes carry absolute tuple indices
+            a.src2 = static_cast<const char *>(chroma);
         } else {
             a.job_code = nullptr;
             a.src = static_cast<const char *>(tensors) + (j0 / h->M) * stride;
+            a.src2 = chroma ? static_cast<const char *>(chroma) + (j0 / h->M) * stride2 : nullptr;
         }
         s = run_t2f(h, a, nj, st);
         nnvisr_status s2 = release_slot(slot, st);
@@ -831,6 +933,47 @@ nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensor
     if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
     if (count == 0) return NNVISR_OK;
     return t2f_common(h, tensors, tensor_stride_bytes, t_h, t_w, out, count, static_cast<cudaStream_t>(stream));
+}
+
+nnvisr_status nnvisr_frames_to_tensor_yuv_batch(nnvisr_handle *h, const int64_t *run_inputs, int64_t num_runs,
+                                                void *luma, int64_t luma_stride_bytes, void *chroma,
+                                                int64_t chroma_stride_bytes, void *stream)
+{
+    g_error.clear();
+    if (!h || (num_runs > 0 && (!run_inputs || !luma || !chroma))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (!h->yuv_in) return fail(NNVISR_ERR_INVALID_ARG, "the network does not take YUV tensors (NNVISR_YUV_INPUT)");
+    if (num_runs < 0) return fail(NNVISR_ERR_INVALID_ARG, "num_runs < 0");
+    if (num_runs == 0) return NNVISR_OK;
+    if (!aligned16(luma) || luma_stride_bytes % 16)
+        return fail(NNVISR_ERR_INVALID_ARG, "luma tensors / stride not 16-byte aligned");
+    if (reinterpret_cast<uintptr_t>(chroma) % h->elem || chroma_stride_bytes % h->elem)
+        return fail(NNVISR_ERR_INVALID_ARG, "chroma tensors / stride not element aligned");
+    if (num_runs > 1 && (luma_stride_bytes < h->N * h->Hp * h->Wp * h->elem ||
+                         chroma_stride_bytes < 2 * h->N * h->Hc * h->Wc * h->elem))
+        return fail(NNVISR_ERR_INVALID_ARG, "tensor stride smaller than the tensor");
+    for (int64_t j = 0; j < num_runs * h->N; ++j)
+        if (run_inputs[j] < h->frames_base || run_inputs[j] >= h->frames_base + h->frames_count)
+            return fail(NNVISR_ERR_INVALID_ARG, "run %lld: frame %lld not bound", (long long)(j / h->N),
+                        (long long)run_inputs[j]);
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    return f2t_indexed(h, run_inputs, num_runs, h->N, luma, luma_stride_bytes, static_cast<cudaStream_t>(stream),
+                       chroma, chroma_stride_bytes);
+}
+
+nnvisr_status nnvisr_tensor_to_frames_yuv_batch(nnvisr_handle *h, const void *luma, int64_t luma_stride_bytes,
+                                                const void *chroma, int64_t chroma_stride_bytes, int64_t t_h,
+                                                int64_t t_w, const nnvisr_frame *out, int64_t count, void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && (!luma || !chroma || !out))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (!h->yuv_out) return fail(NNVISR_ERR_INVALID_ARG, "the network does not produce YUV tensors (NNVISR_YUV_OUTPUT)");
+    if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
+    if (count == 0) return NNVISR_OK;
+    if (reinterpret_cast<uintptr_t>(chroma) % h->elem || chroma_stride_bytes % h->elem)
+        return fail(NNVISR_ERR_INVALID_ARG, "chroma tensors / stride not element aligned");
+    return t2f_common(h, luma, luma_stride_bytes, t_h, t_w, out, count, static_cast<cudaStream_t>(stream), chroma,
+                      chroma_stride_bytes);
 }
 
 nnvisr_status nnvisr_scene_detect(nnvisr_handle *h, int64_t first, int64_t count, double threshold, uint64_t *sad,
@@ -946,8 +1089,7 @@ nnvisr_status nnvisr_frames_to_slots(nnvisr_handle *h, const int64_t *slot_frame
     }
     nnvisr_status s = ensure_device(h);
     if (s) return s;
-    const int64_t slot_bytes = 3 * h->Hp * h->Wp * h->elem;
-    return f2t_indexed(h, slot_frames, count, 1, store, slot_bytes, static_cast<cudaStream_t>(stream));
+    return f2t_indexed(h, slot_frames, count, 1, store, store_slot_bytes(h), static_cast<cudaStream_t>(stream));
 }
 
 nnvisr_status nnvisr_copy_slot(nnvisr_handle *h, void *store, int64_t src, int64_t dst, void *stream)
@@ -958,7 +1100,7 @@ nnvisr_status nnvisr_copy_slot(nnvisr_handle *h, void *store, int64_t src, int64
     if (src == dst) return NNVISR_OK;
     nnvisr_status s = ensure_device(h);
     if (s) return s;
-    const int64_t slot_bytes = 3 * h->Hp * h->Wp * h->elem;
+    const int64_t slot_bytes = store_slot_bytes(h);
     char *base = static_cast<char *>(store);
     cudaError_t e = cudaMemcpyAsync(base + dst * slot_bytes, base + src * slot_bytes, slot_bytes,
                                     cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
@@ -1148,7 +1290,7 @@ nnvisr_status nnvisr_frames_to_tensor_batch_host(nnvisr_handle *h, const nnvisr_
     if (num_runs == 0) return NNVISR_OK;
     if (!aligned16(tensors) || tensor_stride_bytes % 16)
         return fail(NNVISR_ERR_INVALID_ARG, "tensors / stride not 16-byte aligned");
-    const int64_t tbytes = 3 * h->N * h->Hp * h->Wp * h->elem;
+    const int64_t tbytes = in_tuple_bytes(h);
     if (num_runs > 1 && tensor_stride_bytes < tbytes) return fail(NNVISR_ERR_INVALID_ARG, "tensor stride too small");
     for (int64_t j = 0; j < num_runs * h->N; ++j)
         if (run_inputs[j] < base || run_inputs[j] >= base + count)

@@ -99,7 +99,7 @@ class FrameBuffer:
         return self.layout.frame_bytes
 
     def descriptor(self, i: int) -> nv.Frame:
-        base = self.data.data_ptr() + i * self.layout.frame_bytes
+        base = self.data.data_ptr() + int(i) * self.layout.frame_bytes
         f = nv.Frame()
         for p, (off, pitch, _, _) in enumerate(self._planes):
             f.plane[p] = base + off

@@ -17,8 +17,8 @@ from typing import Sequence
 import numpy as np
 
 from .config import (BT601, BT709, BT2020, CHROMA_CENTER, CHROMA_LEFT, DOUBLE_FRAME, EXTRA_FRAME, F16,  # noqa: F401
-                     F32, FULL, INTERPOLATION, LIMITED, RGB, STATUS, YUV420, YUV444, ClipFormat, Config, Frame,
-                     Network)
+                     F32, FULL, INTERPOLATION, LIMITED, RGB, STATUS, YUV420, YUV444, YUV_INPUT, YUV_OUTPUT,
+                     ClipFormat, Config, Frame, Network)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libnnvisr.so")
@@ -65,6 +65,10 @@ def _load():
                                                     C.c_void_p]),
         "nnvisr_tensor_to_frames_batch_host": (st, [H, C.c_void_p, i64, i64, i64, C.POINTER(Frame), i64, C.c_void_p]),
         "nnvisr_host_fence": (st, [H, C.c_void_p]),
+        "nnvisr_chroma_shapes": (st, [H, i64p, i64p]),
+        "nnvisr_frames_to_tensor_yuv_batch": (st, [H, i64p, i64, C.c_void_p, i64, C.c_void_p, i64, C.c_void_p]),
+        "nnvisr_tensor_to_frames_yuv_batch": (st, [H, C.c_void_p, i64, C.c_void_p, i64, i64, i64, C.POINTER(Frame),
+                                                   i64, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -80,7 +84,8 @@ EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version"
             "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch", "nnvisr_scene_detect",
             "nnvisr_shared_slot_offset", "nnvisr_plan_batches", "nnvisr_frames_to_slots", "nnvisr_copy_slot",
             "nnvisr_schedule_outputs", "nnvisr_copy_frames", "nnvisr_frames_to_tensor_batch_host",
-            "nnvisr_tensor_to_frames_batch_host", "nnvisr_host_fence")
+            "nnvisr_tensor_to_frames_batch_host", "nnvisr_host_fence", "nnvisr_chroma_shapes",
+            "nnvisr_frames_to_tensor_yuv_batch", "nnvisr_tensor_to_frames_yuv_batch")
 
 
 def lib():
@@ -134,6 +139,10 @@ class Handle:
         _check(_lib.nnvisr_tensor_shapes(self._h, _i64p(i), _i64p(o)))
         self.in_shape = tuple(int(v) for v in i)
         self.out_shape = tuple(int(v) for v in o)  # minimum; also (Ho, Wo) of output frames
+        _check(_lib.nnvisr_chroma_shapes(self._h, _i64p(i), _i64p(o)))
+        # chroma tensors of the YUV sides (all zeros for an RGB side)
+        self.in_chroma_shape = tuple(int(v) for v in i)
+        self.out_chroma_shape = tuple(int(v) for v in o)
 
     # -- lifetime
     def close(self):
@@ -155,13 +164,12 @@ class Handle:
 
     @property
     def N(self):
-        return self.in_shape[1] // 3
+        return self.cfg.input_count
 
     @property
     def M(self):
-        return self.out_shape[1] // 3
+        return self.cfg.output_count
 
-    # -- planning (host)
     def plan(self, cut):
         cut = np.ascontiguousarray(np.asarray(cut, dtype=np.uint8))
         F = cut.shape[0]
@@ -268,6 +276,18 @@ class Handle:
     def scene_detect(self, first: int, count: int, threshold: float, sad_ptr: int, cut_ptr: int, stream=None):
         """nnvisr_scene_detect: sad (uint64) and cut (uint8) device arrays [count]."""
         _check(_lib.nnvisr_scene_detect(self._h, first, count, threshold, sad_ptr, cut_ptr, _stream_ptr(stream)))
+
+    def frames_to_tensor_yuv_batch(self, run_inputs, luma_ptr: int, luma_stride: int, chroma_ptr: int,
+                                   chroma_stride: int, stream=None):
+        ri = np.ascontiguousarray(np.asarray(run_inputs, dtype=np.int64))
+        nr = ri.shape[0] if ri.ndim > 1 else (ri.shape[0] // self.N if ri.size else 0)
+        _check(_lib.nnvisr_frames_to_tensor_yuv_batch(self._h, _i64p(ri), nr, luma_ptr, luma_stride, chroma_ptr,
+                                                      chroma_stride, _stream_ptr(stream)))
+
+    def tensor_to_frames_yuv_batch(self, luma_ptr: int, luma_stride: int, chroma_ptr: int, chroma_stride: int,
+                                   t_h: int, t_w: int, out: Sequence[Frame], count: int, stream=None):
+        _check(_lib.nnvisr_tensor_to_frames_yuv_batch(self._h, luma_ptr, luma_stride, chroma_ptr, chroma_stride,
+                                                      t_h, t_w, frame_array(out), count, _stream_ptr(stream)))
 
     def tensor_to_frames_batch(self, tensors_ptr: int, stride: int, t_h: int, t_w: int, out: Sequence[Frame],
                                count: int, stream=None):

@@ -40,7 +40,10 @@ def _cfg(**kw):
     (dict(matrix=7), 1, "matrix"),
     (dict(range=3), 1, "range"),
     (dict(family=9), 1, "family"),
-    (dict(chroma_loc=nv.CHROMA_LEFT), 3, "LEFT"),
+    (dict(chroma_loc=5), 1, "siting"),
+    (dict(family=nv.RGB, flags=nv.YUV_INPUT), 1, "YUV"),
+    (dict(family=nv.RGB, flags=nv.YUV_OUTPUT), 1, "YUV"),
+    (dict(flags=32), 1, "flag bits"),
     (dict(input_count=0), 1, "input_count"),
     (dict(input_count=17), 1, "input_count"),
     (dict(output_count=0), 1, "output_count"),
@@ -72,6 +75,21 @@ def test_open_accepts_and_shapes():
             assert h.out_shape == (1, 3 * c.output_count, c.height * c.sy[0] // c.sy[1],
                                    c.width * c.sx[0] // c.sx[1])
     assert nv.open(synth.WORKLOADS["c2"].cfg).in_shape == (1, 15, 1088, 1920)
+
+
+def test_yuv_shapes_and_left_accepted():
+    """NEXT-3 configurations open; YUV sides report luma [1, K, h, w] and
+    chroma [1, 2K, h/2, w/2] (4:2:0) or [1, 2K, h, w] (4:4:4) shapes."""
+    c = _cfg(width=66, height=34, align=8, flags=nv.YUV_INPUT | nv.YUV_OUTPUT, input_count=3,
+             sx=(2, 1), sy=(2, 1), chroma_loc=nv.CHROMA_LEFT)
+    with nv.open(c) as h:
+        assert h.in_shape == (1, 3, 40, 72) and h.in_chroma_shape == (1, 6, 20, 36)
+        assert h.out_shape == (1, 1, 68, 132) and h.out_chroma_shape == (1, 2, 34, 66)
+    with nv.open(_cfg(family=nv.YUV444, flags=nv.YUV_OUTPUT)) as h:
+        assert h.in_shape == (1, 6, 64, 64) and h.in_chroma_shape == (0, 0, 0, 0)
+        assert h.out_shape == (1, 1, 64, 64) and h.out_chroma_shape == (1, 2, 64, 64)
+    with nv.open(_cfg(chroma_loc=nv.CHROMA_LEFT)) as h:
+        assert h.in_shape == (1, 6, 64, 64)
 
 
 def _oracle_plan(cut, n, N, L):
