@@ -46,6 +46,8 @@ def parse():
                    help="t2f converts only the outputs the emission schedule presents (NEXT-1; drops e.g. the "
                         "trailing enhanced lookahead of M = 2n+1 networks), pass-through frames are copied")
     p.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"])
+    p.add_argument("--frames", type=int, default=0,
+                   help="clip frames per rank (0 = the workload's; profiling/sweeps only, recorded in config)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--detect", action="store_true",
                    help="detect scene changes on the GPU each step (NEXT-4) and plan from those flags")
@@ -230,7 +232,7 @@ def main():
     w = synth.WORKLOADS[args.workload]
     cfg = w.cfg
     scaling = args.scaling if args.scaling != "auto" else ("strong" if args.workload == "c5" else "weak")
-    total = w.frames * (world if scaling == "weak" else 1)
+    total = (args.frames or w.frames) * (world if scaling == "weak" else 1)
     h = nv.open(cfg)
     N, M = h.N, h.M
     L = 0 if cfg.flags else ((N - 1) // 2 if cfg.left_context == -1 else cfg.left_context)

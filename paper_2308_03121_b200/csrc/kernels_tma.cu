@@ -85,7 +85,13 @@ constexpr int kSegW = kThreads * kPx;         // columns per tile segment (2048)
 constexpr int kConsumerWarps = kThreads / 32;  // converting warps; one more warp produces
 constexpr int kMaxStages = 8;
 constexpr int kMaxOutBufs = 8;
-constexpr int kBarBytes = 8 * (2 * kMaxStages + kMaxOutBufs);  // mbarriers at the start of dynamic smem
+// per-stage tile header written by the loader, read by the consumers
+struct F2THdr {
+    int u0, nu, x0, x1, ly0, cy0, lw0, cw0;
+};
+// mbarriers (full, empty per stage; ofree, conv per output buffer) and the
+// stage headers at the start of dynamic smem
+constexpr int kBarBytes = 8 * (2 * kMaxStages + 2 * kMaxOutBufs) + 32 * kMaxStages;
 
 // CTA b takes tiles b, b + G, b + 2G, ... (G = grid size): every CTA gets the
 // same mix of frames, whatever each frame's number of destinations.
@@ -180,7 +186,7 @@ struct F2TTile {
 };
 
 template <int FAMILY, typename IN>
-__device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *st, uint64_t *bar)
+__device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *st, uint64_t *bar, F2THdr *hdr)
 {
     using S = F2TStage<FAMILY, IN>;
     const S sg(a.ls, a.cs, a.band);
@@ -189,6 +195,8 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
     const DevFrame f = load_frame(a.frames + a.job_frame[tl.job]);
     F2TWindow w;
     w.set(tl.x0, tl.x1, a.W, S::G, FAMILY == kYUV420);
+    // the consumers' view of the tile (whole rows staged: window = full row)
+    *hdr = F2THdr{tl.u0, tl.nu, tl.x0, tl.x1, tl.ly0, tl.cy0, a.whole ? 0 : w.lw0, a.whole ? 0 : w.cw0};
     const int nl = tl.ly1 - tl.ly0 + 1;
     if constexpr (FAMILY == kYUV420) {
         const int nc = tl.cy1 - tl.cy0 + 1;
@@ -221,24 +229,31 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
     }
 }
 
-// Warp-specialised: warps 0..7 convert (consumers), warp 8 lane 0 is the
-// producer.  Per stage k: full[k] (TMA bytes landed), empty[k] (8 consumer
-// warps done: input stage read AND the tile's output buffer written).  Per
-// output buffer b: ofree[b] (the bulk stores that last read it are done).
-// The producer waits empty, fans the finished tile out with bulk stores,
-// refills the stage, and releases output buffers as the stores drain; no
-// consumer ever waits on a store or on a descriptor load.
+// Warp-specialised: warps 0..7 convert (consumers), warp 8 lane 0 loads
+// (the "loader"), warp 9 lane 0 stores (the "storer").  Per input stage k:
+// full[k] (TMA bytes landed), empty[k] (the 8 consumer warps have read it).
+// Per output buffer b: conv[b] (the consumers have written the tile's
+// converted band into it), ofree[b] (the bulk stores that read it are done).
+// The loader refills a stage as soon as the consumers release it, whatever
+// the stores are doing; the storer fans each converted band out with bulk
+// stores and releases output buffers as the stores drain.  No consumer ever
+// waits on a store, and no load waits on a store.  The loader writes each
+// stage's tile header (F2THdr) before its expect_tx arrive (release), so the
+// consumers read it after their full wait (acquire) instead of decoding the
+// tile index themselves.
 // Output buffer layout: [channel][B*ROWS rows][sw]: with a single segment a
 // channel's band rows are contiguous in the tensor too, one bulk store each.
 template <int FAMILY, typename IN, typename OUT>
-__global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
+__global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
 {
     using S = F2TStage<FAMILY, IN>;
     using V8 = typename Pack<IN>::V8;
     using V4 = typename Pack<IN>::V4;
     constexpr int ROWS = S::ROWS;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages, *ofree = empty + kMaxStages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages, *ofree = empty + kMaxStages,
+             *conv = ofree + kMaxOutBufs;
+    F2THdr *hdr = reinterpret_cast<F2THdr *>(conv + kMaxOutBufs);
     uint8_t *stages = smem + kBarBytes;
     const int nst = a.stages, nob = a.nob, brows = a.band * ROWS;
     const S sg(a.ls, a.cs, a.band);
@@ -252,90 +267,94 @@ __global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
             mbar_init(&full[k], 1);
             mbar_init(&empty[k], kConsumerWarps);
         }
-        for (int b = 0; b < nob; ++b) mbar_init(&ofree[b], 1);
+        for (int b = 0; b < nob; ++b) {
+            mbar_init(&ofree[b], 1);
+            mbar_init(&conv[b], kConsumerWarps);
+        }
         fence_barrier_init();
     }
     __syncthreads();  // the last CTA-wide barrier: roles split below
 
-    if (threadIdx.x >= kThreads) {  // ---------------- producer warp
-        if (threadIdx.x != kThreads) return;
-        for (int k = 0; k < nst && k < tc.count; ++k)
-            f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k]);
-        int lj = -1;
-        DstList dl;
-        const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
-        for (int64_t i = 0; i < tc.count; ++i) {
-            const int k = static_cast<int>(i % nst);
-            mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
-            // fan tile i out to every (run, slot) holding its frame
-            F2TTile tl;
-            tl.set(a, tc.tile(i), ROWS);
-            const int sw = tl.x1 - tl.x0, rows = tl.nu * ROWS;
-            if (tl.job != lj) {
-                lj = tl.job;
-                dl.load(a, tl.job);
+    if (threadIdx.x >= kThreads) {
+        if (threadIdx.x == kThreads) {  // ---------------- loader
+            for (int k = 0; k < nst && k < tc.count; ++k)
+                f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+            for (int64_t i = 0; i + nst < tc.count; ++i) {
+                const int k = static_cast<int>(i % nst);
+                mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
+                fence_proxy_async();
+                f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
             }
-            const OUT *ob = obuf + static_cast<int>(i % nob) * a.ob_elems;
-            const bool whole_rows = tl.x0 == 0 && sw == a.Wp;
-            for (int d = 0; d < dl.nd; ++d) {
-                const int cd = dl.get(a, d);
-                OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
-                                                 static_cast<int64_t>(cd & 31) * a.slot_bytes) +
-                         static_cast<int64_t>(tl.u0 * ROWS) * a.Wp + tl.x0;
-                for (int c = 0; c < 3; ++c) {
-                    if (whole_rows) {
-                        bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
-                    } else {
-                        for (int r = 0; r < rows; ++r)
-                            bulk_s2g(o + c * plane + static_cast<int64_t>(r) * a.Wp, ob + (c * brows + r) * sw,
-                                     sw * sizeof(OUT));
+        } else if (threadIdx.x == kThreads + 32) {  // ---------------- storer
+            int lj = -1;
+            DstList dl;
+            const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
+            const int ahead = a.release_ahead;
+            for (int64_t i = 0; i < tc.count; ++i) {
+                const int b = static_cast<int>(i % nob);
+                mbar_wait(&conv[b], static_cast<uint32_t>((i / nob) & 1));
+                // fan tile i out to every (run, slot) holding its frame
+                F2TTile tl;
+                tl.set(a, tc.tile(i), ROWS);
+                const int sw = tl.x1 - tl.x0, rows = tl.nu * ROWS;
+                if (tl.job != lj) {
+                    lj = tl.job;
+                    dl.load(a, tl.job);
+                }
+                const OUT *ob = obuf + b * a.ob_elems;
+                const bool whole_rows = tl.x0 == 0 && sw == a.Wp;
+                for (int d = 0; d < dl.nd; ++d) {
+                    const int cd = dl.get(a, d);
+                    OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
+                                                     static_cast<int64_t>(cd & 31) * a.slot_bytes) +
+                             static_cast<int64_t>(tl.u0 * ROWS) * a.Wp + tl.x0;
+                    for (int c = 0; c < 3; ++c) {
+                        if (whole_rows) {
+                            bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
+                        } else {
+                            for (int r = 0; r < rows; ++r)
+                                bulk_s2g(o + c * plane + static_cast<int64_t>(r) * a.Wp, ob + (c * brows + r) * sw,
+                                         sw * sizeof(OUT));
+                        }
                     }
                 }
-            }
-            bulk_commit();
-            // refill stage k with tile i + nst
-            if (i + nst < tc.count) {
-                fence_proxy_async();
-                f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k]);
-            }
-            // buffer of tile i+2 (last read by tile i+2-nob's stores) is free
-            // once at most nob-2 store groups are still reading smem
-            if (i + 2 >= nob && i + 2 < tc.count) {
-                switch (nob) {
-                case 2: bulk_wait_read<0>(); break;
-                case 3: bulk_wait_read<1>(); break;
-                case 4: bulk_wait_read<2>(); break;
-                case 5: bulk_wait_read<3>(); break;
-                case 6: bulk_wait_read<4>(); break;
-                case 7: bulk_wait_read<5>(); break;
-                default: bulk_wait_read<6>(); break;
+                bulk_commit();
+                // the buffer of tile j = i + ahead (last read by the stores of
+                // tile j - nob) is free once at most nob - ahead groups are
+                // still reading shared memory
+                const int64_t j = i + ahead;
+                if (j >= nob && j < tc.count) {
+                    switch (nob - ahead) {
+                    case 0: bulk_wait_read<0>(); break;
+                    case 1: bulk_wait_read<1>(); break;
+                    case 2: bulk_wait_read<2>(); break;
+                    case 3: bulk_wait_read<3>(); break;
+                    case 4: bulk_wait_read<4>(); break;
+                    case 5: bulk_wait_read<5>(); break;
+                    case 6: bulk_wait_read<6>(); break;
+                    default: bulk_wait_read<7>(); break;
+                    }
+                    mbar_arrive(&ofree[static_cast<int>(j % nob)]);
                 }
-                mbar_arrive(&ofree[static_cast<int>((i + 2) % nob)]);
             }
+            bulk_wait_all();
         }
-        bulk_wait_all();
         return;
     }
 
     // ------------------------------------------------------------ consumers
     const int cw = a.W >> 1, ch = a.H >> 1;
     for (int64_t i = 0; i < tc.count; ++i) {
-        F2TTile tl;
-        tl.set(a, tc.tile(i), ROWS);
+        const int k = static_cast<int>(i % nst);
+        const int b = static_cast<int>(i % nob);
+        uint8_t *st = stages + k * a.stage_bytes;
+        OUT *ob = obuf + b * a.ob_elems;
+        mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
+        const F2THdr tl = hdr[k];
         const int sw = tl.x1 - tl.x0;
         const int x = tl.x0 + kPx * threadIdx.x;
-        const int k = static_cast<int>(i % nst);
-        uint8_t *st = stages + k * a.stage_bytes;
-        OUT *ob = obuf + static_cast<int>(i % nob) * a.ob_elems;
-        F2TWindow w;
-        w.set(tl.x0, tl.x1, a.W, S::G, FAMILY == kYUV420);
-        if (a.whole) {  // whole rows staged: window = the full row
-            w.lw0 = 0;
-            w.cw0 = 0;
-        }
         const bool fast = x + kPx <= a.W;
-        mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
-        if (i >= nob) mbar_wait(&ofree[static_cast<int>(i % nob)], static_cast<uint32_t>((i / nob - 1) & 1));
+        if (i >= nob) mbar_wait(&ofree[b], static_cast<uint32_t>((i / nob - 1) & 1));
         if (x < tl.x1) {
             for (int u = 0; u < tl.nu; ++u) {
 #pragma unroll
@@ -343,11 +362,11 @@ __global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
                     const int yc = min((tl.u0 + u) * ROWS + r, a.H - 1);
                     int ys[kPx], us[kPx], vs[kPx];
                     if constexpr (FAMILY == kYUV420) {
-                        const IN *L = sg.luma(st, yc - tl.ly0) - w.lw0;
-                        const IN *Cn[2] = {sg.chroma(st, 0, chroma_near(yc) - tl.cy0) - w.cw0,
-                                           sg.chroma(st, 1, chroma_near(yc) - tl.cy0) - w.cw0};
-                        const IN *Cf[2] = {sg.chroma(st, 0, chroma_far(yc, ch) - tl.cy0) - w.cw0,
-                                           sg.chroma(st, 1, chroma_far(yc, ch) - tl.cy0) - w.cw0};
+                        const IN *L = sg.luma(st, yc - tl.ly0) - tl.lw0;
+                        const IN *Cn[2] = {sg.chroma(st, 0, chroma_near(yc) - tl.cy0) - tl.cw0,
+                                           sg.chroma(st, 1, chroma_near(yc) - tl.cy0) - tl.cw0};
+                        const IN *Cf[2] = {sg.chroma(st, 0, chroma_far(yc, ch) - tl.cy0) - tl.cw0,
+                                           sg.chroma(st, 1, chroma_far(yc, ch) - tl.cy0) - tl.cw0};
                         if (fast) {
                             unpack8(*reinterpret_cast<const V8 *>(L + x), ys);
                             const int i0 = x >> 1;
@@ -382,9 +401,9 @@ __global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
 #pragma unroll
                         for (int kk = 0; kk < kPx; ++kk) ys[kk] *= 16;
                     } else {
-                        const IN *P0 = sg.plane(st, 0, yc - tl.ly0) - w.lw0,
-                                 *P1 = sg.plane(st, 1, yc - tl.ly0) - w.lw0,
-                                 *P2 = sg.plane(st, 2, yc - tl.ly0) - w.lw0;
+                        const IN *P0 = sg.plane(st, 0, yc - tl.ly0) - tl.lw0,
+                                 *P1 = sg.plane(st, 1, yc - tl.ly0) - tl.lw0,
+                                 *P2 = sg.plane(st, 2, yc - tl.ly0) - tl.lw0;
                         if (fast) {
                             unpack8(*reinterpret_cast<const V8 *>(P0 + x), ys);
                             unpack8(*reinterpret_cast<const V8 *>(P1 + x), us);
@@ -414,7 +433,10 @@ __global__ void __launch_bounds__(kThreads + 32, 2) f2t_tma(const F2TArgs a)
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
         __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[k]);
+        if ((threadIdx.x & 31) == 0) {
+            mbar_arrive(&empty[k]);
+            mbar_arrive(&conv[b]);
+        }
     }
 }
 
@@ -615,15 +637,16 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     }
     a.tiles = a.tiles / bands * ((a.rowunits + a.band - 1) / a.band);
     const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band);
+    a.release_ahead = std::max(1, std::min(a.nob, env_int("NNVISR_F2T_AHEAD", 1)));
     auto kernel = f2t_tma<FAMILY, IN, OUT>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads + 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads + 64, smem);
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
-    kernel<<<grid, kThreads + 32, smem, s>>>(a);
+    kernel<<<grid, kThreads + 64, smem, s>>>(a);
     return cudaGetLastError();
 }
 
