@@ -68,7 +68,8 @@ struct F2TArgs {
     int32_t tma_ok, rowunits, nseg, stages, stage_bytes;
     int32_t nob, ob_elems;        // output buffers, elements per buffer
     int32_t band, ls, cs, whole;  // band height (row units), staged row strides, whole-row copies
-    int32_t release_ahead;        // storer frees the output buffer of tile i + release_ahead after tile i
+    uint64_t *trace;              // experiment timeline buffer (debug & 8)
+    int32_t debug;                // experiment switches (NNVISR_F2T_DEBUG), 0 in production
     int64_t pitch_y, pitch_c;     // uniform plane pitches of the bound frames (0 = not uniform)
     int64_t tiles;
     F2TColour col;

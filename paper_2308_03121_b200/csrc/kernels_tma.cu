@@ -19,7 +19,9 @@
 // are clamped to the plane and 16-byte aligned.  The host enables this path
 // only when every window is 16-byte aligned (see nnvisr.cpp, tma_ok).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 
@@ -80,6 +82,15 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Experiment timeline (NNVISR_F2T_DEBUG & 8): SM clock of event `ev` of tile
+// i, CTAs 0 and 1, first 128 tiles (see f2t_tma_launch).
+constexpr int kTraceTiles = 128, kTraceEvents = 8;
+__device__ __forceinline__ void trace(const F2TArgs &a, int ev, int64_t i)
+{
+    if ((a.debug & 8) && blockIdx.x < 2 && i < kTraceTiles)
+        a.trace[(blockIdx.x * kTraceEvents + ev) * kTraceTiles + i] = clock64();
+}
 
 constexpr int kSegW = kThreads * kPx;         // columns per tile segment (2048)
 constexpr int kConsumerWarps = kThreads / 32;  // converting warps; one more warp produces
@@ -185,62 +196,72 @@ struct F2TTile {
     }
 };
 
+// The copies that stage tile `tl` (rows clamped to the frame, windows
+// 16-byte aligned): cp(smem dst, global src, bytes) per contiguous piece.
+template <int FAMILY, typename IN, typename CP>
+__device__ __forceinline__ void f2t_copies(const F2TArgs &a, const F2TTile &tl, const F2TWindow &w, const DevFrame &f,
+                                           uint8_t *st, CP &&cp)
+{
+    using S = F2TStage<FAMILY, IN>;
+    const S sg(a.ls, a.cs, a.band);
+    const int nl = tl.ly1 - tl.ly0 + 1;
+    if constexpr (FAMILY == kYUV420) {
+        const int nc = tl.cy1 - tl.cy0 + 1;
+        if (a.whole) {
+            cp(sg.luma(st, 0), row_ptr<IN>(f, 0, tl.ly0), nl * a.ls * sizeof(IN));
+            cp(sg.chroma(st, 0, 0), row_ptr<IN>(f, 1, tl.cy0), nc * a.cs * sizeof(IN));
+            cp(sg.chroma(st, 1, 0), row_ptr<IN>(f, 2, tl.cy0), nc * a.cs * sizeof(IN));
+        } else {
+            const uint32_t lb = (w.lw1 - w.lw0) * sizeof(IN), cb = (w.cw1 - w.cw0) * sizeof(IN);
+            for (int r = 0; r < nl; ++r) cp(sg.luma(st, r), row_ptr<IN>(f, 0, tl.ly0 + r) + w.lw0, lb);
+            for (int p = 0; p < 2; ++p)
+                for (int r = 0; r < nc; ++r) cp(sg.chroma(st, p, r), row_ptr<IN>(f, p + 1, tl.cy0 + r) + w.cw0, cb);
+        }
+    } else {
+        if (a.whole) {
+            for (int p = 0; p < 3; ++p) cp(sg.plane(st, p, 0), row_ptr<IN>(f, p, tl.ly0), nl * a.ls * sizeof(IN));
+        } else {
+            const uint32_t lb = (w.lw1 - w.lw0) * sizeof(IN);
+            for (int p = 0; p < 3; ++p)
+                for (int r = 0; r < nl; ++r) cp(sg.plane(st, p, r), row_ptr<IN>(f, p, tl.ly0 + r) + w.lw0, lb);
+        }
+    }
+}
+
+// Stage tile t: write the consumers' view of the tile (F2THdr), then issue
+// its TMA bulk copies, completing by byte count on `bar`.
 template <int FAMILY, typename IN>
 __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *st, uint64_t *bar, F2THdr *hdr)
 {
     using S = F2TStage<FAMILY, IN>;
-    const S sg(a.ls, a.cs, a.band);
     F2TTile tl;
     tl.set(a, t, S::ROWS);
     const DevFrame f = load_frame(a.frames + a.job_frame[tl.job]);
     F2TWindow w;
     w.set(tl.x0, tl.x1, a.W, S::G, FAMILY == kYUV420);
-    // the consumers' view of the tile (whole rows staged: window = full row)
     *hdr = F2THdr{tl.u0, tl.nu, tl.x0, tl.x1, tl.ly0, tl.cy0, a.whole ? 0 : w.lw0, a.whole ? 0 : w.cw0};
-    const int nl = tl.ly1 - tl.ly0 + 1;
-    if constexpr (FAMILY == kYUV420) {
-        const int nc = tl.cy1 - tl.cy0 + 1;
-        if (a.whole) {
-            const uint32_t lb = nl * a.ls * sizeof(IN), cb = nc * a.cs * sizeof(IN);
-            mbar_arrive_expect_tx(bar, lb + 2 * cb);
-            bulk_g2s(sg.luma(st, 0), row_ptr<IN>(f, 0, tl.ly0), lb, bar);
-            bulk_g2s(sg.chroma(st, 0, 0), row_ptr<IN>(f, 1, tl.cy0), cb, bar);
-            bulk_g2s(sg.chroma(st, 1, 0), row_ptr<IN>(f, 2, tl.cy0), cb, bar);
-        } else {
-            const uint32_t lb = (w.lw1 - w.lw0) * sizeof(IN), cb = (w.cw1 - w.cw0) * sizeof(IN);
-            mbar_arrive_expect_tx(bar, nl * lb + 2 * nc * cb);
-            for (int r = 0; r < nl; ++r) bulk_g2s(sg.luma(st, r), row_ptr<IN>(f, 0, tl.ly0 + r) + w.lw0, lb, bar);
-            for (int p = 0; p < 2; ++p)
-                for (int r = 0; r < nc; ++r)
-                    bulk_g2s(sg.chroma(st, p, r), row_ptr<IN>(f, p + 1, tl.cy0 + r) + w.cw0, cb, bar);
-        }
-    } else {
-        if (a.whole) {
-            const uint32_t lb = nl * a.ls * sizeof(IN);
-            mbar_arrive_expect_tx(bar, 3 * lb);
-            for (int p = 0; p < 3; ++p) bulk_g2s(sg.plane(st, p, 0), row_ptr<IN>(f, p, tl.ly0), lb, bar);
-        } else {
-            const uint32_t lb = (w.lw1 - w.lw0) * sizeof(IN);
-            mbar_arrive_expect_tx(bar, 3 * nl * lb);
-            for (int p = 0; p < 3; ++p)
-                for (int r = 0; r < nl; ++r)
-                    bulk_g2s(sg.plane(st, p, r), row_ptr<IN>(f, p, tl.ly0 + r) + w.lw0, lb, bar);
-        }
+    if (a.debug & 4) {  // experiment: no loads
+        mbar_arrive(bar);
+        return;
     }
+    uint32_t total = 0;
+    f2t_copies<FAMILY, IN>(a, tl, w, f, st, [&](void *, const void *, uint32_t bytes) { total += bytes; });
+    mbar_arrive_expect_tx(bar, total);
+    f2t_copies<FAMILY, IN>(a, tl, w, f, st,
+                           [&](void *dst, const void *src, uint32_t bytes) { bulk_g2s(dst, src, bytes, bar); });
 }
 
-// Warp-specialised: warps 0..7 convert (consumers), warp 8 lane 0 loads
-// (the "loader"), warp 9 lane 0 stores (the "storer").  Per input stage k:
-// full[k] (TMA bytes landed), empty[k] (the 8 consumer warps have read it).
-// Per output buffer b: conv[b] (the consumers have written the tile's
-// converted band into it), ofree[b] (the bulk stores that read it are done).
-// The loader refills a stage as soon as the consumers release it, whatever
-// the stores are doing; the storer fans each converted band out with bulk
-// stores and releases output buffers as the stores drain.  No consumer ever
-// waits on a store, and no load waits on a store.  The loader writes each
-// stage's tile header (F2THdr) before its expect_tx arrive (release), so the
-// consumers read it after their full wait (acquire) instead of decoding the
-// tile index themselves.
+// Warp-specialised: warps 0..7 convert (consumers); lane 0 of warps 8 and 9
+// are the two "storers".  Per input stage k: full[k] (TMA bytes landed).  Per
+// output buffer b: conv[b] (the 8 consumer warps have read tile i's stage and
+// written its converted band into buffer b), ofree[b] (the bulk stores that
+// read it are done).  Storer s handles tiles s, s + 2, ...: on conv[i] it
+// refills tile i's stage with tile i + nst (TMA bulk copies, issued before
+// tile i's stores so they do not queue behind them), frees an older output
+// buffer and fans tile i out with bulk stores.  No consumer ever waits on a
+// store.  Each stage's tile header (F2THdr) is written before the
+// expect_tx arrive (release), so the consumers read it after their full wait
+// (acquire) instead of decoding the tile index themselves.
 // Output buffer layout: [channel][B*ROWS rows][sw]: with a single segment a
 // channel's band rows are contiguous in the tensor too, one bulk store each.
 template <int FAMILY, typename IN, typename OUT>
@@ -251,8 +272,7 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
     using V4 = typename Pack<IN>::V4;
     constexpr int ROWS = S::ROWS;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages, *ofree = empty + kMaxStages,
-             *conv = ofree + kMaxOutBufs;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *ofree = full + 2 * kMaxStages, *conv = ofree + kMaxOutBufs;
     F2THdr *hdr = reinterpret_cast<F2THdr *>(conv + kMaxOutBufs);
     uint8_t *stages = smem + kBarBytes;
     const int nst = a.stages, nob = a.nob, brows = a.band * ROWS;
@@ -263,10 +283,7 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
     tc.init(a.tiles);
     if (tc.count == 0) return;
     if (threadIdx.x == 0) {
-        for (int k = 0; k < nst; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], kConsumerWarps);
-        }
+        for (int k = 0; k < nst; ++k) mbar_init(&full[k], 1);
         for (int b = 0; b < nob; ++b) {
             mbar_init(&ofree[b], 1);
             mbar_init(&conv[b], kConsumerWarps);
@@ -275,24 +292,44 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
     }
     __syncthreads();  // the last CTA-wide barrier: roles split below
 
-    if (threadIdx.x >= kThreads) {
-        if (threadIdx.x == kThreads) {  // ---------------- loader
-            for (int k = 0; k < nst && k < tc.count; ++k)
-                f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
-            for (int64_t i = 0; i + nst < tc.count; ++i) {
-                const int k = static_cast<int>(i % nst);
-                mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
-                fence_proxy_async();
-                f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
-            }
-        } else if (threadIdx.x == kThreads + 32) {  // ---------------- storer
+    if (threadIdx.x >= kThreads) {  // ---------------- storers
+        if ((threadIdx.x & 31) != 0) return;
+        // bulk groups are per thread, so one storer waiting for its own
+        // stores to drain never stalls the other's issue.  The buffer of tile
+        // j = i + r (r = 1 for odd nob, 2 for even) was last read by the
+        // stores of tile j - nob, one of this storer's own tiles: with
+        // P = (nob - r)/2 - 1 >= 0 of its later tiles allowed to be still
+        // reading, it is released BEFORE tile i is issued (issue blocks while
+        // the SM's TMA unit works through earlier stores); with nob = 2
+        // (P < 0, j - nob = i) after tile i has drained.
+        {
+            const int sidx = (threadIdx.x - kThreads) >> 5;
+            if (sidx == 0)
+                for (int k = 0; k < nst && k < tc.count; ++k)
+                    f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+            const int r = (nob & 1) ? 1 : 2, P = (nob - r) / 2 - 1;
             int lj = -1;
             DstList dl;
             const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
-            const int ahead = a.release_ahead;
-            for (int64_t i = 0; i < tc.count; ++i) {
+            for (int64_t i = sidx; i < tc.count; i += 2) {
                 const int b = static_cast<int>(i % nob);
                 mbar_wait(&conv[b], static_cast<uint32_t>((i / nob) & 1));
+                trace(a, 4, i);
+                if (i + nst < tc.count) {  // stage of tile i is free: refill it with tile i + nst
+                    const int k = static_cast<int>(i % nst);
+                    fence_proxy_async();
+                    trace(a, 0, i + nst);
+                    f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+                }
+                const int64_t j = i + r;
+                const bool rel = j >= nob && j < tc.count;
+                if (rel && P >= 0) {
+                    if (P == 0) bulk_wait_read<0>();
+                    else if (P == 1) bulk_wait_read<1>();
+                    else bulk_wait_read<2>();
+                    mbar_arrive(&ofree[static_cast<int>(j % nob)]);
+                    trace(a, 6, i);
+                }
                 // fan tile i out to every (run, slot) holding its frame
                 F2TTile tl;
                 tl.set(a, tc.tile(i), ROWS);
@@ -303,7 +340,8 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
                 }
                 const OUT *ob = obuf + b * a.ob_elems;
                 const bool whole_rows = tl.x0 == 0 && sw == a.Wp;
-                for (int d = 0; d < dl.nd; ++d) {
+                const int nd = (a.debug & 2) ? 0 : dl.nd;
+                for (int d = 0; d < nd; ++d) {
                     const int cd = dl.get(a, d);
                     OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
                                                      static_cast<int64_t>(cd & 31) * a.slot_bytes) +
@@ -312,29 +350,18 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
                         if (whole_rows) {
                             bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
                         } else {
-                            for (int r = 0; r < rows; ++r)
-                                bulk_s2g(o + c * plane + static_cast<int64_t>(r) * a.Wp, ob + (c * brows + r) * sw,
+                            for (int rr = 0; rr < rows; ++rr)
+                                bulk_s2g(o + c * plane + static_cast<int64_t>(rr) * a.Wp, ob + (c * brows + rr) * sw,
                                          sw * sizeof(OUT));
                         }
                     }
                 }
                 bulk_commit();
-                // the buffer of tile j = i + ahead (last read by the stores of
-                // tile j - nob) is free once at most nob - ahead groups are
-                // still reading shared memory
-                const int64_t j = i + ahead;
-                if (j >= nob && j < tc.count) {
-                    switch (nob - ahead) {
-                    case 0: bulk_wait_read<0>(); break;
-                    case 1: bulk_wait_read<1>(); break;
-                    case 2: bulk_wait_read<2>(); break;
-                    case 3: bulk_wait_read<3>(); break;
-                    case 4: bulk_wait_read<4>(); break;
-                    case 5: bulk_wait_read<5>(); break;
-                    case 6: bulk_wait_read<6>(); break;
-                    default: bulk_wait_read<7>(); break;
-                    }
+                trace(a, 5, i);
+                if (rel && P < 0) {
+                    bulk_wait_read<0>();
                     mbar_arrive(&ofree[static_cast<int>(j % nob)]);
+                    trace(a, 6, i);
                 }
             }
             bulk_wait_all();
@@ -344,18 +371,21 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
 
     // ------------------------------------------------------------ consumers
     const int cw = a.W >> 1, ch = a.H >> 1;
+    const int tid = threadIdx.x;
     for (int64_t i = 0; i < tc.count; ++i) {
         const int k = static_cast<int>(i % nst);
         const int b = static_cast<int>(i % nob);
         uint8_t *st = stages + k * a.stage_bytes;
         OUT *ob = obuf + b * a.ob_elems;
         mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
+        if (threadIdx.x == 0) trace(a, 1, i);
         const F2THdr tl = hdr[k];
         const int sw = tl.x1 - tl.x0;
-        const int x = tl.x0 + kPx * threadIdx.x;
+        const int x = tl.x0 + kPx * tid;
         const bool fast = x + kPx <= a.W;
         if (i >= nob) mbar_wait(&ofree[b], static_cast<uint32_t>((i / nob - 1) & 1));
-        if (x < tl.x1) {
+        if (threadIdx.x == 0) trace(a, 2, i);
+        if (x < tl.x1 && !(a.debug & 1)) {
             for (int u = 0; u < tl.nu; ++u) {
 #pragma unroll
                 for (int r = 0; r < ROWS; ++r) {
@@ -433,8 +463,8 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
         __syncwarp();
+        if (threadIdx.x == 0) trace(a, 3, i);
         if ((threadIdx.x & 31) == 0) {
-            mbar_arrive(&empty[k]);
             mbar_arrive(&conv[b]);
         }
     }
@@ -621,9 +651,9 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     a.nob = env_int("NNVISR_F2T_NOB", 0);
     a.stages = env_int("NNVISR_F2T_STAGES", 0);
     if (!a.stages) a.stages = 2;
-    a.stages = std::max(1, std::min(kMaxStages, a.stages));
     if (!a.nob) a.nob = 3;
-    a.nob = std::max(2, std::min(kMaxOutBufs, a.nob));
+    a.stages = std::max(1, std::min(kMaxStages, a.stages));
+    a.nob = std::max(2, std::min(5, a.nob));
     // never exceed the 227 KB a CTA may use: shed output buffers, then band rows
     constexpr int kMaxSmem = 227 * 1024;
     while (kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band) > kMaxSmem) {
@@ -637,16 +667,40 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     }
     a.tiles = a.tiles / bands * ((a.rowunits + a.band - 1) / a.band);
     const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band);
-    a.release_ahead = std::max(1, std::min(a.nob, env_int("NNVISR_F2T_AHEAD", 1)));
+    a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
     auto kernel = f2t_tma<FAMILY, IN, OUT>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads + 64, smem);
+    const int block = kThreads + 64;  // 8 consumer warps, 2 storer warps
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
-    kernel<<<grid, kThreads + 64, smem, s>>>(a);
+    static uint64_t *trace_buf = nullptr;
+    constexpr size_t kTraceBytes = 2 * kTraceEvents * kTraceTiles * sizeof(uint64_t);
+    if (a.debug & 8) {
+        if (!trace_buf) cudaMalloc(&trace_buf, kTraceBytes);
+        cudaMemsetAsync(trace_buf, 0, kTraceBytes, s);
+        a.trace = trace_buf;
+    }
+    kernel<<<grid, block, smem, s>>>(a);
+    if ((a.debug & 8) && std::getenv("NNVISR_F2T_TRACE")) {  // dump the launch's timeline (experiments only)
+        std::vector<uint64_t> h(kTraceBytes / sizeof(uint64_t));
+        cudaMemcpyAsync(h.data(), trace_buf, kTraceBytes, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (FILE *fp = std::fopen(std::getenv("NNVISR_F2T_TRACE"), "w")) {
+            std::fprintf(fp, "# stages %d nob %d band %d stage_bytes %d tiles %lld grid %d\n", a.stages, a.nob, a.band, a.stage_bytes, (long long)a.tiles, grid);
+            for (int c = 0; c < 2; ++c)
+                for (int i = 0; i < kTraceTiles; ++i) {
+                    std::fprintf(fp, "%d %d", c, i);
+                    for (int ev = 0; ev < kTraceEvents; ++ev)
+                        std::fprintf(fp, " %llu", (unsigned long long)h[(c * kTraceEvents + ev) * kTraceTiles + i]);
+                    std::fprintf(fp, "\n");
+                }
+            std::fclose(fp);
+        }
+    }
     return cudaGetLastError();
 }
 
