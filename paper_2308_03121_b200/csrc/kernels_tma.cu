@@ -79,6 +79,21 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+// wait until at most n (>= 0) of this thread's bulk groups are still reading
+// shared memory (n > 7: 7, i.e. waits longer than needed)
+__device__ __forceinline__ void bulk_wait_read_le(int n)
+{
+    switch (n) {
+    case 0: bulk_wait_read<0>(); break;
+    case 1: bulk_wait_read<1>(); break;
+    case 2: bulk_wait_read<2>(); break;
+    case 3: bulk_wait_read<3>(); break;
+    case 4: bulk_wait_read<4>(); break;
+    case 5: bulk_wait_read<5>(); break;
+    case 6: bulk_wait_read<6>(); break;
+    default: bulk_wait_read<7>(); break;
+    }
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -264,15 +279,16 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
 // (acquire) instead of decoding the tile index themselves.
 // Output buffer layout: [channel][B*ROWS rows][sw]: with a single segment a
 // channel's band rows are contiguous in the tensor too, one bulk store each.
-template <int FAMILY, typename IN, typename OUT>
-__global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
+template <int FAMILY, typename IN, typename OUT, bool LOADER>
+__global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2) f2t_tma(const F2TArgs a)
 {
     using S = F2TStage<FAMILY, IN>;
     using V8 = typename Pack<IN>::V8;
     using V4 = typename Pack<IN>::V4;
     constexpr int ROWS = S::ROWS;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *ofree = full + 2 * kMaxStages, *conv = ofree + kMaxOutBufs;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages, *ofree = empty + kMaxStages,
+             *conv = ofree + kMaxOutBufs;
     F2THdr *hdr = reinterpret_cast<F2THdr *>(conv + kMaxOutBufs);
     uint8_t *stages = smem + kBarBytes;
     const int nst = a.stages, nob = a.nob, brows = a.band * ROWS;
@@ -283,7 +299,10 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
     tc.init(a.tiles);
     if (tc.count == 0) return;
     if (threadIdx.x == 0) {
-        for (int k = 0; k < nst; ++k) mbar_init(&full[k], 1);
+        for (int k = 0; k < nst; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kConsumerWarps);
+        }
         for (int b = 0; b < nob; ++b) {
             mbar_init(&ofree[b], 1);
             mbar_init(&conv[b], kConsumerWarps);
@@ -292,86 +311,112 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
     }
     __syncthreads();  // the last CTA-wide barrier: roles split below
 
-    if (threadIdx.x >= kThreads) {  // ---------------- storers
+    if (threadIdx.x >= kThreads) {
         if ((threadIdx.x & 31) != 0) return;
-        // bulk groups are per thread, so one storer waiting for its own
-        // stores to drain never stalls the other's issue.  The buffer of tile
-        // j = i + r (r = 1 for odd nob, 2 for even) was last read by the
-        // stores of tile j - nob, one of this storer's own tiles: with
-        // P = (nob - r)/2 - 1 >= 0 of its later tiles allowed to be still
-        // reading, it is released BEFORE tile i is issued (issue blocks while
-        // the SM's TMA unit works through earlier stores); with nob = 2
-        // (P < 0, j - nob = i) after tile i has drained.
-        {
-            const int sidx = (threadIdx.x - kThreads) >> 5;
-            if (sidx == 0)
-                for (int k = 0; k < nst && k < tc.count; ++k)
-                    f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
-            const int r = (nob & 1) ? 1 : 2, P = (nob - r) / 2 - 1;
-            int lj = -1;
-            DstList dl;
-            const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
-            for (int64_t i = sidx; i < tc.count; i += 2) {
-                const int b = static_cast<int>(i % nob);
-                mbar_wait(&conv[b], static_cast<uint32_t>((i / nob) & 1));
-                trace(a, 4, i);
-                if (i + nst < tc.count) {  // stage of tile i is free: refill it with tile i + nst
-                    const int k = static_cast<int>(i % nst);
-                    fence_proxy_async();
-                    trace(a, 0, i + nst);
-                    f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
-                }
-                const int64_t j = i + r;
-                const bool rel = j >= nob && j < tc.count;
-                if (rel && P >= 0) {
-                    if (P == 0) bulk_wait_read<0>();
-                    else if (P == 1) bulk_wait_read<1>();
-                    else bulk_wait_read<2>();
-                    mbar_arrive(&ofree[static_cast<int>(j % nob)]);
-                    trace(a, 6, i);
-                }
-                // fan tile i out to every (run, slot) holding its frame
-                F2TTile tl;
-                tl.set(a, tc.tile(i), ROWS);
-                const int sw = tl.x1 - tl.x0, rows = tl.nu * ROWS;
-                if (tl.job != lj) {
-                    lj = tl.job;
-                    dl.load(a, tl.job);
-                }
-                const OUT *ob = obuf + b * a.ob_elems;
-                const bool whole_rows = tl.x0 == 0 && sw == a.Wp;
-                const int nd = (a.debug & 2) ? 0 : dl.nd;
-                for (int d = 0; d < nd; ++d) {
-                    const int cd = dl.get(a, d);
-                    OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
-                                                     static_cast<int64_t>(cd & 31) * a.slot_bytes) +
-                             static_cast<int64_t>(tl.u0 * ROWS) * a.Wp + tl.x0;
-                    for (int c = 0; c < 3; ++c) {
-                        if (whole_rows) {
-                            bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
-                        } else {
-                            for (int rr = 0; rr < rows; ++rr)
-                                bulk_s2g(o + c * plane + static_cast<int64_t>(rr) * a.Wp, ob + (c * brows + rr) * sw,
-                                         sw * sizeof(OUT));
-                        }
+        if (LOADER && threadIdx.x == kThreads + 64) {  // ---------------- loader (LOADER variant)
+            for (int k = 0; k < nst && k < tc.count; ++k)
+                f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+            for (int64_t i = 0; i + nst < tc.count; ++i) {
+                const int k = static_cast<int>(i % nst);
+                mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
+                fence_proxy_async();
+                trace(a, 0, i + nst);
+                f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+            }
+            return;
+        }
+        // ---------------- storers
+        // NS = a.nstorers storers (lane 0 of warps 8, 9); storer s fans out
+        // tiles s, s + NS, ...  Bulk groups are per thread, so one storer
+        // waiting for its own stores to drain never stalls another's issue.
+        // Every destination's stores form one bulk group; eb[m] = groups
+        // committed through this storer's tile i - m*NS.  The buffer of tile
+        // j = i + r (r >= 1, (nob - r) % NS == 0) was last read by the
+        // stores of tile j - nob, this storer's own tile `back` = (nob-r)/NS
+        // tiles earlier.  back == 0: released once tile i has drained.
+        // Otherwise released either BEFORE tile i is issued (release_first:
+        // issue blocks while the SM's TMA unit works through earlier stores,
+        // so the consumers get the buffer early) or right after (a deeper
+        // store queue), once at most the groups committed since tile j - nob
+        // are still reading.  a.throttle > 0 caps this storer's groups still
+        // reading shared memory.
+        const int NS = a.nstorers;
+        const int sidx = (threadIdx.x - kThreads) >> 5;
+        if (sidx >= NS) return;
+        if (!LOADER && sidx == 0)
+            for (int k = 0; k < nst && k < tc.count; ++k)
+                f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+        const int r = NS == 1 ? 1 : ((nob & 1) ? 1 : 2), back = (nob - r) / NS;
+        int lj = -1;
+        DstList dl;
+        const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
+        int ng = 0;                 // groups committed by this storer
+        int eb1 = 0, eb2 = 0, eb3 = 0, eb4 = 0;  // back <= 4 (nob <= 5)
+        for (int64_t i = sidx; i < tc.count; i += NS) {
+            const int b = static_cast<int>(i % nob);
+            mbar_wait(&conv[b], static_cast<uint32_t>((i / nob) & 1));
+            trace(a, 4, i);
+            if (!LOADER && i + nst < tc.count) {  // stage of tile i is free: refill it with tile i + nst
+                const int k = static_cast<int>(i % nst);
+                fence_proxy_async();
+                trace(a, 0, i + nst);
+                f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+            }
+            const int64_t j = i + r;
+            const bool rel = j >= nob && j < tc.count;
+            const int eb = back == 1 ? eb1 : back == 2 ? eb2 : back == 3 ? eb3 : eb4;
+            if (rel && back > 0 && a.release_first) {
+                bulk_wait_read_le(ng - eb);
+                mbar_arrive(&ofree[static_cast<int>(j % nob)]);
+                trace(a, 6, i);
+            }
+            // fan tile i out to every (run, slot) holding its frame
+            F2TTile tl;
+            tl.set(a, tc.tile(i), ROWS);
+            const int sw = tl.x1 - tl.x0, rows = tl.nu * ROWS;
+            if (tl.job != lj) {
+                lj = tl.job;
+                dl.load(a, tl.job);
+            }
+            const OUT *ob = obuf + b * a.ob_elems;
+            const bool whole_rows = tl.x0 == 0 && sw == a.Wp;
+            const int nd = (a.debug & 2) ? 0 : dl.nd;
+            for (int d = 0; d < nd; ++d) {
+                const int cd = dl.get(a, d);
+                OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
+                                                 static_cast<int64_t>(cd & 31) * a.slot_bytes) +
+                         static_cast<int64_t>(tl.u0 * ROWS) * a.Wp + tl.x0;
+                if (a.throttle > 0) bulk_wait_read_le(a.throttle - 1);
+                for (int c = 0; c < 3; ++c) {
+                    if (whole_rows) {
+                        bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
+                    } else {
+                        for (int rr = 0; rr < rows; ++rr)
+                            bulk_s2g(o + c * plane + static_cast<int64_t>(rr) * a.Wp, ob + (c * brows + rr) * sw,
+                                     sw * sizeof(OUT));
                     }
                 }
                 bulk_commit();
-                trace(a, 5, i);
-                if (rel && P < 0) {
-                    bulk_wait_read<0>();
-                    mbar_arrive(&ofree[static_cast<int>(j % nob)]);
-                    trace(a, 6, i);
-                }
+                ++ng;
             }
-            bulk_wait_all();
+            trace(a, 5, i);
+            if (rel && (back == 0 || !a.release_first)) {
+                bulk_wait_read_le(back == 0 ? 0 : ng - eb);
+                mbar_arrive(&ofree[static_cast<int>(j % nob)]);
+                trace(a, 6, i);
+            }
+            eb4 = eb3;
+            eb3 = eb2;
+            eb2 = eb1;
+            eb1 = ng;
         }
+        bulk_wait_all();
         return;
     }
 
     // ------------------------------------------------------------ consumers
     const int cw = a.W >> 1, ch = a.H >> 1;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x % kThreads;
     for (int64_t i = 0; i < tc.count; ++i) {
         const int k = static_cast<int>(i % nst);
         const int b = static_cast<int>(i % nob);
@@ -465,6 +510,7 @@ __global__ void __launch_bounds__(kThreads + 64, 2) f2t_tma(const F2TArgs a)
         __syncwarp();
         if (threadIdx.x == 0) trace(a, 3, i);
         if ((threadIdx.x & 31) == 0) {
+            if (LOADER) mbar_arrive(&empty[k]);
             mbar_arrive(&conv[b]);
         }
     }
@@ -648,10 +694,18 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     a.tiles = a.tiles / ((int64_t)a.rowunits * a.nseg) * bands * a.nseg;  // jobs * bands * nseg
     a.stage_bytes = stage_bytes(a.band);
     a.ob_elems = ob_bytes(a.band) / (int)sizeof(OUT);
-    a.nob = env_int("NNVISR_F2T_NOB", 0);
-    a.stages = env_int("NNVISR_F2T_STAGES", 0);
-    if (!a.stages) a.stages = 2;
-    if (!a.nob) a.nob = 3;
+    // Two pipeline shapes, from the B200 sweeps (profiles/r01/f2t_sweep.txt):
+    //  * two CTAs per SM when 2 stages + 2 output buffers fit in half the
+    //    SM's shared memory (4K 4:2:0 split into 2 segments, 720p): the two
+    //    storers also issue the loads (10 warps: 96 registers) and release
+    //    the next output buffer before issuing a tile;
+    //  * else one CTA per SM (1080p whole rows, 4K 4:4:4 fp32): a dedicated
+    //    loader warp, 3 output buffers, release after issuing (a deeper
+    //    store queue).
+    constexpr int kSmSmem = 228 * 1024, kCtaReserve = 1024;
+    const bool two = 2 * (kBarBytes + 2 * a.stage_bytes + 2 * ob_bytes(a.band) + kCtaReserve) <= kSmSmem;
+    a.stages = env_int("NNVISR_F2T_STAGES", 2);
+    a.nob = env_int("NNVISR_F2T_NOB", two ? 2 : 3);
     a.stages = std::max(1, std::min(kMaxStages, a.stages));
     a.nob = std::max(2, std::min(5, a.nob));
     // never exceed the 227 KB a CTA may use: shed output buffers, then band rows
@@ -667,12 +721,17 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     }
     a.tiles = a.tiles / bands * ((a.rowunits + a.band - 1) / a.band);
     const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band);
+    const bool fits2 = 2 * (smem + kCtaReserve) <= kSmSmem;
+    a.throttle = env_int("NNVISR_F2T_THROTTLE", 0);
+    a.nstorers = std::max(1, std::min(2, env_int("NNVISR_F2T_STORERS", 2)));
+    a.release_first = env_int("NNVISR_F2T_RELFIRST", fits2 ? 1 : 0);
     a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
-    auto kernel = f2t_tma<FAMILY, IN, OUT>;
+    int loader = env_int("NNVISR_F2T_LOADER", fits2 ? 0 : 1);
+    auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true> : f2t_tma<FAMILY, IN, OUT, false>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    const int block = kThreads + 64;  // 8 consumer warps, 2 storer warps
+    const int block = kThreads + (loader ? 96 : 64);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(std::max<int64_t>(
