@@ -100,6 +100,7 @@ struct T2FArgs {
     int32_t vec_in;           // tensor rows allow 16-byte loads
     int32_t vec_out;          // output planes allow vector stores
     int32_t tma_ok, rowunits, nseg, stages, stage_bytes, segw;
+    int32_t cthreads;  // TMA path: consumer threads per CTA (segw / 8 rounded up to warps)
     int64_t tiles;
     T2FColour col;
     int32_t left;  // 4:2:0 chroma siting: 0 centre, 1 LEFT (generic kernels only)

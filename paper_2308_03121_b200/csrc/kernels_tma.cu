@@ -53,12 +53,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         "{\n\t"
         ".reg .pred P1;\n\t"
         "LAB_WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@P1 bra DONE;\n\t"
         "bra LAB_WAIT;\n\t"
         "DONE:\n\t"
         "}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep until the phase completes, fewer polls
         : "memory");
 }
 // global -> shared bulk copy (TMA engine; SASS UBLKCP), completes on `bar`.
@@ -517,44 +517,54 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
 }
 
 // ------------------------------------------------------------------ t2f
-// Stage layout (values of TIN): [ROWS][3 channels][seg_w].
-template <int FAMILY, typename TIN> struct T2FStage {
-    static constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
-    static constexpr int BYTES = ROWS * 3 * kSegW * sizeof(TIN);
-    __device__ static TIN *row(uint8_t *st, int r, int c) { return reinterpret_cast<TIN *>(st) + (r * 3 + c) * kSegW; }
+// Stage layout (values of TIN): [ROWS][3 channels][segw], segw = the launch's
+// (equal) segment width.  The producer writes each stage's T2FHdr before its
+// expect_tx arrive, so the consumers read the tile's output frame, rows and
+// columns after their full wait instead of decoding the tile index.
+struct T2FHdr {
+    int job, y0, x0, x1;
 };
 
 template <int FAMILY, typename TIN>
-__device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *st, uint64_t *bar)
+__device__ __forceinline__ TIN *t2f_row_ptr(uint8_t *st, int segw, int r, int c)
 {
-    using S = T2FStage<FAMILY, TIN>;
+    return reinterpret_cast<TIN *>(st) + (r * 3 + c) * segw;
+}
+
+template <int FAMILY, typename TIN>
+__device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *st, uint64_t *bar, T2FHdr *hdr)
+{
+    constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
     int job, ru, x0;
     decode_tile(t, a.rowunits, a.nseg, a.segw, job, ru, x0);
     const int x1 = min(x0 + a.segw, a.Wo);
     int tup, o;
     t2f_job(a, job, tup, o);
+    *hdr = T2FHdr{job, ru * ROWS, x0, x1};
     const int64_t plane = a.th * a.tw;
     const TIN *src = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
-                     static_cast<int64_t>(3 * o) * plane + static_cast<int64_t>(ru * S::ROWS) * a.tw + x0;
+                     static_cast<int64_t>(3 * o) * plane + static_cast<int64_t>(ru * ROWS) * a.tw + x0;
     const uint32_t bytes = (x1 - x0) * sizeof(TIN);
-    mbar_arrive_expect_tx(bar, S::ROWS * 3 * bytes);
+    mbar_arrive_expect_tx(bar, ROWS * 3 * bytes);
 #pragma unroll
-    for (int r = 0; r < S::ROWS; ++r)
+    for (int r = 0; r < ROWS; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) bulk_g2s(S::row(st, r, c), src + c * plane + r * a.tw, bytes, bar);
+        for (int c = 0; c < 3; ++c)
+            bulk_g2s(t2f_row_ptr<FAMILY, TIN>(st, a.segw, r, c), src + c * plane + r * a.tw, bytes, bar);
 }
 
-// Warp-specialised like f2t_tma: warps 0..7 convert and store with st.global,
-// warp 8 lane 0 keeps the stages full.
+// Warp-specialised like f2t_tma: a.cthreads consumer threads (segw / 8,
+// rounded up to whole warps) convert and store with st.global; lane 0 of the
+// last warp keeps the stages full.
 template <int FAMILY, typename OS, typename TIN, typename AR>
 __global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tma(const T2FArgs a)
 {
-    using S = T2FStage<FAMILY, TIN>;
-    constexpr int ROWS = S::ROWS;
+    constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages;
+    T2FHdr *hdr = reinterpret_cast<T2FHdr *>(empty + kMaxStages);
     uint8_t *stages = smem + kBarBytes;
-    const int nst = a.stages;
+    const int nst = a.stages, nct = a.cthreads;
 
     TileCursor tc;
     tc.init(a.tiles);
@@ -562,21 +572,21 @@ __global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tm
     if (threadIdx.x == 0) {
         for (int k = 0; k < nst; ++k) {
             mbar_init(&full[k], 1);
-            mbar_init(&empty[k], kConsumerWarps);
+            mbar_init(&empty[k], nct / 32);
         }
         fence_barrier_init();
     }
     __syncthreads();
 
-    if (threadIdx.x >= kThreads) {  // ---------------- producer warp
-        if (threadIdx.x != kThreads) return;
+    if (threadIdx.x >= nct) {  // ---------------- producer warp
+        if (threadIdx.x != nct) return;
         for (int k = 0; k < nst && k < tc.count; ++k)
-            t2f_issue<FAMILY, TIN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k]);
+            t2f_issue<FAMILY, TIN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
         for (int64_t i = 0; i + nst < tc.count; ++i) {
             const int k = static_cast<int>(i % nst);
             mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
             fence_proxy_async();
-            t2f_issue<FAMILY, TIN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k]);
+            t2f_issue<FAMILY, TIN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
         }
         return;
     }
@@ -585,32 +595,28 @@ __global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tm
     const T2FConst<AR> c(a.col);
     int cj = -1;
     DevFrame f;
+    const int xo = kPx * threadIdx.x;  // column within the segment
     for (int64_t i = 0; i < tc.count; ++i) {
         const int k = static_cast<int>(i % nst);
-        const int64_t t = tc.tile(i);
-        int job, ru, x0;
-        decode_tile(t, a.rowunits, a.nseg, a.segw, job, ru, x0);
-        const int x1 = min(x0 + a.segw, a.Wo);
-        const int y0 = ru * ROWS;
-        const int xo = kPx * threadIdx.x;  // column within the segment
-        if (job != cj) {
-            cj = job;
-            f = load_frame(a.out + job);
-        }
         uint8_t *st = stages + k * a.stage_bytes;
         mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
-        if (x0 + xo < x1) {
-            const int x = x0 + xo;
+        const T2FHdr h = hdr[k];
+        if (h.job != cj) {
+            cj = h.job;
+            f = load_frame(a.out + cj);
+        }
+        if (h.x0 + xo < h.x1) {
+            const int x = h.x0 + xo;
             AR sb[4], sr[4];
 #pragma unroll
             for (int r = 0; r < ROWS; ++r) {
                 float R[kPx], G[kPx], B[kPx];
-                tload8(S::row(st, r, 0) + xo, R);
-                tload8(S::row(st, r, 1) + xo, G);
-                tload8(S::row(st, r, 2) + xo, B);
-                t2f_row<FAMILY, OS, AR>(c, a.col, f, x, y0 + r, r, R, G, B, kPx, a.vec_out, sb, sr);
+                tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, r, 0) + xo, R);
+                tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, r, 1) + xo, G);
+                tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, r, 2) + xo, B);
+                t2f_row<FAMILY, OS, AR>(c, a.col, f, x, h.y0 + r, r, R, G, B, kPx, a.vec_out, sb, sr);
             }
-            if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, y0, sb, sr, kPx, a.vec_out);
+            if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, h.y0, sb, sr, kPx, a.vec_out);
         }
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[k]);
@@ -639,25 +645,29 @@ int env_int(const char *name, int dflt)
 // output staging buffers).  Stages: `default_stages` (tools/sweep_t2f.sh on
 // B200, profiles/r01/t2f_sweep.txt), else as many as fit in `budget`.
 template <typename K, typename A>
-cudaError_t launch_tma(K kernel, A a, int stage_bytes, int extra, int budget, int default_stages, cudaStream_t s)
+cudaError_t launch_tma(K kernel, A a, int rows, int elem, int budget, int default_stages, cudaStream_t s)
 {
     if (a.tiles <= 0) return cudaSuccess;
-    a.stage_bytes = (stage_bytes + 127) / 128 * 128;
-    // equal segments of a multiple of 32 columns (<= 2048): no thin tail tile
+    // equal segments of a multiple of 32 columns (<= 2048): no thin tail tile;
+    // a stage holds one tile's rows x 3 channels x segw values, and the
+    // consumer threads are the tile's 8-column groups (whole warps)
     a.segw = std::min(kSegW, ((a.Wo + a.nseg - 1) / a.nseg + 31) / 32 * 32);
+    a.cthreads = std::min(kThreads, (a.segw / kPx + 31) / 32 * 32);
+    a.stage_bytes = (rows * 3 * a.segw * elem + 127) / 128 * 128;
     budget = env_int("NNVISR_T2F_SMEM_KB", budget / 1024) * 1024;
     a.stages = env_int("NNVISR_T2F_STAGES", default_stages);
-    if (a.stages <= 0) a.stages = (budget - extra) / a.stage_bytes;
+    if (a.stages <= 0) a.stages = budget / a.stage_bytes;
     a.stages = std::max(2, std::min(kMaxStages, a.stages));
-    const int smem = kBarBytes + a.stages * a.stage_bytes + extra;
+    const int smem = kBarBytes + a.stages * a.stage_bytes;
+    const int block = a.cthreads + 32;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads + 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
-    kernel<<<grid, kThreads + 32, smem, s>>>(a);
+    kernel<<<grid, block, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -777,17 +787,20 @@ cudaError_t f2t_tma_dispatch(int bits, int dtype, const F2TArgs &a, cudaStream_t
 template <int FAMILY>
 cudaError_t t2f_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t s)
 {
-    constexpr int BH = T2FStage<FAMILY, __half>::BYTES, BF = T2FStage<FAMILY, float>::BYTES;
+    // input stages: NNVISR_T2F_STAGES, else as many as fit in 50 KB (two at
+    // 1080p/4K, three at 720p; tools/sweep.sh t2f on B200, profiles/r01/t2f_sweep2.txt)
+    constexpr int R = FAMILY == kYUV420 ? 2 : 1, kBudget = 50 * 1024;
+    const int st = env_int("NNVISR_T2F_STAGES", 0);
     if (bits == 8) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, BH, 0, 72 * 1024, 2, s);
-        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, BF, 0, 72 * 1024, 2, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, R, 2, kBudget, st, s);
+        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, R, 4, kBudget, st, s);
     }
     if (bits == 10) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, BH, 0, 72 * 1024, 2, s);
-        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, BF, 0, 72 * 1024, 2, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, R, 2, kBudget, st, s);
+        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, R, 4, kBudget, st, s);
     }
-    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, BH, 0, 72 * 1024, 3, s);
-    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, BF, 0, 72 * 1024, 3, s);
+    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, R, 2, kBudget, st, s);
+    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, R, 4, kBudget, st, s);
 }
 
 }  // namespace
