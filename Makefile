@@ -1,7 +1,7 @@
 # Builds the product library (sm_100a) and the CPU oracle (test infrastructure).
 NVCC    ?= nvcc
 ARCH    ?= -gencode arch=compute_100a,code=sm_100a
-NVFLAGS ?= -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC,-Wall -Iinclude -Xptxas -v
+NVFLAGS ?= -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC,-Wall -Iinclude -Xptxas -v $(EXTRA)
 PKG      = paper_2308_03121_b200
 SRC      = $(PKG)/csrc/nnvisr.cpp $(PKG)/csrc/kernels.cu $(PKG)/csrc/kernels_tma.cu $(PKG)/csrc/kernels_yuv.cu $(PKG)/csrc/scene.cu
 HDR      = include/nnvisr.h $(PKG)/csrc/internal.h $(PKG)/csrc/common.cuh

@@ -119,10 +119,15 @@ __device__ __forceinline__ void f2t_colour(const F2TColour &c, int ys, int us, i
     }
 }
 
-// fp16 tensors near zero: a difference of O(1) terms rounded in fp32 can be
-// off by more than one fp16 ULP once |v| < 2^-9 (the ULP there is < 2^-19).
-// Those (rare) pixels are recomputed in fp64 and rounded once to fp16; the
-// returned float is that fp16 value exactly, so the RNE store reproduces it.
+// fp16 tensors near zero: R', G', B' are sums of O(1) terms whose fp32
+// evaluation errs by up to ~2^-22.3 (one rounding of Y' <= 1.2 and of Pb, Pr,
+// the rounded matrix constants, at most two FMA roundings).  Against the
+// oracle's single double->fp16 rounding that stays within 1 fp16 ULP while
+// the ULP exceeds the error, i.e. for |v| >= 2^-11 (ULP 2^-21).  Values below
+// 2^-9 (a 4x margin; also measured faster than 2^-11 at 1080p on B200,
+// tools/ab.sh) are recomputed in fp64 and rounded once to fp16; the returned
+// float is that fp16 value exactly, so the RNE store reproduces it.
+// (tests/test_gpu_fp16_exhaustive.py: every 8-bit triple, all matrices.)
 __device__ __forceinline__ float3 f2t_colour_precise(const F2TColour &c, int ys, int us, int vs)
 {
     const double Y = static_cast<double>(ys - c.y_off) * c.y_scale_d;
@@ -159,6 +164,18 @@ __device__ __forceinline__ void hup(const int (&c)[6], int (&h)[kPx])
         h[2 * m] = 3 * c[m + 1] + c[m];
         h[2 * m + 1] = 3 * c[m + 1] + c[m + 2];
     }
+}
+
+// hup of the staged chroma row C around an item's 8 columns (i0 = x / 2):
+// samples i0-1 .. i0+4, the outer two clamped to [0, cw).
+template <typename IN, typename V4>
+__device__ __forceinline__ void hup_row(const IN *C, int i0, int cw, int (&h)[kPx])
+{
+    int c[6];
+    unpack4(*reinterpret_cast<const V4 *>(C + i0), &c[1]);
+    c[0] = C[max(i0 - 1, 0)];
+    c[5] = C[min(i0 + 4, cw - 1)];
+    hup(c, h);
 }
 
 // LEFT (MPEG-2) siting: chroma i is co-sited with luma column 2i, so even

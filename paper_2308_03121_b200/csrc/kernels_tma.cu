@@ -98,14 +98,21 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Experiment timeline (NNVISR_F2T_DEBUG & 8): SM clock of event `ev` of tile
-// i, CTAs 0 and 1, first 128 tiles (see f2t_tma_launch).
+// Experiment timeline (build with -DNNVISR_F2T_TRACE, run with
+// NNVISR_F2T_DEBUG=8): SM clock of event `ev` of tile i, CTAs 0 and 1, first
+// 128 tiles (see f2t_tma_launch).  Compiled out otherwise.
 constexpr int kTraceTiles = 128, kTraceEvents = 8;
-__device__ __forceinline__ void trace(const F2TArgs &a, int ev, int64_t i)
-{
-    if ((a.debug & 8) && blockIdx.x < 2 && i < kTraceTiles)
-        a.trace[(blockIdx.x * kTraceEvents + ev) * kTraceTiles + i] = clock64();
-}
+#ifdef NNVISR_F2T_TRACE
+#define NNVISR_TRACE(cond, ev, i)                                                                 \
+    do {                                                                                          \
+        if ((cond) && (a.debug & 8) && blockIdx.x < 2 && (i) < kTraceTiles)                       \
+            a.trace[(blockIdx.x * kTraceEvents + (ev)) * kTraceTiles + (i)] = clock64();          \
+    } while (0)
+#else
+#define NNVISR_TRACE(cond, ev, i) \
+    do {                          \
+    } while (0)
+#endif
 
 constexpr int kSegW = kThreads * kPx;         // columns per tile segment (2048)
 constexpr int kConsumerWarps = kThreads / 32;  // converting warps; one more warp produces
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                 const int k = static_cast<int>(i % nst);
                 mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
                 fence_proxy_async();
-                trace(a, 0, i + nst);
+                NNVISR_TRACE(true, 0, i + nst);
                 f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
             }
             return;
@@ -355,11 +362,11 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
         for (int64_t i = sidx; i < tc.count; i += NS) {
             const int b = static_cast<int>(i % nob);
             mbar_wait(&conv[b], static_cast<uint32_t>((i / nob) & 1));
-            trace(a, 4, i);
+            NNVISR_TRACE(true, 4, i);
             if (!LOADER && i + nst < tc.count) {  // stage of tile i is free: refill it with tile i + nst
                 const int k = static_cast<int>(i % nst);
                 fence_proxy_async();
-                trace(a, 0, i + nst);
+                NNVISR_TRACE(true, 0, i + nst);
                 f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
             }
             const int64_t j = i + r;
@@ -368,7 +375,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
             if (rel && back > 0 && a.release_first) {
                 bulk_wait_read_le(ng - eb);
                 mbar_arrive(&ofree[static_cast<int>(j % nob)]);
-                trace(a, 6, i);
+                NNVISR_TRACE(true, 6, i);
             }
             // fan tile i out to every (run, slot) holding its frame
             F2TTile tl;
@@ -399,11 +406,11 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                 bulk_commit();
                 ++ng;
             }
-            trace(a, 5, i);
+            NNVISR_TRACE(true, 5, i);
             if (rel && (back == 0 || !a.release_first)) {
                 bulk_wait_read_le(back == 0 ? 0 : ng - eb);
                 mbar_arrive(&ofree[static_cast<int>(j % nob)]);
-                trace(a, 6, i);
+                NNVISR_TRACE(true, 6, i);
             }
             eb4 = eb3;
             eb3 = eb2;
@@ -416,65 +423,79 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
 
     // ------------------------------------------------------------ consumers
     const int cw = a.W >> 1, ch = a.H >> 1;
-    const int tid = threadIdx.x % kThreads;
+    const int tid = threadIdx.x;
+    int k = 0, b = 0;            // stage and output buffer of tile i
+    uint32_t fph = 0, bround = 0;  // full[k] wait parity; (i / nob) & 1
     for (int64_t i = 0; i < tc.count; ++i) {
-        const int k = static_cast<int>(i % nst);
-        const int b = static_cast<int>(i % nob);
         uint8_t *st = stages + k * a.stage_bytes;
         OUT *ob = obuf + b * a.ob_elems;
-        mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
-        if (threadIdx.x == 0) trace(a, 1, i);
+        mbar_wait(&full[k], fph);
+        NNVISR_TRACE(threadIdx.x == 0, 1, i);
         const F2THdr tl = hdr[k];
         const int sw = tl.x1 - tl.x0;
         const int x = tl.x0 + kPx * tid;
         const bool fast = x + kPx <= a.W;
-        if (i >= nob) mbar_wait(&ofree[b], static_cast<uint32_t>((i / nob - 1) & 1));
-        if (threadIdx.x == 0) trace(a, 2, i);
+        if (i >= nob) mbar_wait(&ofree[b], bround ^ 1u);
+        NNVISR_TRACE(threadIdx.x == 0, 2, i);
         if (x < tl.x1 && !(a.debug & 1)) {
             for (int u = 0; u < tl.nu; ++u) {
+                const int y0 = (tl.u0 + u) * ROWS;
+                OUT *orow = ob + (u * ROWS) * sw + (x - tl.x0);
+                if constexpr (FAMILY == kYUV420) {
+                    if (fast && y0 + 1 < a.H) {
+                        // both luma rows of the pair inside the frame: rows
+                        // 2j and 2j+1 share the near chroma row j, whose
+                        // horizontal pass is done once (reading A5: row 2j
+                        // adds 3*near + far row j-1, row 2j+1 far row j+1)
+                        const int j = y0 >> 1, i0 = x >> 1;
+                        int hn[2][kPx];
+#pragma unroll
+                        for (int p = 0; p < 2; ++p)
+                            hup_row<IN, V4>(sg.chroma(st, p, j - tl.cy0) - tl.cw0, i0, cw, hn[p]);
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            const int jf = r ? min(j + 1, ch - 1) : max(j - 1, 0);
+                            int ys[kPx], us[kPx], vs[kPx];
+                            unpack8(*reinterpret_cast<const V8 *>(sg.luma(st, y0 + r - tl.ly0) - tl.lw0 + x), ys);
+#pragma unroll
+                            for (int p = 0; p < 2; ++p) {
+                                int hf[kPx];
+                                hup_row<IN, V4>(sg.chroma(st, p, jf - tl.cy0) - tl.cw0, i0, cw, hf);
+#pragma unroll
+                                for (int kk = 0; kk < kPx; ++kk) {
+                                    const int s2 = 3 * hn[p][kk] + hf[kk];
+                                    if (p == 0) us[kk] = s2; else vs[kk] = s2;
+                                }
+                            }
+#pragma unroll
+                            for (int kk = 0; kk < kPx; ++kk) ys[kk] *= 16;
+                            Row8<OUT> o3[3];
+                            f2t_row<FAMILY, OUT>(a.col, ys, us, vs, o3);
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) o3[c].store(orow + (c * brows + r) * sw);
+                        }
+                        continue;
+                    }
+                }
 #pragma unroll
                 for (int r = 0; r < ROWS; ++r) {
-                    const int yc = min((tl.u0 + u) * ROWS + r, a.H - 1);
+                    const int yc = min(y0 + r, a.H - 1);
                     int ys[kPx], us[kPx], vs[kPx];
                     if constexpr (FAMILY == kYUV420) {
+                        // ragged right edge or padding rows: per-sample clamped taps
                         const IN *L = sg.luma(st, yc - tl.ly0) - tl.lw0;
                         const IN *Cn[2] = {sg.chroma(st, 0, chroma_near(yc) - tl.cy0) - tl.cw0,
                                            sg.chroma(st, 1, chroma_near(yc) - tl.cy0) - tl.cw0};
                         const IN *Cf[2] = {sg.chroma(st, 0, chroma_far(yc, ch) - tl.cy0) - tl.cw0,
                                            sg.chroma(st, 1, chroma_far(yc, ch) - tl.cy0) - tl.cw0};
-                        if (fast) {
-                            unpack8(*reinterpret_cast<const V8 *>(L + x), ys);
-                            const int i0 = x >> 1;
 #pragma unroll
-                            for (int p = 0; p < 2; ++p) {
-                                int h[2][kPx];
-#pragma unroll
-                                for (int q = 0; q < 2; ++q) {
-                                    const IN *C = q == 0 ? Cn[p] : Cf[p];
-                                    int c[6];
-                                    unpack4(*reinterpret_cast<const V4 *>(C + i0), &c[1]);
-                                    c[0] = C[max(i0 - 1, 0)];
-                                    c[5] = C[min(i0 + 4, cw - 1)];
-                                    hup(c, h[q]);
-                                }
-#pragma unroll
-                                for (int kk = 0; kk < kPx; ++kk) {
-                                    const int s2 = 3 * h[0][kk] + h[1][kk];
-                                    if (p == 0) us[kk] = s2; else vs[kk] = s2;
-                                }
-                            }
-                        } else {
-#pragma unroll
-                            for (int kk = 0; kk < kPx; ++kk) {
-                                const int xc = min(x + kk, a.W - 1);
-                                ys[kk] = L[xc];
-                                const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
-                                us[kk] = 9 * Cn[0][in_] + 3 * Cn[0][if_] + 3 * Cf[0][in_] + Cf[0][if_];
-                                vs[kk] = 9 * Cn[1][in_] + 3 * Cn[1][if_] + 3 * Cf[1][in_] + Cf[1][if_];
-                            }
+                        for (int kk = 0; kk < kPx; ++kk) {
+                            const int xc = min(x + kk, a.W - 1);
+                            ys[kk] = 16 * L[xc];
+                            const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
+                            us[kk] = 9 * Cn[0][in_] + 3 * Cn[0][if_] + 3 * Cf[0][in_] + Cf[0][if_];
+                            vs[kk] = 9 * Cn[1][in_] + 3 * Cn[1][if_] + 3 * Cf[1][in_] + Cf[1][if_];
                         }
-#pragma unroll
-                        for (int kk = 0; kk < kPx; ++kk) ys[kk] *= 16;
                     } else {
                         const IN *P0 = sg.plane(st, 0, yc - tl.ly0) - tl.lw0,
                                  *P1 = sg.plane(st, 1, yc - tl.ly0) - tl.lw0,
@@ -502,16 +523,24 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                     Row8<OUT> o3[3];
                     f2t_row<FAMILY, OUT>(a.col, ys, us, vs, o3);
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) o3[c].store(ob + (c * brows + u * ROWS + r) * sw + (x - tl.x0));
+                    for (int c = 0; c < 3; ++c) o3[c].store(orow + (c * brows + r) * sw);
                 }
             }
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
         __syncwarp();
-        if (threadIdx.x == 0) trace(a, 3, i);
+        NNVISR_TRACE(threadIdx.x == 0, 3, i);
         if ((threadIdx.x & 31) == 0) {
             if (LOADER) mbar_arrive(&empty[k]);
             mbar_arrive(&conv[b]);
+        }
+        if (++k == nst) {
+            k = 0;
+            fph ^= 1u;
+        }
+        if (++b == nob) {
+            b = 0;
+            bround ^= 1u;
         }
     }
 }

@@ -21,7 +21,8 @@ from .config import (BT601, BT709, BT2020, CHROMA_CENTER, CHROMA_LEFT, DOUBLE_FR
                      ClipFormat, Config, Frame, Network)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnnvisr.so")
+# NNVISR_LIBNAME selects another in-tree build of the library (A/B experiments)
+LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("NNVISR_LIBNAME", "libnnvisr.so")))
 
 
 class NnvisrError(RuntimeError):
