@@ -72,9 +72,11 @@ struct F2TArgs {
     int32_t release_first;        // storers free the next output buffer before (1) or after (0) issuing a tile
     int32_t throttle;             // > 0: at most this many destination store groups per storer in flight
     uint64_t *trace;              // experiment timeline buffer (debug & 8)
+    int32_t sleep_ns;             // experiment: consumer sleep per tile (debug & 16)
     int32_t debug;                // experiment switches (NNVISR_F2T_DEBUG), 0 in production
     int64_t pitch_y, pitch_c;     // uniform plane pitches of the bound frames (0 = not uniform)
     int64_t tiles;
+    unsigned long long *tile_counter;  // TMA path: zeroed per launch, dynamic tile scheduler
     F2TColour col;
     // 4:2:0 chroma siting of this launch: 0 centre, 1 LEFT (generic kernels only)
     int32_t left;
@@ -102,6 +104,7 @@ struct T2FArgs {
     int32_t tma_ok, rowunits, nseg, stages, stage_bytes, segw;
     int32_t cthreads;  // TMA path: consumer threads per CTA (segw / 8 rounded up to warps)
     int64_t tiles;
+    unsigned long long *tile_counter;  // TMA path: zeroed per launch, dynamic tile scheduler
     T2FColour col;
     int32_t left;  // 4:2:0 chroma siting: 0 centre, 1 LEFT (generic kernels only)
     // YUV-native tensors (NEXT-3): output slot o of tuple c reads luma plane o

@@ -101,14 +101,35 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // Experiment timeline (build with -DNNVISR_F2T_TRACE, run with
 // NNVISR_F2T_DEBUG=8): SM clock of event `ev` of tile i, CTAs 0 and 1, first
 // 128 tiles (see f2t_tma_launch).  Compiled out otherwise.
-constexpr int kTraceTiles = 128, kTraceEvents = 8;
+constexpr int kTraceTiles = 128, kTraceEvents = 8, kTraceCtas = 1024;
+__device__ __forceinline__ uint64_t gtimer()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
 #ifdef NNVISR_F2T_TRACE
 #define NNVISR_TRACE(cond, ev, i)                                                                 \
     do {                                                                                          \
         if ((cond) && (a.debug & 8) && blockIdx.x < 2 && (i) < kTraceTiles)                       \
             a.trace[(blockIdx.x * kTraceEvents + (ev)) * kTraceTiles + (i)] = clock64();          \
     } while (0)
+// per-CTA record after the tile timelines: [start ns, end ns, smid] (globaltimer)
+#define NNVISR_TRACE_CTA(slot, val)                                                                   \
+    do {                                                                                              \
+        if ((a.debug & 8) && blockIdx.x < kTraceCtas)                                                 \
+            a.trace[2 * kTraceEvents * kTraceTiles + 3 * blockIdx.x + (slot)] = (val);               \
+    } while (0)
 #else
+#define NNVISR_TRACE_CTA(slot, val) \
+    do {                            \
+    } while (0)
 #define NNVISR_TRACE(cond, ev, i) \
     do {                          \
     } while (0)
@@ -122,21 +143,38 @@ constexpr int kMaxOutBufs = 8;
 struct F2THdr {
     int u0, nu, x0, x1, ly0, cy0, lw0, cw0;
 };
-// mbarriers (full, empty per stage; ofree, conv per output buffer) and the
-// stage headers at the start of dynamic smem
-constexpr int kBarBytes = 8 * (2 * kMaxStages + 2 * kMaxOutBufs) + 32 * kMaxStages;
+// mbarriers (full, empty per stage; ofree, conv per output buffer), the
+// stage headers and the ring of local tile -> launch tile ids (f2t) at the
+// start of dynamic smem
+constexpr int kTileRing = 16;  // >= stages + output buffers + 1
+constexpr int kBarBytes = 8 * (2 * kMaxStages + 2 * kMaxOutBufs) + 32 * kMaxStages + 8 * kTileRing;
 
-// CTA b takes tiles b, b + G, b + 2G, ... (G = grid size): every CTA gets the
-// same mix of frames, whatever each frame's number of destinations.
-struct TileCursor {
-    int64_t count;  // tiles of this CTA
-    __device__ __forceinline__ void init(int64_t tiles)
+// The tiles one CTA processes, in order: dynamic (a zeroed per-launch
+// counter: each fetch takes the next unprocessed tile of the launch, so fast
+// SMs take more tiles and no CTA is left finishing a long static share; every
+// CTA ends with exactly one fetch past the end) or, without a counter,
+// static (tiles b, b + G, ...).  One thread per CTA fetches, in order.
+struct TileSource {
+    unsigned long long *counter;
+    int64_t tiles, next;
+    // skip: local tiles fetched by another thread first (static mode)
+    __device__ __forceinline__ void init(unsigned long long *c, int64_t n, int skip = 0)
     {
-        count = tiles > blockIdx.x ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        counter = c;
+        tiles = n;
+        next = blockIdx.x + static_cast<int64_t>(skip) * gridDim.x;
     }
-    __device__ __forceinline__ int64_t tile(int64_t i) const
+    // next tile of this CTA, or -1 when the launch has none left
+    __device__ __forceinline__ int64_t fetch()
     {
-        return blockIdx.x + i * static_cast<int64_t>(gridDim.x);
+        int64_t t;
+        if (counter) {
+            t = static_cast<int64_t>(atomicAdd(counter, 1ull));
+        } else {
+            t = next;
+            next += gridDim.x;
+        }
+        return t < tiles ? t : -1;
     }
 };
 
@@ -251,11 +289,17 @@ __device__ __forceinline__ void f2t_copies(const F2TArgs &a, const F2TTile &tl, 
 }
 
 // Stage tile t: write the consumers' view of the tile (F2THdr), then issue
-// its TMA bulk copies, completing by byte count on `bar`.
+// its TMA bulk copies, completing by byte count on `bar`.  t < 0: the
+// end-of-work header (u0 = -1), the stage's phase completed without data.
 template <int FAMILY, typename IN>
 __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *st, uint64_t *bar, F2THdr *hdr)
 {
     using S = F2TStage<FAMILY, IN>;
+    if (t < 0) {
+        hdr->u0 = -1;
+        mbar_arrive(bar);
+        return;
+    }
     F2TTile tl;
     tl.set(a, t, S::ROWS);
     const DevFrame f = load_frame(a.frames + a.job_frame[tl.job]);
@@ -301,10 +345,8 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
     const int nst = a.stages, nob = a.nob, brows = a.band * ROWS;
     const S sg(a.ls, a.cs, a.band);
     OUT *obuf = reinterpret_cast<OUT *>(stages + nst * a.stage_bytes);
+    int64_t *tile_of = reinterpret_cast<int64_t *>(hdr + kMaxStages);  // [kTileRing]: local tile -> launch tile
 
-    TileCursor tc;
-    tc.init(a.tiles);
-    if (tc.count == 0) return;
     if (threadIdx.x == 0) {
         for (int k = 0; k < nst; ++k) {
             mbar_init(&full[k], 1);
@@ -318,17 +360,34 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
     }
     __syncthreads();  // the last CTA-wide barrier: roles split below
 
+    // Dynamic tiles (TileSource): one thread fetches them in local order --
+    // the loader (LOADER), else storer 0 for the first nst local tiles and
+    // consumer thread 0 for local tile i + nst while converting tile i.  The
+    // first fetch past the end gives local tile m the end-of-work header;
+    // tile_of[] holds -1 from m on.  The consumers stop at m, arriving on
+    // conv for m and m + 1 so both storers see the end.
     if (threadIdx.x >= kThreads) {
         if ((threadIdx.x & 31) != 0) return;
         if (LOADER && threadIdx.x == kThreads + 64) {  // ---------------- loader (LOADER variant)
-            for (int k = 0; k < nst && k < tc.count; ++k)
-                f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
-            for (int64_t i = 0; i + nst < tc.count; ++i) {
-                const int k = static_cast<int>(i % nst);
-                mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
-                fence_proxy_async();
-                NNVISR_TRACE(true, 0, i + nst);
-                f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+            TileSource ts;
+            ts.init(a.tile_counter, a.tiles);
+            int k = 0;
+            uint32_t rnd = 0;  // (i / nst) & 1
+            for (int64_t i = 0;; ++i) {
+                if (i >= nst) {  // stage k was last used by local tile i - nst
+                    mbar_wait(&empty[k], rnd ^ 1u);
+                    fence_proxy_async();
+                }
+                const int64_t t = ts.fetch();
+                tile_of[i % kTileRing] = t;
+                if (t < 0) tile_of[(i + 1) % kTileRing] = -1;
+                NNVISR_TRACE(true, 0, i);
+                f2t_issue<FAMILY, IN>(a, t, stages + k * a.stage_bytes, &full[k], &hdr[k]);
+                if (t < 0) break;
+                if (++k == nst) {
+                    k = 0;
+                    rnd ^= 1u;
+                }
             }
             return;
         }
@@ -346,32 +405,51 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
         // so the consumers get the buffer early) or right after (a deeper
         // store queue), once at most the groups committed since tile j - nob
         // are still reading.  a.throttle > 0 caps this storer's groups still
-        // reading shared memory.
+        // reading shared memory.  A storer reaching the end-of-work tile still
+        // frees buffer j (the consumers' closing arrival may wait on it).
         const int NS = a.nstorers;
         const int sidx = (threadIdx.x - kThreads) >> 5;
         if (sidx >= NS) return;
-        if (!LOADER && sidx == 0)
-            for (int k = 0; k < nst && k < tc.count; ++k)
-                f2t_issue<FAMILY, IN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+        if (!LOADER && sidx == 0) {
+            TileSource ts;
+            ts.init(a.tile_counter, a.tiles);
+            bool end = false;
+            for (int k = 0; k < nst; ++k) {
+                const int64_t t = end ? -1 : ts.fetch();
+                tile_of[k] = t;
+                if (!end) f2t_issue<FAMILY, IN>(a, t, stages + k * a.stage_bytes, &full[k], &hdr[k]);
+                end = t < 0;
+            }
+            if (end) tile_of[nst % kTileRing] = -1;
+        }
         const int r = NS == 1 ? 1 : ((nob & 1) ? 1 : 2), back = (nob - r) / NS;
         int lj = -1;
         DstList dl;
         const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp;
         int ng = 0;                 // groups committed by this storer
         int eb1 = 0, eb2 = 0, eb3 = 0, eb4 = 0;  // back <= 4 (nob <= 5)
-        for (int64_t i = sidx; i < tc.count; i += NS) {
+        for (int64_t i = sidx;; i += NS) {
             const int b = static_cast<int>(i % nob);
             mbar_wait(&conv[b], static_cast<uint32_t>((i / nob) & 1));
             NNVISR_TRACE(true, 4, i);
-            if (!LOADER && i + nst < tc.count) {  // stage of tile i is free: refill it with tile i + nst
+            const int64_t t = tile_of[i % kTileRing];
+            const int64_t j = i + r;
+            const int eb = back == 1 ? eb1 : back == 2 ? eb2 : back == 3 ? eb3 : eb4;
+            if (t < 0) {  // end of work: free buffer j, drain, exit
+                if (j >= nob) {
+                    bulk_wait_read_le(back == 0 ? 0 : ng - eb);
+                    mbar_arrive(&ofree[static_cast<int>(j % nob)]);
+                }
+                break;
+            }
+            if (!LOADER) {  // stage of tile i is free: refill it with local tile i + nst
                 const int k = static_cast<int>(i % nst);
                 fence_proxy_async();
                 NNVISR_TRACE(true, 0, i + nst);
-                f2t_issue<FAMILY, IN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+                f2t_issue<FAMILY, IN>(a, tile_of[(i + nst) % kTileRing], stages + k * a.stage_bytes, &full[k],
+                                      &hdr[k]);
             }
-            const int64_t j = i + r;
-            const bool rel = j >= nob && j < tc.count;
-            const int eb = back == 1 ? eb1 : back == 2 ? eb2 : back == 3 ? eb3 : eb4;
+            const bool rel = j >= nob;
             if (rel && back > 0 && a.release_first) {
                 bulk_wait_read_le(ng - eb);
                 mbar_arrive(&ofree[static_cast<int>(j % nob)]);
@@ -379,7 +457,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
             }
             // fan tile i out to every (run, slot) holding its frame
             F2TTile tl;
-            tl.set(a, tc.tile(i), ROWS);
+            tl.set(a, t, ROWS);
             const int sw = tl.x1 - tl.x0, rows = tl.nu * ROWS;
             if (tl.job != lj) {
                 lj = tl.job;
@@ -422,16 +500,35 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
     }
 
     // ------------------------------------------------------------ consumers
+    if (threadIdx.x == 0) {
+        NNVISR_TRACE_CTA(0, gtimer());
+        NNVISR_TRACE_CTA(2, smid());
+    }
     const int cw = a.W >> 1, ch = a.H >> 1;
     const int tid = threadIdx.x;
     int k = 0, b = 0;            // stage and output buffer of tile i
     uint32_t fph = 0, bround = 0;  // full[k] wait parity; (i / nob) & 1
-    for (int64_t i = 0; i < tc.count; ++i) {
+    TileSource ts;
+    ts.init(a.tile_counter, a.tiles, nst);
+    for (int64_t i = 0;; ++i) {
         uint8_t *st = stages + k * a.stage_bytes;
         OUT *ob = obuf + b * a.ob_elems;
         mbar_wait(&full[k], fph);
         NNVISR_TRACE(threadIdx.x == 0, 1, i);
         const F2THdr tl = hdr[k];
+        if (tl.u0 < 0) {  // end of work at local tile i: release both storers
+            for (int64_t e = i; e <= i + 1; ++e) {
+                const int be = static_cast<int>(e % nob);
+                if (e >= nob) mbar_wait(&ofree[be], static_cast<uint32_t>(((e / nob) & 1) ^ 1));
+                __syncwarp();
+                if ((threadIdx.x & 31) == 0) mbar_arrive(&conv[be]);
+            }
+            break;
+        }
+        // non-LOADER: thread 0 fetches local tile i + nst (the storer of tile
+        // i stages it); the atomic's latency hides behind this tile's work
+        int64_t next_t = 0;
+        if (!LOADER && threadIdx.x == 0) next_t = ts.fetch();
         const int sw = tl.x1 - tl.x0;
         const int x = tl.x0 + kPx * tid;
         const bool fast = x + kPx <= a.W;
@@ -528,6 +625,11 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
             }
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
+        if (a.debug & 16) __nanosleep(a.sleep_ns);  // experiment: slower consumers
+        if (!LOADER && threadIdx.x == 0) {
+            tile_of[(i + nst) % kTileRing] = next_t;
+            if (next_t < 0) tile_of[(i + nst + 1) % kTileRing] = -1;
+        }
         __syncwarp();
         NNVISR_TRACE(threadIdx.x == 0, 3, i);
         if ((threadIdx.x & 31) == 0) {
@@ -543,6 +645,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
             bround ^= 1u;
         }
     }
+    if (threadIdx.x == 0) NNVISR_TRACE_CTA(1, gtimer());
 }
 
 // ------------------------------------------------------------------ t2f
@@ -560,10 +663,17 @@ __device__ __forceinline__ TIN *t2f_row_ptr(uint8_t *st, int segw, int r, int c)
     return reinterpret_cast<TIN *>(st) + (r * 3 + c) * segw;
 }
 
+// Stage tile t; t < 0: write the end-of-work header (job -1) and complete
+// the stage's phase without data.
 template <int FAMILY, typename TIN>
 __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *st, uint64_t *bar, T2FHdr *hdr)
 {
     constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
+    if (t < 0) {
+        hdr->job = -1;
+        mbar_arrive(bar);
+        return;
+    }
     int job, ru, x0;
     decode_tile(t, a.rowunits, a.nseg, a.segw, job, ru, x0);
     const int x1 = min(x0 + a.segw, a.Wo);
@@ -595,9 +705,6 @@ __global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tm
     uint8_t *stages = smem + kBarBytes;
     const int nst = a.stages, nct = a.cthreads;
 
-    TileCursor tc;
-    tc.init(a.tiles);
-    if (tc.count == 0) return;
     if (threadIdx.x == 0) {
         for (int k = 0; k < nst; ++k) {
             mbar_init(&full[k], 1);
@@ -609,13 +716,23 @@ __global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tm
 
     if (threadIdx.x >= nct) {  // ---------------- producer warp
         if (threadIdx.x != nct) return;
-        for (int k = 0; k < nst && k < tc.count; ++k)
-            t2f_issue<FAMILY, TIN>(a, tc.tile(k), stages + k * a.stage_bytes, &full[k], &hdr[k]);
-        for (int64_t i = 0; i + nst < tc.count; ++i) {
-            const int k = static_cast<int>(i % nst);
-            mbar_wait(&empty[k], static_cast<uint32_t>((i / nst) & 1));
-            fence_proxy_async();
-            t2f_issue<FAMILY, TIN>(a, tc.tile(i + nst), stages + k * a.stage_bytes, &full[k], &hdr[k]);
+        TileSource ts;
+        ts.init(a.tile_counter, a.tiles);
+        // stage k of local tile i; stop after staging the end-of-work header
+        int k = 0;
+        uint32_t rnd = 0;  // (i / nst) & 1
+        for (int64_t i = 0;; ++i) {
+            if (i >= nst) {  // stage k was last used by local tile i - nst
+                mbar_wait(&empty[k], rnd ^ 1u);
+                fence_proxy_async();
+            }
+            const int64_t t = ts.fetch();
+            t2f_issue<FAMILY, TIN>(a, t, stages + k * a.stage_bytes, &full[k], &hdr[k]);
+            if (t < 0) break;
+            if (++k == nst) {
+                k = 0;
+                rnd ^= 1u;
+            }
         }
         return;
     }
@@ -625,11 +742,13 @@ __global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tm
     int cj = -1;
     DevFrame f;
     const int xo = kPx * threadIdx.x;  // column within the segment
-    for (int64_t i = 0; i < tc.count; ++i) {
-        const int k = static_cast<int>(i % nst);
+    int k = 0;
+    uint32_t fph = 0;
+    for (;;) {
         uint8_t *st = stages + k * a.stage_bytes;
-        mbar_wait(&full[k], static_cast<uint32_t>((i / nst) & 1));
+        mbar_wait(&full[k], fph);
         const T2FHdr h = hdr[k];
+        if (h.job < 0) break;
         if (h.job != cj) {
             cj = h.job;
             f = load_frame(a.out + cj);
@@ -649,6 +768,10 @@ __global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tm
         }
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[k]);
+        if (++k == nst) {
+            k = 0;
+            fph ^= 1u;
+        }
     }
 }
 
@@ -764,6 +887,7 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     a.throttle = env_int("NNVISR_F2T_THROTTLE", 0);
     a.nstorers = std::max(1, std::min(2, env_int("NNVISR_F2T_STORERS", 2)));
     a.release_first = env_int("NNVISR_F2T_RELFIRST", fits2 ? 1 : 0);
+    a.sleep_ns = env_int("NNVISR_F2T_SLEEP", 0);
     a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
     int loader = env_int("NNVISR_F2T_LOADER", fits2 ? 0 : 1);
     auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true> : f2t_tma<FAMILY, IN, OUT, false>;
@@ -776,7 +900,7 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>(a.tiles, static_cast<int64_t>(sms()) * std::max(per_sm, 1))));
     static uint64_t *trace_buf = nullptr;
-    constexpr size_t kTraceBytes = 2 * kTraceEvents * kTraceTiles * sizeof(uint64_t);
+    constexpr size_t kTraceBytes = (2 * kTraceEvents * kTraceTiles + 3 * kTraceCtas) * sizeof(uint64_t);
     if (a.debug & 8) {
         if (!trace_buf) cudaMalloc(&trace_buf, kTraceBytes);
         cudaMemsetAsync(trace_buf, 0, kTraceBytes, s);
@@ -796,6 +920,11 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
                         std::fprintf(fp, " %llu", (unsigned long long)h[(c * kTraceEvents + ev) * kTraceTiles + i]);
                     std::fprintf(fp, "\n");
                 }
+            for (int c = 0; c < grid && c < kTraceCtas; ++c) {
+                const uint64_t *q = &h[2 * kTraceEvents * kTraceTiles + 3 * c];
+                std::fprintf(fp, "cta %d %llu %llu %llu\n", c, (unsigned long long)q[0], (unsigned long long)q[1],
+                             (unsigned long long)q[2]);
+            }
             std::fclose(fp);
         }
     }

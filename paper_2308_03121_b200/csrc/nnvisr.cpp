@@ -463,6 +463,19 @@ nnvisr_status acquire_slot(nnvisr_handle *h, UploadSlot **out)
     return NNVISR_OK;
 }
 
+// Append a zeroed 64-bit tile counter (the TMA kernels' dynamic tile
+// scheduler) after the `bytes` already staged in the slot; returns its device
+// address and grows `bytes`.  It is uploaded with the tables, so every launch
+// starts from 0 and the slot's event guards its reuse.
+constexpr size_t kCounterBytes = 16;  // alignment slack + the counter
+unsigned long long *append_counter(UploadSlot *s, size_t &bytes)
+{
+    const size_t off = (bytes + 7) & ~size_t(7);
+    std::memset(static_cast<char *>(s->host) + off, 0, 8);
+    bytes = off + 8;
+    return reinterpret_cast<unsigned long long *>(static_cast<char *>(s->dev) + off);
+}
+
 nnvisr_status upload(UploadSlot *s, size_t bytes, cudaStream_t st)
 {
     cudaError_t e = cudaMemcpyAsync(s->dev, s->host, bytes, cudaMemcpyHostToDevice, st);
@@ -709,8 +722,11 @@ nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, 
     int32_t *tab = reinterpret_cast<int32_t *>(static_cast<char *>(slot->host) + sizeof(DevFrame) * h->N);
     const int64_t J = build_f2t_jobs(key.data(), 1, h->N, 0, tab);
     const size_t tab_ints = 2 * J + 1 + h->N;
-    if ((s = upload(slot, sizeof(DevFrame) * h->N + sizeof(int32_t) * tab_ints, st))) return s;
+    size_t bytes = sizeof(DevFrame) * h->N + sizeof(int32_t) * tab_ints;
+    unsigned long long *counter = append_counter(slot, bytes);
+    if ((s = upload(slot, bytes, st))) return s;
     F2TArgs a = f2t_args(h);
+    a.tile_counter = counter;
     const int32_t *dtab = reinterpret_cast<const int32_t *>(static_cast<char *>(slot->dev) + sizeof(DevFrame) * h->N);
     a.frames = static_cast<const DevFrame *>(slot->dev);
     a.job_frame = dtab;
@@ -753,7 +769,7 @@ static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, 
 {
     // an upload slot holds 3 ints per (run, slot) plus one; runs per launch
     // are also bounded by the 5-bit slot / run encoding of dst_code
-    const int64_t max_runs = std::min<int64_t>((int64_t)(kSlotBytes / sizeof(int32_t) - 1) / (3 * per_run),
+    const int64_t max_runs = std::min<int64_t>((int64_t)((kSlotBytes - kCounterBytes) / sizeof(int32_t) - 1) / (3 * per_run),
                                                (int64_t)(INT32_MAX / 32));
     F2TArgs a = f2t_args(h);
     a.frames = tab.dev;
@@ -771,7 +787,9 @@ static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, 
             release_slot(slot, st);
             continue;
         }
-        if ((s = upload(slot, sizeof(int32_t) * (2 * J + 1 + nr * per_run), st))) return s;
+        size_t bytes = sizeof(int32_t) * (2 * J + 1 + nr * per_run);
+        a.tile_counter = append_counter(slot, bytes);
+        if ((s = upload(slot, bytes, st))) return s;
         const int32_t *dtab = static_cast<const int32_t *>(slot->dev);
         a.job_frame = dtab;
         a.job_dst = dtab + J;
@@ -890,14 +908,17 @@ static nnvisr_status t2f_common(nnvisr_handle *h, const void *tensors, int64_t s
                      (a.twc * h->elem) % al == 0;
     }
     const size_t per_job = sizeof(DevFrame) + (skipped ? sizeof(int32_t) : 0);
-    const int64_t per_slot = skipped ? (int64_t)(kSlotBytes / per_job) : (int64_t)(kSlotBytes / sizeof(DevFrame)) / h->M * h->M;
+    const int64_t per_slot = skipped ? (int64_t)((kSlotBytes - kCounterBytes) / per_job)
+                                     : (int64_t)((kSlotBytes - kCounterBytes) / sizeof(DevFrame)) / h->M * h->M;
     for (int64_t j0 = 0; j0 < jobs; j0 += per_slot) {
         const int64_t nj = std::min(per_slot, jobs - j0);
         UploadSlot *slot = nullptr;
         if ((s = acquire_slot(h, &slot))) return s;
         std::memcpy(slot->host, desc + j0, sizeof(DevFrame) * nj);
         if (skipped) std::memcpy(static_cast<char *>(slot->host) + sizeof(DevFrame) * nj, codes.data() + j0, sizeof(int32_t) * nj);
-        if ((s = upload(slot, per_job * nj, st))) return s;
+        size_t bytes = per_job * nj;
+        a.tile_counter = append_counter(slot, bytes);
+        if ((s = upload(slot, bytes, st))) return s;
         a.out = static_cast<const DevFrame *>(slot->dev);
         if (skipped) {
             a.job_code = reinterpret_cast<const int32_t *>(static_cast<char *>(slot->dev) + sizeof(DevFrame) * nj);

@@ -4,7 +4,9 @@ import sys
 
 import numpy as np
 
-rows = [l.split() for l in open(sys.argv[1]) if not l.startswith("#")]
+lines = open(sys.argv[1]).read().splitlines()
+rows = [l.split() for l in lines if not l.startswith("#") and not l.startswith("cta")]
+ctas = np.array([[int(x) for x in l.split()[1:]] for l in lines if l.startswith("cta")], dtype=np.float64)
 hdr = open(sys.argv[1]).readline().strip()
 mhz = float(sys.argv[2]) if len(sys.argv) > 2 else 1965.0
 print(hdr)
@@ -30,3 +32,11 @@ for cta in (0, 1):
         print("tile  L_issue C_full C_ofree C_done S_conv S_commit S_release(j)")
         for i in range(min(n, 24)):
             print(f"{i:4d} " + " ".join(f"{x:7.2f}" for x in us[i, :7]))
+
+if len(ctas):
+    t0 = ctas[:, 1].min()
+    start, end, sm = (ctas[:, 1] - t0) / 1e3, (ctas[:, 2] - t0) / 1e3, ctas[:, 3].astype(int)
+    print(f"CTAs {len(ctas)}: start max {start.max():.1f} us; end min {end.min():.1f} median {np.median(end):.1f}"
+          f" max {end.max():.1f} us; slowest 8 (cta, sm, end):",
+          [(int(i), int(sm[i]), round(end[i], 1)) for i in np.argsort(end)[-8:]])
+    print("fastest 8:", [(int(i), int(sm[i]), round(end[i], 1)) for i in np.argsort(end)[:8]])
