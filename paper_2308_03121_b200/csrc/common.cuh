@@ -100,8 +100,12 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b)
 }
 
 // ------------------------------------------------------------ f2t colour
-// Steps A5-A6: dequantise (exact integer offset, one fp32 rounding) and the
-// inverse matrix with no clamp (reading A4).  Inputs are 16 x code.
+// Steps A5-A6: dequantise and apply the inverse matrix with no clamp (reading
+// A4).  Inputs are 16 x code.  Y' = (ys - y_off) * y_scale (exact integer
+// offset, one fp32 rounding); the chroma offsets are exact integers too and
+// the chroma scale is folded into the matrix constants (r_v = r_pr * c_scale
+// etc., each rounded once from double), so R' = Y' + r_v * (vs - c_off) is one
+// FMA.
 template <int FAMILY>
 __device__ __forceinline__ void f2t_colour(const F2TColour &c, int ys, int us, int vs, float &R, float &G, float &B)
 {
@@ -111,22 +115,20 @@ __device__ __forceinline__ void f2t_colour(const F2TColour &c, int ys, int us, i
         B = static_cast<float>(vs - c.y_off) * c.y_scale;
     } else {
         const float Y = static_cast<float>(ys - c.y_off) * c.y_scale;
-        const float Pb = static_cast<float>(us - c.c_off) * c.c_scale;
-        const float Pr = static_cast<float>(vs - c.c_off) * c.c_scale;
-        R = fmaf(c.r_pr, Pr, Y);
-        B = fmaf(c.b_pb, Pb, Y);
-        G = fmaf(-c.g_pr, Pr, fmaf(-c.g_pb, Pb, Y));
+        const float du = static_cast<float>(us - c.c_off), dv = static_cast<float>(vs - c.c_off);
+        R = fmaf(c.r_v, dv, Y);
+        B = fmaf(c.b_u, du, Y);
+        G = fmaf(-c.g_v, dv, fmaf(-c.g_u, du, Y));
     }
 }
 
 // fp16 tensors near zero: R', G', B' are sums of O(1) terms whose fp32
-// evaluation errs by up to ~2^-22.3 (one rounding of Y' <= 1.2 and of Pb, Pr,
-// the rounded matrix constants, at most two FMA roundings).  Against the
-// oracle's single double->fp16 rounding that stays within 1 fp16 ULP while
-// the ULP exceeds the error, i.e. for |v| >= 2^-11 (ULP 2^-21).  Values below
-// 2^-9 (a 4x margin; also measured faster than 2^-11 at 1080p on B200,
-// tools/ab.sh) are recomputed in fp64 and rounded once to fp16; the returned
-// float is that fp16 value exactly, so the RNE store reproduces it.
+// evaluation errs by up to ~2^-23 (one rounding of Y' <= 1.2, the rounded
+// folded constants, the FMA roundings).  Against the oracle's single
+// double->fp16 rounding that stays within 1 fp16 ULP while the ULP exceeds
+// the error, i.e. for |v| >= 2^-11 (ULP 2^-21).  Pixels with a value below
+// 2^-9 (a 4x margin) are recomputed in fp64 and rounded once to fp16; the
+// returned float is that fp16 value exactly, so the RNE store reproduces it.
 // (tests/test_gpu_fp16_exhaustive.py: every 8-bit triple, all matrices.)
 __device__ __forceinline__ float3 f2t_colour_precise(const F2TColour &c, int ys, int us, int vs)
 {
@@ -137,14 +139,14 @@ __device__ __forceinline__ float3 f2t_colour_precise(const F2TColour &c, int ys,
                        __half2float(__double2half(Y - c.g_pb_d * Pb - c.g_pr_d * Pr)),
                        __half2float(__double2half(Y + c.b_pb_d * Pb)));
 }
+constexpr float kF16Tiny = 1.0f / 512.0f;  // 2^-9
 
 template <int FAMILY, typename OUT>
 __device__ __forceinline__ void f2t_pixel(const F2TColour &c, int ys, int us, int vs, float &R, float &G, float &B)
 {
     f2t_colour<FAMILY>(c, ys, us, vs, R, G, B);
     if (FAMILY != kRGB && sizeof(OUT) == 2) {
-        constexpr float kTiny = 1.0f / 512.0f;
-        if (fabsf(R) < kTiny || fabsf(G) < kTiny || fabsf(B) < kTiny) {
+        if (fabsf(R) < kF16Tiny || fabsf(G) < kF16Tiny || fabsf(B) < kF16Tiny) {
             const float3 p = f2t_colour_precise(c, ys, us, vs);
             R = p.x;
             G = p.y;

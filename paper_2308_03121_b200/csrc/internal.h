@@ -29,6 +29,7 @@ struct F2TColour {
     int32_t u_off;  // YUV-native chroma U = P + 1/2 = (16*code - u_off) * c_scale (reading A22)
     float y_scale, c_scale;
     float r_pr, b_pb, g_pb, g_pr;
+    float r_v, b_u, g_u, g_v;  // r_pr * c_scale, b_pb * c_scale, g_pb * c_scale, g_pr * c_scale (rounded once)
     double y_scale_d, c_scale_d, r_pr_d, b_pb_d, g_pb_d, g_pr_d;
 };
 

@@ -271,6 +271,11 @@ nnvisr_status nnvisr_open(const nnvisr_clip_format *fmt, const nnvisr_network *n
     h->f2c.b_pb_d = 2.0 * (1.0 - kb);
     h->f2c.g_pb_d = kb * 2.0 * (1.0 - kb) / kg;
     h->f2c.g_pr_d = kr * 2.0 * (1.0 - kr) / kg;
+    // chroma scale folded into the matrix (common.cuh f2t_colour), rounded once
+    h->f2c.r_v = (float)(h->f2c.r_pr_d * h->f2c.c_scale_d);
+    h->f2c.b_u = (float)(h->f2c.b_pb_d * h->f2c.c_scale_d);
+    h->f2c.g_u = (float)(h->f2c.g_pb_d * h->f2c.c_scale_d);
+    h->f2c.g_v = (float)(h->f2c.g_pr_d * h->f2c.c_scale_d);
     // B2/B4 constants
     T2FColour &c = h->t2c;
     c.kr = kr; c.kb = kb; c.db = 2.0 * (1.0 - kb); c.dr = 2.0 * (1.0 - kr);
