@@ -696,7 +696,7 @@ __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *
 // rounded up to whole warps) convert and store with st.global; lane 0 of the
 // last warp keeps the stages full.
 template <int FAMILY, typename OS, typename TIN, typename AR>
-__global__ void __launch_bounds__(kThreads + 32, sizeof(AR) == 4 ? 3 : 2) t2f_tma(const T2FArgs a)
+__global__ void __launch_bounds__(kThreads + 32, (FAMILY == kYUV420 && sizeof(AR) == 8) ? 2 : 3) t2f_tma(const T2FArgs a)
 {
     constexpr int ROWS = FAMILY == kYUV420 ? 2 : 1;
     extern __shared__ __align__(128) uint8_t smem[];
