@@ -71,9 +71,7 @@ struct F2TArgs {
     int32_t band, ls, cs, whole;  // band height (row units), staged row strides, whole-row copies
     int32_t nstorers;             // storer threads (1 or 2)
     int32_t release_first;        // storers free the next output buffer before (1) or after (0) issuing a tile
-    int32_t throttle;             // > 0: at most this many destination store groups per storer in flight
     uint64_t *trace;              // experiment timeline buffer (debug & 8)
-    int32_t sleep_ns;             // experiment: consumer sleep per tile (debug & 16)
     int32_t debug;                // experiment switches (NNVISR_F2T_DEBUG), 0 in production
     int64_t pitch_y, pitch_c;     // uniform plane pitches of the bound frames (0 = not uniform)
     int64_t tiles;

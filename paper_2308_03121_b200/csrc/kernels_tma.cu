@@ -404,8 +404,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
         // issue blocks while the SM's TMA unit works through earlier stores,
         // so the consumers get the buffer early) or right after (a deeper
         // store queue), once at most the groups committed since tile j - nob
-        // are still reading.  a.throttle > 0 caps this storer's groups still
-        // reading shared memory.  A storer reaching the end-of-work tile still
+        // are still reading.  A storer reaching the end-of-work tile still
         // frees buffer j (the consumers' closing arrival may wait on it).
         const int NS = a.nstorers;
         const int sidx = (threadIdx.x - kThreads) >> 5;
@@ -471,7 +470,6 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                 OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
                                                  static_cast<int64_t>(cd & 31) * a.slot_bytes) +
                          static_cast<int64_t>(tl.u0 * ROWS) * a.Wp + tl.x0;
-                if (a.throttle > 0) bulk_wait_read_le(a.throttle - 1);
                 for (int c = 0; c < 3; ++c) {
                     if (whole_rows) {
                         bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
@@ -625,7 +623,6 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
             }
         }
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
-        if (a.debug & 16) __nanosleep(a.sleep_ns);  // experiment: slower consumers
         if (!LOADER && threadIdx.x == 0) {
             tile_of[(i + nst) % kTileRing] = next_t;
             if (next_t < 0) tile_of[(i + nst + 1) % kTileRing] = -1;
@@ -884,10 +881,8 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     a.tiles = a.tiles / bands * ((a.rowunits + a.band - 1) / a.band);
     const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band);
     const bool fits2 = 2 * (smem + kCtaReserve) <= kSmSmem;
-    a.throttle = env_int("NNVISR_F2T_THROTTLE", 0);
     a.nstorers = std::max(1, std::min(2, env_int("NNVISR_F2T_STORERS", 2)));
     a.release_first = env_int("NNVISR_F2T_RELFIRST", fits2 ? 1 : 0);
-    a.sleep_ns = env_int("NNVISR_F2T_SLEEP", 0);
     a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
     int loader = env_int("NNVISR_F2T_LOADER", fits2 ? 0 : 1);
     auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true> : f2t_tma<FAMILY, IN, OUT, false>;
