@@ -76,6 +76,7 @@ struct F2TArgs {
     int64_t pitch_y, pitch_c;     // uniform plane pitches of the bound frames (0 = not uniform)
     int64_t tiles;
     unsigned long long *tile_counter;  // TMA path: zeroed per launch, dynamic tile scheduler
+    int64_t jobs, dests;               // distinct frames and (run, slot) destinations of the launch
     F2TColour col;
     // 4:2:0 chroma siting of this launch: 0 centre, 1 LEFT (generic kernels only)
     int32_t left;

@@ -846,8 +846,17 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     // (profiles/r01/f2t_sweep.txt): bands of 2 row units with 3 output buffers
     // for whole-row frames and 4:4:4; single row units for 4:2:0 frames wider
     // than one 2048-column segment (per-row copies, chroma halo rows)
+    // Low fan-out launches (store mode, Fig. 1 slots: <= 2 destinations per
+    // frame) are bound by the conversion itself: when bands of 2 would leave
+    // one CTA per SM they take single row units, so two CTAs (16 converting
+    // warps) share an SM.
+    constexpr int kSmSmem = 228 * 1024, kCtaReserve = 1024;
+    auto fits_two = [&](int B) {
+        return 2 * (kBarBytes + 2 * stage_bytes(B) + 2 * ob_bytes(B) + kCtaReserve) <= kSmSmem;
+    };
+    const bool low_fanout = a.dests > 0 && a.dests <= 2 * a.jobs;
     int B = env_int("NNVISR_F2T_BAND", 0);
-    if (B <= 0) B = (FAMILY == kYUV420 && a.nseg > 1) ? 1 : 2;
+    if (B <= 0) B = ((FAMILY == kYUV420 && a.nseg > 1) || (low_fanout && !fits_two(2))) ? 1 : 2;
     a.band = std::max(1, std::min(B, a.rowunits));
     const int bands = (a.rowunits + a.band - 1) / a.band;
     a.tiles = a.tiles / ((int64_t)a.rowunits * a.nseg) * bands * a.nseg;  // jobs * bands * nseg
@@ -861,8 +870,7 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     //  * else one CTA per SM (1080p whole rows, 4K 4:4:4 fp32): a dedicated
     //    loader warp, 3 output buffers, release after issuing (a deeper
     //    store queue).
-    constexpr int kSmSmem = 228 * 1024, kCtaReserve = 1024;
-    const bool two = 2 * (kBarBytes + 2 * a.stage_bytes + 2 * ob_bytes(a.band) + kCtaReserve) <= kSmSmem;
+    const bool two = fits_two(a.band);
     a.stages = env_int("NNVISR_F2T_STAGES", 2);
     a.nob = env_int("NNVISR_F2T_NOB", two ? 2 : 3);
     a.stages = std::max(1, std::min(kMaxStages, a.stages));

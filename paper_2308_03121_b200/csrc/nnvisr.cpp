@@ -580,9 +580,11 @@ int64_t store_slot_bytes(const nnvisr_handle *h)
     return h->yuv_in ? (h->Hp * h->Wp + 2 * h->Hc * h->Wc) * h->elem : 3 * h->Hp * h->Wp * h->elem;
 }
 
-nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, cudaStream_t st)
+nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, int64_t dests, cudaStream_t st)
 {
     a.items = jobs * a.units;
+    a.jobs = jobs;
+    a.dests = dests;
     // TMA-pipelined path: every copy window 16-byte aligned (planes and
     // pitches aligned, width a multiple of 32 samples) and 16-byte stores
     const int rows = h->fmt.family == NNVISR_YUV420 ? 2 : 1;
@@ -740,7 +742,7 @@ nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, 
     set_f2t_dst(h, a, static_cast<char *>(tensor), 0, nullptr, 0, h->N);
     a.vec_in = vec;
     uniform_pitches(h, in, h->N, a.pitch_y, a.pitch_c);
-    s = run_f2t(h, a, J, st);
+    s = run_f2t(h, a, J, tab[2 * J], st);
     nnvisr_status s2 = release_slot(slot, st);
     return s ? s : s2;
 }
@@ -801,7 +803,7 @@ static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, 
         a.dst_code = dtab + 2 * J + 1;
         set_f2t_dst(h, a, static_cast<char *>(dst) + r0 * run_stride, run_stride,
                     dst2 ? static_cast<char *>(dst2) + r0 * run_stride2 : nullptr, run_stride2, per_run);
-        s = run_f2t(h, a, J, st);
+        s = run_f2t(h, a, J, tbl[2 * J], st);
         nnvisr_status s2 = release_slot(slot, st);
         if (s) return s;
         if (s2) return s2;
