@@ -155,6 +155,63 @@ __device__ __forceinline__ void f2t_pixel(const F2TColour &c, int ys, int us, in
     }
 }
 
+// ---- float-input variant (TMA 4:2:0 fast path).  Integer samples are
+// turned into floats with the magic-number trick: for 0 <= v < 2^23 the
+// float with bits 0x4B000000 | v is exactly 2^23 + v, and subtracting
+// (2^23 + offset) leaves the exact integer v - offset (one PRMT/LOP3 + one
+// FADD instead of an I2F).  Every later step works on exact small integers
+// until the colour FMAs, so the results equal the integer path bit for bit.
+constexpr uint32_t kMagicBits = 0x4B000000u;
+constexpr float kMagic = 8388608.0f;  // 2^23
+__device__ __forceinline__ float mag(uint32_t bits) { return __uint_as_float(bits); }
+// 4 packed samples -> 4 magic floats
+__device__ __forceinline__ void mag4(uint2 q, float *f)  // 16-bit
+{
+    f[0] = mag(__byte_perm(q.x, kMagicBits, 0x7610));
+    f[1] = mag(__byte_perm(q.x, kMagicBits, 0x7632));
+    f[2] = mag(__byte_perm(q.y, kMagicBits, 0x7610));
+    f[3] = mag(__byte_perm(q.y, kMagicBits, 0x7632));
+}
+__device__ __forceinline__ void mag4(uint32_t q, float *f)  // 8-bit
+{
+    f[0] = mag(__byte_perm(q, kMagicBits, 0x7650));
+    f[1] = mag(__byte_perm(q, kMagicBits, 0x7651));
+    f[2] = mag(__byte_perm(q, kMagicBits, 0x7652));
+    f[3] = mag(__byte_perm(q, kMagicBits, 0x7653));
+}
+__device__ __forceinline__ void mag8(uint4 q, float (&f)[kPx])  // 16-bit
+{
+    mag4(make_uint2(q.x, q.y), f);
+    mag4(make_uint2(q.z, q.w), f + 4);
+}
+__device__ __forceinline__ void mag8(uint2 q, float (&f)[kPx])  // 8-bit
+{
+    mag4(q.x, f);
+    mag4(q.y, f + 4);
+}
+
+// R', G', B' from dyv = code_Y - y_off/16, du = (16x upsampled Cb) - c_off,
+// dv likewise (all exact integers held in floats): the same arithmetic as
+// f2t_colour (Y' = 16*dyv*y_scale exactly), fp16 near-zero values in fp64.
+template <typename OUT>
+__device__ __forceinline__ void f2t_pixel_f(const F2TColour &c, float ys16, float dyv, float du, float dv, float &R,
+                                            float &G, float &B)
+{
+    const float Y = dyv * ys16;
+    R = fmaf(c.r_v, dv, Y);
+    B = fmaf(c.b_u, du, Y);
+    G = fmaf(-c.g_v, dv, fmaf(-c.g_u, du, Y));
+    if (sizeof(OUT) == 2) {
+        if (fabsf(R) < kF16Tiny || fabsf(G) < kF16Tiny || fabsf(B) < kF16Tiny) {
+            const double Yd = 16.0 * static_cast<double>(dyv) * c.y_scale_d;
+            const double Pb = static_cast<double>(du) * c.c_scale_d, Pr = static_cast<double>(dv) * c.c_scale_d;
+            R = __half2float(__double2half(Yd + c.r_pr_d * Pr));
+            G = __half2float(__double2half(Yd - c.g_pb_d * Pb - c.g_pr_d * Pr));
+            B = __half2float(__double2half(Yd + c.b_pb_d * Pb));
+        }
+    }
+}
+
 // Horizontal 2x upsample of one chroma row around an item's 8 columns:
 // c[0] = sample i0-1 (clamped), c[1..4] = i0..i0+3, c[5] = i0+4 (clamped).
 // Even luma column 2m: 3*c[m+1] + c[m];  odd 2m+1: 3*c[m+1] + c[m+2]

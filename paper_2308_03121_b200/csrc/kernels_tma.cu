@@ -538,34 +538,56 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                 OUT *orow = ob + (u * ROWS) * sw + (x - tl.x0);
                 if constexpr (FAMILY == kYUV420) {
                     if (fast && y0 + 1 < a.H) {
-                        // both luma rows of the pair inside the frame: rows
-                        // 2j and 2j+1 share the near chroma row j, whose
-                        // horizontal pass is done once (reading A5: row 2j
-                        // adds 3*near + far row j-1, row 2j+1 far row j+1)
+                        // both luma rows of the pair inside the frame (reading
+                        // A5: row 2j takes 3*row j + row j-1 of chroma, row
+                        // 2j+1 3*row j + row j+1, clamped; then (3/4, 1/4)
+                        // horizontally).  Chroma rows j-1, j, j+1 are
+                        // converted once (magic floats minus c_off/16, so the
+                        // weight-16 sums come out as us - c_off exactly) and
+                        // filtered vertically first.
                         const int j = y0 >> 1, i0 = x >> 1;
-                        int hn[2][kPx];
+                        const int jr[3] = {max(j - 1, 0), j, min(j + 1, ch - 1)};
+                        const float coff = kMagic + static_cast<float>(a.col.c_off >> 4);
+                        float cd[2][2][kPx];  // [plane][row of the pair][column]: chroma - c_off
 #pragma unroll
-                        for (int p = 0; p < 2; ++p)
-                            hup_row<IN, V4>(sg.chroma(st, p, j - tl.cy0) - tl.cw0, i0, cw, hn[p]);
+                        for (int p = 0; p < 2; ++p) {
+                            float f[3][6];
 #pragma unroll
-                        for (int r = 0; r < 2; ++r) {
-                            const int jf = r ? min(j + 1, ch - 1) : max(j - 1, 0);
-                            int ys[kPx], us[kPx], vs[kPx];
-                            unpack8(*reinterpret_cast<const V8 *>(sg.luma(st, y0 + r - tl.ly0) - tl.lw0 + x), ys);
+                            for (int q = 0; q < 3; ++q) {
+                                const IN *C = sg.chroma(st, p, jr[q] - tl.cy0) - tl.cw0;
+                                mag4(*reinterpret_cast<const V4 *>(C + i0), &f[q][1]);
+                                f[q][0] = mag(kMagicBits | C[max(i0 - 1, 0)]);
+                                f[q][5] = mag(kMagicBits | C[min(i0 + 4, cw - 1)]);
 #pragma unroll
-                            for (int p = 0; p < 2; ++p) {
-                                int hf[kPx];
-                                hup_row<IN, V4>(sg.chroma(st, p, jf - tl.cy0) - tl.cw0, i0, cw, hf);
-#pragma unroll
-                                for (int kk = 0; kk < kPx; ++kk) {
-                                    const int s2 = 3 * hn[p][kk] + hf[kk];
-                                    if (p == 0) us[kk] = s2; else vs[kk] = s2;
-                                }
+                                for (int t = 0; t < 6; ++t) f[q][t] -= coff;
                             }
 #pragma unroll
-                            for (int kk = 0; kk < kPx; ++kk) ys[kk] *= 16;
+                            for (int r = 0; r < 2; ++r) {
+                                float v[6];
+#pragma unroll
+                                for (int t = 0; t < 6; ++t) v[t] = fmaf(3.0f, f[1][t], f[r ? 2 : 0][t]);
+#pragma unroll
+                                for (int m = 0; m < 4; ++m) {
+                                    cd[p][r][2 * m] = fmaf(3.0f, v[m + 1], v[m]);
+                                    cd[p][r][2 * m + 1] = fmaf(3.0f, v[m + 1], v[m + 2]);
+                                }
+                            }
+                        }
+                        const float yoff = kMagic + static_cast<float>(a.col.y_off >> 4);
+                        const float ys16 = 16.0f * a.col.y_scale;
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            float dy[kPx];
+                            mag8(*reinterpret_cast<const V8 *>(sg.luma(st, y0 + r - tl.ly0) - tl.lw0 + x), dy);
+                            float R[kPx], G[kPx], B[kPx];
+#pragma unroll
+                            for (int kk = 0; kk < kPx; ++kk)
+                                f2t_pixel_f<OUT>(a.col, ys16, dy[kk] - yoff, cd[0][r][kk], cd[1][r][kk], R[kk], G[kk],
+                                                 B[kk]);
                             Row8<OUT> o3[3];
-                            f2t_row<FAMILY, OUT>(a.col, ys, us, vs, o3);
+                            o3[0].set(R);
+                            o3[1].set(G);
+                            o3[2].set(B);
 #pragma unroll
                             for (int c = 0; c < 3; ++c) o3[c].store(orow + (c * brows + r) * sw);
                         }
