@@ -15,6 +15,7 @@ Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every key).
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -46,6 +47,10 @@ def parse():
                    help="t2f converts only the outputs the emission schedule presents (NEXT-1; drops e.g. the "
                         "trailing enhanced lookahead of M = 2n+1 networks), pass-through frames are copied")
     p.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"])
+    p.add_argument("--tensors", default="rgb", choices=["rgb", "yuv"],
+                   help="network tensor format: RGB (default) or YUV-native luma + chroma tensors (NEXT-3)")
+    p.add_argument("--chroma-loc", default="center", choices=["center", "left"],
+                   help="4:2:0 chroma siting: centre (default) or LEFT / MPEG-2 (NEXT-3)")
     p.add_argument("--frames", type=int, default=0,
                    help="clip frames per rank (0 = the workload's; profiling/sweeps only, recorded in config)")
     p.add_argument("--no-e2e", action="store_true")
@@ -233,6 +238,11 @@ def main():
     cfg = w.cfg
     scaling = args.scaling if args.scaling != "auto" else ("strong" if args.workload == "c5" else "weak")
     total = (args.frames or w.frames) * (world if scaling == "weak" else 1)
+    yuv = args.tensors == "yuv"
+    if yuv:
+        cfg = dataclasses.replace(cfg, flags=cfg.flags | nv.YUV_INPUT | nv.YUV_OUTPUT)
+    if args.chroma_loc == "left":
+        cfg = dataclasses.replace(cfg, chroma_loc=nv.CHROMA_LEFT)
     h = nv.open(cfg)
     N, M = h.N, h.M
     L = 0 if cfg.flags else ((N - 1) // 2 if cfg.left_context == -1 else cfg.left_context)
@@ -255,6 +265,12 @@ def main():
     esz = 2 if cfg.dtype == nv.F16 else 4
     in_elems = int(np.prod(in_shape))
     out_elems = int(np.prod(out_shape))
+    # YUV-native tensors: luma [1, N, Hp, Wp] + chroma [1, 2N, Hc, Wc] per tuple
+    # (in_shape / out_shape are the luma tensors), separate buffers
+    in_c = int(np.prod(h.in_chroma_shape)) if yuv else 0
+    out_c = int(np.prod(h.out_chroma_shape)) if yuv else 0
+    in_l, out_l = in_elems, out_elems
+    in_elems, out_elems = in_l + in_c, out_l + out_c
     Ho, Wo = out_shape[2], out_shape[3]
     olay = w.out_layout()
     t2f_bytes = out_elems * esz + M * olay.payload_bytes()
@@ -267,6 +283,12 @@ def main():
     n_out = max(tchunk, -(-4 * l2 // (out_elems * esz)))
     tens_in = torch.empty((fchunk, in_elems), dtype=tdt, device=dev)
     tens_out = synth.random_tensor((n_out, out_elems), cfg.dtype, w.seed + 99, device=dev)
+    if yuv:
+        if args.f2t_mode != "materialize":
+            raise SystemExit("--tensors yuv supports --f2t-mode materialize only")
+        tin_l, tin_c = torch.empty((fchunk, in_l), dtype=tdt, device=dev), torch.empty((fchunk, in_c), dtype=tdt, device=dev)
+        tout_l = synth.random_tensor((n_out, out_l), cfg.dtype, w.seed + 99, device=dev)
+        tout_c = synth.random_tensor((n_out, out_c), cfg.dtype, w.seed + 98, device=dev)
     ofb = FrameBuffer(olay, tchunk * M, device=dev)
     ofb_desc = ofb.descriptors()
     store = None
@@ -342,8 +364,15 @@ def main():
             else:
                 for c0 in range(0, len(runs), fchunk):
                     sel = runs[c0:c0 + fchunk]
-                    timed("f2t", record, len(sel), len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz,
-                          lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
+                    nbytes = len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz
+                    if yuv:
+                        timed("f2t", record, len(sel), nbytes,
+                              lambda sel=sel: h.frames_to_tensor_yuv_batch(sel, tin_l.data_ptr(), in_l * esz,
+                                                                           tin_c.data_ptr(), in_c * esz, stream))
+                    else:
+                        timed("f2t", record, len(sel), nbytes,
+                              lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz,
+                                                                       stream))
             sched = h.schedule_outputs(cut_win.cpu().numpy())[s.begin - s.window_first:] if args.emit else None
             for c0 in range(0, len(runs), tchunk):
                 nb = min(tchunk, len(runs) - c0)
@@ -362,9 +391,15 @@ def main():
                             else:
                                 copies.append((int(runs[c0 + j][-src - 1]), ofb_desc[j * M]))
                 nbytes = nconv * (out_elems // M * esz + olay.payload_bytes())
-                timed("t2f", record, nb, nbytes,
-                      lambda o0=o0, nb=nb, desc=desc: h.tensor_to_frames_batch(tens_out[o0].data_ptr(), out_elems * esz,
-                                                                              Ho, Wo, desc, nb, stream))
+                if yuv:
+                    timed("t2f", record, nb, nbytes,
+                          lambda o0=o0, nb=nb, desc=desc: h.tensor_to_frames_yuv_batch(
+                              tout_l[o0].data_ptr(), out_l * esz, tout_c[o0].data_ptr(), out_c * esz, Ho, Wo, desc,
+                              nb, stream))
+                else:
+                    timed("t2f", record, nb, nbytes,
+                          lambda o0=o0, nb=nb, desc=desc: h.tensor_to_frames_batch(
+                              tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo, desc, nb, stream))
                 if copies:
                     h.copy_frames([c[0] for c in copies], [c[1] for c in copies], stream)
         return len(runs)
@@ -435,7 +470,7 @@ def main():
 
     # ---- e2e: host (pinned) frames in, host frames out, through the C ABI
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not yuv:
         e2e = run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, min(8, fchunk, tchunk), in_elems,
                       out_elems, esz, stream, dev, world, plan_local, scaling, frames_all)
 
@@ -456,6 +491,9 @@ def main():
                        "clip_frames_per_rank": s.owned, "input_tensor": list(in_shape),
                        "output_tensor": list(out_shape), "tensor_dtype": "f16" if cfg.dtype == nv.F16 else "f32",
                        "tuples_per_launch": {"f2t": fchunk, "t2f": tchunk}, "f2t_mode": args.f2t_mode,
+                       "tensors": ("YUV-native: luma %s + chroma %s per tuple" % (list(in_shape), list(h.in_chroma_shape))
+                                   if yuv else "RGB"),
+                       "chroma_loc": args.chroma_loc,
                        "t2f_outputs": "emitted only (NEXT-1 schedule)" if args.emit else "all M slots per tuple",
                        "scene_flags": ("detected on the GPU each step (threshold %g)" % args.detect_threshold
                                        if args.detect else "given (synthetic cut pattern)"),
