@@ -525,6 +525,19 @@ __device__ __forceinline__ void tload8_stream(const float *p, float (&x)[kPx])
 {
     tunpack8(ld_stream_v4(p), ld_stream_v4(p + 4), x);
 }
+// 4 tensor values from shared memory (8-byte aligned fp16, 16-byte fp32)
+__device__ __forceinline__ void tload4s(const __half *p, float (&x)[4])
+{
+    const uint2 v = *reinterpret_cast<const uint2 *>(p);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&v.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&v.y));
+    x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+}
+__device__ __forceinline__ void tload4s(const float *p, float (&x)[4])
+{
+    const float4 v = *reinterpret_cast<const float4 *>(p);
+    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+}
 __device__ __forceinline__ float tload1(const __half *p) { return __half2float(p[0]); }
 __device__ __forceinline__ float tload1(const float *p) { return p[0]; }
 

@@ -794,6 +794,145 @@ __global__ void __launch_bounds__(kThreads + 32, (FAMILY == kYUV420 && sizeof(AR
     }
 }
 
+// ------------------------------------------------------------------ t2f, YUV-native tensors
+// NEXT-3 (§3.1, reading A22): the network's output is a
+// luma tensor [M][th][tw] and a chroma tensor [2M][thc][twc]; step B4 only
+// (scale, RNE, clamp).  Same pipeline as t2f_tma; a stage holds the tile's
+// ROWS luma rows and its chroma row of each plane (4:2:0: half width, the
+// row unit's chroma row):  [ROWS][segw] luma | [2][segwc] chroma.
+template <int FAMILY, typename TIN>
+__device__ __forceinline__ void t2f_yuv_issue(const T2FArgs &a, int64_t t, uint8_t *st, uint64_t *bar, T2FHdr *hdr)
+{
+    constexpr bool SUB = FAMILY == kYUV420;
+    constexpr int ROWS = SUB ? 2 : 1;
+    if (t < 0) {
+        hdr->job = -1;
+        mbar_arrive(bar);
+        return;
+    }
+    int job, ru, x0;
+    decode_tile(t, a.rowunits, a.nseg, a.segw, job, ru, x0);
+    const int x1 = min(x0 + a.segw, a.Wo);
+    int tup, o;
+    t2f_job(a, job, tup, o);
+    *hdr = T2FHdr{job, ru * ROWS, x0, x1};
+    const int segwc = SUB ? a.segw >> 1 : a.segw;
+    const int64_t lplane = a.th * a.tw, cplane = a.thc * a.twc;
+    const TIN *ls = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
+                    static_cast<int64_t>(o) * lplane + static_cast<int64_t>(ru * ROWS) * a.tw + x0;
+    const int cy = SUB ? ru : ru * ROWS, cx0 = SUB ? x0 >> 1 : x0;
+    const TIN *cs = reinterpret_cast<const TIN *>(a.src2 + static_cast<int64_t>(tup) * a.tensor_stride2) +
+                    static_cast<int64_t>(2 * o) * cplane + static_cast<int64_t>(cy) * a.twc + cx0;
+    const uint32_t lb = (x1 - x0) * sizeof(TIN), cb = (SUB ? (x1 - x0) >> 1 : x1 - x0) * sizeof(TIN);
+    mbar_arrive_expect_tx(bar, ROWS * lb + 2 * cb);
+    TIN *sv = reinterpret_cast<TIN *>(st);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) bulk_g2s(sv + r * a.segw, ls + r * a.tw, lb, bar);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) bulk_g2s(sv + ROWS * a.segw + p * segwc, cs + p * cplane, cb, bar);
+}
+
+template <int FAMILY, typename OS, typename TIN, typename AR>
+__global__ void __launch_bounds__(kThreads + 32, (FAMILY == kYUV420 && sizeof(AR) == 8) ? 2 : 3)
+    t2f_yuv_tma(const T2FArgs a)
+{
+    constexpr bool SUB = FAMILY == kYUV420;
+    constexpr int ROWS = SUB ? 2 : 1, NC = SUB ? 4 : 8;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + kMaxStages;
+    T2FHdr *hdr = reinterpret_cast<T2FHdr *>(empty + kMaxStages);
+    uint8_t *stages = smem + kBarBytes;
+    const int nst = a.stages, nct = a.cthreads;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < nst; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], nct / 32);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (threadIdx.x >= nct) {  // ---------------- producer lane
+        if (threadIdx.x != nct) return;
+        TileSource ts;
+        ts.init(a.tile_counter, a.tiles);
+        int k = 0;
+        uint32_t rnd = 0;
+        for (int64_t i = 0;; ++i) {
+            if (i >= nst) {
+                mbar_wait(&empty[k], rnd ^ 1u);
+                fence_proxy_async();
+            }
+            const int64_t t = ts.fetch();
+            t2f_yuv_issue<FAMILY, TIN>(a, t, stages + k * a.stage_bytes, &full[k], &hdr[k]);
+            if (t < 0) break;
+            if (++k == nst) {
+                k = 0;
+                rnd ^= 1u;
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------ consumers
+    const T2FConst<AR> c(a.col);
+    const int segwc = SUB ? a.segw >> 1 : a.segw;
+    int cj = -1;
+    DevFrame f;
+    const int xo = kPx * threadIdx.x;
+    int k = 0;
+    uint32_t fph = 0;
+    for (;;) {
+        const TIN *sv = reinterpret_cast<const TIN *>(stages + k * a.stage_bytes);
+        mbar_wait(&full[k], fph);
+        const T2FHdr h = hdr[k];
+        if (h.job < 0) break;
+        if (h.job != cj) {
+            cj = h.job;
+            f = load_frame(a.out + cj);
+        }
+        if (h.x0 + xo < h.x1) {
+            const int x = h.x0 + xo;
+            // luma: code = rne(clamp(Y' * ys + yo))
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+                float v[kPx];
+                tload8(sv + r * a.segw + xo, v);
+                uint32_t q[kPx];
+#pragma unroll
+                for (int kk = 0; kk < kPx; ++kk) q[kk] = quant_direct(static_cast<AR>(v[kk]), c.yd, c.yod, c.maxc);
+                store_samples8(row_ptr_w<OS>(f, 0, h.y0 + r) + x, q);
+            }
+            // chroma: code = rne(clamp(U * cs + (co - cs/2)))  (reading A22)
+            const int cxo = SUB ? xo >> 1 : xo, cy = SUB ? h.y0 >> 1 : h.y0, cx = SUB ? x >> 1 : x;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const TIN *cp_ = sv + ROWS * a.segw + p * segwc + cxo;
+                uint32_t q[NC];
+                if constexpr (NC == 8) {
+                    float v[8];
+                    tload8(cp_, v);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) q[kk] = quant_direct(static_cast<AR>(v[kk]), c.csd, c.co2d, c.maxc);
+                    store_samples8(row_ptr_w<OS>(f, 1 + p, cy) + cx, q);
+                } else {
+                    float v[4];
+                    tload4s(cp_, v);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) q[kk] = quant_direct(static_cast<AR>(v[kk]), c.csd, c.co2d, c.maxc);
+                    store_samples4(row_ptr_w<OS>(f, 1 + p, cy) + cx, q);
+                }
+            }
+        }
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[k]);
+        if (++k == nst) {
+            k = 0;
+            fph ^= 1u;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ launch
 int sms()
 {
@@ -816,7 +955,7 @@ int env_int(const char *name, int dflt)
 // output staging buffers).  Stages: `default_stages` (tools/sweep_t2f.sh on
 // B200, profiles/r01/t2f_sweep.txt), else as many as fit in `budget`.
 template <typename K, typename A>
-cudaError_t launch_tma(K kernel, A a, int rows, int elem, int budget, int default_stages, cudaStream_t s)
+cudaError_t launch_tma(K kernel, A a, int vals_per_col, int elem, int budget, int default_stages, cudaStream_t s)
 {
     if (a.tiles <= 0) return cudaSuccess;
     // equal segments of a multiple of 32 columns (<= 2048): no thin tail tile;
@@ -824,7 +963,7 @@ cudaError_t launch_tma(K kernel, A a, int rows, int elem, int budget, int defaul
     // consumer threads are the tile's 8-column groups (whole warps)
     a.segw = std::min(kSegW, ((a.Wo + a.nseg - 1) / a.nseg + 31) / 32 * 32);
     a.cthreads = std::min(kThreads, (a.segw / kPx + 31) / 32 * 32);
-    a.stage_bytes = (rows * 3 * a.segw * elem + 127) / 128 * 128;
+    a.stage_bytes = (vals_per_col * a.segw * elem + 127) / 128 * 128;
     budget = env_int("NNVISR_T2F_SMEM_KB", budget / 1024) * 1024;
     a.stages = env_int("NNVISR_T2F_STAGES", default_stages);
     if (a.stages <= 0) a.stages = budget / a.stage_bytes;
@@ -975,18 +1114,41 @@ cudaError_t t2f_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t
     constexpr int R = FAMILY == kYUV420 ? 2 : 1, kBudget = 50 * 1024;
     const int st = env_int("NNVISR_T2F_STAGES", 0);
     if (bits == 8) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, R, 2, kBudget, st, s);
-        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, R, 4, kBudget, st, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, 3 * R, 2, kBudget, st, s);
+        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, 3 * R, 4, kBudget, st, s);
     }
     if (bits == 10) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, R, 2, kBudget, st, s);
-        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, R, 4, kBudget, st, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, 3 * R, 2, kBudget, st, s);
+        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, 3 * R, 4, kBudget, st, s);
     }
-    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, R, 2, kBudget, st, s);
-    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, R, 4, kBudget, st, s);
+    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, 3 * R, 2, kBudget, st, s);
+    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, 3 * R, 4, kBudget, st, s);
+}
+
+template <int FAMILY>
+cudaError_t t2f_yuv_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t s)
+{
+    constexpr int V = 3, kBudget = 50 * 1024;  // values per column: ROWS luma + 2 chroma (halved for 4:2:0)
+    const int st = env_int("NNVISR_T2F_STAGES", 0);
+    if (bits == 8) {
+        if (dtype == kF16) return launch_tma(t2f_yuv_tma<FAMILY, uint8_t, __half, float>, a, V, 2, kBudget, st, s);
+        return launch_tma(t2f_yuv_tma<FAMILY, uint8_t, float, float>, a, V, 4, kBudget, st, s);
+    }
+    if (bits == 10) {
+        if (dtype == kF16) return launch_tma(t2f_yuv_tma<FAMILY, uint16_t, __half, float>, a, V, 2, kBudget, st, s);
+        return launch_tma(t2f_yuv_tma<FAMILY, uint16_t, float, float>, a, V, 4, kBudget, st, s);
+    }
+    if (dtype == kF16) return launch_tma(t2f_yuv_tma<FAMILY, uint16_t, __half, double>, a, V, 2, kBudget, st, s);
+    return launch_tma(t2f_yuv_tma<FAMILY, uint16_t, float, double>, a, V, 4, kBudget, st, s);
 }
 
 }  // namespace
+
+cudaError_t launch_t2f_yuv_tma(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s)
+{
+    if (family == kYUV420) return t2f_yuv_tma_dispatch<kYUV420>(bits, dtype, a, s);
+    return t2f_yuv_tma_dispatch<kYUV444>(bits, dtype, a, s);
+}
 
 cudaError_t launch_f2t_tma(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s)
 {

@@ -290,6 +290,7 @@ cudaError_t launch_f2t_yuv(int family, int bits, int dtype, const F2TArgs &a, cu
 
 cudaError_t launch_t2f_yuv(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s)
 {
+    if (a.tma_ok && (family == kYUV420 || family == kYUV444)) return launch_t2f_yuv_tma(family, bits, dtype, a, s);
     if (family == kYUV420) return t2f_family<kYUV420>(bits, dtype, a, s);
     if (family == kYUV444) return t2f_family<kYUV444>(bits, dtype, a, s);
     return cudaErrorInvalidValue;

@@ -655,8 +655,12 @@ nnvisr_status run_t2f(nnvisr_handle *h, T2FArgs a, int64_t jobs, cudaStream_t st
     a.rowunits = (int32_t)(h->Ho / rows);
     a.nseg = (int32_t)((h->Wo + kThreads * kPx - 1) / (kThreads * kPx));
     a.tiles = jobs * a.rowunits * a.nseg;
+    // YUV-native tensors (NEXT-3): the chroma rows staged by TMA must be
+    // 16-byte aligned too (their base, strides and rows)
+    const bool yuv_ok = !a.yuv || (reinterpret_cast<uintptr_t>(a.src2) % 16 == 0 && a.tensor_stride2 % 16 == 0 &&
+                                   (a.thc * a.twc * h->elem) % 16 == 0 && (a.twc * h->elem) % 16 == 0);
     a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wo % 32 == 0 && a.tensor_stride % 16 == 0 &&
-               !a.yuv && !a.left;
+               reinterpret_cast<uintptr_t>(a.src) % 16 == 0 && yuv_ok && !a.left;
     cudaError_t e = launch_t2f(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "t2f kernel launch");
     return NNVISR_OK;

@@ -309,3 +309,43 @@ def test_yuv_calls_reject_wrong_handle():
         with pytest.raises(nv.NnvisrError) as e:
             h.tensor_to_frames_yuv_batch(x.data_ptr(), 0, x.data_ptr(), 0, 16, 32, [nv.Frame()], 1)
         assert "YUV_OUTPUT" in e.value.message
+
+
+@pytest.mark.parametrize("family,bits,dtype", YUV_CASES)
+@pytest.mark.parametrize("W,H,sx,pad", [(256, 24, (1, 1), 0), (128, 12, (2, 1), 32), (2080, 8, (1, 1), 0)])
+def test_yuv_t2f_tma_parity(family, bits, dtype, W, H, sx, pad, monkeypatch):
+    """YUV-native tensors at 16-byte aligned geometries (the TMA-pipelined
+    t2f_yuv_tma path: output width a multiple of 32, aligned tensor rows;
+    2080 columns = two segments) against the oracle, and bit-identical to
+    the generic kernel (NNVISR_FORCE_GENERIC=1) on the same inputs."""
+    rs = np.random.default_rng(1300 + bits + 3 * family + dtype + W)
+    sub = family == nv.YUV420
+    matrix, rng_ = ((nv.BT709, nv.LIMITED), (nv.BT2020, nv.FULL))[int(rs.integers(2))]
+    cfg = _cfg(family, bits, dtype, matrix, rng_, W, H, M=3, sx=sx, flags=nv.YUV_OUTPUT)
+    outs = []
+    for generic in (False, True):
+        if generic:
+            monkeypatch.setenv("NNVISR_FORCE_GENERIC", "1")
+        with nv.open(cfg) as h:
+            M = h.M
+            Ho, Wo = h.out_shape[2], h.out_shape[3]
+            th, tw = Ho + 2, Wo + pad
+            thc, twc = (th // 2, tw // 2) if sub else (th, tw)
+            C = 2
+            luma = synth.random_tensor((C, M, th, tw), dtype, 77 + W, device=DEV)
+            chroma = synth.random_tensor((C, 2 * M, thc, twc), dtype, 78 + W, device=DEV)
+            olay = FrameLayout(Wo, Ho, family, bits)
+            out = FrameBuffer(olay, C * M, device=DEV)
+            h.tensor_to_frames_yuv_batch(luma.data_ptr(), luma[0].numel() * luma.element_size(), chroma.data_ptr(),
+                                         chroma[0].numel() * chroma.element_size(), th, tw, out.descriptors(), C)
+            torch.cuda.synchronize()
+            outs.append(out.data.clone())
+            if not generic:
+                stats = CodeStats()
+                for c in range(C):
+                    ref = O.t2f_yuv(luma[c:c + 1].cpu().numpy(), chroma[c:c + 1].cpu().numpy(), M, Wo, Ho, family,
+                                    bits, matrix, rng_)
+                    for o in range(M):
+                        stats.add(out.host_planes(c * M + o), ref[o], f"yuv t2f tma {W}x{H} {c} {o}")
+                stats.check(f"yuv t2f tma fam={family} bits={bits}")
+    assert torch.equal(outs[0], outs[1])
