@@ -325,6 +325,33 @@ template <> struct Row8<float> {
     }
 };
 
+// 4 packed tensor values of one chroma row
+template <typename OUT> struct Row4;
+template <> struct Row4<__half> {
+    uint2 v;
+    __device__ __forceinline__ void set(const float (&x)[4]) { v = make_uint2(pack_half2(x[0], x[1]), pack_half2(x[2], x[3])); }
+    __device__ __forceinline__ void store(__half *p) const { *reinterpret_cast<uint2 *>(p) = v; }
+    __device__ __forceinline__ void store_n(__half *p, int n) const
+    {
+        const uint32_t w[2] = {v.x, v.y};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < n) reinterpret_cast<uint16_t *>(p)[k] = static_cast<uint16_t>(w[k >> 1] >> (16 * (k & 1)));
+    }
+};
+template <> struct Row4<float> {
+    float4 v;
+    __device__ __forceinline__ void set(const float (&x)[4]) { v = make_float4(x[0], x[1], x[2], x[3]); }
+    __device__ __forceinline__ void store(float *p) const { *reinterpret_cast<float4 *>(p) = v; }
+    __device__ __forceinline__ void store_n(float *p, int n) const
+    {
+        const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < n) p[k] = x[k];
+    }
+};
+
 // One row of 16x codes -> the three packed channel rows.
 template <int FAMILY, typename OUT>
 __device__ __forceinline__ void f2t_row(const F2TColour &c, const int (&ys)[kPx], const int (&us)[kPx],

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -330,7 +331,7 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
 // (acquire) instead of decoding the tile index themselves.
 // Output buffer layout: [channel][B*ROWS rows][sw]: with a single segment a
 // channel's band rows are contiguous in the tensor too, one bulk store each.
-template <int FAMILY, typename IN, typename OUT, bool LOADER>
+template <int FAMILY, typename IN, typename OUT, bool LOADER, bool YUVN>
 __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2) f2t_tma(const F2TArgs a)
 {
     using S = F2TStage<FAMILY, IN>;
@@ -470,6 +471,35 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                 OUT *o = reinterpret_cast<OUT *>(a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride +
                                                  static_cast<int64_t>(cd & 31) * a.slot_bytes) +
                          static_cast<int64_t>(tl.u0 * ROWS) * a.Wp + tl.x0;
+                if constexpr (YUVN) {
+                    // luma rows to the luma tensor; the row units' chroma rows
+                    // (one per unit) to the two chroma planes of dst2
+                    constexpr bool SUB = FAMILY == kYUV420;
+                    const int swc = SUB ? sw >> 1 : sw;
+                    if (whole_rows) {
+                        bulk_s2g(o, ob, rows * sw * sizeof(OUT));
+                    } else {
+                        for (int rr = 0; rr < rows; ++rr)
+                            bulk_s2g(o + static_cast<int64_t>(rr) * a.Wp, ob + rr * sw, sw * sizeof(OUT));
+                    }
+                    char *cb = a.dst2 + static_cast<int64_t>(cd >> 5) * a.run_stride2 +
+                               static_cast<int64_t>(cd & 31) * a.slot_bytes2;
+                    const OUT *oc = ob + brows * sw;
+                    for (int pc = 0; pc < 2; ++pc) {
+                        OUT *q = reinterpret_cast<OUT *>(cb + pc * a.cplane_bytes) +
+                                 static_cast<int64_t>(tl.u0) * a.Wc + (SUB ? tl.x0 >> 1 : tl.x0);
+                        const OUT *src = oc + pc * a.band * swc;
+                        if (whole_rows) {
+                            bulk_s2g(q, src, tl.nu * swc * sizeof(OUT));
+                        } else {
+                            for (int rr = 0; rr < tl.nu; ++rr)
+                                bulk_s2g(q + static_cast<int64_t>(rr) * a.Wc, src + rr * swc, swc * sizeof(OUT));
+                        }
+                    }
+                    bulk_commit();
+                    ++ng;
+                    continue;
+                }
                 for (int c = 0; c < 3; ++c) {
                     if (whole_rows) {
                         bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
@@ -532,7 +562,60 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
         const bool fast = x + kPx <= a.W;
         if (i >= nob) mbar_wait(&ofree[b], bround ^ 1u);
         NNVISR_TRACE(threadIdx.x == 0, 2, i);
-        if (x < tl.x1 && !(a.debug & 1)) {
+        if constexpr (YUVN) {
+            // YUV-native tensors (NEXT-3, reading A22): no matrix, no
+            // resampling: luma Y' = (16c - y_off) * y_scale, chroma
+            // U = (16c - u_off) * c_scale of the unit's own chroma row, each
+            // one exact integer offset and one fp32 rounding
+            constexpr bool SUB = FAMILY == kYUV420;
+            constexpr int NC = SUB ? 4 : kPx;
+            using RowC = typename std::conditional<SUB, Row4<OUT>, Row8<OUT>>::type;
+            const int swc = SUB ? sw >> 1 : sw, cx = SUB ? x >> 1 : x, cwid = SUB ? cw : a.W;
+            if (x < tl.x1) {
+                for (int u = 0; u < tl.nu; ++u) {
+#pragma unroll
+                    for (int r = 0; r < ROWS; ++r) {
+                        const int yc = min((tl.u0 + u) * ROWS + r, a.H - 1);
+                        const IN *L = (SUB ? sg.luma(st, yc - tl.ly0) : sg.plane(st, 0, yc - tl.ly0)) - tl.lw0;
+                        int c[kPx];
+                        if (fast) {
+                            unpack8(*reinterpret_cast<const V8 *>(L + x), c);
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < kPx; ++kk) c[kk] = L[min(x + kk, a.W - 1)];
+                        }
+                        float v[kPx];
+#pragma unroll
+                        for (int kk = 0; kk < kPx; ++kk)
+                            v[kk] = static_cast<float>(16 * c[kk] - a.col.y_off) * a.col.y_scale;
+                        Row8<OUT> o1;
+                        o1.set(v);
+                        o1.store(ob + (u * ROWS + r) * sw + (x - tl.x0));
+                    }
+                    const int jc = SUB ? min(tl.u0 + u, ch - 1) : min(tl.u0 + u, a.H - 1);
+#pragma unroll
+                    for (int pc = 0; pc < 2; ++pc) {
+                        const IN *Cr = (SUB ? sg.chroma(st, pc, jc - tl.cy0) - tl.cw0
+                                            : sg.plane(st, 1 + pc, jc - tl.ly0) - tl.lw0);
+                        int c[NC];
+                        if (fast) {
+                            if constexpr (SUB) unpack4(*reinterpret_cast<const V4 *>(Cr + cx), c);
+                            else unpack8(*reinterpret_cast<const V8 *>(Cr + cx), c);
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < NC; ++kk) c[kk] = Cr[min(cx + kk, cwid - 1)];
+                        }
+                        float v[NC];
+#pragma unroll
+                        for (int kk = 0; kk < NC; ++kk)
+                            v[kk] = static_cast<float>(16 * c[kk] - a.col.u_off) * a.col.c_scale;
+                        RowC oc;
+                        oc.set(v);
+                        oc.store(ob + brows * sw + (pc * a.band + u) * swc + (cx - (SUB ? tl.x0 >> 1 : tl.x0)));
+                    }
+                }
+            }
+        } else if (x < tl.x1 && !(a.debug & 1)) {
             for (int u = 0; u < tl.nu; ++u) {
                 const int y0 = (tl.u0 + u) * ROWS;
                 OUT *orow = ob + (u * ROWS) * sw + (x - tl.x0);
@@ -985,7 +1068,7 @@ cudaError_t launch_tma(K kernel, A a, int vals_per_col, int elem, int budget, in
 // run time from the segment width min(2048, Wp), to keep two CTAs per SM
 // (<= 112 KB each) with 3 output buffers where they fit (more bulk stores in
 // flight), else 2.
-template <int FAMILY, typename IN, typename OUT>
+template <int FAMILY, typename IN, typename OUT, bool YUVN>
 cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
 {
     using S = F2TStage<FAMILY, IN>;
@@ -1054,7 +1137,7 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     a.release_first = env_int("NNVISR_F2T_RELFIRST", fits2 ? 1 : 0);
     a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
     int loader = env_int("NNVISR_F2T_LOADER", fits2 ? 0 : 1);
-    auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true> : f2t_tma<FAMILY, IN, OUT, false>;
+    auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true, YUVN> : f2t_tma<FAMILY, IN, OUT, false, YUVN>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -1095,15 +1178,15 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     return cudaGetLastError();
 }
 
-template <int FAMILY>
+template <int FAMILY, bool YUVN = false>
 cudaError_t f2t_tma_dispatch(int bits, int dtype, const F2TArgs &a, cudaStream_t s)
 {
     if (bits == 8) {
-        if (dtype == kF16) return f2t_tma_launch<FAMILY, uint8_t, __half>(a, s);
-        return f2t_tma_launch<FAMILY, uint8_t, float>(a, s);
+        if (dtype == kF16) return f2t_tma_launch<FAMILY, uint8_t, __half, YUVN>(a, s);
+        return f2t_tma_launch<FAMILY, uint8_t, float, YUVN>(a, s);
     }
-    if (dtype == kF16) return f2t_tma_launch<FAMILY, uint16_t, __half>(a, s);
-    return f2t_tma_launch<FAMILY, uint16_t, float>(a, s);
+    if (dtype == kF16) return f2t_tma_launch<FAMILY, uint16_t, __half, YUVN>(a, s);
+    return f2t_tma_launch<FAMILY, uint16_t, float, YUVN>(a, s);
 }
 
 template <int FAMILY>
@@ -1143,6 +1226,12 @@ cudaError_t t2f_yuv_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStre
 }
 
 }  // namespace
+
+cudaError_t launch_f2t_yuv_tma(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s)
+{
+    if (family == kYUV420) return f2t_tma_dispatch<kYUV420, true>(bits, dtype, a, s);
+    return f2t_tma_dispatch<kYUV444, true>(bits, dtype, a, s);
+}
 
 cudaError_t launch_t2f_yuv_tma(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s)
 {

@@ -24,33 +24,6 @@ namespace nnvisr {
 namespace {
 using namespace dev;
 
-// 4 packed tensor values of one chroma row
-template <typename OUT> struct Row4;
-template <> struct Row4<__half> {
-    uint2 v;
-    __device__ __forceinline__ void set(const float (&x)[4]) { v = make_uint2(pack_half2(x[0], x[1]), pack_half2(x[2], x[3])); }
-    __device__ __forceinline__ void store(__half *p) const { *reinterpret_cast<uint2 *>(p) = v; }
-    __device__ __forceinline__ void store_n(__half *p, int n) const
-    {
-        const uint32_t w[2] = {v.x, v.y};
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (k < n) reinterpret_cast<uint16_t *>(p)[k] = static_cast<uint16_t>(w[k >> 1] >> (16 * (k & 1)));
-    }
-};
-template <> struct Row4<float> {
-    float4 v;
-    __device__ __forceinline__ void set(const float (&x)[4]) { v = make_float4(x[0], x[1], x[2], x[3]); }
-    __device__ __forceinline__ void store(float *p) const { *reinterpret_cast<float4 *>(p) = v; }
-    __device__ __forceinline__ void store_n(float *p, int n) const
-    {
-        const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (k < n) p[k] = x[k];
-    }
-};
-
 template <int NC> struct RowN;
 template <> struct RowN<4> { template <typename OUT> using T = Row4<OUT>; };
 template <> struct RowN<8> { template <typename OUT> using T = Row8<OUT>; };
@@ -283,6 +256,7 @@ cudaError_t t2f_family(int bits, int dtype, const T2FArgs &a, cudaStream_t s)
 
 cudaError_t launch_f2t_yuv(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s)
 {
+    if (a.tma_ok && (family == kYUV420 || family == kYUV444)) return launch_f2t_yuv_tma(family, bits, dtype, a, s);
     if (family == kYUV420) return f2t_family<kYUV420>(bits, dtype, a, s);
     if (family == kYUV444) return f2t_family<kYUV444>(bits, dtype, a, s);
     return cudaErrorInvalidValue;

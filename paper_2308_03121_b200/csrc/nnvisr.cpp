@@ -591,7 +591,14 @@ nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, int64_t dests, 
     a.rowunits = (int32_t)(h->Hp / rows);
     a.nseg = (int32_t)((h->Wp + kThreads * kPx - 1) / (kThreads * kPx));
     a.tiles = jobs * a.rowunits * a.nseg;
-    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->fmt.width % 32 == 0 && !a.yuv && !a.left;
+    // YUV-native tensors (NEXT-3): the chroma rows written by bulk stores
+    // must be 16-byte aligned too
+    const bool yuv_ok = !a.yuv || (reinterpret_cast<uintptr_t>(a.dst2) % 16 == 0 && a.run_stride2 % 16 == 0 &&
+                                   a.slot_bytes2 % 16 == 0 && a.cplane_bytes % 16 == 0 &&
+                                   (a.Wc * h->elem) % 16 == 0);
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->fmt.width % 32 == 0 &&
+               reinterpret_cast<uintptr_t>(a.dst) % 16 == 0 && a.run_stride % 16 == 0 && a.slot_bytes % 16 == 0 &&
+               yuv_ok && !a.left;
     cudaError_t e = launch_f2t(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "f2t kernel launch");
     return NNVISR_OK;

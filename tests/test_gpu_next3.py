@@ -349,3 +349,46 @@ def test_yuv_t2f_tma_parity(family, bits, dtype, W, H, sx, pad, monkeypatch):
                         stats.add(out.host_planes(c * M + o), ref[o], f"yuv t2f tma {W}x{H} {c} {o}")
                 stats.check(f"yuv t2f tma fam={family} bits={bits}")
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("family,bits,dtype", YUV_CASES)
+@pytest.mark.parametrize("W,H,align", [(256, 12, 16), (2080, 6, 32)])
+def test_yuv_f2t_tma_parity(family, bits, dtype, W, H, align, monkeypatch):
+    """YUV-native input tensors at 16-byte aligned geometries (the
+    TMA-pipelined f2t_tma<..., YUVN> path; 2080 columns = two segments,
+    padding rows/columns replicated per plane) against the oracle, and
+    bit-identical to the generic kernel (NNVISR_FORCE_GENERIC=1)."""
+    rs = np.random.default_rng(1700 + bits + 3 * family + dtype + W)
+    matrix, rng_ = ((nv.BT709, nv.LIMITED), (nv.BT2020, nv.FULL))[int(rs.integers(2))]
+    cfg = _cfg(family, bits, dtype, matrix, rng_, W, H, N=3, align=align, flags=nv.YUV_INPUT)
+    lay = FrameLayout(W, H, family, bits)
+    host = [synth.random_planes(lay, int(rs.integers(1 << 30))) for _ in range(4)]
+    runs = np.array([[0, 1, 1], [3, 3, 2], [2, 0, 1]], np.int64)
+    res = []
+    for generic in (False, True):
+        if generic:
+            monkeypatch.setenv("NNVISR_FORCE_GENERIC", "1")
+        buf = FrameBuffer(lay, 4, device=DEV)
+        for i, p in enumerate(host):
+            buf.set_planes(i, p)
+        with nv.open(cfg) as h:
+            _, N, Hp, Wp = h.in_shape
+            _, _, Hc, Wc = h.in_chroma_shape
+            nl, nc = N * Hp * Wp, 2 * N * Hc * Wc
+            luma = torch.full((3, -(-nl // 8) * 8), float("nan"), dtype=_tdt(dtype), device=DEV)
+            chroma = torch.full((3, -(-nc // 8) * 8), float("nan"), dtype=_tdt(dtype), device=DEV)
+            h.bind_frames(buf.descriptors())
+            h.frames_to_tensor_yuv_batch(runs, luma.data_ptr(), luma.shape[1] * luma.element_size(),
+                                         chroma.data_ptr(), chroma.shape[1] * chroma.element_size())
+            torch.cuda.synchronize()
+            res.append((luma.clone(), chroma.clone()))
+            if not generic:
+                for r in range(3):
+                    rl, rc = O.f2t_yuv([host[i] for i in runs[r]], W, H, family, bits, matrix, rng_, Hp, Wp,
+                                       _odt(dtype))
+                    assert_tensor_close(luma[r, :nl].reshape(1, N, Hp, Wp).cpu().numpy(), rl, f"luma run {r}")
+                    assert_tensor_close(chroma[r, :nc].reshape(1, 2 * N, Hc, Wc).cpu().numpy(), rc,
+                                        f"chroma run {r}")
+    for x, y in zip(res[0], res[1]):
+        assert torch.equal(x.view(torch.int16 if x.dtype == torch.float16 else torch.int32),
+                           y.view(torch.int16 if y.dtype == torch.float16 else torch.int32))
