@@ -76,7 +76,8 @@ enum { NNVISR_LIMITED = 0, NNVISR_FULL = 1 };
  * block (bilinear 3/4,1/4 up; 2x2 box mean down); LEFT = MPEG-2, horizontally
  * co-sited with even luma columns, vertically centred (up: 1 | 1/2,1/2
  * horizontally; down: [1,2,1]/4 horizontally, 1/2,1/2 vertically; SPEC.md
- * S:339-347).  LEFT runs on the generic (non-TMA) kernels. */
+ * S:339-347).  Both sitings run on the TMA-pipelined kernels where the
+ * geometry allows (16-byte aligned rows, width a multiple of 32). */
 enum { NNVISR_CHROMA_CENTER = 0, NNVISR_CHROMA_LEFT = 1 };
 /* tensor element type */
 enum { NNVISR_F32 = 0, NNVISR_F16 = 1 };

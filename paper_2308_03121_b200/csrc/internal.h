@@ -78,7 +78,7 @@ struct F2TArgs {
     unsigned long long *tile_counter;  // TMA path: zeroed per launch, dynamic tile scheduler
     int64_t jobs, dests;               // distinct frames and (run, slot) destinations of the launch
     F2TColour col;
-    // 4:2:0 chroma siting of this launch: 0 centre, 1 LEFT (generic kernels only)
+    // 4:2:0 chroma siting of this launch: 0 centre, 1 LEFT
     int32_t left;
     // YUV-native tensors (NEXT-3, kernels_yuv.cu): the luma of (run, slot) at
     // dst + run*run_stride + slot*slot_bytes ([Hp][Wp]); its chroma planes U,
@@ -103,10 +103,11 @@ struct T2FArgs {
     int32_t vec_out;          // output planes allow vector stores
     int32_t tma_ok, rowunits, nseg, stages, stage_bytes, segw;
     int32_t cthreads;  // TMA path: consumer threads per CTA (segw / 8 rounded up to warps)
+    int32_t lpad;      // TMA path: values staged left of each row segment (LEFT siting), else 0
     int64_t tiles;
     unsigned long long *tile_counter;  // TMA path: zeroed per launch, dynamic tile scheduler
     T2FColour col;
-    int32_t left;  // 4:2:0 chroma siting: 0 centre, 1 LEFT (generic kernels only)
+    int32_t left;  // 4:2:0 chroma siting: 0 centre, 1 LEFT
     // YUV-native tensors (NEXT-3): output slot o of tuple c reads luma plane o
     // of src + c*tensor_stride ([th][tw]) and chroma planes 2o, 2o+1 of
     // src2 + c*tensor_stride2 ([thc][twc])

@@ -534,6 +534,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
     }
     const int cw = a.W >> 1, ch = a.H >> 1;
     const int tid = threadIdx.x;
+    const bool left = FAMILY == kYUV420 && a.left;  // 4:2:0 chroma siting (reading A5)
     int k = 0, b = 0;            // stage and output buffer of tile i
     uint32_t fph = 0, bround = 0;  // full[k] wait parity; (i / nob) & 1
     TileSource ts;
@@ -649,10 +650,18 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                                 float v[6];
 #pragma unroll
                                 for (int t = 0; t < 6; ++t) v[t] = fmaf(3.0f, f[1][t], f[r ? 2 : 0][t]);
+                                if (!left) {
 #pragma unroll
-                                for (int m = 0; m < 4; ++m) {
-                                    cd[p][r][2 * m] = fmaf(3.0f, v[m + 1], v[m]);
-                                    cd[p][r][2 * m + 1] = fmaf(3.0f, v[m + 1], v[m + 2]);
+                                    for (int m = 0; m < 4; ++m) {
+                                        cd[p][r][2 * m] = fmaf(3.0f, v[m + 1], v[m]);
+                                        cd[p][r][2 * m + 1] = fmaf(3.0f, v[m + 1], v[m + 2]);
+                                    }
+                                } else {  // LEFT (MPEG-2): co-sited even columns, (1/2, 1/2) odd
+#pragma unroll
+                                    for (int m = 0; m < 4; ++m) {
+                                        cd[p][r][2 * m] = 4.0f * v[m + 1];
+                                        cd[p][r][2 * m + 1] = 2.0f * (v[m + 1] + v[m + 2]);
+                                    }
                                 }
                             }
                         }
@@ -692,9 +701,16 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                         for (int kk = 0; kk < kPx; ++kk) {
                             const int xc = min(x + kk, a.W - 1);
                             ys[kk] = 16 * L[xc];
-                            const int in_ = xc >> 1, if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
-                            us[kk] = 9 * Cn[0][in_] + 3 * Cn[0][if_] + 3 * Cf[0][in_] + Cf[0][if_];
-                            vs[kk] = 9 * Cn[1][in_] + 3 * Cn[1][if_] + 3 * Cf[1][in_] + Cf[1][if_];
+                            const int in_ = xc >> 1;
+                            if (!left) {
+                                const int if_ = (xc & 1) ? min(in_ + 1, cw - 1) : max(in_ - 1, 0);
+                                us[kk] = 9 * Cn[0][in_] + 3 * Cn[0][if_] + 3 * Cf[0][in_] + Cf[0][if_];
+                                vs[kk] = 9 * Cn[1][in_] + 3 * Cn[1][if_] + 3 * Cf[1][in_] + Cf[1][if_];
+                            } else {  // LEFT: co-sited column xc/2 (even xc) or the mean of xc/2 and xc/2+1
+                                const int i1 = (xc & 1) ? min(in_ + 1, cw - 1) : in_;
+                                us[kk] = 2 * (3 * (Cn[0][in_] + Cn[0][i1]) + Cf[0][in_] + Cf[0][i1]);
+                                vs[kk] = 2 * (3 * (Cn[1][in_] + Cn[1][i1]) + Cf[1][in_] + Cf[1][i1]);
+                            }
                         }
                     } else {
                         const IN *P0 = sg.plane(st, 0, yc - tl.ly0) - tl.lw0,
@@ -759,10 +775,12 @@ struct T2FHdr {
     int job, y0, x0, x1;
 };
 
+// Staged row (r, c): stride segw + lpad values, the segment's first column at
+// offset lpad (LEFT siting stages the column left of the segment there).
 template <int FAMILY, typename TIN>
-__device__ __forceinline__ TIN *t2f_row_ptr(uint8_t *st, int segw, int r, int c)
+__device__ __forceinline__ TIN *t2f_row_ptr(uint8_t *st, int segw, int lpad, int r, int c)
 {
-    return reinterpret_cast<TIN *>(st) + (r * 3 + c) * segw;
+    return reinterpret_cast<TIN *>(st) + (r * 3 + c) * (segw + lpad) + lpad;
 }
 
 // Stage tile t; t < 0: write the end-of-work header (job -1) and complete
@@ -785,13 +803,16 @@ __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *
     const int64_t plane = a.th * a.tw;
     const TIN *src = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
                      static_cast<int64_t>(3 * o) * plane + static_cast<int64_t>(ru * ROWS) * a.tw + x0;
-    const uint32_t bytes = (x1 - x0) * sizeof(TIN);
+    // LEFT siting: also the lpad values left of the segment (x0 > 0; 16 bytes)
+    const int pre = x0 > 0 ? a.lpad : 0;
+    const uint32_t bytes = (x1 - x0 + pre) * sizeof(TIN);
     mbar_arrive_expect_tx(bar, ROWS * 3 * bytes);
 #pragma unroll
     for (int r = 0; r < ROWS; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
-            bulk_g2s(t2f_row_ptr<FAMILY, TIN>(st, a.segw, r, c), src + c * plane + r * a.tw, bytes, bar);
+            bulk_g2s(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, c) - pre, src + c * plane + r * a.tw - pre, bytes,
+                     bar);
 }
 
 // Warp-specialised like f2t_tma: a.cthreads consumer threads (segw / 8,
@@ -858,15 +879,36 @@ __global__ void __launch_bounds__(kThreads + 32, (FAMILY == kYUV420 && sizeof(AR
         if (h.x0 + xo < h.x1) {
             const int x = h.x0 + xo;
             AR sb[4], sr[4];
+            if (FAMILY == kYUV420 && a.lpad) {
+                // LEFT (MPEG-2) siting: per row the [1,2,1] taps need B-Y', R-Y'
+                // of column x-1 (column 0 at x = 0), staged left of the segment
+                const int xl = x > 0 ? xo - 1 : xo;
 #pragma unroll
-            for (int r = 0; r < ROWS; ++r) {
-                float R[kPx], G[kPx], B[kPx];
-                tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, r, 0) + xo, R);
-                tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, r, 1) + xo, G);
-                tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, r, 2) + xo, B);
-                t2f_row<FAMILY, OS, AR>(c, a.col, f, x, h.y0 + r, r, R, G, B, kPx, a.vec_out, sb, sr);
+                for (int r = 0; r < ROWS; ++r) {
+                    const TIN *p0 = t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 0);
+                    const TIN *p1 = t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 1);
+                    const TIN *p2 = t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 2);
+                    const AR r_ = tload1(p0 + xl), g_ = tload1(p1 + xl), b_ = tload1(p2 + xl);
+                    const AR Yl = fma_(c.kb, b_ - g_, fma_(c.kr, r_ - g_, g_));
+                    float R[kPx], G[kPx], B[kPx];
+                    tload8(p0 + xo, R);
+                    tload8(p1 + xo, G);
+                    tload8(p2 + xo, B);
+                    t2f_row<FAMILY, OS, AR, true>(c, a.col, f, x, h.y0 + r, r, R, G, B, kPx, a.vec_out, sb, sr,
+                                                  b_ - Yl, r_ - Yl);
+                }
+                if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR, true>(c, f, x, h.y0, sb, sr, kPx, a.vec_out);
+            } else {
+#pragma unroll
+                for (int r = 0; r < ROWS; ++r) {
+                    float R[kPx], G[kPx], B[kPx];
+                    tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 0) + xo, R);
+                    tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 1) + xo, G);
+                    tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 2) + xo, B);
+                    t2f_row<FAMILY, OS, AR>(c, a.col, f, x, h.y0 + r, r, R, G, B, kPx, a.vec_out, sb, sr);
+                }
+                if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, h.y0, sb, sr, kPx, a.vec_out);
             }
-            if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, h.y0, sb, sr, kPx, a.vec_out);
         }
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[k]);
@@ -1046,7 +1088,7 @@ cudaError_t launch_tma(K kernel, A a, int vals_per_col, int elem, int budget, in
     // consumer threads are the tile's 8-column groups (whole warps)
     a.segw = std::min(kSegW, ((a.Wo + a.nseg - 1) / a.nseg + 31) / 32 * 32);
     a.cthreads = std::min(kThreads, (a.segw / kPx + 31) / 32 * 32);
-    a.stage_bytes = (vals_per_col * a.segw * elem + 127) / 128 * 128;
+    a.stage_bytes = (vals_per_col * (a.segw + a.lpad) * elem + 127) / 128 * 128;
     budget = env_int("NNVISR_T2F_SMEM_KB", budget / 1024) * 1024;
     a.stages = env_int("NNVISR_T2F_STAGES", default_stages);
     if (a.stages <= 0) a.stages = budget / a.stage_bytes;
@@ -1196,16 +1238,18 @@ cudaError_t t2f_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t
     // 1080p/4K, three at 720p; tools/sweep.sh t2f on B200, profiles/r01/t2f_sweep2.txt)
     constexpr int R = FAMILY == kYUV420 ? 2 : 1, kBudget = 50 * 1024;
     const int st = env_int("NNVISR_T2F_STAGES", 0);
+    T2FArgs b = a;
+    b.lpad = (FAMILY == kYUV420 && a.left) ? 16 / (dtype == kF16 ? 2 : 4) : 0;  // LEFT: 16 bytes left of each row
     if (bits == 8) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, a, 3 * R, 2, kBudget, st, s);
-        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, a, 3 * R, 4, kBudget, st, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint8_t, __half, float>, b, 3 * R, 2, kBudget, st, s);
+        return launch_tma(t2f_tma<FAMILY, uint8_t, float, float>, b, 3 * R, 4, kBudget, st, s);
     }
     if (bits == 10) {
-        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, a, 3 * R, 2, kBudget, st, s);
-        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, a, 3 * R, 4, kBudget, st, s);
+        if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, float>, b, 3 * R, 2, kBudget, st, s);
+        return launch_tma(t2f_tma<FAMILY, uint16_t, float, float>, b, 3 * R, 4, kBudget, st, s);
     }
-    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, a, 3 * R, 2, kBudget, st, s);
-    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, a, 3 * R, 4, kBudget, st, s);
+    if (dtype == kF16) return launch_tma(t2f_tma<FAMILY, uint16_t, __half, double>, b, 3 * R, 2, kBudget, st, s);
+    return launch_tma(t2f_tma<FAMILY, uint16_t, float, double>, b, 3 * R, 4, kBudget, st, s);
 }
 
 template <int FAMILY>

@@ -598,7 +598,7 @@ nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, int64_t dests, 
                                    (a.Wc * h->elem) % 16 == 0);
     a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->fmt.width % 32 == 0 &&
                reinterpret_cast<uintptr_t>(a.dst) % 16 == 0 && a.run_stride % 16 == 0 && a.slot_bytes % 16 == 0 &&
-               yuv_ok && !a.left;
+               yuv_ok;
     cudaError_t e = launch_f2t(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "f2t kernel launch");
     return NNVISR_OK;
@@ -667,7 +667,7 @@ nnvisr_status run_t2f(nnvisr_handle *h, T2FArgs a, int64_t jobs, cudaStream_t st
     const bool yuv_ok = !a.yuv || (reinterpret_cast<uintptr_t>(a.src2) % 16 == 0 && a.tensor_stride2 % 16 == 0 &&
                                    (a.thc * a.twc * h->elem) % 16 == 0 && (a.twc * h->elem) % 16 == 0);
     a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wo % 32 == 0 && a.tensor_stride % 16 == 0 &&
-               reinterpret_cast<uintptr_t>(a.src) % 16 == 0 && yuv_ok && !a.left;
+               reinterpret_cast<uintptr_t>(a.src) % 16 == 0 && yuv_ok;
     cudaError_t e = launch_t2f(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "t2f kernel launch");
     return NNVISR_OK;

@@ -392,3 +392,47 @@ def test_yuv_f2t_tma_parity(family, bits, dtype, W, H, align, monkeypatch):
     for x, y in zip(res[0], res[1]):
         assert torch.equal(x.view(torch.int16 if x.dtype == torch.float16 else torch.int32),
                            y.view(torch.int16 if y.dtype == torch.float16 else torch.int32))
+
+
+@pytest.mark.parametrize("bits,dtype", LEFT_CASES)
+@pytest.mark.parametrize("W,H", [(256, 12), (2080, 6)])
+def test_left_tma_parity(bits, dtype, W, H, monkeypatch):
+    """LEFT (MPEG-2) siting on the TMA-pipelined kernels (aligned
+    geometries; 2080 columns = two segments, so the t2f [1,2,1] tap of a
+    segment's first column reads the column staged left of it): f2t and t2f
+    against the oracle, bit-identical to the generic kernels."""
+    rs = np.random.default_rng(2100 + bits + dtype + W)
+    matrix, rng_ = ((nv.BT709, nv.LIMITED), (nv.BT2020, nv.FULL))[int(rs.integers(2))]
+    cfg = _cfg(nv.YUV420, bits, dtype, matrix, rng_, W, H, N=3, M=1, align=16, left=True)
+    lay = FrameLayout(W, H, nv.YUV420, bits)
+    host = [synth.random_planes(lay, int(rs.integers(1 << 30))) for _ in range(3)]
+    res = []
+    for generic in (False, True):
+        if generic:
+            monkeypatch.setenv("NNVISR_FORCE_GENERIC", "1")
+        buf = FrameBuffer(lay, 3, device=DEV)
+        for i, p in enumerate(host):
+            buf.set_planes(i, p)
+        with nv.open(cfg) as h:
+            t = torch.empty(h.in_shape, dtype=_tdt(dtype), device=DEV)
+            h.frames_to_tensor([buf.descriptor(i) for i in (1, 2, 0)], t.data_ptr())
+            Ho, Wo = h.out_shape[2], h.out_shape[3]
+            to = synth.random_tensor((2, 3, Ho, Wo), dtype, 91 + W, device=DEV)
+            olay = FrameLayout(Wo, Ho, nv.YUV420, bits)
+            out = FrameBuffer(olay, 2, device=DEV)
+            h.tensor_to_frames_batch(to.data_ptr(), to[0].numel() * to.element_size(), Ho, Wo, out.descriptors(), 2)
+            torch.cuda.synchronize()
+            res.append((t.clone(), out.data.clone()))
+            if not generic:
+                ref = O.f2t([host[1], host[2], host[0]], W, H, nv.YUV420, bits, matrix, rng_, h.in_shape[2],
+                            h.in_shape[3], _odt(dtype), siting=O.CHROMA_LEFT)
+                assert_tensor_close(t.cpu().numpy(), ref, f"LEFT f2t tma {W}")
+                stats = CodeStats()
+                for c in range(2):
+                    refo = O.t2f(to[c:c + 1].cpu().numpy(), 1, Wo, Ho, nv.YUV420, bits, matrix, rng_,
+                                 siting=O.CHROMA_LEFT)
+                    stats.add(out.host_planes(c), refo[0], f"LEFT t2f tma {W} {c}")
+                stats.check(f"LEFT t2f tma bits={bits}")
+    assert torch.equal(res[0][0].view(torch.int16 if dtype == nv.F16 else torch.int32),
+                       res[1][0].view(torch.int16 if dtype == nv.F16 else torch.int32))
+    assert torch.equal(res[0][1], res[1][1])
