@@ -123,13 +123,14 @@ __device__ __forceinline__ void f2t_colour(const F2TColour &c, int ys, int us, i
 }
 
 // fp16 tensors near zero: R', G', B' are sums of O(1) terms whose fp32
-// evaluation errs by up to ~2^-23 (one rounding of Y' <= 1.2, the rounded
+// evaluation errs by at most ~2^-23 (one rounding of Y' <= 1.2, the rounded
 // folded constants, the FMA roundings).  Against the oracle's single
 // double->fp16 rounding that stays within 1 fp16 ULP while the ULP exceeds
-// the error, i.e. for |v| >= 2^-11 (ULP 2^-21).  Pixels with a value below
-// 2^-9 (a 4x margin) are recomputed in fp64 and rounded once to fp16; the
-// returned float is that fp16 value exactly, so the RNE store reproduces it.
-// (tests/test_gpu_fp16_exhaustive.py: every 8-bit triple, all matrices.)
+// the error: for |v| >= 2^-11 the ULP is >= 2^-21, four times the bound.
+// Pixels with a value below 2^-11 are recomputed in fp64 and rounded once to
+// fp16; the returned float is that fp16 value exactly, so the RNE store
+// reproduces it.  (tests/test_gpu_fp16_exhaustive.py: every 8-bit triple,
+// all matrices and ranges.)
 __device__ __forceinline__ float3 f2t_colour_precise(const F2TColour &c, int ys, int us, int vs)
 {
     const double Y = static_cast<double>(ys - c.y_off) * c.y_scale_d;
@@ -139,7 +140,7 @@ __device__ __forceinline__ float3 f2t_colour_precise(const F2TColour &c, int ys,
                        __half2float(__double2half(Y - c.g_pb_d * Pb - c.g_pr_d * Pr)),
                        __half2float(__double2half(Y + c.b_pb_d * Pb)));
 }
-constexpr float kF16Tiny = 1.0f / 512.0f;  // 2^-9
+constexpr float kF16Tiny = 1.0f / 2048.0f;  // 2^-11
 
 template <int FAMILY, typename OUT>
 __device__ __forceinline__ void f2t_pixel(const F2TColour &c, int ys, int us, int vs, float &R, float &G, float &B)

@@ -22,8 +22,8 @@ struct DevFrame {
 //   luma / RGB channel : v = (16*code - y_off) * y_scale
 //   chroma             : P = (s - c_off) * c_scale, s = 16 x the (upsampled) code
 //   R = Y + r_pr*Pr ;  B = Y + b_pb*Pb ;  G = Y - g_pb*Pb - g_pr*Pr
-//   fp16 tensors: values with |v| < 2^-9 (an fp16 ULP there is not safely
-//   coarser than the fp32 rounding error below 2^-11) are recomputed in fp64 with the *_d constants.
+//   fp16 tensors: values with |v| < 2^-11 (below which an fp16 ULP is not
+//   safely coarser than the fp32 rounding error) are recomputed in fp64 with the *_d constants.
 struct F2TColour {
     int32_t y_off, c_off;
     int32_t u_off;  // YUV-native chroma U = P + 1/2 = (16*code - u_off) * c_scale (reading A22)

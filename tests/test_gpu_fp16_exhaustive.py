@@ -2,7 +2,7 @@
 10-bit triples, for all three matrices and both ranges (4:4:4, one 4096x4096
 frame holding each triple once), against the oracle: within 1 fp16 ULP
 (north_star).  This pins the kernels' near-zero handling (fp32 evaluation,
-fp64 recompute only for |v| < 2^-9, common.cuh f2t_pixel) on every value the
+fp64 recompute only for |v| < 2^-11, common.cuh f2t_pixel) on every value the
 8-bit formats can produce, including all cancellations to ~0."""
 import numpy as np
 import pytest

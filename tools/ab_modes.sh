@@ -1,7 +1,12 @@
-for lib in libnnvisr_e.so libnnvisr_b.so libnnvisr_e.so libnnvisr_b.so; do
- for spec in "c2 materialize" "c2 store" "c5 materialize" "c4 materialize" "c4 batch"; do set -- $spec
-  NNVISR_LIBNAME=$lib python bench.py --workload $1 --frames 240 --f2t-mode $2 --steps 5 --warmup 2 --no-e2e --no-cpu-baseline > gpurun_out/x.json 2>/dev/null
-  python -c "
-import json;d=json.load(open('gpurun_out/x.json'));v=d['per_direction']['f2t']; print('$lib $1 $2', round(v['achieved_gbs']), round(v['fps']))"
+#!/bin/bash
+# Same-box A/B over bench modes: tools/ab_modes.sh "lib1 lib2" "wl:mode wl:mode ..." [rounds]
+libs=$1; specs=$2; rounds=${3:-2}
+for r in $(seq $rounds); do
+ for lib in $libs; do
+  for spec in $specs; do wl=${spec%%:*}; mode=${spec##*:}
+   NNVISR_LIBNAME=$lib python bench.py --workload $wl --frames 240 --f2t-mode $mode --steps 5 --warmup 2 --no-e2e --no-cpu-baseline > gpurun_out/x.json 2>/dev/null
+   python -c "
+import json;d=json.load(open('gpurun_out/x.json'));v=d['per_direction']['f2t']; print('$lib $wl $mode', round(v['achieved_gbs']), round(v['fps']))"
+  done
  done
 done
