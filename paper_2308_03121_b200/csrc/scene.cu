@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kThreads) sad_kernel(const DevFrame *frames, i
     if (nf <= 0) return;
     const int y0 = blockIdx.x * kSadRowsPerBlock, y1 = min(y0 + kSadRowsPerBlock, H);
     const int groups = (W + kPx - 1) / kPx;
+    // per-thread sums fit 32 bits (<= 8 rows x 8 columns x 65535 per column group pass)
     unsigned long long acc[kSadFrames];
 #pragma unroll
     for (int j = 0; j < kSadFrames; ++j) acc[j] = 0;
@@ -48,22 +49,25 @@ __global__ void __launch_bounds__(kThreads) sad_kernel(const DevFrame *frames, i
             for (int g = threadIdx.x; g < groups; g += kThreads) {
                 const int x = g * kPx;
                 if (x + kPx > W) continue;
+                // all kSadFrames + 1 rows' loads first (independent, in flight
+                // together; frames past the group's end re-read its last one)
+                V8 q[kSadFrames + 1];
+#pragma unroll
+                for (int j = 0; j <= kSadFrames; ++j)
+                    q[j] = *reinterpret_cast<const V8 *>(row_ptr<IN>(load_frame(frames + f0 + min(j, nf)), 0, y) + x);
                 int prev[kPx];
-                unpack8(*reinterpret_cast<const V8 *>(row_ptr<IN>(load_frame(frames + f0), 0, y) + x), prev);
+                unpack8(q[0], prev);
 #pragma unroll
                 for (int j = 0; j < kSadFrames; ++j) {
-                    if (j < nf) {
-                        int cur[kPx];
-                        unpack8(*reinterpret_cast<const V8 *>(row_ptr<IN>(load_frame(frames + f0 + j + 1), 0, y) + x),
-                                cur);
-                        uint32_t d = 0;
+                    int cur[kPx];
+                    unpack8(q[j + 1], cur);
+                    uint32_t d = 0;
 #pragma unroll
-                        for (int k = 0; k < kPx; ++k) {
-                            d += static_cast<uint32_t>(abs(cur[k] - prev[k]));
-                            prev[k] = cur[k];
-                        }
-                        acc[j] += d;
+                    for (int k = 0; k < kPx; ++k) {
+                        d += static_cast<uint32_t>(abs(cur[k] - prev[k]));
+                        prev[k] = cur[k];
                     }
+                    acc[j] += d;
                 }
             }
         }
