@@ -31,7 +31,7 @@ constexpr int kSadFrames = 8;  // consecutive frames per block: each frame row i
 // read from memory once (plus the group's first frame, shared with the
 // previous group).
 template <typename IN>
-__global__ void __launch_bounds__(kThreads) sad_kernel(const DevFrame *frames, int count, int W, int H, int vec,
+__global__ void __launch_bounds__(kThreads, 4) sad_kernel(const DevFrame *frames, int count, int W, int H, int vec,
                                                        int rgb, unsigned long long *sad)
 {
     using V8 = typename Pack<IN>::V8;
@@ -45,31 +45,39 @@ __global__ void __launch_bounds__(kThreads) sad_kernel(const DevFrame *frames, i
 #pragma unroll
     for (int j = 0; j < kSadFrames; ++j) acc[j] = 0;
     if (vec && !rgb) {
-        for (int y = y0; y < y1; ++y) {
-            for (int g = threadIdx.x; g < groups; g += kThreads) {
-                const int x = g * kPx;
-                if (x + kPx > W) continue;
-                // all kSadFrames + 1 rows' loads first (independent, in flight
-                // together; frames past the group's end re-read its last one)
-                V8 q[kSadFrames + 1];
+        // one (row, 8-column group): all kSadFrames + 1 rows' loads first
+        // (independent, in flight together; frames past the group's end
+        // re-read its last one), then the differences
+        auto item = [&](int y, int g) {
+            const int x = g * kPx;
+            if (x + kPx > W) return;
+            V8 q[kSadFrames + 1];
 #pragma unroll
-                for (int j = 0; j <= kSadFrames; ++j)
-                    q[j] = *reinterpret_cast<const V8 *>(row_ptr<IN>(load_frame(frames + f0 + min(j, nf)), 0, y) + x);
-                int prev[kPx];
-                unpack8(q[0], prev);
+            for (int j = 0; j <= kSadFrames; ++j)
+                q[j] = *reinterpret_cast<const V8 *>(row_ptr<IN>(load_frame(frames + f0 + min(j, nf)), 0, y) + x);
+            int prev[kPx];
+            unpack8(q[0], prev);
 #pragma unroll
-                for (int j = 0; j < kSadFrames; ++j) {
-                    int cur[kPx];
-                    unpack8(q[j + 1], cur);
-                    uint32_t d = 0;
+            for (int j = 0; j < kSadFrames; ++j) {
+                int cur[kPx];
+                unpack8(q[j + 1], cur);
+                uint32_t d = 0;
 #pragma unroll
-                    for (int k = 0; k < kPx; ++k) {
-                        d += static_cast<uint32_t>(abs(cur[k] - prev[k]));
-                        prev[k] = cur[k];
-                    }
-                    acc[j] += d;
+                for (int k = 0; k < kPx; ++k) {
+                    d += static_cast<uint32_t>(abs(cur[k] - prev[k]));
+                    prev[k] = cur[k];
                 }
+                acc[j] += d;
             }
+        };
+        if (groups < (3 * kThreads) / 4) {
+            // narrow frames: (row, group) items over all the block's rows, so
+            // every thread has work
+            const int items = (y1 - y0) * groups;
+            for (int it = threadIdx.x; it < items; it += kThreads) item(y0 + it / groups, it % groups);
+        } else {
+            for (int y = y0; y < y1; ++y)
+                for (int g = threadIdx.x; g < groups; g += kThreads) item(y, g);
         }
     } else {
         for (int y = y0; y < y1; ++y) {
