@@ -245,8 +245,8 @@ struct F2TTile {
     {
         const int bands = (a.rowunits + a.band - 1) / a.band;
         int band;
-        decode_tile(t, bands, a.nseg, kSegW, job, band, x0);
-        x1 = min(x0 + kSegW, a.Wp);
+        decode_tile(t, bands, a.nseg, a.fsegw, job, band, x0);
+        x1 = min(x0 + a.fsegw, a.Wp);
         u0 = band * a.band;
         nu = min(a.band, a.rowunits - u0);
         ly0 = min(u0 * ROWS, a.H - 1);
@@ -559,10 +559,12 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
         int64_t next_t = 0;
         if (!LOADER && threadIdx.x == 0) next_t = ts.fetch();
         const int sw = tl.x1 - tl.x0;
-        const int x = tl.x0 + kPx * tid;
-        const bool fast = x + kPx <= a.W;
         if (i >= nob) mbar_wait(&ofree[b], bround ^ 1u);
         NNVISR_TRACE(threadIdx.x == 0, 2, i);
+        // a segment wider than kSegW (wide whole-row tiles): each thread
+        // converts one 8-column group per kSegW columns
+        for (int x = tl.x0 + kPx * tid; x < tl.x1; x += kSegW) {
+        const bool fast = x + kPx <= a.W;
         if constexpr (YUVN) {
             // YUV-native tensors (NEXT-3, reading A22): no matrix, no
             // resampling: luma Y' = (16c - y_off) * y_scale, chroma
@@ -743,6 +745,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                 }
             }
         }
+        }  // column groups
         fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk stores
         if (!LOADER && threadIdx.x == 0) {
             tile_of[(i + nst) % kTileRing] = next_t;
@@ -1116,7 +1119,16 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     using S = F2TStage<FAMILY, IN>;
     constexpr int ROWS = S::ROWS;
     if (a.tiles <= 0) return cudaSuccess;
-    const int segw = std::min(kSegW, (a.Wp + 31) / 32 * 32);
+    // segment width: kSegW (the host's nseg), or -- wide mode, frames up to
+    // 2 x kSegW wide -- the whole padded row in one tile (whole-row copies and
+    // stores; each consumer thread takes two column groups)
+    const int64_t jobs_ = a.tiles / ((int64_t)a.rowunits * a.nseg);
+    // (4:2:0 only: measured +5% at 4K; 4:4:4 fp32 tiles are faster split)
+    const bool wide = env_int("NNVISR_F2T_WIDE", FAMILY == kYUV420 ? 1 : 0) && a.Wp > kSegW && a.Wp <= 2 * kSegW;
+    a.fsegw = wide ? (a.Wp + 31) / 32 * 32 : kSegW;
+    a.nseg = (a.Wp + a.fsegw - 1) / a.fsegw;
+    a.tiles = jobs_ * a.rowunits * a.nseg;
+    const int segw = std::min(a.fsegw, (a.Wp + 31) / 32 * 32);
     const int lcap = (segw + 2 * S::G - 1) / (2 * S::G) * (2 * S::G);  // ccap*sizeof(IN) stays 16-byte aligned
     const int ccap = lcap / 2 + 2 * S::G;
     // whole rows: one segment, and every bound frame's pitches are the staged strides
@@ -1142,7 +1154,7 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     };
     const bool low_fanout = a.dests > 0 && a.dests <= 2 * a.jobs;
     int B = env_int("NNVISR_F2T_BAND", 0);
-    if (B <= 0) B = ((FAMILY == kYUV420 && a.nseg > 1) || (low_fanout && !fits_two(2))) ? 1 : 2;
+    if (B <= 0) B = ((FAMILY == kYUV420 && (a.nseg > 1 || a.fsegw > kSegW)) || (low_fanout && !fits_two(2))) ? 1 : 2;
     a.band = std::max(1, std::min(B, a.rowunits));
     const int bands = (a.rowunits + a.band - 1) / a.band;
     a.tiles = a.tiles / ((int64_t)a.rowunits * a.nseg) * bands * a.nseg;  // jobs * bands * nseg
@@ -1158,7 +1170,7 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     //    store queue).
     const bool two = fits_two(a.band);
     a.stages = env_int("NNVISR_F2T_STAGES", 2);
-    a.nob = env_int("NNVISR_F2T_NOB", two ? 2 : 3);
+    a.nob = env_int("NNVISR_F2T_NOB", (two || a.fsegw > kSegW) ? 2 : 3);
     a.stages = std::max(1, std::min(kMaxStages, a.stages));
     a.nob = std::max(2, std::min(5, a.nob));
     // never exceed the 227 KB a CTA may use: shed output buffers, then band rows
