@@ -194,14 +194,12 @@ __device__ __forceinline__ void mag8(uint2 q, float (&f)[kPx])  // 8-bit
 // R', G', B' from dyv = code_Y - y_off/16, du = (16x upsampled Cb) - c_off,
 // dv likewise (all exact integers held in floats): the same arithmetic as
 // f2t_colour (Y' = 16*dyv*y_scale exactly), fp16 near-zero values in fp64.
+// fp16 near-zero values (see f2t_colour_precise): recompute the pixel in
+// fp64 from dyv = code_Y - y_off/16, du = 16x Cb - c_off, dv likewise.
 template <typename OUT>
-__device__ __forceinline__ void f2t_pixel_f(const F2TColour &c, float ys16, float dyv, float du, float dv, float &R,
-                                            float &G, float &B)
+__device__ __forceinline__ void f2t_fix_tiny(const F2TColour &c, float dyv, float du, float dv, float &R, float &G,
+                                             float &B)
 {
-    const float Y = dyv * ys16;
-    R = fmaf(c.r_v, dv, Y);
-    B = fmaf(c.b_u, du, Y);
-    G = fmaf(-c.g_v, dv, fmaf(-c.g_u, du, Y));
     if (sizeof(OUT) == 2) {
         if (fabsf(R) < kF16Tiny || fabsf(G) < kF16Tiny || fabsf(B) < kF16Tiny) {
             const double Yd = 16.0 * static_cast<double>(dyv) * c.y_scale_d;

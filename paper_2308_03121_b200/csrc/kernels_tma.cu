@@ -645,18 +645,32 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                                 f[q][0] = mag(kMagicBits | C[max(i0 - 1, 0)]);
                                 f[q][5] = mag(kMagicBits | C[min(i0 + 4, cw - 1)]);
 #pragma unroll
-                                for (int t = 0; t < 6; ++t) f[q][t] -= coff;
+                                for (int t = 0; t < 6; t += 2) {  // packed f32x2 (sm_100 FADD2 / FFMA2)
+                                    const float2 d2 = __fadd2_rn(make_float2(f[q][t], f[q][t + 1]),
+                                                                 make_float2(-coff, -coff));
+                                    f[q][t] = d2.x;
+                                    f[q][t + 1] = d2.y;
+                                }
                             }
 #pragma unroll
                             for (int r = 0; r < 2; ++r) {
                                 float v[6];
 #pragma unroll
-                                for (int t = 0; t < 6; ++t) v[t] = fmaf(3.0f, f[1][t], f[r ? 2 : 0][t]);
+                                for (int t = 0; t < 6; t += 2) {
+                                    const float2 v2 = __ffma2_rn(make_float2(3.0f, 3.0f),
+                                                                 make_float2(f[1][t], f[1][t + 1]),
+                                                                 make_float2(f[r ? 2 : 0][t], f[r ? 2 : 0][t + 1]));
+                                    v[t] = v2.x;
+                                    v[t + 1] = v2.y;
+                                }
                                 if (!left) {
 #pragma unroll
                                     for (int m = 0; m < 4; ++m) {
-                                        cd[p][r][2 * m] = fmaf(3.0f, v[m + 1], v[m]);
-                                        cd[p][r][2 * m + 1] = fmaf(3.0f, v[m + 1], v[m + 2]);
+                                        const float2 h2 = __ffma2_rn(make_float2(3.0f, 3.0f),
+                                                                     make_float2(v[m + 1], v[m + 1]),
+                                                                     make_float2(v[m], v[m + 2]));
+                                        cd[p][r][2 * m] = h2.x;
+                                        cd[p][r][2 * m + 1] = h2.y;
                                     }
                                 } else {  // LEFT (MPEG-2): co-sited even columns, (1/2, 1/2) odd
 #pragma unroll
@@ -669,15 +683,31 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                         }
                         const float yoff = kMagic + static_cast<float>(a.col.y_off >> 4);
                         const float ys16 = 16.0f * a.col.y_scale;
+                        const float2 yo2 = make_float2(-yoff, -yoff), ys2 = make_float2(ys16, ys16);
+                        const float2 rv2 = make_float2(a.col.r_v, a.col.r_v), bu2 = make_float2(a.col.b_u, a.col.b_u);
+                        const float2 gu2 = make_float2(-a.col.g_u, -a.col.g_u), gv2 = make_float2(-a.col.g_v, -a.col.g_v);
 #pragma unroll
                         for (int r = 0; r < 2; ++r) {
                             float dy[kPx];
                             mag8(*reinterpret_cast<const V8 *>(sg.luma(st, y0 + r - tl.ly0) - tl.lw0 + x), dy);
                             float R[kPx], G[kPx], B[kPx];
 #pragma unroll
-                            for (int kk = 0; kk < kPx; ++kk)
-                                f2t_pixel_f<OUT>(a.col, ys16, dy[kk] - yoff, cd[0][r][kk], cd[1][r][kk], R[kk], G[kk],
-                                                 B[kk]);
+                            for (int m = 0; m < 4; ++m) {  // pixels 2m, 2m+1 in f32x2 (same per-lane rounding)
+                                const float2 dyv = __fadd2_rn(make_float2(dy[2 * m], dy[2 * m + 1]), yo2);
+                                const float2 Y = __fmul2_rn(dyv, ys2);
+                                const float2 du = make_float2(cd[0][r][2 * m], cd[0][r][2 * m + 1]);
+                                const float2 dv = make_float2(cd[1][r][2 * m], cd[1][r][2 * m + 1]);
+                                const float2 R2 = __ffma2_rn(rv2, dv, Y), B2 = __ffma2_rn(bu2, du, Y);
+                                const float2 G2 = __ffma2_rn(gv2, dv, __ffma2_rn(gu2, du, Y));
+                                R[2 * m] = R2.x;
+                                R[2 * m + 1] = R2.y;
+                                G[2 * m] = G2.x;
+                                G[2 * m + 1] = G2.y;
+                                B[2 * m] = B2.x;
+                                B[2 * m + 1] = B2.y;
+                                f2t_fix_tiny<OUT>(a.col, dyv.x, du.x, dv.x, R[2 * m], G[2 * m], B[2 * m]);
+                                f2t_fix_tiny<OUT>(a.col, dyv.y, du.y, dv.y, R[2 * m + 1], G[2 * m + 1], B[2 * m + 1]);
+                            }
                             Row8<OUT> o3[3];
                             o3[0].set(R);
                             o3[1].set(G);
