@@ -1,17 +1,25 @@
 // kernels_tma.cu -- TMA-pipelined conversion kernels (sm_100a).
 //
 // The hot path is a pair of streaming passes (SURVEY.md §8(a) A3-A7 and
-// B1-B4).  Both kernels here are persistent: each CTA walks a contiguous range
-// of tiles, a tile being one row unit (a 4:2:0 row pair, else one row) times
-// a segment of up to 2048 columns, i.e. 8 columns per thread.  Thread 0 keeps
-// a ring of S shared-memory stages full with TMA bulk copies
-// (cp.async.bulk.shared::cluster.global, completion counted in bytes on one
-// mbarrier per stage) -- for frames->tensor the tile's luma rows together with
-// its co-sited chroma rows and their one-sample halo (north_star: "TMA or
-// shared-memory staging of luma tiles together with their co-sited chroma
-// rows"), for tensor->frames the tile's R', G', B' rows.  All threads convert
-// from shared memory and store with 128-bit st.global, while the copies of the
-// next S-1 tiles are in flight.
+// B1-B4).  All kernels here are persistent, warp-specialised pipelines:
+//
+//  * a tile is a band of row units (a 4:2:0 row pair, else one row) times a
+//    segment of up to 2048 columns (8 columns per consumer thread; 4:2:0
+//    frames up to 4096 columns can be one "wide" whole-row segment);
+//  * tiles are handed out dynamically: each launch uploads a zeroed tile
+//    counter with its work tables and one thread per CTA fetches tiles in
+//    order (TileSource), so fast SMs take more tiles;
+//  * one thread stages each tile into a shared-memory stage with TMA bulk
+//    copies (cp.async.bulk.shared::cluster.global, completion counted in bytes
+//    on the stage's `full` mbarrier) and writes the stage's tile header --
+//    for frames->tensor the band's luma rows with their co-sited chroma rows
+//    and one-row halo (north_star: "TMA or shared-memory staging of luma tiles
+//    together with their co-sited chroma rows"), for tensor->frames the
+//    tile's R', G', B' (or luma and chroma) rows;
+//  * consumer warps convert from shared memory while the next stages load;
+//    f2t writes the converted band to an output buffer that storer threads fan
+//    out to every tuple slot holding the frame with TMA bulk stores
+//    (cp.async.bulk.global.shared::cta); t2f stores codes with st.global.
 //
 // Coordinates outside the frame are clamped when shared memory is read
 // (padding replicates the last row/column, reading A6; chroma taps clamp to
@@ -137,7 +145,7 @@ __device__ __forceinline__ uint32_t smid()
 #endif
 
 constexpr int kSegW = kThreads * kPx;         // columns per tile segment (2048)
-constexpr int kConsumerWarps = kThreads / 32;  // converting warps; one more warp produces
+constexpr int kConsumerWarps = kThreads / 32;  // converting warps of f2t_tma
 constexpr int kMaxStages = 8;
 constexpr int kMaxOutBufs = 8;
 // per-stage tile header written by the loader, read by the consumers

@@ -41,3 +41,38 @@ def test_f2t_fp16_every_triple(bits, matrix, rng_):
         torch.cuda.synchronize()
         ref = oracle_f2t(lay, [host], H, W, cfg)
         assert_tensor_close(t.cpu().numpy(), ref, f"fp16 f2t bits={bits} matrix={matrix} range={rng_}")
+
+
+def _planes420(variant):
+    """4096x4096 4:2:0 8-bit: chroma constant over 8x8-sample blocks, one block
+    per (Cb, Cr) pair (all 65536); luma runs through all 256 codes in every
+    16x16 block (reversed in variant 1), so the block interiors hold every
+    (Y, Cb, Cr) combination the upsample can reach exactly."""
+    y, x = np.mgrid[0:H, 0:W]
+    luma = ((y % 16) * 16 + x % 16).astype(np.uint8)
+    if variant:
+        luma = (255 - luma).astype(np.uint8)
+    j, i = np.mgrid[0:H // 2, 0:W // 2]
+    b = (j // 8) * 256 + (i // 8)
+    return [luma, (b & 255).astype(np.uint8), (b >> 8).astype(np.uint8)]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("matrix", [nv.BT601, nv.BT709, nv.BT2020])
+@pytest.mark.parametrize("rng_", [nv.LIMITED, nv.FULL])
+def test_f2t_fp16_420_every_pair(variant, matrix, rng_):
+    """The 4:2:0 TMA fast path (float chroma filters, packed f32x2 colour,
+    fp64 near-zero recompute) over every (Cb, Cr) pair and every luma code,
+    against the oracle within 1 fp16 ULP."""
+    cfg = nv.Config(W, H, nv.YUV420, 8, matrix, rng_, input_count=1, output_count=1, n=1, left_context=-1,
+                    flags=0, align=1, dtype=nv.F16, sx=(1, 1), sy=(1, 1))
+    lay = FrameLayout(W, H, nv.YUV420, 8)
+    host = _planes420(variant)
+    buf = FrameBuffer(lay, 1, device="cuda")
+    buf.set_planes(0, host)
+    with nv.open(cfg) as h:
+        t = torch.empty(h.in_shape, dtype=torch.float16, device="cuda")
+        h.frames_to_tensor([buf.descriptor(0)], t.data_ptr())
+        torch.cuda.synchronize()
+        ref = oracle_f2t(lay, [host], H, W, cfg)
+        assert_tensor_close(t.cpu().numpy(), ref, f"fp16 4:2:0 f2t matrix={matrix} range={rng_}")
