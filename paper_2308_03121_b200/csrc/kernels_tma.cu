@@ -1111,6 +1111,8 @@ int sms()
     return n;
 }
 
+// Tuning knobs for experiments and sweeps (NNVISR_F2T_* / NNVISR_T2F_*,
+// DESIGN.md §6): read at each launch; unset = the built-in choice.
 int env_int(const char *name, int dflt)
 {
     const char *v = std::getenv(name);
