@@ -3,6 +3,7 @@
 //
 // Citations: PAPER.md = /root/reference/PAPER.md (arXiv 2308.03121); readings
 // A1..A16 are listed in DESIGN.md §3.
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys / ncu --nvtx
 #include "nnvisr.h"
 
 #include <algorithm>
@@ -20,6 +21,14 @@
 using namespace nnvisr;
 
 namespace {
+
+// Scoped NVTX range around each host entry point that plans or launches.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 thread_local std::string g_error;
 std::atomic<int64_t> g_launches{0};
@@ -354,6 +363,7 @@ nnvisr_status nnvisr_chroma_shapes(const nnvisr_handle *h, int64_t in_nchw[4], i
 nnvisr_status nnvisr_plan(const nnvisr_handle *h, int64_t num_frames, const uint8_t *cut,
                           int64_t *run_inputs, int64_t *run_fresh, int64_t cap, int64_t *num_runs)
 {
+    NvtxRange nvtx_("nnvisr_plan");
     g_error.clear();
     if (!h || !num_runs) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (num_frames < 0) return fail(NNVISR_ERR_INVALID_ARG, "num_frames < 0");
@@ -377,6 +387,7 @@ nnvisr_status nnvisr_plan_range(const nnvisr_handle *h, int64_t num_frames, int6
                                 const uint8_t *cut, int64_t fresh_begin, int64_t fresh_end,
                                 int64_t *run_inputs, int64_t *run_fresh, int64_t cap, int64_t *num_runs)
 {
+    NvtxRange nvtx_("nnvisr_plan_range");
     g_error.clear();
     if (!h || !num_runs) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (num_frames < 0 || first < 0 || count < 0 || first + count > num_frames)
@@ -715,6 +726,7 @@ nnvisr_status nnvisr_bind_frames(nnvisr_handle *h, int64_t base, const nnvisr_fr
 
 nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, void *tensor, void *stream)
 {
+    NvtxRange nvtx_("nnvisr_frames_to_tensor");
     g_error.clear();
     if (!h || !in || !tensor) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (!aligned16(tensor)) return fail(NNVISR_ERR_INVALID_ARG, "tensor pointer not 16-byte aligned");
@@ -825,6 +837,7 @@ static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, 
 nnvisr_status nnvisr_frames_to_tensor_batch(nnvisr_handle *h, const int64_t *run_inputs, int64_t num_runs,
                                             void *tensors, int64_t tensor_stride_bytes, void *stream)
 {
+    NvtxRange nvtx_("nnvisr_frames_to_tensor_batch");
     g_error.clear();
     if (!h || (num_runs > 0 && (!run_inputs || !tensors))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (num_runs < 0) return fail(NNVISR_ERR_INVALID_ARG, "num_runs < 0");
@@ -850,6 +863,7 @@ nnvisr_status nnvisr_frames_to_tensor_batch(nnvisr_handle *h, const int64_t *run
 
 nnvisr_status nnvisr_frames_to_store(nnvisr_handle *h, int64_t first, int64_t count, void *store, void *stream)
 {
+    NvtxRange nvtx_("nnvisr_frames_to_store");
     g_error.clear();
     if (!h || (count > 0 && !store)) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
@@ -958,6 +972,7 @@ static nnvisr_status t2f_common(nnvisr_handle *h, const void *tensors, int64_t s
 nnvisr_status nnvisr_tensor_to_frames(nnvisr_handle *h, const void *tensor, int64_t t_h, int64_t t_w,
                                       const nnvisr_frame *out, void *stream)
 {
+    NvtxRange nvtx_("nnvisr_tensor_to_frames");
     g_error.clear();
     if (!h || !tensor || !out) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     return t2f_common(h, tensor, 0, t_h, t_w, out, 1, static_cast<cudaStream_t>(stream));
@@ -967,6 +982,7 @@ nnvisr_status nnvisr_tensor_to_frames_batch(nnvisr_handle *h, const void *tensor
                                             int64_t t_h, int64_t t_w, const nnvisr_frame *out, int64_t count,
                                             void *stream)
 {
+    NvtxRange nvtx_("nnvisr_tensor_to_frames_batch");
     g_error.clear();
     if (!h || (count > 0 && (!tensors || !out))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
@@ -978,6 +994,7 @@ nnvisr_status nnvisr_frames_to_tensor_yuv_batch(nnvisr_handle *h, const int64_t 
                                                 void *luma, int64_t luma_stride_bytes, void *chroma,
                                                 int64_t chroma_stride_bytes, void *stream)
 {
+    NvtxRange nvtx_("nnvisr_frames_to_tensor_yuv_batch");
     g_error.clear();
     if (!h || (num_runs > 0 && (!run_inputs || !luma || !chroma))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (!h->yuv_in) return fail(NNVISR_ERR_INVALID_ARG, "the network does not take YUV tensors (NNVISR_YUV_INPUT)");
@@ -1004,6 +1021,7 @@ nnvisr_status nnvisr_tensor_to_frames_yuv_batch(nnvisr_handle *h, const void *lu
                                                 const void *chroma, int64_t chroma_stride_bytes, int64_t t_h,
                                                 int64_t t_w, const nnvisr_frame *out, int64_t count, void *stream)
 {
+    NvtxRange nvtx_("nnvisr_tensor_to_frames_yuv_batch");
     g_error.clear();
     if (!h || (count > 0 && (!luma || !chroma || !out))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (!h->yuv_out) return fail(NNVISR_ERR_INVALID_ARG, "the network does not produce YUV tensors (NNVISR_YUV_OUTPUT)");
@@ -1018,6 +1036,7 @@ nnvisr_status nnvisr_tensor_to_frames_yuv_batch(nnvisr_handle *h, const void *lu
 nnvisr_status nnvisr_scene_detect(nnvisr_handle *h, int64_t first, int64_t count, double threshold, uint64_t *sad,
                                   uint8_t *cut, void *stream)
 {
+    NvtxRange nvtx_("nnvisr_scene_detect");
     g_error.clear();
     if (!h || (count > 0 && (!sad || !cut))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (count < 0 || count > INT32_MAX) return fail(NNVISR_ERR_INVALID_ARG, "bad count");
@@ -1115,6 +1134,7 @@ nnvisr_status nnvisr_plan_batches(const nnvisr_handle *h, int64_t num_frames, co
 nnvisr_status nnvisr_frames_to_slots(nnvisr_handle *h, const int64_t *slot_frames, int64_t count, void *store,
                                      void *stream)
 {
+    NvtxRange nvtx_("nnvisr_frames_to_slots");
     g_error.clear();
     if (!h || (count > 0 && (!slot_frames || !store))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
@@ -1203,6 +1223,7 @@ nnvisr_status nnvisr_schedule_outputs(const nnvisr_handle *h, int64_t num_frames
 nnvisr_status nnvisr_copy_frames(nnvisr_handle *h, const int64_t *src_frames, const nnvisr_frame *out, int64_t count,
                                  void *stream)
 {
+    NvtxRange nvtx_("nnvisr_copy_frames");
     g_error.clear();
     if (!h || (count > 0 && (!src_frames || !out))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (count <= 0) return count < 0 ? fail(NNVISR_ERR_INVALID_ARG, "count < 0") : NNVISR_OK;
@@ -1322,6 +1343,7 @@ nnvisr_status nnvisr_frames_to_tensor_batch_host(nnvisr_handle *h, const nnvisr_
                                                  int64_t count, const int64_t *run_inputs, int64_t num_runs,
                                                  void *tensors, int64_t tensor_stride_bytes, void *stream)
 {
+    NvtxRange nvtx_("nnvisr_frames_to_tensor_batch_host");
     g_error.clear();
     if (!h || (count > 0 && !host_frames) || (num_runs > 0 && (!run_inputs || !tensors)))
         return fail(NNVISR_ERR_INVALID_ARG, "null argument");
@@ -1364,6 +1386,7 @@ nnvisr_status nnvisr_tensor_to_frames_batch_host(nnvisr_handle *h, const void *t
                                                  int64_t t_h, int64_t t_w, const nnvisr_frame *host_out, int64_t count,
                                                  void *stream)
 {
+    NvtxRange nvtx_("nnvisr_tensor_to_frames_batch_host");
     g_error.clear();
     if (!h || (count > 0 && (!tensors || !host_out))) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
     if (count < 0) return fail(NNVISR_ERR_INVALID_ARG, "count < 0");
