@@ -1307,7 +1307,9 @@ cudaError_t t2f_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t
 template <int FAMILY>
 cudaError_t t2f_yuv_tma_dispatch(int bits, int dtype, const T2FArgs &a, cudaStream_t s)
 {
-    constexpr int V = 3, kBudget = 50 * 1024;  // values per column: ROWS luma + 2 chroma (halved for 4:2:0)
+    // values per column: ROWS luma + 2 chroma (halved for 4:2:0); stages fitting
+    // 30 KB (2-3; B200 sweep: 720p 5.9 -> 6.5 TB/s against 50 KB)
+    constexpr int V = 3, kBudget = 30 * 1024;
     const int st = env_int("NNVISR_T2F_STAGES", 0);
     if (bits == 8) {
         if (dtype == kF16) return launch_tma(t2f_yuv_tma<FAMILY, uint8_t, __half, float>, a, V, 2, kBudget, st, s);
