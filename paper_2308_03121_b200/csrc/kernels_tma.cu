@@ -229,19 +229,22 @@ struct F2TWindow {
     int lw0, lw1, cw0, cw1;
     __device__ __forceinline__ void set(int x0, int x1, int W, int G, bool chroma420)
     {
+        // window ends are rounded up to whole 16-byte groups: a width that is
+        // not a multiple of 16 bytes reads into the row's pitch padding (the
+        // host requires 16-byte pitches), never past the row's allocation
         const int xr = min(x1, W);
         if (x0 < W) {
             lw0 = x0;
-            lw1 = xr;
+            lw1 = (xr + G - 1) / G * G;
         } else {  // a segment of padding columns only: they replicate column W-1
-            lw0 = W - G;
-            lw1 = W;
+            lw0 = (W - 1) / G * G;
+            lw1 = (W + G - 1) / G * G;
         }
         if (chroma420) {
             const int cw = W >> 1;
             const int lo = (min(x0, W - 1) >> 1) - 1;
             cw0 = max(0, (lo >= 0 ? lo : -G) / G * G);
-            cw1 = min(cw, ((xr >> 1) + 1 + G - 1) / G * G);
+            cw1 = min((cw + G - 1) / G * G, ((xr >> 1) + 1 + G - 1) / G * G);
         }
     }
 };

@@ -597,7 +597,8 @@ nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, int64_t dests, 
     a.jobs = jobs;
     a.dests = dests;
     // TMA-pipelined path: every copy window 16-byte aligned (planes and
-    // pitches aligned, width a multiple of 32 samples) and 16-byte stores
+    // pitches 16-byte aligned; windows rounded up into the pitch padding, so
+    // any width) and 16-byte tensor rows for the bulk stores
     const int rows = h->fmt.family == NNVISR_YUV420 ? 2 : 1;
     a.rowunits = (int32_t)(h->Hp / rows);
     a.nseg = (int32_t)((h->Wp + kThreads * kPx - 1) / (kThreads * kPx));
@@ -607,7 +608,7 @@ nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, int64_t dests, 
     const bool yuv_ok = !a.yuv || (reinterpret_cast<uintptr_t>(a.dst2) % 16 == 0 && a.run_stride2 % 16 == 0 &&
                                    a.slot_bytes2 % 16 == 0 && a.cplane_bytes % 16 == 0 &&
                                    (a.Wc * h->elem) % 16 == 0);
-    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->fmt.width % 32 == 0 &&
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out &&
                reinterpret_cast<uintptr_t>(a.dst) % 16 == 0 && a.run_stride % 16 == 0 && a.slot_bytes % 16 == 0 &&
                yuv_ok;
     cudaError_t e = launch_f2t(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
@@ -677,7 +678,10 @@ nnvisr_status run_t2f(nnvisr_handle *h, T2FArgs a, int64_t jobs, cudaStream_t st
     // 16-byte aligned too (their base, strides and rows)
     const bool yuv_ok = !a.yuv || (reinterpret_cast<uintptr_t>(a.src2) % 16 == 0 && a.tensor_stride2 % 16 == 0 &&
                                    (a.thc * a.twc * h->elem) % 16 == 0 && (a.twc * h->elem) % 16 == 0);
-    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wo % 32 == 0 && a.tensor_stride % 16 == 0 &&
+    // segments of whole 8-column groups with 16-byte copies: Wo % 8 (and
+    // % 16 for the half-width YUV-native chroma rows)
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wo % (a.yuv ? 16 : 8) == 0 &&
+               a.tensor_stride % 16 == 0 &&
                reinterpret_cast<uintptr_t>(a.src) % 16 == 0 && yuv_ok;
     cudaError_t e = launch_t2f(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "t2f kernel launch");

@@ -313,3 +313,44 @@ def test_launch_count_and_no_fallback():
     before = nv.launch_count()
     test_deterministic_repeat()
     assert nv.launch_count() >= before + 2
+
+
+@pytest.mark.parametrize("family", [nv.YUV420, nv.YUV444, nv.RGB])
+@pytest.mark.parametrize("bits,dtype", [(8, nv.F16), (10, nv.F32), (16, nv.F16)])
+def test_tma_odd_widths_match_generic(family, bits, dtype, monkeypatch):
+    """Widths that are not multiples of 32 on the TMA kernels (f2t copy windows
+    rounded up into the pitch padding; t2f segments of whole 8-column groups):
+    720 / 1000 / 1366-wide frames, against the oracle and bit-identical to the
+    generic kernels."""
+    for W, H, sx in ((720, 10, (1, 1)), (500, 6, (2, 1)), (1366, 4, (1, 1))):
+        rs = np.random.default_rng(W + bits + family)
+        cfg = _small_cfg(family, bits, dtype, nv.BT709, nv.LIMITED, W, H, M=1, N=3, align=8, sx=sx)
+        lay = FrameLayout(W, H, family, bits)
+        host = [synth.random_planes(lay, int(rs.integers(1 << 30))) for _ in range(3)]
+        res = []
+        for generic in (False, True):
+            if generic:
+                monkeypatch.setenv("NNVISR_FORCE_GENERIC", "1")
+            buf = FrameBuffer(lay, 3, device=DEV)
+            for i, p in enumerate(host):
+                buf.set_planes(i, p)
+            with nv.open(cfg) as h:
+                t = torch.empty(h.in_shape, dtype=torch.float16 if dtype == nv.F16 else torch.float32, device=DEV)
+                h.frames_to_tensor([buf.descriptor(i) for i in (0, 2, 1)], t.data_ptr())
+                Ho, Wo = h.out_shape[2], h.out_shape[3]
+                to = synth.random_tensor((2, 3, Ho, Wo), dtype, W, device=DEV)
+                olay = FrameLayout(Wo, Ho, family, bits)
+                out = FrameBuffer(olay, 2, device=DEV)
+                h.tensor_to_frames_batch(to.data_ptr(), to[0].numel() * to.element_size(), Ho, Wo,
+                                         out.descriptors(), 2)
+                torch.cuda.synchronize()
+                res.append((t.clone(), out.data.clone()))
+                if not generic:
+                    ref = oracle_f2t(lay, [host[0], host[2], host[1]], h.in_shape[2], h.in_shape[3], cfg)
+                    assert_tensor_close(_tensor_np(t), ref, f"odd-width f2t {W}")
+                    tn = _tensor_np(to)
+                    for c in range(2):
+                        refo = oracle_t2f(tn[c:c + 1], 1, olay, cfg)
+                        assert_codes_close(out.host_planes(c), refo[0], f"odd-width t2f {W} {c}")
+            monkeypatch.delenv("NNVISR_FORCE_GENERIC", raising=False)
+        assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1]), W
