@@ -77,7 +77,7 @@ enum { NNVISR_LIMITED = 0, NNVISR_FULL = 1 };
  * co-sited with even luma columns, vertically centred (up: 1 | 1/2,1/2
  * horizontally; down: [1,2,1]/4 horizontally, 1/2,1/2 vertically; SPEC.md
  * S:339-347).  Both sitings run on the TMA-pipelined kernels where the
- * geometry allows (16-byte aligned rows, width a multiple of 32). */
+ * geometry allows (16-byte aligned planes, pitches and tensor rows). */
 enum { NNVISR_CHROMA_CENTER = 0, NNVISR_CHROMA_LEFT = 1 };
 /* tensor element type */
 enum { NNVISR_F32 = 0, NNVISR_F16 = 1 };

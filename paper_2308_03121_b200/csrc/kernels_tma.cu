@@ -847,9 +847,13 @@ __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *
     const int64_t plane = a.th * a.tw;
     const TIN *src = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
                      static_cast<int64_t>(3 * o) * plane + static_cast<int64_t>(ru * ROWS) * a.tw + x0;
-    // LEFT siting: also the lpad values left of the segment (x0 > 0; 16 bytes)
+    // LEFT siting: also the lpad values left of the segment (x0 > 0; 16 bytes);
+    // a ragged end (output width not a multiple of 8) is copied up to the next
+    // 16 bytes, inside the tensor row (its width is a 16-byte multiple)
     const int pre = x0 > 0 ? a.lpad : 0;
-    const uint32_t bytes = (x1 - x0 + pre) * sizeof(TIN);
+    constexpr int G = 16 / sizeof(TIN);
+    const int xe = (x1 + G - 1) / G * G;
+    const uint32_t bytes = (xe - x0 + pre) * sizeof(TIN);
     mbar_arrive_expect_tx(bar, ROWS * 3 * bytes);
 #pragma unroll
     for (int r = 0; r < ROWS; ++r)
@@ -922,6 +926,9 @@ __global__ void __launch_bounds__(kThreads + 32, (FAMILY == kYUV420 && sizeof(AR
         }
         if (h.x0 + xo < h.x1) {
             const int x = h.x0 + xo;
+            // the last group of a ragged row stores only its valid columns
+            const int nv = min(kPx, h.x1 - x);
+            const bool vec = a.vec_out && nv == kPx;
             AR sb[4], sr[4];
             if (FAMILY == kYUV420 && a.lpad) {
                 // LEFT (MPEG-2) siting: per row the [1,2,1] taps need B-Y', R-Y'
@@ -938,10 +945,10 @@ __global__ void __launch_bounds__(kThreads + 32, (FAMILY == kYUV420 && sizeof(AR
                     tload8(p0 + xo, R);
                     tload8(p1 + xo, G);
                     tload8(p2 + xo, B);
-                    t2f_row<FAMILY, OS, AR, true>(c, a.col, f, x, h.y0 + r, r, R, G, B, kPx, a.vec_out, sb, sr,
-                                                  b_ - Yl, r_ - Yl);
+                    t2f_row<FAMILY, OS, AR, true>(c, a.col, f, x, h.y0 + r, r, R, G, B, nv, vec, sb, sr, b_ - Yl,
+                                                  r_ - Yl);
                 }
-                if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR, true>(c, f, x, h.y0, sb, sr, kPx, a.vec_out);
+                if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR, true>(c, f, x, h.y0, sb, sr, nv, vec);
             } else {
 #pragma unroll
                 for (int r = 0; r < ROWS; ++r) {
@@ -949,9 +956,9 @@ __global__ void __launch_bounds__(kThreads + 32, (FAMILY == kYUV420 && sizeof(AR
                     tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 0) + xo, R);
                     tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 1) + xo, G);
                     tload8(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, 2) + xo, B);
-                    t2f_row<FAMILY, OS, AR>(c, a.col, f, x, h.y0 + r, r, R, G, B, kPx, a.vec_out, sb, sr);
+                    t2f_row<FAMILY, OS, AR>(c, a.col, f, x, h.y0 + r, r, R, G, B, nv, vec, sb, sr);
                 }
-                if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, h.y0, sb, sr, kPx, a.vec_out);
+                if constexpr (FAMILY == kYUV420) t2f_chroma420<OS, AR>(c, f, x, h.y0, sb, sr, nv, vec);
             }
         }
         __syncwarp();

@@ -678,9 +678,9 @@ nnvisr_status run_t2f(nnvisr_handle *h, T2FArgs a, int64_t jobs, cudaStream_t st
     // 16-byte aligned too (their base, strides and rows)
     const bool yuv_ok = !a.yuv || (reinterpret_cast<uintptr_t>(a.src2) % 16 == 0 && a.tensor_stride2 % 16 == 0 &&
                                    (a.thc * a.twc * h->elem) % 16 == 0 && (a.twc * h->elem) % 16 == 0);
-    // segments of whole 8-column groups with 16-byte copies: Wo % 8 (and
-    // % 16 for the half-width YUV-native chroma rows)
-    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wo % (a.yuv ? 16 : 8) == 0 &&
+    // any output width for RGB tensors (a ragged last group stores its valid
+    // columns); YUV-native: Wo % 16 (16-byte half-width chroma rows)
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && (!a.yuv || h->Wo % 16 == 0) &&
                a.tensor_stride % 16 == 0 &&
                reinterpret_cast<uintptr_t>(a.src) % 16 == 0 && yuv_ok;
     cudaError_t e = launch_t2f(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);
