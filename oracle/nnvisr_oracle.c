@@ -3,7 +3,7 @@
  *
  * A plain, slow, scalar, double-precision CPU implementation of what the
  * NNVISR frame<->tensor hot path computes (arXiv 2308.03121, §3.1 and
- * §3.3; the silent points follow the readings A1..A15 listed in DESIGN.md §3,
+ * §3.3; the silent points follow the readings A1..A22 listed in DESIGN.md §3,
  * which restate SURVEY.md §8(c)).  Only tests/, __graft_entry__.smoke() and
  * bench.py's cpu_baseline / --impl reference leg may load this library.  The
  * product path (paper_2308_03121_b200/) never links, imports or calls it, and
@@ -24,6 +24,8 @@
  *                          fields, LEFT == 4:4:4 path, down/up identity)
  *   oracle_f2t_yuv / oracle_t2f_yuv pinned (range endpoints, affine shape,
  *                          gray vs RGB path, exact round trip, B4 specials)
+ *   oracle_scene_detect    pinned (SPEC scenedetect examples, numpy SAD)
+ *   oracle_rgb_to_codes / oracle_codes_to_rgb  pinned (colour-bar table)
  *   chroma siting / padding / channel order / even-N centring: conventions,
  *   "parity unpinned" beyond internal consistency (readings A5-A8).
  */
