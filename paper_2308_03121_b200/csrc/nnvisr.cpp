@@ -608,7 +608,9 @@ nnvisr_status run_f2t(nnvisr_handle *h, F2TArgs a, int64_t jobs, int64_t dests, 
     const bool yuv_ok = !a.yuv || (reinterpret_cast<uintptr_t>(a.dst2) % 16 == 0 && a.run_stride2 % 16 == 0 &&
                                    a.slot_bytes2 % 16 == 0 && a.cplane_bytes % 16 == 0 &&
                                    (a.Wc * h->elem) % 16 == 0);
-    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out &&
+    // (the padded width Wp a multiple of 8: whole 8-column groups in the
+    // consumers' output staging rows)
+    a.tma_ok = !h->force_generic && a.vec_in && a.vec_out && h->Wp % kPx == 0 &&
                reinterpret_cast<uintptr_t>(a.dst) % 16 == 0 && a.run_stride % 16 == 0 && a.slot_bytes % 16 == 0 &&
                yuv_ok;
     cudaError_t e = launch_f2t(h->fmt.family, h->fmt.bits, h->net.dtype, a, st);

@@ -1,0 +1,111 @@
+"""Seeded random configurations through the C ABI against the oracle: clip
+family / depth / matrix / range / siting, tensor format (RGB or YUV-native)
+and dtype, frame size (odd widths included: TMA and generic paths), window
+length, alignment, scale factor and cut pattern, drawn from one generator.
+Bars as in test_gpu_parity (fp32 1e-6, fp16 1 ULP, codes +-1 with >= 99.9%
+exact, pooled over the case)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2308_03121_b200 import nnvisr as nv
+from paper_2308_03121_b200 import synth
+from paper_2308_03121_b200.frames import FrameBuffer, FrameLayout
+
+from .helpers import CodeStats, assert_tensor_close
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _draw(seed):
+    rs = np.random.default_rng(seed)
+    family = int(rs.choice([nv.YUV420, nv.YUV444, nv.RGB]))
+    yuv = family != nv.RGB and rs.random() < 0.3
+    left = family == nv.YUV420 and not yuv and rs.random() < 0.3
+    W = int(rs.integers(1, 160)) * 2 + (0 if family == nv.YUV420 else int(rs.integers(0, 2)))
+    H = int(rs.integers(1, 12)) * 2
+    interp = rs.random() < 0.3  # paper grouping: n = 1, extra + double frame, M = 2n + 1 = 3
+    return dict(family=family, bits=int(rs.choice([8, 10, 16])), dtype=int(rs.choice([nv.F32, nv.F16])),
+                matrix=int(rs.integers(0, 3)), rng_=int(rs.integers(0, 2)), W=W, H=H,
+                N=2 if interp else int(rs.integers(1, 6)), M=3 if interp else 1, interp=interp,
+                align=int(rs.choice([1, 2, 8, 16, 32])), sx=int(rs.choice([1, 2])), yuv=yuv, left=left,
+                F=int(rs.integers(3, 9)), seed=int(rs.integers(1 << 30)))
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_random_configuration(seed):
+    p = _draw(seed)
+    if p["family"] == nv.YUV420 and p["sx"] == 1 and p["W"] % 2:
+        pytest.skip("odd 4:2:0 width")
+    flags = (nv.YUV_INPUT | nv.YUV_OUTPUT) if p["yuv"] else 0
+    if p["interp"]:
+        flags |= nv.INTERPOLATION | nv.EXTRA_FRAME | nv.DOUBLE_FRAME
+    M = p["M"]
+    cfg = nv.Config(p["W"], p["H"], p["family"], p["bits"], p["matrix"], p["rng_"], input_count=p["N"],
+                    output_count=M, n=1, left_context=0 if p["interp"] else -1, flags=flags, align=p["align"],
+                    dtype=p["dtype"],
+                    sx=(p["sx"], 1), sy=(p["sx"], 1),
+                    chroma_loc=nv.CHROMA_LEFT if p["left"] else nv.CHROMA_CENTER)
+    lay = FrameLayout(p["W"], p["H"], p["family"], p["bits"])
+    rs = np.random.default_rng(p["seed"])
+    F = p["F"]
+    host = [synth.random_planes(lay, int(rs.integers(1 << 30))) for _ in range(F)]
+    buf = FrameBuffer(lay, F, device=DEV)
+    for i, pl in enumerate(host):
+        buf.set_planes(i, pl)
+    cut = (rs.random(F) < 0.3).astype(np.uint8)
+    odt = O.F16 if p["dtype"] == nv.F16 else O.F32
+    tdt = torch.float16 if p["dtype"] == nv.F16 else torch.float32
+    siting = O.CHROMA_LEFT if p["left"] else O.CHROMA_CENTER
+    with nv.open(cfg) as h:
+        runs, _ = h.plan(cut)
+        oruns, _ = O.plan(cut, 1, p["N"], 0 if p["interp"] else (p["N"] - 1) // 2)
+        assert np.array_equal(runs, oruns)
+        _, N, Hp, Wp = h.in_shape
+        per = N * Hp * Wp + (int(np.prod(h.in_chroma_shape)) if p["yuv"] else 2 * N * Hp * Wp)
+        pstride = -(-per // 8) * 8
+        t = torch.full((len(runs), pstride), float("nan"), dtype=tdt, device=DEV)
+        h.bind_frames(buf.descriptors())
+        h.frames_to_tensor_batch(runs, t.data_ptr(), pstride * t.element_size())
+        Ho, Wo = h.out_shape[2], h.out_shape[3]
+        olay = FrameLayout(Wo, Ho, p["family"], p["bits"])
+        if p["yuv"]:
+            _, _, thc, twc = h.out_chroma_shape
+            oper = M * Ho * Wo + 2 * M * thc * twc
+        else:
+            oper = 3 * M * Ho * Wo
+        ostride = -(-oper // 8) * 8
+        to = synth.random_tensor((2, ostride), p["dtype"], p["seed"] + 1, device=DEV)
+        out = FrameBuffer(olay, 2 * M, device=DEV)
+        h.tensor_to_frames_batch(to.data_ptr(), ostride * to.element_size(), Ho, Wo, out.descriptors(), 2)
+        torch.cuda.synchronize()
+        tn = t.cpu().numpy()
+        for r, run in enumerate(runs):
+            frames = [host[i] for i in run]
+            if p["yuv"]:
+                rl, rc = O.f2t_yuv(frames, p["W"], p["H"], p["family"], p["bits"], p["matrix"], p["rng_"], Hp, Wp,
+                                   odt)
+                nl = N * Hp * Wp
+                assert_tensor_close(tn[r, :nl].reshape(rl.shape), rl, f"{p} run {r} luma")
+                assert_tensor_close(tn[r, nl:nl + rc.size].reshape(rc.shape), rc, f"{p} run {r} chroma")
+            else:
+                ref = O.f2t(frames, p["W"], p["H"], p["family"], p["bits"], p["matrix"], p["rng_"], Hp, Wp, odt,
+                            siting=siting)
+                assert_tensor_close(tn[r, :ref.size].reshape(ref.shape), ref, f"{p} run {r}")
+        ton = to.cpu().numpy()
+        stats = CodeStats()
+        for c in range(2):
+            if p["yuv"]:
+                _, _, thc, twc = h.out_chroma_shape
+                lu = ton[c, :M * Ho * Wo].reshape(1, M, Ho, Wo)
+                ch = ton[c, M * Ho * Wo:M * Ho * Wo + 2 * M * thc * twc].reshape(1, 2 * M, thc, twc)
+                ref = O.t2f_yuv(lu, ch, M, Wo, Ho, p["family"], p["bits"], p["matrix"], p["rng_"])
+            else:
+                ref = O.t2f(ton[c, :3 * M * Ho * Wo].reshape(1, 3 * M, Ho, Wo), M, Wo, Ho, p["family"], p["bits"],
+                            p["matrix"], p["rng_"], siting=siting)
+            for o in range(M):
+                stats.add(out.host_planes(c * M + o), ref[o], f"{p} t2f {c}.{o}")
+        if stats.total >= 4000:
+            stats.check(f"{p}")
