@@ -1258,7 +1258,10 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
         a.trace = trace_buf;
     }
     kernel<<<grid, block, smem, s>>>(a);
-    if ((a.debug & 8) && std::getenv("NNVISR_F2T_TRACE")) {  // dump the launch's timeline (experiments only)
+    static int traced_launch = 0;  // NNVISR_F2T_TRACE_LAUNCH = k: dump only the k-th traced launch
+    const bool dump = (a.debug & 8) && std::getenv("NNVISR_F2T_TRACE") &&
+                      traced_launch++ == env_int("NNVISR_F2T_TRACE_LAUNCH", traced_launch - 1);
+    if (dump) {  // dump the launch's timeline (experiments only)
         std::vector<uint64_t> h(kTraceBytes / sizeof(uint64_t));
         cudaMemcpyAsync(h.data(), trace_buf, kTraceBytes, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
