@@ -303,9 +303,17 @@ def main():
         store = torch.empty((per_launch * bmax, slot_bytes // esz), dtype=tdt, device=dev)
     stream = torch.cuda.Stream(device=dev)
 
+    # the flags the planner reads: on one GPU without --detect they are host
+    # data (no device round trip per step); otherwise they come from the
+    # device (halo exchange / GPU scene detection) each step
+    host_flags = world == 1 and not args.detect
+    cut_host = cut_all[s.window_first:s.window_first + s.window_count].copy()
+
+    def flags_now():
+        return cut_host if host_flags else cut_win.cpu().numpy()
+
     def plan_local():
-        cw = cut_win.cpu().numpy()
-        return h.plan_range(total, s.window_first, cw, s.begin, s.end)
+        return h.plan_range(total, s.window_first, flags_now(), s.begin, s.end)
 
     # per launch: (start event, end event, units, algorithmic bytes)
     ev_pairs = {"f2t": [], "t2f": [], "detect": []}
@@ -350,7 +358,7 @@ def main():
                     timed("f2t", record, 0, len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz,
                           lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
             elif args.f2t_mode == "batch":
-                batches = h.plan_batches(cut_win.cpu().numpy(), args.batch)
+                batches = h.plan_batches(flags_now(), args.batch)
                 for c0 in range(0, len(batches), per_launch):
                     grp = batches[c0:c0 + per_launch]
                     sf = np.full(len(grp) * bmax, -1, np.int64)
@@ -373,7 +381,7 @@ def main():
                         timed("f2t", record, len(sel), nbytes,
                               lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz,
                                                                        stream))
-            sched = h.schedule_outputs(cut_win.cpu().numpy())[s.begin - s.window_first:] if args.emit else None
+            sched = h.schedule_outputs(flags_now())[s.begin - s.window_first:] if args.emit else None
             for c0 in range(0, len(runs), tchunk):
                 nb = min(tchunk, len(runs) - c0)
                 o0 = (c0 // tchunk * tchunk) % n_out
