@@ -53,6 +53,9 @@ def parse():
                    help="4:2:0 chroma siting: centre (default) or LEFT / MPEG-2 (NEXT-3)")
     p.add_argument("--frames", type=int, default=0,
                    help="clip frames per rank (0 = the workload's; profiling/sweeps only, recorded in config)")
+    p.add_argument("--halo", default="p2p", choices=["p2p", "peer"],
+                   help="N > 1: copy the halo frames each step (NCCL P2P) or read them in place from the "
+                        "neighbours' buffers (nnvisr_peer_import; only the flags travel)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--detect", action="store_true",
                    help="detect scene changes on the GPU each step (NEXT-4) and plan from those flags")
@@ -256,7 +259,12 @@ def main():
     synth.generate_clip(w, device=dev, frames=s.owned, first=s.begin, total_frames=total, out=win, out_offset=s.left)
     cut_win = torch.zeros(s.window_count, dtype=torch.uint8, device=dev)
     cut_win[s.left:s.left + s.owned] = torch.from_numpy(cut_all[s.begin:s.end]).to(dev)
-    h.bind_frames(win.descriptors(), base=s.window_first)
+    peer = None
+    if world > 1 and args.halo == "peer":
+        peer = sh.PeerHalo(s, win.data)
+        h.bind_frames(peer.descriptors(lay), base=s.window_first)
+    else:
+        h.bind_frames(win.descriptors(), base=s.window_first)
 
     # buffers (rings larger than L2 so no step re-reads L2-resident data)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -336,7 +344,7 @@ def main():
     def step(record: bool):
         if world > 1:
             with torch.cuda.stream(stream):
-                sh.halo_exchange(s, win.data, cut_win)
+                sh.halo_exchange(s, None if peer else win.data, cut_win)
         if args.detect:
             # the flags the plan consumes come from the frames themselves
             with torch.cuda.stream(stream):
@@ -507,7 +515,7 @@ def main():
                                        if args.detect else "given (synthetic cut pattern)"),
                        "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB, t2f input ring "
                                     f"{n_out} x {out_elems * esz / 1e6:.0f} MB >= 4 x L2 ({l2 / 1e6:.0f} MB)",
-                       "parallelism": f"frame-range shards x{world}, halo P2P"},
+                       "parallelism": f"frame-range shards x{world}, halo " + ("peer-mapped" if peer else "P2P")},
             "unit_definition": "1 frame = one tuple through frames->tensor plus its network output through "
                                "tensor->frames (n = 1: one tuple per clip frame)",
             "per_direction": per_dir,
@@ -519,6 +527,8 @@ def main():
             "seed": w.seed,
         }
         print(json.dumps(line), flush=True)
+    if peer:
+        peer.close()
     h.close()
     if world > 1:
         dist.destroy_process_group()

@@ -353,6 +353,39 @@ nnvisr_status nnvisr_copy_slot(nnvisr_handle *h, void *store, int64_t src, int64
 nnvisr_status nnvisr_scene_detect(nnvisr_handle *h, int64_t first, int64_t count, double threshold,
                                   uint64_t *sad, uint8_t *cut, void *stream);
 
+/* ---- Multi-GPU halo by peer mapping (rank r's tuples
+ * near its shard edges read up to L frames owned by rank r-1 and N-1-L
+ * frames owned by rank r+1, §3.2 P:347-358 sliding windows).  One
+ * process per GPU.  Instead of copying those frames, each rank exports the
+ * device buffer that holds its own frames, its neighbours import it, and the
+ * halo frames are bound (nnvisr_bind_frames) as descriptors pointing into
+ * the neighbour's buffer: the f2t kernels then read them in place, over
+ * NVLink between GPUs.  The caller exchanges the handles (e.g. with
+ * torch.distributed all_gather_object) and orders the neighbour's writes
+ * before the reads (a barrier or an interprocess event), as it would order a
+ * copy.  The cut flags of the halo frames are host data and travel with the
+ * caller's own exchange. */
+typedef struct {
+    uint8_t ipc[64];  /* CUDA IPC memory handle of the allocation holding the pointer */
+    int64_t offset;   /* the pointer's byte offset inside that allocation */
+} nnvisr_peer_handle;
+
+/* Export device pointer dev_ptr (inside any cudaMalloc allocation, e.g. a
+ * torch tensor's data_ptr()) of the current process.  The allocation must
+ * outlive every importer's use.  NNVISR_ERR_INVALID_ARG for a null or host
+ * pointer, NNVISR_ERR_CUDA if the allocation cannot be exported. */
+nnvisr_status nnvisr_peer_export(const void *dev_ptr, nnvisr_peer_handle *out);
+
+/* Map an exported buffer of ANOTHER process into this one (on the current
+ * device; peer access is enabled lazily) and return the device pointer that
+ * corresponds to the exporter's dev_ptr.  Importing a handle in the process
+ * that exported it fails with NNVISR_ERR_CUDA (CUDA IPC forbids it). */
+nnvisr_status nnvisr_peer_import(const nnvisr_peer_handle *in, void **dev_ptr);
+
+/* Unmap a pointer returned by nnvisr_peer_import (after the work reading it
+ * has completed).  NNVISR_ERR_INVALID_ARG for a pointer not imported here. */
+nnvisr_status nnvisr_peer_close(void *dev_ptr);
+
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t nnvisr_launch_count(void);
 

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1423,6 +1425,79 @@ nnvisr_status nnvisr_tensor_to_frames_batch_host(nnvisr_handle *h, const void *t
         return cuda_fail(e, "cudaEventRecord");
     g.used = true;
     h->d2h_any = true;
+    return NNVISR_OK;
+}
+
+// ---- peer mapping (multi-GPU halo) ----
+
+static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(((nnvisr_peer_handle *)nullptr)->ipc), "IPC handle size");
+
+nnvisr_status nnvisr_peer_export(const void *dev_ptr, nnvisr_peer_handle *out)
+{
+    g_error.clear();
+    if (!dev_ptr || !out) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, dev_ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaPointerGetAttributes");
+    if (at.type != cudaMemoryTypeDevice) return fail(NNVISR_ERR_INVALID_ARG, "not a device pointer");
+    // IPC exports whole allocations: find the one holding dev_ptr (a caching
+    // allocator hands out pointers inside larger cudaMalloc blocks)
+    using AddressRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+    static AddressRange range = nullptr;
+    if (!range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+            return fail(NNVISR_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+        range = reinterpret_cast<AddressRange>(fn);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+        return fail(NNVISR_ERR_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t ih;
+    e = cudaIpcGetMemHandle(&ih, reinterpret_cast<void *>(base));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    std::memcpy(out->ipc, &ih, sizeof ih);
+    out->offset = static_cast<int64_t>(reinterpret_cast<unsigned long long>(dev_ptr) - base);
+    return NNVISR_OK;
+}
+
+namespace {
+std::mutex g_peer_mu;
+std::map<uintptr_t, void *> g_peer_bases;  // imported pointer -> mapped allocation base
+}  // namespace
+
+nnvisr_status nnvisr_peer_import(const nnvisr_peer_handle *in, void **dev_ptr)
+{
+    g_error.clear();
+    if (!in || !dev_ptr) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (in->offset < 0) return fail(NNVISR_ERR_INVALID_ARG, "negative offset");
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, in->ipc, sizeof ih);
+    void *base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    *dev_ptr = static_cast<char *>(base) + in->offset;
+    std::lock_guard<std::mutex> lk(g_peer_mu);
+    g_peer_bases[reinterpret_cast<uintptr_t>(*dev_ptr)] = base;
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_peer_close(void *dev_ptr)
+{
+    g_error.clear();
+    void *base = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_peer_mu);
+        auto it = g_peer_bases.find(reinterpret_cast<uintptr_t>(dev_ptr));
+        if (it == g_peer_bases.end()) return fail(NNVISR_ERR_INVALID_ARG, "pointer was not imported by nnvisr_peer_import");
+        base = it->second;
+        g_peer_bases.erase(it);
+    }
+    cudaError_t e = cudaIpcCloseMemHandle(base);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
     return NNVISR_OK;
 }
 

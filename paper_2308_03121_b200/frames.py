@@ -80,6 +80,16 @@ class FrameLayout:
         return rec
 
 
+def descriptor_at(layout: FrameLayout, base: int) -> nv.Frame:
+    """The frame descriptor of a packed frame record of `layout` at device
+    address `base` (a local buffer, or a neighbour's mapped by nnvisr_peer_import)."""
+    f = nv.Frame()
+    for p, (off, pitch, _, _) in enumerate(layout.planes()):
+        f.plane[p] = base + off
+        f.pitch[p] = pitch
+    return f
+
+
 class FrameBuffer:
     """`count` frames of one layout in a single uint8 tensor [count, frame_bytes]."""
 
@@ -99,12 +109,7 @@ class FrameBuffer:
         return self.layout.frame_bytes
 
     def descriptor(self, i: int) -> nv.Frame:
-        base = self.data.data_ptr() + int(i) * self.layout.frame_bytes
-        f = nv.Frame()
-        for p, (off, pitch, _, _) in enumerate(self._planes):
-            f.plane[p] = base + off
-            f.pitch[p] = pitch
-        return f
+        return descriptor_at(self.layout, self.data.data_ptr() + int(i) * self.layout.frame_bytes)
 
     def descriptors(self, indices=None):
         idx = range(self.count) if indices is None else indices

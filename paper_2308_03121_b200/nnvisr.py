@@ -32,6 +32,11 @@ class NnvisrError(RuntimeError):
         self.message = message
 
 
+class PeerHandle(C.Structure):
+    """nnvisr_peer_handle: CUDA IPC handle of an allocation + the pointer's offset in it."""
+    _fields_ = [("ipc", C.c_uint8 * 64), ("offset", C.c_int64)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build()")
@@ -70,6 +75,9 @@ def _load():
         "nnvisr_frames_to_tensor_yuv_batch": (st, [H, i64p, i64, C.c_void_p, i64, C.c_void_p, i64, C.c_void_p]),
         "nnvisr_tensor_to_frames_yuv_batch": (st, [H, C.c_void_p, i64, C.c_void_p, i64, i64, i64, C.POINTER(Frame),
                                                    i64, C.c_void_p]),
+        "nnvisr_peer_export": (st, [C.c_void_p, C.POINTER(PeerHandle)]),
+        "nnvisr_peer_import": (st, [C.POINTER(PeerHandle), C.POINTER(C.c_void_p)]),
+        "nnvisr_peer_close": (st, [C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -86,7 +94,8 @@ EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version"
             "nnvisr_shared_slot_offset", "nnvisr_plan_batches", "nnvisr_frames_to_slots", "nnvisr_copy_slot",
             "nnvisr_schedule_outputs", "nnvisr_copy_frames", "nnvisr_frames_to_tensor_batch_host",
             "nnvisr_tensor_to_frames_batch_host", "nnvisr_host_fence", "nnvisr_chroma_shapes",
-            "nnvisr_frames_to_tensor_yuv_batch", "nnvisr_tensor_to_frames_yuv_batch")
+            "nnvisr_frames_to_tensor_yuv_batch", "nnvisr_tensor_to_frames_yuv_batch", "nnvisr_peer_export",
+            "nnvisr_peer_import", "nnvisr_peer_close")
 
 
 def lib():
@@ -117,6 +126,27 @@ def _stream_ptr(stream) -> int | None:
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+def peer_export(dev_ptr: int) -> bytes:
+    """nnvisr_peer_export: a device pointer of this process as portable bytes
+    (send them to the neighbouring ranks)."""
+    h = PeerHandle()
+    _check(_lib.nnvisr_peer_export(dev_ptr, C.byref(h)))
+    return bytes(h)
+
+
+def peer_import(handle: bytes) -> int:
+    """nnvisr_peer_import: map another process's exported pointer here."""
+    h = PeerHandle.from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(_lib.nnvisr_peer_import(C.byref(h), C.byref(p)))
+    return int(p.value)
+
+
+def peer_close(dev_ptr: int) -> None:
+    """nnvisr_peer_close: unmap a pointer returned by peer_import."""
+    _check(_lib.nnvisr_peer_close(dev_ptr))
 
 
 def frame_array(frames: Sequence[Frame]):

@@ -251,3 +251,12 @@ def test_schedule_outputs_matches_oracle():
         cut = np.zeros(9, np.uint8)
         cut[4] = 1
         assert h.schedule_outputs(cut) == [[(0, t)] for t in range(9)]
+
+
+def test_peer_calls_validate_arguments():
+    # argument checks only (no device work): null pointers, an unknown import
+    for bad in (lambda: nv.peer_export(0), lambda: nv.peer_close(0x1000)):
+        with pytest.raises(nv.NnvisrError) as ei:
+            bad()
+        assert ei.value.status == 2
+    assert len(nv.PeerHandle().ipc) == 64

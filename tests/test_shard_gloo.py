@@ -96,3 +96,34 @@ def test_shard_geometry():
     assert (s.begin, s.end, s.left, s.right) == (75, 100, 2, 0)
     with pytest.raises(ValueError):
         sh.shard_of(5, 4, 1, 2, 2)  # a 1-frame shard is shorter than the halo
+
+
+@pytest.mark.parametrize("world,L,R", [(2, 2, 2), (3, 1, 1), (4, 0, 1), (8, 1, 2), (3, 2, 0)])
+def test_peer_halo_addresses_name_the_owners_rows(world, L, R):
+    """PeerHalo.frame_address: an owned row is the rank's own buffer row; a
+    halo row is the owning neighbour's row of that same global frame (its
+    own rows, never its halo), for every rank and every window row."""
+    total, fb = 40, 1000
+    shards = [sh.shard_of(total, world, r, L, R) for r in range(world)]
+    bases = [(r + 1) << 32 for r in range(world)]
+
+    class _Win:  # stands in for the window tensor (data_ptr, shape)
+        def __init__(self, r, count):
+            self.r, self.shape = r, (count, fb)
+
+        def data_ptr(self):
+            return bases[self.r]
+
+    for r, s in enumerate(shards):
+        p = sh.PeerHalo.__new__(sh.PeerHalo)
+        p.s, p.window, p.frame_bytes = s, _Win(r, s.window_count), fb
+        p.peer = {q: bases[q] for q in (r - 1, r + 1) if 0 <= q < world}
+        for k in range(s.window_count):
+            g = s.window_first + k
+            addr = p.frame_address(k)
+            owner = next(q for q in range(world) if shards[q].begin <= g < shards[q].end)
+            row = (addr - bases[owner]) // fb
+            assert (addr - bases[owner]) % fb == 0 and 0 <= row < shards[owner].window_count
+            assert shards[owner].window_first + row == g
+            assert shards[owner].left <= row < shards[owner].left + shards[owner].owned
+            assert owner == r or abs(owner - r) == 1
