@@ -24,7 +24,23 @@ $(LIB): $(PKG)/build/nnvisr.o $(PKG)/build/kernels.o $(PKG)/build/kernels_tma.o 
 $(ORACLE): oracle/nnvisr_oracle.c
 	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -Wall -fPIC -shared -o $@ $< -lm
 
-clean:
-	rm -rf $(PKG)/build $(LIB) $(ORACLE)
+# checked build (device-side bounds checks, -DNNVISR_CHECKED): select it with
+# NNVISR_LIBNAME=libnnvisr_checked.so (tools/checked_tests.sh)
+CHK      = $(PKG)/libnnvisr_checked.so
+checked: $(CHK)
 
-.PHONY: all clean
+$(PKG)/build_checked/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p $(PKG)/build_checked
+	$(NVCC) $(NVFLAGS) -DNNVISR_CHECKED -c $< -o $@ 2> $(PKG)/build_checked/$*.ptxas.txt || (cat $(PKG)/build_checked/$*.ptxas.txt; false)
+
+$(PKG)/build_checked/%.o: $(PKG)/csrc/%.cpp $(HDR)
+	@mkdir -p $(PKG)/build_checked
+	$(NVCC) $(NVFLAGS) -DNNVISR_CHECKED -c $< -o $@
+
+$(CHK): $(PKG)/build_checked/nnvisr.o $(PKG)/build_checked/kernels.o $(PKG)/build_checked/kernels_tma.o $(PKG)/build_checked/kernels_yuv.o $(PKG)/build_checked/scene.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
+
+clean:
+	rm -rf $(PKG)/build $(PKG)/build_checked $(LIB) $(CHK) $(ORACLE)
+
+.PHONY: all checked clean

@@ -5,10 +5,46 @@
 
 #include <cuda_fp16.h>
 
+#include <cstdio>
+
 #include "internal.h"
 
 namespace nnvisr {
 namespace dev {
+
+// ------------------------------------------------------------ checked builds
+// `make checked` (-DNNVISR_CHECKED, libnnvisr_checked.so): compute-sanitizer
+// is closed on the GPU pool, so the kernels check their own accesses -- every
+// shared-memory vector access of the staging kernels lies inside the dynamic
+// shared memory, every TMA copy is 16-byte aligned and, in f2t, lands inside
+// its stage / reads inside its output buffer and a bound frame's planes.  A
+// failed check prints the site and traps (the launch fails loudly).
+#ifdef NNVISR_CHECKED
+extern __shared__ __align__(16) uint8_t nnvisr_dsmem[];  // aliases every kernel's dynamic smem
+__device__ __forceinline__ bool smem_ok(const void *p, uint32_t n)
+{
+    if (!__isShared(p)) return true;
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const uint32_t o = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(nnvisr_dsmem));
+    return o >= b && o + n <= b + dyn;
+}
+#define NNVISR_CHECK(cond)                                                                                   \
+    do {                                                                                                     \
+        if (!(cond)) {                                                                                       \
+            printf("nnvisr check failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,       \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                       \
+            __trap();                                                                                        \
+        }                                                                                                    \
+    } while (0)
+#define NNVISR_CHECK_SMEM(p, n) NNVISR_CHECK(::nnvisr::dev::smem_ok((p), (n)))
+#else
+#define NNVISR_CHECK(cond) \
+    do {                   \
+    } while (0)
+#define NNVISR_CHECK_SMEM(p, n) NNVISR_CHECK(true)
+#endif
 
 // ------------------------------------------------------------------ memory
 __device__ __forceinline__ uint4 ld_stream_v4(const void *p)
@@ -294,7 +330,11 @@ template <> struct Row8<__half> {
     {
         v = make_uint4(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]), pack_half2(x[4], x[5]), pack_half2(x[6], x[7]));
     }
-    __device__ __forceinline__ void store(__half *p) const { *reinterpret_cast<uint4 *>(p) = v; }
+    __device__ __forceinline__ void store(__half *p) const
+    {
+        NNVISR_CHECK_SMEM(p, 16);
+        *reinterpret_cast<uint4 *>(p) = v;
+    }
     __device__ __forceinline__ void store_n(__half *p, int n) const
     {
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -312,6 +352,7 @@ template <> struct Row8<float> {
     }
     __device__ __forceinline__ void store(float *p) const
     {
+        NNVISR_CHECK_SMEM(p, 32);
         reinterpret_cast<float4 *>(p)[0] = a;
         reinterpret_cast<float4 *>(p)[1] = b;
     }
@@ -329,7 +370,11 @@ template <typename OUT> struct Row4;
 template <> struct Row4<__half> {
     uint2 v;
     __device__ __forceinline__ void set(const float (&x)[4]) { v = make_uint2(pack_half2(x[0], x[1]), pack_half2(x[2], x[3])); }
-    __device__ __forceinline__ void store(__half *p) const { *reinterpret_cast<uint2 *>(p) = v; }
+    __device__ __forceinline__ void store(__half *p) const
+    {
+        NNVISR_CHECK_SMEM(p, 8);
+        *reinterpret_cast<uint2 *>(p) = v;
+    }
     __device__ __forceinline__ void store_n(__half *p, int n) const
     {
         const uint32_t w[2] = {v.x, v.y};
@@ -341,7 +386,11 @@ template <> struct Row4<__half> {
 template <> struct Row4<float> {
     float4 v;
     __device__ __forceinline__ void set(const float (&x)[4]) { v = make_float4(x[0], x[1], x[2], x[3]); }
-    __device__ __forceinline__ void store(float *p) const { *reinterpret_cast<float4 *>(p) = v; }
+    __device__ __forceinline__ void store(float *p) const
+    {
+        NNVISR_CHECK_SMEM(p, 16);
+        *reinterpret_cast<float4 *>(p) = v;
+    }
     __device__ __forceinline__ void store_n(float *p, int n) const
     {
         const float x[4] = {v.x, v.y, v.z, v.w};
@@ -541,9 +590,14 @@ __device__ __forceinline__ void tunpack8(uint4 a, uint4 b, float (&x)[kPx])
     x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y); x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
 }
 // 8 tensor values from memory (global or shared), 16-byte aligned
-__device__ __forceinline__ void tload8(const __half *p, float (&x)[kPx]) { tunpack8(*reinterpret_cast<const uint4 *>(p), x); }
+__device__ __forceinline__ void tload8(const __half *p, float (&x)[kPx])
+{
+    NNVISR_CHECK_SMEM(p, 16);
+    tunpack8(*reinterpret_cast<const uint4 *>(p), x);
+}
 __device__ __forceinline__ void tload8(const float *p, float (&x)[kPx])
 {
+    NNVISR_CHECK_SMEM(p, 32);
     tunpack8(reinterpret_cast<const uint4 *>(p)[0], reinterpret_cast<const uint4 *>(p)[1], x);
 }
 __device__ __forceinline__ void tload8_stream(const __half *p, float (&x)[kPx]) { tunpack8(ld_stream_v4(p), x); }
@@ -554,6 +608,7 @@ __device__ __forceinline__ void tload8_stream(const float *p, float (&x)[kPx])
 // 4 tensor values from shared memory (8-byte aligned fp16, 16-byte fp32)
 __device__ __forceinline__ void tload4s(const __half *p, float (&x)[4])
 {
+    NNVISR_CHECK_SMEM(p, 8);
     const uint2 v = *reinterpret_cast<const uint2 *>(p);
     const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&v.x));
     const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&v.y));
@@ -561,11 +616,20 @@ __device__ __forceinline__ void tload4s(const __half *p, float (&x)[4])
 }
 __device__ __forceinline__ void tload4s(const float *p, float (&x)[4])
 {
+    NNVISR_CHECK_SMEM(p, 16);
     const float4 v = *reinterpret_cast<const float4 *>(p);
     x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
 }
-__device__ __forceinline__ float tload1(const __half *p) { return __half2float(p[0]); }
-__device__ __forceinline__ float tload1(const float *p) { return p[0]; }
+__device__ __forceinline__ float tload1(const __half *p)
+{
+    NNVISR_CHECK_SMEM(p, 2);
+    return __half2float(p[0]);
+}
+__device__ __forceinline__ float tload1(const float *p)
+{
+    NNVISR_CHECK_SMEM(p, 4);
+    return p[0];
+}
 
 // One output row y (row r of the item) of R', G', B' -> luma codes (and
 // 4:4:4 chroma codes, or the 4:2:0 partial 2x2 sums of B-Y', R-Y').

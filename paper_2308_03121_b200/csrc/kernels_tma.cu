@@ -73,6 +73,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 // global -> shared bulk copy (TMA engine; SASS UBLKCP), completes on `bar`.
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
 {
+    NNVISR_CHECK(((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 15) == 0);
+    NNVISR_CHECK_SMEM(dst, bytes);
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
@@ -81,6 +83,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // shared -> global bulk store (TMA engine), tracked by bulk groups
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes)
 {
+    NNVISR_CHECK(((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 15) == 0);
+    NNVISR_CHECK_SMEM(src, bytes);
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
                  "r"(bytes)
                  : "memory");
@@ -224,6 +228,16 @@ template <int FAMILY, typename IN> struct F2TStage {
     __device__ IN *plane(uint8_t *st, int p, int row) const { return reinterpret_cast<IN *>(st) + (p * B + row) * ls; }
 };
 
+// A vector of staged samples (checked builds: inside the tile's stage).
+template <typename V>
+__device__ __forceinline__ V ld_stage(const void *p, const uint8_t *st, int stage_bytes)
+{
+    NNVISR_CHECK(static_cast<const uint8_t *>(p) >= st && static_cast<const uint8_t *>(p) + sizeof(V) <= st + stage_bytes);
+    (void)st;
+    (void)stage_bytes;
+    return *reinterpret_cast<const V *>(p);
+}
+
 // Copy windows of a segment [x0, x1): luma [lw0, lw1), chroma [cw0, cw1).
 struct F2TWindow {
     int lw0, lw1, cw0, cw1;
@@ -325,8 +339,20 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
     uint32_t total = 0;
     f2t_copies<FAMILY, IN>(a, tl, w, f, st, [&](void *, const void *, uint32_t bytes) { total += bytes; });
     mbar_arrive_expect_tx(bar, total);
-    f2t_copies<FAMILY, IN>(a, tl, w, f, st,
-                           [&](void *dst, const void *src, uint32_t bytes) { bulk_g2s(dst, src, bytes, bar); });
+    f2t_copies<FAMILY, IN>(a, tl, w, f, st, [&](void *dst, const void *src, uint32_t bytes) {
+#ifdef NNVISR_CHECKED
+        // into this stage, from inside one of the frame's planes
+        NNVISR_CHECK(static_cast<uint8_t *>(dst) >= st && static_cast<uint8_t *>(dst) + bytes <= st + a.stage_bytes);
+        bool inside = false;
+        for (int p = 0; p < 3; ++p) {
+            const int rows = (p > 0 && FAMILY == kYUV420) ? a.H >> 1 : a.H;
+            const char *lo = static_cast<const char *>(f.plane[p]);
+            inside |= static_cast<const char *>(src) >= lo && static_cast<const char *>(src) + bytes <= lo + rows * f.pitch[p];
+        }
+        NNVISR_CHECK(inside);
+#endif
+        bulk_g2s(dst, src, bytes, bar);
+    });
 }
 
 // Warp-specialised: warps 0..7 convert (consumers); lane 0 of warps 8 and 9
@@ -475,6 +501,12 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                 dl.load(a, tl.job);
             }
             const OUT *ob = obuf + b * a.ob_elems;
+            // checked builds: every bulk store reads inside this tile's output buffer
+            auto s2g_ob = [&](OUT *dst, const OUT *src, uint32_t bytes) {
+                NNVISR_CHECK(src >= ob && reinterpret_cast<const char *>(src) + bytes <=
+                                              reinterpret_cast<const char *>(ob + a.ob_elems));
+                bulk_s2g(dst, src, bytes);
+            };
             const bool whole_rows = tl.x0 == 0 && sw == a.Wp;
             const int nd = (a.debug & 2) ? 0 : dl.nd;
             for (int d = 0; d < nd; ++d) {
@@ -488,10 +520,10 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                     constexpr bool SUB = FAMILY == kYUV420;
                     const int swc = SUB ? sw >> 1 : sw;
                     if (whole_rows) {
-                        bulk_s2g(o, ob, rows * sw * sizeof(OUT));
+                        s2g_ob(o, ob, rows * sw * sizeof(OUT));
                     } else {
                         for (int rr = 0; rr < rows; ++rr)
-                            bulk_s2g(o + static_cast<int64_t>(rr) * a.Wp, ob + rr * sw, sw * sizeof(OUT));
+                            s2g_ob(o + static_cast<int64_t>(rr) * a.Wp, ob + rr * sw, sw * sizeof(OUT));
                     }
                     char *cb = a.dst2 + static_cast<int64_t>(cd >> 5) * a.run_stride2 +
                                static_cast<int64_t>(cd & 31) * a.slot_bytes2;
@@ -501,10 +533,10 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                                  static_cast<int64_t>(tl.u0) * a.Wc + (SUB ? tl.x0 >> 1 : tl.x0);
                         const OUT *src = oc + pc * a.band * swc;
                         if (whole_rows) {
-                            bulk_s2g(q, src, tl.nu * swc * sizeof(OUT));
+                            s2g_ob(q, src, tl.nu * swc * sizeof(OUT));
                         } else {
                             for (int rr = 0; rr < tl.nu; ++rr)
-                                bulk_s2g(q + static_cast<int64_t>(rr) * a.Wc, src + rr * swc, swc * sizeof(OUT));
+                                s2g_ob(q + static_cast<int64_t>(rr) * a.Wc, src + rr * swc, swc * sizeof(OUT));
                         }
                     }
                     bulk_commit();
@@ -513,10 +545,10 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                 }
                 for (int c = 0; c < 3; ++c) {
                     if (whole_rows) {
-                        bulk_s2g(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
+                        s2g_ob(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
                     } else {
                         for (int rr = 0; rr < rows; ++rr)
-                            bulk_s2g(o + c * plane + static_cast<int64_t>(rr) * a.Wp, ob + (c * brows + rr) * sw,
+                            s2g_ob(o + c * plane + static_cast<int64_t>(rr) * a.Wp, ob + (c * brows + rr) * sw,
                                      sw * sizeof(OUT));
                     }
                 }
@@ -593,7 +625,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                         const IN *L = (SUB ? sg.luma(st, yc - tl.ly0) : sg.plane(st, 0, yc - tl.ly0)) - tl.lw0;
                         int c[kPx];
                         if (fast) {
-                            unpack8(*reinterpret_cast<const V8 *>(L + x), c);
+                            unpack8(ld_stage<V8>(L + x, st, a.stage_bytes), c);
                         } else {
 #pragma unroll
                             for (int kk = 0; kk < kPx; ++kk) c[kk] = L[min(x + kk, a.W - 1)];
@@ -604,6 +636,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                             v[kk] = static_cast<float>(16 * c[kk] - a.col.y_off) * a.col.y_scale;
                         Row8<OUT> o1;
                         o1.set(v);
+                        NNVISR_CHECK(ob + (u * ROWS + r) * sw + (x - tl.x0) + kPx <= ob + a.ob_elems);
                         o1.store(ob + (u * ROWS + r) * sw + (x - tl.x0));
                     }
                     const int jc = SUB ? min(tl.u0 + u, ch - 1) : min(tl.u0 + u, a.H - 1);
@@ -613,8 +646,8 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                                             : sg.plane(st, 1 + pc, jc - tl.ly0) - tl.lw0);
                         int c[NC];
                         if (fast) {
-                            if constexpr (SUB) unpack4(*reinterpret_cast<const V4 *>(Cr + cx), c);
-                            else unpack8(*reinterpret_cast<const V8 *>(Cr + cx), c);
+                            if constexpr (SUB) unpack4(ld_stage<V4>(Cr + cx, st, a.stage_bytes), c);
+                            else unpack8(ld_stage<V8>(Cr + cx, st, a.stage_bytes), c);
                         } else {
 #pragma unroll
                             for (int kk = 0; kk < NC; ++kk) c[kk] = Cr[min(cx + kk, cwid - 1)];
@@ -625,6 +658,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                             v[kk] = static_cast<float>(16 * c[kk] - a.col.u_off) * a.col.c_scale;
                         RowC oc;
                         oc.set(v);
+                        NNVISR_CHECK(ob + brows * sw + (pc * a.band + u) * swc + (cx - (SUB ? tl.x0 >> 1 : tl.x0)) + NC <= ob + a.ob_elems);
                         oc.store(ob + brows * sw + (pc * a.band + u) * swc + (cx - (SUB ? tl.x0 >> 1 : tl.x0)));
                     }
                 }
@@ -652,7 +686,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
 #pragma unroll
                             for (int q = 0; q < 3; ++q) {
                                 const IN *C = sg.chroma(st, p, jr[q] - tl.cy0) - tl.cw0;
-                                mag4(*reinterpret_cast<const V4 *>(C + i0), &f[q][1]);
+                                mag4(ld_stage<V4>(C + i0, st, a.stage_bytes), &f[q][1]);
                                 f[q][0] = mag(kMagicBits | C[max(i0 - 1, 0)]);
                                 f[q][5] = mag(kMagicBits | C[min(i0 + 4, cw - 1)]);
 #pragma unroll
@@ -700,7 +734,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
 #pragma unroll
                         for (int r = 0; r < 2; ++r) {
                             float dy[kPx];
-                            mag8(*reinterpret_cast<const V8 *>(sg.luma(st, y0 + r - tl.ly0) - tl.lw0 + x), dy);
+                            mag8(ld_stage<V8>(sg.luma(st, y0 + r - tl.ly0) - tl.lw0 + x, st, a.stage_bytes), dy);
                             float R[kPx], G[kPx], B[kPx];
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {  // pixels 2m, 2m+1 in f32x2 (same per-lane rounding)
@@ -724,7 +758,12 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                             o3[1].set(G);
                             o3[2].set(B);
 #pragma unroll
-                            for (int c = 0; c < 3; ++c) o3[c].store(orow + (c * brows + r) * sw);
+                            for (int c = 0; c < 3; ++c) {
+#ifdef NNVISR_CHECKED
+                                NNVISR_CHECK(orow + (c * brows + r) * sw >= ob && orow + (c * brows + r) * sw + kPx <= ob + a.ob_elems);
+#endif
+                                o3[c].store(orow + (c * brows + r) * sw);
+                            }
                         }
                         continue;
                     }
@@ -760,9 +799,9 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                                  *P1 = sg.plane(st, 1, yc - tl.ly0) - tl.lw0,
                                  *P2 = sg.plane(st, 2, yc - tl.ly0) - tl.lw0;
                         if (fast) {
-                            unpack8(*reinterpret_cast<const V8 *>(P0 + x), ys);
-                            unpack8(*reinterpret_cast<const V8 *>(P1 + x), us);
-                            unpack8(*reinterpret_cast<const V8 *>(P2 + x), vs);
+                            unpack8(ld_stage<V8>(P0 + x, st, a.stage_bytes), ys);
+                            unpack8(ld_stage<V8>(P1 + x, st, a.stage_bytes), us);
+                            unpack8(ld_stage<V8>(P2 + x, st, a.stage_bytes), vs);
                         } else {
 #pragma unroll
                             for (int kk = 0; kk < kPx; ++kk) {
@@ -782,7 +821,12 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                     Row8<OUT> o3[3];
                     f2t_row<FAMILY, OUT>(a.col, ys, us, vs, o3);
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) o3[c].store(orow + (c * brows + r) * sw);
+                    for (int c = 0; c < 3; ++c) {
+#ifdef NNVISR_CHECKED
+                        NNVISR_CHECK(orow + (c * brows + r) * sw >= ob && orow + (c * brows + r) * sw + kPx <= ob + a.ob_elems);
+#endif
+                        o3[c].store(orow + (c * brows + r) * sw);
+                    }
                 }
             }
         }
@@ -1248,6 +1292,7 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     a.nstorers = std::max(1, std::min(2, env_int("NNVISR_F2T_STORERS", 2)));
     a.release_first = env_int("NNVISR_F2T_RELFIRST", fits2 ? 1 : 0);
     a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
+    if (a.debug & 16) a.ob_elems -= 8;  // negative control: buffers too short (a checked build must trap)
     int loader = env_int("NNVISR_F2T_LOADER", fits2 ? 0 : 1);
     auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true, YUVN> : f2t_tma<FAMILY, IN, OUT, false, YUVN>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
