@@ -902,9 +902,21 @@ __device__ __forceinline__ void t2f_issue(const T2FArgs &a, int64_t t, uint8_t *
 #pragma unroll
     for (int r = 0; r < ROWS; ++r)
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < 3; ++c) {
+#ifdef NNVISR_CHECKED
+            {  // into this stage, from inside output slot o's three channels of tuple tup
+                const uint8_t *d = reinterpret_cast<const uint8_t *>(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, c) - pre);
+                const TIN *q = src + c * plane + r * a.tw - pre;
+                const TIN *lo = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
+                                static_cast<int64_t>(3 * o) * plane;
+                NNVISR_CHECK(d >= st && d + bytes <= st + a.stage_bytes);
+                NNVISR_CHECK(q >= lo && reinterpret_cast<const char *>(q) + bytes <=
+                                            reinterpret_cast<const char *>(lo + 3 * plane));
+            }
+#endif
             bulk_g2s(t2f_row_ptr<FAMILY, TIN>(st, a.segw, a.lpad, r, c) - pre, src + c * plane + r * a.tw - pre, bytes,
                      bar);
+        }
 }
 
 // Warp-specialised like f2t_tma: a.cthreads consumer threads (segw / 8,
@@ -1047,6 +1059,19 @@ __device__ __forceinline__ void t2f_yuv_issue(const T2FArgs &a, int64_t t, uint8
     mbar_arrive_expect_tx(bar, ROWS * lb + 2 * cb);
     TIN *sv = reinterpret_cast<TIN *>(st);
 #pragma unroll
+#ifdef NNVISR_CHECKED
+    {  // into this stage, from inside the slot's luma plane / two chroma planes
+        const TIN *l0 = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
+                        static_cast<int64_t>(o) * lplane;
+        const TIN *c0 = reinterpret_cast<const TIN *>(a.src2 + static_cast<int64_t>(tup) * a.tensor_stride2) +
+                        static_cast<int64_t>(2 * o) * cplane;
+        NNVISR_CHECK(reinterpret_cast<const uint8_t *>(sv + ROWS * a.segw + 2 * segwc) <= st + a.stage_bytes);
+        NNVISR_CHECK(ls >= l0 && reinterpret_cast<const char *>(ls + (ROWS - 1) * a.tw) + lb <=
+                                     reinterpret_cast<const char *>(l0 + lplane));
+        NNVISR_CHECK(cs >= c0 && reinterpret_cast<const char *>(cs + cplane) + cb <=
+                                     reinterpret_cast<const char *>(c0 + 2 * cplane));
+    }
+#endif
     for (int r = 0; r < ROWS; ++r) bulk_g2s(sv + r * a.segw, ls + r * a.tw, lb, bar);
 #pragma unroll
     for (int p = 0; p < 2; ++p) bulk_g2s(sv + ROWS * a.segw + p * segwc, cs + p * cplane, cb, bar);
