@@ -8,7 +8,9 @@ codes +-1 with >= 99.9% exact):
 * degenerate clips: one frame, every frame a scene of its own (each tuple is
   one frame repeated), a cut on the last frame;
 * the maximum alignment (256): padding rows / columns replicate the edge;
-* many outputs per run (interpolation, n = 5, extra + double frame, M = 11).
+* many outputs per run (interpolation, n = 5, extra + double frame, M = 11);
+* very wide frames (4400 and 8192 columns: f2t in 3-4 segments, t2f rows of
+  8800 / 16384 columns).
 """
 import numpy as np
 import pytest
@@ -148,3 +150,30 @@ def test_many_outputs_per_run():
             for o in range(h.M):
                 stats.add(fb.host_planes(r * h.M + o), ref[o], f"run {r} out {o}")
         stats.check("M = 11")
+
+
+@pytest.mark.parametrize("family,bits,dtype", [(nv.YUV420, 10, nv.F16), (nv.YUV444, 16, nv.F32),
+                                               (nv.RGB, 8, nv.F16), (nv.YUV420, 8, nv.F32)])
+@pytest.mark.parametrize("W", [4400, 8192])
+def test_very_wide_frames(family, bits, dtype, W):
+    """Frames wider than two 2048-column segments (f2t split into 3-4
+    segments with chroma halo columns at every seam; t2f output rows of
+    8800 / 16384 columns at x2): every tuple against the oracle."""
+    H, F = 4, 3
+    cfg = nv.Config(W, H, family, bits, nv.BT2020, nv.LIMITED, input_count=3, output_count=1, n=1, left_context=-1,
+                    flags=0, align=16, dtype=dtype, sx=(2, 1), sy=(2, 1))
+    lay = FrameLayout(W, H, family, bits)
+    buf, host = _clip(lay, F, W + bits)
+    cut = np.zeros(F, np.uint8)
+    with nv.open(cfg) as h:
+        _check_all_runs(h, cfg, lay, buf, host, cut)
+        Ho, Wo = h.out_shape[2], h.out_shape[3]
+        olay = FrameLayout(Wo, Ho, family, bits)
+        to = synth.random_tensor((1, 3, Ho, Wo), dtype, W, device=DEV)
+        out = FrameBuffer(olay, 1, device=DEV)
+        h.tensor_to_frames_batch(to.data_ptr(), to[0].numel() * to.element_size(), Ho, Wo, out.descriptors(), 1)
+        torch.cuda.synchronize()
+        ref = oracle_t2f(to.cpu().numpy(), 1, olay, cfg)
+        stats = CodeStats()
+        stats.add(out.host_planes(0), ref[0], f"W={W}")
+        stats.check(f"W={W}")
