@@ -1317,7 +1317,9 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     a.nstorers = std::max(1, std::min(2, env_int("NNVISR_F2T_STORERS", 2)));
     a.release_first = env_int("NNVISR_F2T_RELFIRST", fits2 ? 1 : 0);
     a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
-    if (a.debug & 16) a.ob_elems -= 8;  // negative control: buffers too short (a checked build must trap)
+#ifdef NNVISR_CHECKED
+    if (a.debug & 16) a.ob_elems -= 8;  // negative control: buffers too short (the checked build must trap)
+#endif
     int loader = env_int("NNVISR_F2T_LOADER", fits2 ? 0 : 1);
     auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true, YUVN> : f2t_tma<FAMILY, IN, OUT, false, YUVN>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
