@@ -71,6 +71,7 @@ struct F2TArgs {
     int32_t band, ls, cs, whole;  // band height (row units), staged row strides, whole-row copies
     int32_t fsegw;                // TMA path: columns per tile segment (kSegW, or the whole row up to 2 x kSegW)
     int32_t nstorers;             // storer threads (1 or 2)
+    int32_t cthreads;             // TMA path: converting threads per CTA (multiple of 32, <= kThreads)
     int32_t release_first;        // storers free the next output buffer before (1) or after (0) issuing a tile
     uint64_t *trace;              // experiment timeline buffer (debug & 8)
     int32_t debug;                // experiment switches (NNVISR_F2T_DEBUG), 0 in production

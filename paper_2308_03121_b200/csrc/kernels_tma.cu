@@ -149,7 +149,6 @@ __device__ __forceinline__ uint32_t smid()
 #endif
 
 constexpr int kSegW = kThreads * kPx;         // columns per tile segment (2048)
-constexpr int kConsumerWarps = kThreads / 32;  // converting warps of f2t_tma
 constexpr int kMaxStages = 8;
 constexpr int kMaxOutBufs = 8;
 // per-stage tile header written by the loader, read by the consumers
@@ -384,15 +383,16 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
     const S sg(a.ls, a.cs, a.band);
     OUT *obuf = reinterpret_cast<OUT *>(stages + nst * a.stage_bytes);
     int64_t *tile_of = reinterpret_cast<int64_t *>(hdr + kMaxStages);  // [kTileRing]: local tile -> launch tile
+    const int CT = a.cthreads;  // converting threads (warps 0 .. CT/32-1); storers / loader follow
 
     if (threadIdx.x == 0) {
         for (int k = 0; k < nst; ++k) {
             mbar_init(&full[k], 1);
-            mbar_init(&empty[k], kConsumerWarps);
+            mbar_init(&empty[k], CT / 32);
         }
         for (int b = 0; b < nob; ++b) {
             mbar_init(&ofree[b], 1);
-            mbar_init(&conv[b], kConsumerWarps);
+            mbar_init(&conv[b], CT / 32);
         }
         fence_barrier_init();
     }
@@ -404,9 +404,9 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
     // first fetch past the end gives local tile m the end-of-work header;
     // tile_of[] holds -1 from m on.  The consumers stop at m, arriving on
     // conv for m and m + 1 so both storers see the end.
-    if (threadIdx.x >= kThreads) {
+    if (threadIdx.x >= CT) {
         if ((threadIdx.x & 31) != 0) return;
-        if (LOADER && threadIdx.x == kThreads + 64) {  // ---------------- loader (LOADER variant)
+        if (LOADER && threadIdx.x == CT + 64) {  // ---------------- loader (LOADER variant)
             TileSource ts;
             ts.init(a.tile_counter, a.tiles);
             int k = 0;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
         // are still reading.  A storer reaching the end-of-work tile still
         // frees buffer j (the consumers' closing arrival may wait on it).
         const int NS = a.nstorers;
-        const int sidx = (threadIdx.x - kThreads) >> 5;
+        const int sidx = (threadIdx.x - CT) >> 5;
         if (sidx >= NS) return;
         if (!LOADER && sidx == 0) {
             TileSource ts;
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
         NNVISR_TRACE(threadIdx.x == 0, 2, i);
         // a segment wider than kSegW (wide whole-row tiles): each thread
         // converts one 8-column group per kSegW columns
-        for (int x = tl.x0 + kPx * tid; x < tl.x1; x += kSegW) {
+        for (int x = tl.x0 + kPx * tid; x < tl.x1; x += CT * kPx) {
         const bool fast = x + kPx <= a.W;
         if constexpr (YUVN) {
             // YUV-native tensors (NEXT-3, reading A22): no matrix, no
@@ -1315,6 +1315,14 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     const int smem = kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band);
     const bool fits2 = 2 * (smem + kCtaReserve) <= kSmSmem;
     a.nstorers = std::max(1, std::min(2, env_int("NNVISR_F2T_STORERS", 2)));
+    // converting threads: one per 8-column group of a single-segment row
+    // (a 1280-column row: 160 -- no idle warps; measured +1-3% at 720p), else
+    // kThreads (segments of kSegW columns, or wide tiles with two groups per
+    // thread).  NNVISR_F2T_CT raises it (experiments).
+    {
+        const int fit = (a.nseg == 1 && a.fsegw <= kSegW) ? std::min(kThreads, (a.Wp / kPx + 31) / 32 * 32) : kThreads;
+        a.cthreads = std::max(fit, std::min(kThreads, (env_int("NNVISR_F2T_CT", 0) + 31) / 32 * 32));
+    }
     a.release_first = env_int("NNVISR_F2T_RELFIRST", fits2 ? 1 : 0);
     a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
 #ifdef NNVISR_CHECKED
@@ -1325,7 +1333,7 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    const int block = kThreads + (loader ? 96 : 64);
+    const int block = a.cthreads + (loader ? 96 : 64);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
     if (e != cudaSuccess) return e;
     const int grid = static_cast<int>(std::max<int64_t>(
