@@ -89,8 +89,13 @@ def halo_exchange(s: Shard, window: torch.Tensor | None, cut_window: torch.Tenso
         if s.right:
             ops += [dist.P2POp(dist.irecv, b[own1:own1 + s.right], s.rank + 1, group) for b in bufs]
     if ops:
+        nvtx = torch.cuda.is_available()  # NVTX range for nsys / ncu --nvtx
+        if nvtx:
+            torch.cuda.nvtx.range_push("nnvisr_halo_exchange")
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        if nvtx:
+            torch.cuda.nvtx.range_pop()
 
 
 def cut_window_of(cut: np.ndarray, s: Shard) -> np.ndarray:
