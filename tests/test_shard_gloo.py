@@ -46,6 +46,11 @@ def _worker(rank, world, port, total, N, L, cut, q):
         ok_frames = all(np.array_equal(win[i].numpy(), _frame_record(s.window_first + i))
                         for i in range(s.window_count))
         ok_flags = np.array_equal(cwin.numpy(), cut[s.window_first:s.window_first + s.window_count])
+        # flags-only exchange (the peer-mapped halo reads the frames in place)
+        cwin2 = torch.zeros_like(cwin)
+        cwin2[s.left:s.left + s.owned] = cwin[s.left:s.left + s.owned]
+        sh.halo_exchange(s, None, cwin2)
+        ok_flags = ok_flags and torch.equal(cwin2, cwin)
         cfg = nv.Config(64, 64, input_count=N, output_count=1, left_context=L)
         with nv.open(cfg) as h:
             ins, fresh = h.plan_range(total, s.window_first, cwin.numpy(), s.begin, s.end)
