@@ -1324,7 +1324,14 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
         a.cthreads = std::max(fit, std::min(kThreads, (env_int("NNVISR_F2T_CT", 0) + 31) / 32 * 32));
     }
     a.release_first = env_int("NNVISR_F2T_RELFIRST", fits2 ? 1 : 0);
-    a.debug = env_int("NNVISR_F2T_DEBUG", 0);  // experiments only: 1 no conversion, 2 no stores, 4 no loads
+    // experiment switches (NNVISR_F2T_DEBUG: 1 no conversion, 2 no stores, 4 no
+    // loads, 8 timeline, 16 short buffers) exist only in experiment, trace and
+    // checked builds: the product library always converts, loads and stores
+#if defined(NNVISR_EXPERIMENTS) || defined(NNVISR_F2T_TRACE) || defined(NNVISR_CHECKED)
+    a.debug = env_int("NNVISR_F2T_DEBUG", 0);
+#else
+    a.debug = 0;
+#endif
 #ifdef NNVISR_CHECKED
     if (a.debug & 16) a.ob_elems -= 8;  // negative control: buffers too short (the checked build must trap)
 #endif
