@@ -28,6 +28,15 @@
  *     cudaStream_t passed as void*; NULL = legacy default stream) and the call
  *     returns after enqueueing.  Asynchronous faults surface at the caller's
  *     synchronisation, or as NNVISR_ERR_CUDA from a later call.
+ *   - CUDA graphs: the device calls (frames->tensor, tensor->frames, their
+ *     batch / store / YUV forms) may be captured (cudaStreamBeginCapture, or
+ *     torch.cuda.graph) on `stream`.  A captured call records its launches
+ *     with tables of its own (kept until nnvisr_close), so every replay
+ *     converts the same runs / outputs, reading the frames and tensors at
+ *     the addresses of capture time and the frame table bound at that time.
+ *     The graph must not be replayed after nnvisr_close, nor after a
+ *     nnvisr_bind_frames call that binds more frames than were bound at
+ *     capture (the table may move).  The host-buffer calls are not capturable.
  *   - A handle is bound to the CUDA device that is current at its first
  *     device call; it is used by one host thread at a time.  nnvisr_open,
  *     nnvisr_tensor_shapes, nnvisr_plan*, nnvisr_close and nnvisr_last_error

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -75,6 +76,7 @@ struct UploadSlot {
     void *dev = nullptr;
     cudaEvent_t done = nullptr;
     bool pending = false;
+    bool captured = false;  // owned by a CUDA graph capture (never recycled)
 };
 constexpr size_t kSlotBytes = size_t(1) << 20;
 constexpr int kSlots = 8;
@@ -99,6 +101,7 @@ struct nnvisr_handle {
     int device = -1;
     UploadSlot slots[kSlots];
     int next_slot = 0;
+    std::vector<std::unique_ptr<UploadSlot>> captured;  // slots of calls recorded into CUDA graphs
     DevFrame *frames = nullptr;
     int64_t frames_cap = 0, frames_base = 0, frames_count = 0;
     bool frames_vec = false;
@@ -316,6 +319,11 @@ nnvisr_status nnvisr_close(nnvisr_handle *h)
             if (s.host) cudaFreeHost(s.host);
             if (s.dev) cudaFree(s.dev);
         }
+        if (!h->captured.empty()) cudaDeviceSynchronize();  // replays of captured graphs may still read them
+        for (auto &s : h->captured) {
+            if (s->host) cudaFreeHost(s->host);
+            if (s->dev) cudaFree(s->dev);
+        }
         if (h->frames) cudaFree(h->frames);
         if (h->h2d) cudaStreamSynchronize(h->h2d);
         if (h->d2h) cudaStreamSynchronize(h->d2h);
@@ -468,12 +476,34 @@ nnvisr_status ensure_device(nnvisr_handle *h)
 }
 
 // Take the next upload slot, waiting for its previous consumer if needed.
-nnvisr_status acquire_slot(nnvisr_handle *h, UploadSlot **out)
+// On a stream that is being captured into a CUDA graph the call gets a slot
+// of its own instead (kept until nnvisr_close): the graph's memcpy node
+// re-uploads the same tables, tile counter zeroed, at every replay.
+nnvisr_status acquire_slot(nnvisr_handle *h, UploadSlot **out, cudaStream_t st)
 {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(st, &cs);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
+    if (cs == cudaStreamCaptureStatusActive) {
+        auto c = std::make_unique<UploadSlot>();
+        c->captured = true;
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;  // allocations are allowed here
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        e = cudaHostAlloc(&c->host, kSlotBytes, cudaHostAllocDefault);
+        if (e == cudaSuccess) e = cudaMalloc(&c->dev, kSlotBytes);
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        if (e != cudaSuccess) {
+            if (c->host) cudaFreeHost(c->host);
+            return cuda_fail(e, "allocating a capture upload slot");
+        }
+        *out = c.get();
+        h->captured.push_back(std::move(c));
+        return NNVISR_OK;
+    }
     UploadSlot &s = h->slots[h->next_slot];
     h->next_slot = (h->next_slot + 1) % kSlots;
     if (s.pending) {
-        cudaError_t e = cudaEventSynchronize(s.done);
+        e = cudaEventSynchronize(s.done);
         if (e != cudaSuccess) return cuda_fail(e, "waiting for an upload slot");
         s.pending = false;
     }
@@ -503,6 +533,7 @@ nnvisr_status upload(UploadSlot *s, size_t bytes, cudaStream_t st)
 
 nnvisr_status release_slot(UploadSlot *s, cudaStream_t st)
 {
+    if (s->captured) return NNVISR_OK;
     cudaError_t e = cudaEventRecord(s->done, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
     s->pending = true;
@@ -747,7 +778,7 @@ nnvisr_status nnvisr_frames_to_tensor(nnvisr_handle *h, const nnvisr_frame *in, 
     if (s) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     UploadSlot *slot = nullptr;
-    if ((s = acquire_slot(h, &slot))) return s;
+    if ((s = acquire_slot(h, &slot, st))) return s;
     // [DevFrame x N][job_frame, job_dst, dst_code]; identical descriptors are
     // one job (a frame repeated in the tuple is converted once)
     std::vector<int64_t> key(h->N);
@@ -817,7 +848,7 @@ static nnvisr_status f2t_indexed_table(nnvisr_handle *h, const FrameTable &tab, 
     for (int64_t r0 = 0; r0 < runs; r0 += max_runs) {
         const int64_t nr = std::min(max_runs, runs - r0);
         UploadSlot *slot = nullptr;
-        nnvisr_status s = acquire_slot(h, &slot);
+        nnvisr_status s = acquire_slot(h, &slot, st);
         if (s) return s;
         int32_t *tbl = static_cast<int32_t *>(slot->host);
         const int64_t J = build_f2t_jobs(frame_idx + r0 * per_run, nr, per_run, tab.base, tbl);
@@ -953,7 +984,7 @@ static nnvisr_status t2f_common(nnvisr_handle *h, const void *tensors, int64_t s
     for (int64_t j0 = 0; j0 < jobs; j0 += per_slot) {
         const int64_t nj = std::min(per_slot, jobs - j0);
         UploadSlot *slot = nullptr;
-        if ((s = acquire_slot(h, &slot))) return s;
+        if ((s = acquire_slot(h, &slot, st))) return s;
         std::memcpy(slot->host, desc + j0, sizeof(DevFrame) * nj);
         if (skipped) std::memcpy(static_cast<char *>(slot->host) + sizeof(DevFrame) * nj, codes.data() + j0, sizeof(int32_t) * nj);
         size_t bytes = per_job * nj;
