@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--halo", default="p2p", choices=["p2p", "peer"],
                    help="N > 1: copy the halo frames each step (NCCL P2P) or read them in place from the "
                         "neighbours' buffers (nnvisr_peer_import; only the flags travel)")
+    p.add_argument("--graph", action="store_true",
+                   help="replay the step's launches as one CUDA graph (captured once; re-captured when the "
+                        "plan changes); for launch-bound small clips (c1)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--detect", action="store_true",
                    help="detect scene changes on the GPU each step (NEXT-4) and plan from those flags")
@@ -341,7 +344,7 @@ def main():
         b.record(stream)
         ev_pairs[kind].append((a, b, units, nbytes))
 
-    def step(record: bool):
+    def step(record: bool, planned=None):
         if world > 1:
             with torch.cuda.stream(stream):
                 sh.halo_exchange(s, None if peer else win.data, cut_win)
@@ -352,7 +355,7 @@ def main():
                       lambda: h.scene_detect(s.window_first, s.window_count, args.detect_threshold, sad_d.data_ptr(),
                                              cut_d.data_ptr(), stream))
                 cut_win.copy_(cut_d)
-        runs, _ = plan_local()
+        runs = plan_local()[0] if planned is None else planned
         with torch.cuda.stream(stream):
             if args.f2t_mode == "store":
                 # each window frame converted once into the frame-major store;
@@ -431,6 +434,37 @@ def main():
         step(False)
     barrier()
 
+    # --graph: the step's device work captured once as a CUDA graph (the
+    # library records its launches with upload tables of their own); every
+    # timed step still plans on the host and replays the graph when the plan
+    # is the captured one (else runs eagerly).  Per-kernel times come from one
+    # eager recorded step before the timed region (graph replays are timed as
+    # a whole).
+    graph = None
+    if args.graph:
+        if world > 1 or args.detect or args.emit or yuv or args.f2t_mode != "materialize":
+            raise SystemExit("--graph supports one GPU, materialised RGB tuples, no --emit / --detect")
+        step(True)
+        barrier()
+        runs_cap = plan_local()[0]
+        graph = torch.cuda.CUDAGraph()
+        lc0 = nv.launch_count()
+        with torch.cuda.graph(graph, stream=stream):
+            step(False, runs_cap)
+        graph_launches = nv.launch_count() - lc0
+        graph.replay()
+        barrier()
+
+    def timed_step():
+        if graph is None:
+            return step(True)
+        runs = plan_local()[0]
+        if np.array_equal(runs, runs_cap):
+            with torch.cuda.stream(stream):
+                graph.replay()
+            return len(runs)
+        return step(False, runs)
+
     # ---- timed region: K steps, device time via CUDA events on `stream`
     launches0 = nv.launch_count()
     with ClockSampler(local) as clk:
@@ -439,10 +473,12 @@ def main():
         t_start.record(stream)
         tuples = 0
         for _ in range(args.steps):
-            tuples += step(True)
+            tuples += timed_step()
         t_end.record(stream)
         barrier()
     launches = nv.launch_count() - launches0
+    if graph is not None:  # replays do not pass through the library's launch counter
+        launches += graph_launches * args.steps
     ms_total = t_start.elapsed_time(t_end)
     ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if world > 1:
@@ -515,7 +551,9 @@ def main():
                                        if args.detect else "given (synthetic cut pattern)"),
                        "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB, t2f input ring "
                                     f"{n_out} x {out_elems * esz / 1e6:.0f} MB >= 4 x L2 ({l2 / 1e6:.0f} MB)",
-                       "parallelism": f"frame-range shards x{world}, halo " + ("peer-mapped" if peer else "P2P")},
+                       "parallelism": f"frame-range shards x{world}, halo " + ("peer-mapped" if peer else "P2P"),
+                       "launch": ("CUDA graph replay per step (host plan each step; kernel times from an eager step)"
+                                  if graph is not None else "eager launches")},
             "unit_definition": "1 frame = one tuple through frames->tensor plus its network output through "
                                "tensor->frames (n = 1: one tuple per clip frame)",
             "per_direction": per_dir,
