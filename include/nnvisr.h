@@ -31,7 +31,8 @@
  *   - CUDA graphs: the device calls (frames->tensor, tensor->frames, their
  *     batch / store / YUV forms) may be captured (cudaStreamBeginCapture, or
  *     torch.cuda.graph) on `stream`.  A captured call records its launches
- *     with tables of its own (kept until nnvisr_close), so every replay
+ *     with tables of its own (kept until nnvisr_release_graph_tables or
+ *     nnvisr_close), so every replay
  *     converts the same runs / outputs, reading the frames and tensors at
  *     the addresses of capture time and the frame table bound at that time.
  *     The graph must not be replayed after nnvisr_close, nor after a
@@ -394,6 +395,13 @@ nnvisr_status nnvisr_peer_import(const nnvisr_peer_handle *in, void **dev_ptr);
 /* Unmap a pointer returned by nnvisr_peer_import (after the work reading it
  * has completed).  NNVISR_ERR_INVALID_ARG for a pointer not imported here. */
 nnvisr_status nnvisr_peer_close(void *dev_ptr);
+
+/* Free the upload tables of every call captured into a CUDA graph so far
+ * (see "CUDA graphs" above).  The caller must have destroyed those graphs
+ * (or will never replay them again) and no replay may be in flight; a server
+ * that re-captures when its plan changes calls this between captures.  The
+ * handle's own ring of upload slots is untouched. */
+nnvisr_status nnvisr_release_graph_tables(nnvisr_handle *h);
 
 /* Number of CUDA kernels this library has launched in this process. */
 int64_t nnvisr_launch_count(void);

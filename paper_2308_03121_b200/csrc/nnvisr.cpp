@@ -1532,6 +1532,21 @@ nnvisr_status nnvisr_peer_close(void *dev_ptr)
     return NNVISR_OK;
 }
 
+nnvisr_status nnvisr_release_graph_tables(nnvisr_handle *h)
+{
+    g_error.clear();
+    if (!h) return fail(NNVISR_ERR_INVALID_ARG, "null handle");
+    if (h->captured.empty()) return NNVISR_OK;
+    cudaError_t e = cudaDeviceSynchronize();  // no replay may still read them
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize");
+    for (auto &c : h->captured) {
+        if (c->host) cudaFreeHost(c->host);
+        if (c->dev) cudaFree(c->dev);
+    }
+    h->captured.clear();
+    return NNVISR_OK;
+}
+
 nnvisr_status nnvisr_host_fence(nnvisr_handle *h, void *stream)
 {
     g_error.clear();

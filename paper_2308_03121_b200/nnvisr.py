@@ -78,6 +78,7 @@ def _load():
         "nnvisr_peer_export": (st, [C.c_void_p, C.POINTER(PeerHandle)]),
         "nnvisr_peer_import": (st, [C.POINTER(PeerHandle), C.POINTER(C.c_void_p)]),
         "nnvisr_peer_close": (st, [C.c_void_p]),
+        "nnvisr_release_graph_tables": (st, [H]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -95,7 +96,7 @@ EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version"
             "nnvisr_schedule_outputs", "nnvisr_copy_frames", "nnvisr_frames_to_tensor_batch_host",
             "nnvisr_tensor_to_frames_batch_host", "nnvisr_host_fence", "nnvisr_chroma_shapes",
             "nnvisr_frames_to_tensor_yuv_batch", "nnvisr_tensor_to_frames_yuv_batch", "nnvisr_peer_export",
-            "nnvisr_peer_import", "nnvisr_peer_close")
+            "nnvisr_peer_import", "nnvisr_peer_close", "nnvisr_release_graph_tables")
 
 
 def lib():
@@ -236,6 +237,10 @@ class Handle:
         ri = np.ascontiguousarray(run_inputs, dtype=np.int64)
         nr = ri.shape[0] if ri.ndim == 2 else ri.size // self.N
         _check(_lib.nnvisr_frames_to_tensor_batch(self._h, _i64p(ri), nr, tensors_ptr, stride, _stream_ptr(stream)))
+
+    def release_graph_tables(self):
+        """nnvisr_release_graph_tables: free the tables of captured calls (graphs destroyed first)."""
+        _check(_lib.nnvisr_release_graph_tables(self._h))
 
     def frames_to_store(self, first: int, count: int, store_ptr: int, stream=None):
         _check(_lib.nnvisr_frames_to_store(self._h, first, count, store_ptr, _stream_ptr(stream)))

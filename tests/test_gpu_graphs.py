@@ -72,7 +72,19 @@ def test_graph_replay_matches_eager(name, frames):
         assert not torch.equal(t_ref2.view(torch.uint8), t_ref.view(torch.uint8))
         assert torch.equal(t_g.view(torch.uint8), t_ref2.view(torch.uint8))
         assert torch.equal(o_g.data, o_ref2)
+        # a server re-capturing after a plan change: free the old tables first
         del g
+        h.release_graph_tables()
+        g2 = torch.cuda.CUDAGraph()
+        t_g.fill_(float("nan"))
+        with torch.cuda.graph(g2):
+            h.frames_to_tensor_batch(runs[:1], t_g.data_ptr(), per * t_g.element_size(),
+                                     stream=torch.cuda.current_stream())
+        g2.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(t_g[0].view(torch.uint8), t_ref2[0].view(torch.uint8))
+        del g2
+        h.release_graph_tables()
 
 
 def test_graph_store_and_yuv_forms():
