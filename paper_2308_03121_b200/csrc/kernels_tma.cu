@@ -354,9 +354,10 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
     });
 }
 
-// Warp-specialised: warps 0..7 convert (consumers); lane 0 of warps 8 and 9
-// are the two "storers".  Per input stage k: full[k] (TMA bytes landed).  Per
-// output buffer b: conv[b] (the 8 consumer warps have read tile i's stage and
+// Warp-specialised: warps 0 .. CT/32-1 convert (consumers, CT = a.cthreads <=
+// 256: one thread per 8-column group of the segment); lane 0 of the next two
+// warps are the two "storers".  Per input stage k: full[k] (TMA bytes landed).
+// Per output buffer b: conv[b] (every consumer warp has read tile i's stage and
 // written its converted band into buffer b), ofree[b] (the bulk stores that
 // read it are done).  Storer s handles tiles s, s + 2, ...: on conv[i] it
 // refills tile i's stage with tile i + nst (TMA bulk copies, issued before
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
             return;
         }
         // ---------------- storers
-        // NS = a.nstorers storers (lane 0 of warps 8, 9); storer s fans out
+        // NS = a.nstorers storers (lane 0 of warps CT/32, CT/32 + 1); storer s fans out
         // tiles s, s + NS, ...  Bulk groups are per thread, so one storer
         // waiting for its own stores to drain never stalls another's issue.
         // Every destination's stores form one bulk group; eb[m] = groups
