@@ -1374,6 +1374,48 @@ nnvisr_status copy_frame_planes(const nnvisr_frame &dst, const nnvisr_frame &src
     return NNVISR_OK;
 }
 
+// Frames count..: dst[i] <- src[i] (plane[0] == NULL on either side: skipped).
+// When the packed layout has no padding at all (pitch = row bytes, planes
+// and frames back to back) and consecutive frames sit back to back on both
+// sides, a run of them moves as ONE copy (small frames: one call instead of
+// three per frame); otherwise plane by plane.
+nnvisr_status copy_frames_coalesced(const nnvisr_frame *dst, const nnvisr_frame *src, int64_t count,
+                                    const PackedLayout &L, cudaMemcpyKind kind, cudaStream_t st)
+{
+    bool gapless = L.frame_bytes == L.off[2] + L.pitch[2] * L.rows[2];
+    for (int p = 0; p < 3; ++p) {
+        gapless = gapless && L.pitch[p] == L.row_bytes[p];
+        if (p < 2) gapless = gapless && L.off[p + 1] == L.off[p] + L.pitch[p] * L.rows[p];
+    }
+    auto at = [&](const nnvisr_frame &f, const char *base) {
+        for (int p = 0; p < 3; ++p)
+            if (static_cast<const char *>(f.plane[p]) != base + L.off[p] || f.pitch[p] != L.pitch[p]) return false;
+        return true;
+    };
+    for (int64_t i = 0; i < count;) {
+        if (!dst[i].plane[0] || !src[i].plane[0]) {
+            ++i;
+            continue;
+        }
+        const char *sb = static_cast<const char *>(src[i].plane[0]);
+        const char *db = static_cast<const char *>(dst[i].plane[0]);
+        int64_t j = i;
+        while (gapless && j < count && dst[j].plane[0] && src[j].plane[0] && at(src[j], sb + (j - i) * L.frame_bytes) &&
+               at(dst[j], db + (j - i) * L.frame_bytes))
+            ++j;
+        if (j - i >= 2) {
+            cudaError_t e = cudaMemcpyAsync(const_cast<char *>(db), sb, (j - i) * L.frame_bytes, kind, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync (host frames)");
+            i = j;
+            continue;
+        }
+        nnvisr_status s = copy_frame_planes(dst[i], src[i], L, kind, st);
+        if (s) return s;
+        ++i;
+    }
+    return NNVISR_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1409,8 +1451,7 @@ nnvisr_status nnvisr_frames_to_tensor_batch_host(nnvisr_handle *h, const nnvisr_
     cudaError_t e;
     // the kernels that last read this staging slot must be done before the upload
     if (g.used && (e = cudaStreamWaitEvent(h->h2d, g.free_ev, 0)) != cudaSuccess) return cuda_fail(e, "wait");
-    for (int64_t i = 0; i < count; ++i)
-        if ((s = copy_frame_planes(g.desc[i], host_frames[i], L, cudaMemcpyHostToDevice, h->h2d))) return s;
+    if ((s = copy_frames_coalesced(g.desc.data(), host_frames, count, L, cudaMemcpyHostToDevice, h->h2d))) return s;
     if ((e = cudaEventRecord(g.ready_ev, h->h2d)) != cudaSuccess || (e = cudaStreamWaitEvent(st, g.ready_ev, 0)) != cudaSuccess)
         return cuda_fail(e, "upload event");
     const FrameTable tab{g.table, base, true, L.pitch[0], L.pitch[1]};
@@ -1449,9 +1490,7 @@ nnvisr_status nnvisr_tensor_to_frames_batch_host(nnvisr_handle *h, const void *t
     if ((s = t2f_common(h, tensors, tensor_stride_bytes, t_h, t_w, dev_out.data(), count, st))) return s;
     if ((e = cudaEventRecord(g.ready_ev, st)) != cudaSuccess || (e = cudaStreamWaitEvent(h->d2h, g.ready_ev, 0)) != cudaSuccess)
         return cuda_fail(e, "download event");
-    for (int64_t j = 0; j < jobs; ++j)
-        if (host_out[j].plane[0] && (s = copy_frame_planes(host_out[j], g.desc[j], L, cudaMemcpyDeviceToHost, h->d2h)))
-            return s;
+    if ((s = copy_frames_coalesced(host_out, g.desc.data(), jobs, L, cudaMemcpyDeviceToHost, h->d2h))) return s;
     if ((e = cudaEventRecord(g.free_ev, h->d2h)) != cudaSuccess || (e = cudaEventRecord(h->d2h_last, h->d2h)) != cudaSuccess)
         return cuda_fail(e, "cudaEventRecord");
     g.used = true;
