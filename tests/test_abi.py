@@ -260,3 +260,9 @@ def test_peer_calls_validate_arguments():
             bad()
         assert ei.value.status == 2
     assert len(nv.PeerHandle().ipc) == 64
+
+
+def test_release_graph_tables_without_captures():
+    assert nv.lib().nnvisr_release_graph_tables(None) == 2  # INVALID_ARG: null handle
+    with nv.open(_cfg()) as h:
+        h.release_graph_tables()  # nothing captured: a no-op, no device touched
