@@ -12,7 +12,7 @@
  *     P:313-328);
  *   - the tuple plan: which frames form each tuple, never crossing a scene
  *     change (§3.2, §3.3).
- * Where the paper is silent the readings A1..A16 of DESIGN.md §3 apply
+ * Where the paper is silent the readings A1..A22 of DESIGN.md §3 apply
  * (centre chroma siting, replicate padding, round-half-even, ...).
  *
  * Conventions shared by every call:
