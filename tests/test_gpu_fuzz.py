@@ -3,7 +3,9 @@ family / depth / matrix / range / siting, tensor format (RGB or YUV-native)
 and dtype, frame size (odd widths included: TMA and generic paths), window
 length, alignment, scale factor and cut pattern, drawn from one generator.
 Bars as in test_gpu_parity (fp32 1e-6, fp16 1 ULP, codes +-1 with >= 99.9%
-exact, pooled over the case)."""
+exact, pooled over the case).  NNVISR_FUZZ_SEEDS=n runs n seeds (default 100)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -34,7 +36,7 @@ def _draw(seed):
                 F=int(rs.integers(3, 9)), seed=int(rs.integers(1 << 30)))
 
 
-@pytest.mark.parametrize("seed", range(100))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("NNVISR_FUZZ_SEEDS", "100"))))
 def test_random_configuration(seed):
     p = _draw(seed)
     if p["family"] == nv.YUV420 and p["sx"] == 1 and p["W"] % 2:
