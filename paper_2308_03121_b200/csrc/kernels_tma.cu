@@ -1244,25 +1244,33 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     // stores; each consumer thread takes two column groups)
     const int64_t jobs_ = a.tiles / ((int64_t)a.rowunits * a.nseg);
     // (4:2:0 only: measured +5% at 4K; 4:4:4 fp32 tiles are faster split)
-    const bool wide = env_int("NNVISR_F2T_WIDE", FAMILY == kYUV420 ? 1 : 0) && a.Wp > kSegW && a.Wp <= 2 * kSegW;
-    a.fsegw = wide ? (a.Wp + 31) / 32 * 32 : kSegW;
-    a.nseg = (a.Wp + a.fsegw - 1) / a.fsegw;
-    a.tiles = jobs_ * a.rowunits * a.nseg;
-    const int segw = std::min(a.fsegw, (a.Wp + 31) / 32 * 32);
-    const int lcap = (segw + 2 * S::G - 1) / (2 * S::G) * (2 * S::G);  // ccap*sizeof(IN) stays 16-byte aligned
-    const int ccap = lcap / 2 + 2 * S::G;
-    // whole rows: one segment, and every bound frame's pitches are the staged strides
-    const int sb = sizeof(IN);
-    const bool whole = a.nseg == 1 && a.pitch_y > 0 && a.pitch_y % 16 == 0 && a.pitch_y / sb <= 4 * lcap &&
-                       (FAMILY != kYUV420 || (a.pitch_c > 0 && a.pitch_c % 16 == 0));
-    a.whole = whole;
-    a.ls = whole ? a.pitch_y / sb : lcap;
-    a.cs = whole ? (FAMILY == kYUV420 ? a.pitch_c / sb : a.ls) : ccap;
+    int segw = 0;
     auto stage_bytes = [&](int B) { return (S(a.ls, a.cs, B).bytes() + 127) / 128 * 128; };
     // RGB: 3 planes of the band's rows; YUV-native: the luma rows plus the
     // units' two chroma rows (half width in 4:2:0)
     constexpr int kObRows = YUVN ? (FAMILY == kYUV420 ? ROWS + 1 : ROWS + 2) : 3 * ROWS;
     auto ob_bytes = [&](int B) { return (kObRows * B * segw * (int)sizeof(OUT) + 127) / 128 * 128; };
+    auto segment = [&](bool wide) {
+        a.fsegw = wide ? (a.Wp + 31) / 32 * 32 : kSegW;
+        a.nseg = (a.Wp + a.fsegw - 1) / a.fsegw;
+        a.tiles = jobs_ * a.rowunits * a.nseg;
+        segw = std::min(a.fsegw, (a.Wp + 31) / 32 * 32);
+        const int lcap = (segw + 2 * S::G - 1) / (2 * S::G) * (2 * S::G);  // ccap*sizeof(IN) stays 16-byte aligned
+        const int ccap = lcap / 2 + 2 * S::G;
+        // whole rows: one segment, and every bound frame's pitches are the staged strides
+        const int sb = sizeof(IN);
+        const bool whole = a.nseg == 1 && a.pitch_y > 0 && a.pitch_y % 16 == 0 && a.pitch_y / sb <= 4 * lcap &&
+                           (FAMILY != kYUV420 || (a.pitch_c > 0 && a.pitch_c % 16 == 0));
+        a.whole = whole;
+        a.ls = whole ? a.pitch_y / sb : lcap;
+        a.cs = whole ? (FAMILY == kYUV420 ? a.pitch_c / sb : a.ls) : ccap;
+    };
+    constexpr int kMaxSmem = 227 * 1024;
+    const bool wide = env_int("NNVISR_F2T_WIDE", FAMILY == kYUV420 ? 1 : 0) && a.Wp > kSegW && a.Wp <= 2 * kSegW;
+    segment(wide);
+    // a whole-row tile must fit one stage and two output buffers of a single
+    // row unit (16-bit fp32 4:2:0 rows near 4096 columns do not): else segments
+    if (wide && kBarBytes + stage_bytes(1) + 2 * ob_bytes(1) > kMaxSmem) segment(false);
     // band height and buffering, from the tools/sweep_f2t.sh sweep on B200
     // (profiles/r01/f2t_sweep.txt): bands of 2 row units with 3 output buffers
     // for whole-row frames and 4:4:4; single row units for 4:2:0 frames wider
@@ -1302,7 +1310,6 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     a.stages = std::max(1, std::min(kMaxStages, a.stages));
     a.nob = std::max(2, std::min(5, a.nob));
     // never exceed the 227 KB a CTA may use: shed output buffers, then band rows
-    constexpr int kMaxSmem = 227 * 1024;
     while (kBarBytes + a.stages * a.stage_bytes + a.nob * ob_bytes(a.band) > kMaxSmem) {
         if (a.nob > 2) --a.nob;
         else if (a.stages > 1) --a.stages;

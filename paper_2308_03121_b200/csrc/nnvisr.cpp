@@ -83,7 +83,15 @@ constexpr int kSlots = 8;
 
 }  // namespace
 
-void nnvisr::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// Called right before each kernel launch.  The launch reports its own errors
+// through cudaGetLastError(), so a stale, non-sticky error left by an earlier
+// failed runtime call (returned to its caller already) is dropped here
+// rather than pinned on this launch.
+void nnvisr::count_launch()
+{
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    (void)cudaGetLastError();
+}
 
 struct nnvisr_handle {
     nnvisr_clip_format fmt{};

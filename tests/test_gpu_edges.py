@@ -177,3 +177,33 @@ def test_very_wide_frames(family, bits, dtype, W):
         stats = CodeStats()
         stats.add(out.host_planes(0), ref[0], f"W={W}")
         stats.check(f"W={W}")
+
+
+@pytest.mark.parametrize("W,family,bits,dtype", [(4036, nv.YUV420, 16, nv.F32), (4090, nv.YUV420, 10, nv.F32),
+                                                 (2518, nv.YUV444, 16, nv.F32)])
+def test_wide_rows_that_do_not_fit_one_tile(W, family, bits, dtype):
+    """4:2:0 rows just under 4096 columns with 16-bit samples and fp32 tensors:
+    a whole-row tile (one stage + two output buffers) exceeds a CTA's shared
+    memory, so f2t falls back to 2048-column segments (found by the wide fuzz,
+    seed 483); every tuple against the oracle."""
+    H, F = 2, 3
+    cfg = _window_cfg(W, H, 3, family=family, bits=bits, dtype=dtype, align=8)
+    lay = FrameLayout(W, H, family, bits)
+    buf, host = _clip(lay, F, W)
+    with nv.open(cfg) as h:
+        _check_all_runs(h, cfg, lay, buf, host, np.zeros(F, np.uint8))
+
+
+def test_failed_call_does_not_poison_the_next_launch():
+    """A call that fails inside the CUDA runtime (here: importing a peer
+    handle in the exporting process) leaves no stale error behind: the next
+    conversion launches and checks out."""
+    x = torch.zeros(1 << 16, dtype=torch.uint8, device=DEV)
+    with pytest.raises(nv.NnvisrError):
+        nv.peer_import(nv.peer_export(x.data_ptr()))
+    W, H, F = 64, 16, 3
+    cfg = _window_cfg(W, H, 3, bits=8, dtype=nv.F32)
+    lay = FrameLayout(W, H, nv.YUV420, 8)
+    buf, host = _clip(lay, F, 5)
+    with nv.open(cfg) as h:
+        _check_all_runs(h, cfg, lay, buf, host, np.zeros(F, np.uint8))

@@ -3,7 +3,8 @@ family / depth / matrix / range / siting, tensor format (RGB or YUV-native)
 and dtype, frame size (odd widths included: TMA and generic paths), window
 length, alignment, scale factor and cut pattern, drawn from one generator.
 Bars as in test_gpu_parity (fp32 1e-6, fp16 1 ULP, codes +-1 with >= 99.9%
-exact, pooled over the case).  NNVISR_FUZZ_SEEDS=n runs n seeds (default 100)."""
+exact, pooled over the case).  NNVISR_FUZZ_SEEDS=n runs n seeds (default 100),
+NNVISR_FUZZ_WIDE_SEEDS=n as many 1000-5200-column frames (default 20)."""
 import os
 
 import numpy as np
@@ -21,13 +22,17 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-def _draw(seed):
+def _draw(seed, wide=False):
     rs = np.random.default_rng(seed)
     family = int(rs.choice([nv.YUV420, nv.YUV444, nv.RGB]))
     yuv = family != nv.RGB and rs.random() < 0.3
     left = family == nv.YUV420 and not yuv and rs.random() < 0.3
-    W = int(rs.integers(1, 160)) * 2 + (0 if family == nv.YUV420 else int(rs.integers(0, 2)))
-    H = int(rs.integers(1, 12)) * 2
+    if wide:  # 1000-5200 columns: wide whole-row tiles, 2-3 segments, seams
+        W = int(rs.integers(500, 2600)) * 2 + (0 if family == nv.YUV420 else int(rs.integers(0, 2)))
+        H = int(rs.integers(1, 3)) * 2
+    else:
+        W = int(rs.integers(1, 160)) * 2 + (0 if family == nv.YUV420 else int(rs.integers(0, 2)))
+        H = int(rs.integers(1, 12)) * 2
     interp = rs.random() < 0.3  # paper grouping: n = 1, extra + double frame, M = 2n + 1 = 3
     return dict(family=family, bits=int(rs.choice([8, 10, 16])), dtype=int(rs.choice([nv.F32, nv.F16])),
                 matrix=int(rs.integers(0, 3)), rng_=int(rs.integers(0, 2)), W=W, H=H,
@@ -38,7 +43,15 @@ def _draw(seed):
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("NNVISR_FUZZ_SEEDS", "100"))))
 def test_random_configuration(seed):
-    p = _draw(seed)
+    _check(_draw(seed))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("NNVISR_FUZZ_WIDE_SEEDS", "20"))))
+def test_random_wide_configuration(seed):
+    _check(_draw(10 ** 6 + seed, wide=True))
+
+
+def _check(p):
     if p["family"] == nv.YUV420 and p["sx"] == 1 and p["W"] % 2:
         pytest.skip("odd 4:2:0 width")
     flags = (nv.YUV_INPUT | nv.YUV_OUTPUT) if p["yuv"] else 0
