@@ -4,7 +4,8 @@ and dtype, frame size (odd widths included: TMA and generic paths), window
 length, alignment, scale factor and cut pattern, drawn from one generator.
 Bars as in test_gpu_parity (fp32 1e-6, fp16 1 ULP, codes +-1 with >= 99.9%
 exact, pooled over the case).  NNVISR_FUZZ_SEEDS=n runs n seeds (default 100),
-NNVISR_FUZZ_WIDE_SEEDS=n as many 1000-5200-column frames (default 20)."""
+NNVISR_FUZZ_WIDE_SEEDS=n as many 1000-5200-column frames (default 20),
+NNVISR_FUZZ_TALL_SEEDS=n frames of up to 600 rows (default 10)."""
 import os
 
 import numpy as np
@@ -22,12 +23,15 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-def _draw(seed, wide=False):
+def _draw(seed, wide=False, tall=False):
     rs = np.random.default_rng(seed)
     family = int(rs.choice([nv.YUV420, nv.YUV444, nv.RGB]))
     yuv = family != nv.RGB and rs.random() < 0.3
     left = family == nv.YUV420 and not yuv and rs.random() < 0.3
-    if wide:  # 1000-5200 columns: wide whole-row tiles, 2-3 segments, seams
+    if tall:  # up to 600 rows of up to 96 columns: many bands, ragged band tails
+        W = int(rs.integers(1, 48)) * 2 + (0 if family == nv.YUV420 else int(rs.integers(0, 2)))
+        H = int(rs.integers(20, 300)) * 2
+    elif wide:  # 1000-5200 columns: wide whole-row tiles, 2-3 segments, seams
         W = int(rs.integers(500, 2600)) * 2 + (0 if family == nv.YUV420 else int(rs.integers(0, 2)))
         H = int(rs.integers(1, 3)) * 2
     else:
@@ -49,6 +53,11 @@ def test_random_configuration(seed):
 @pytest.mark.parametrize("seed", range(int(os.environ.get("NNVISR_FUZZ_WIDE_SEEDS", "20"))))
 def test_random_wide_configuration(seed):
     _check(_draw(10 ** 6 + seed, wide=True))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("NNVISR_FUZZ_TALL_SEEDS", "10"))))
+def test_random_tall_configuration(seed):
+    _check(_draw(2 * 10 ** 6 + seed, tall=True))
 
 
 def _check(p):
