@@ -1,4 +1,5 @@
-"""Seeded random configurations through the C ABI against the oracle: clip
+"""Seeded random configurations through the C ABI against the oracle (and,
+without interpolation, store mode byte-identical to the materialised tuples): clip
 family / depth / matrix / range / siting, tensor format (RGB or YUV-native)
 and dtype, frame size (odd widths included: TMA and generic paths), window
 length, alignment, scale factor and cut pattern, drawn from one generator.
@@ -105,6 +106,19 @@ def _check(p):
         out = FrameBuffer(olay, 2 * M, device=DEV)
         h.tensor_to_frames_batch(to.data_ptr(), ostride * to.element_size(), Ho, Wo, out.descriptors(), 2)
         torch.cuda.synchronize()
+        if not p["yuv"] and not p["interp"]:
+            # store mode (one destination per frame): every run over
+            # consecutive frames is a window of the store, byte-identical to
+            # its materialised tensor (checked against the oracle below)
+            slot = 3 * Hp * Wp
+            st = torch.full((F, slot), float("nan"), dtype=tdt, device=DEV)
+            h.frames_to_store(0, F, st.data_ptr())
+            torch.cuda.synchronize()
+            for r, run in enumerate(runs):
+                if np.all(np.diff(run) == 1):
+                    nin = len(run)  # frames per tuple (in_shape[1] is 3 x that)
+                    win = st[run[0]:run[0] + nin].reshape(-1)
+                    assert torch.equal(win.view(torch.uint8), t[r, :nin * slot].view(torch.uint8)), (p, r)
         tn = t.cpu().numpy()
         for r, run in enumerate(runs):
             frames = [host[i] for i in run]
