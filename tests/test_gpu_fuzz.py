@@ -1,5 +1,6 @@
 """Seeded random configurations through the C ABI against the oracle (and,
-without interpolation, store mode byte-identical to the materialised tuples): clip
+without interpolation, store mode byte-identical to the materialised tuples; for
+a third of the seeds, the host-buffer calls byte-identical to the device calls): clip
 family / depth / matrix / range / siting, tensor format (RGB or YUV-native)
 and dtype, frame size (odd widths included: TMA and generic paths), window
 length, alignment, scale factor and cut pattern, drawn from one generator.
@@ -119,6 +120,21 @@ def _check(p):
                     nin = len(run)  # frames per tuple (in_shape[1] is 3 x that)
                     win = st[run[0]:run[0] + nin].reshape(-1)
                     assert torch.equal(win.view(torch.uint8), t[r, :nin * slot].view(torch.uint8)), (p, r)
+        if not p["yuv"] and p["seed"] % 3 == 0:
+            # the host-buffer calls (staging, coalesced copies where the host
+            # layout allows) give the same bytes as the device calls
+            hb = FrameBuffer(lay, F, device="cpu", pin=True)
+            hb.data.copy_(buf.data.cpu())
+            th = torch.full_like(t, float("nan"))
+            h.frames_to_tensor_batch_host(hb.descriptors(), 0, runs, th.data_ptr(), pstride * t.element_size())
+            ho = FrameBuffer(olay, 2 * M, device="cpu", pin=True)
+            stream = torch.cuda.current_stream()
+            h.tensor_to_frames_batch_host(to.data_ptr(), ostride * to.element_size(), Ho, Wo, ho.descriptors(), 2,
+                                          stream)
+            h.host_fence(stream)
+            torch.cuda.synchronize()
+            assert torch.equal(th.view(torch.uint8), t.view(torch.uint8)), p
+            assert torch.equal(ho.data, out.data.cpu()), p
         tn = t.cpu().numpy()
         for r, run in enumerate(runs):
             frames = [host[i] for i in run]
