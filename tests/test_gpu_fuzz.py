@@ -1,6 +1,7 @@
 """Seeded random configurations through the C ABI against the oracle (and,
 without interpolation, store mode byte-identical to the materialised tuples; for
-a third of the seeds, the host-buffer calls byte-identical to the device calls): clip
+a third of the seeds, the host-buffer calls byte-identical to the device calls;
+scene detection with exact SADs): clip
 family / depth / matrix / range / siting, tensor format (RGB or YUV-native)
 and dtype, frame size (odd widths included: TMA and generic paths), window
 length, alignment, scale factor and cut pattern, drawn from one generator.
@@ -135,6 +136,15 @@ def _check(p):
             torch.cuda.synchronize()
             assert torch.equal(th.view(torch.uint8), t.view(torch.uint8)), p
             assert torch.equal(ho.data, out.data.cpu()), p
+        # scene detection over the clip (NEXT-4): exact SADs, same decisions
+        thr = (0.0, 0.01, 0.15, 0.3)[p["seed"] % 4]
+        sad = torch.zeros(F, dtype=torch.int64, device=DEV)
+        flg = torch.zeros(F, dtype=torch.uint8, device=DEV)
+        h.scene_detect(0, F, thr, sad.data_ptr(), flg.data_ptr())
+        torch.cuda.synchronize()
+        osad, ocut = O.scene_detect(host, p["W"], p["H"], p["family"], p["bits"], p["matrix"], p["rng_"], thr)
+        assert np.array_equal(sad.cpu().numpy().astype(np.uint64), osad), p
+        assert np.array_equal(flg.cpu().numpy(), ocut), p
         tn = t.cpu().numpy()
         for r, run in enumerate(runs):
             frames = [host[i] for i in run]
