@@ -1,7 +1,7 @@
 """Seeded random configurations through the C ABI against the oracle (and,
 without interpolation, store mode byte-identical to the materialised tuples; for
 a third of the seeds, the host-buffer calls byte-identical to the device calls;
-scene detection with exact SADs): clip
+scene detection with exact SADs; for interpolation, the Fig. 1 batch store): clip
 family / depth / matrix / range / siting, tensor format (RGB or YUV-native)
 and dtype, frame size (odd widths included: TMA and generic paths), window
 length, alignment, scale factor and cut pattern, drawn from one generator.
@@ -15,6 +15,7 @@ import numpy as np
 import pytest
 import torch
 
+from oracle import batch_store as B
 from oracle import oracle as O
 from paper_2308_03121_b200 import nnvisr as nv
 from paper_2308_03121_b200 import synth
@@ -136,6 +137,22 @@ def _check(p):
             torch.cuda.synchronize()
             assert torch.equal(th.view(torch.uint8), t.view(torch.uint8)), p
             assert torch.equal(ho.data, out.data.cpu()), p
+        if p["interp"] and not p["yuv"]:
+            # Fig. 1 batches (NEXT-2): the plan equals the oracle's, and every
+            # lane's slot in the batch store equals the materialised tuple's
+            b = 2 + p["seed"] % 2
+            slot = 3 * Hp * Wp
+            batches = h.plan_batches(cut, b)
+            assert [x["slots"] for x in batches] == [x["slots"] for x in B.plan_batches(cut, 1, True, b)], p
+            for x in batches:
+                sst = torch.full((len(x["slots"]), slot), float("nan"), dtype=tdt, device=DEV)
+                h.frames_to_slots(x["slots"], sst.data_ptr())
+                torch.cuda.synchronize()
+                for j, r in enumerate(x["lanes"]):
+                    for k in range(len(runs[r])):
+                        off = nv.shared_slot_offset(1, b, 0, k, j) if x["shared"] else k * b + j
+                        assert torch.equal(sst[off].view(torch.uint8),
+                                           t[r, k * slot:(k + 1) * slot].view(torch.uint8)), (p, x, j, k)
         # scene detection over the clip (NEXT-4): exact SADs, same decisions
         thr = (0.0, 0.01, 0.15, 0.3)[p["seed"] % 4]
         sad = torch.zeros(F, dtype=torch.int64, device=DEV)
