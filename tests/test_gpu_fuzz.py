@@ -16,6 +16,7 @@ import pytest
 import torch
 
 from oracle import batch_store as B
+from oracle import emission as E
 from oracle import oracle as O
 from paper_2308_03121_b200 import nnvisr as nv
 from paper_2308_03121_b200 import synth
@@ -137,6 +138,8 @@ def _check(p):
             torch.cuda.synchronize()
             assert torch.equal(th.view(torch.uint8), t.view(torch.uint8)), p
             assert torch.equal(ho.data, out.data.cpu()), p
+        if p["interp"]:  # the emission schedule (NEXT-1) equals the oracle's
+            assert h.schedule_outputs(cut) == E.schedule_outputs(cut, 1, 2, 3, True, True), p
         if p["interp"] and not p["yuv"]:
             # Fig. 1 batches (NEXT-2): the plan equals the oracle's, and every
             # lane's slot in the batch store equals the materialised tuple's
