@@ -1,7 +1,8 @@
 """Seeded random configurations through the C ABI against the oracle (and,
 without interpolation, store mode byte-identical to the materialised tuples; for
 a third of the seeds, the host-buffer calls byte-identical to the device calls;
-scene detection with exact SADs; for interpolation, the Fig. 1 batch store): clip
+scene detection with exact SADs; for interpolation, the Fig. 1 batch store and the
+emission schedule; for sliding windows, 2-4 emulated frame-range shards): clip
 family / depth / matrix / range / siting, tensor format (RGB or YUV-native)
 and dtype, frame size (odd widths included: TMA and generic paths), window
 length, alignment, scale factor and cut pattern, drawn from one generator.
@@ -19,6 +20,7 @@ from oracle import batch_store as B
 from oracle import emission as E
 from oracle import oracle as O
 from paper_2308_03121_b200 import nnvisr as nv
+from paper_2308_03121_b200 import shard as sh
 from paper_2308_03121_b200 import synth
 from paper_2308_03121_b200.frames import FrameBuffer, FrameLayout
 
@@ -138,6 +140,30 @@ def _check(p):
             torch.cuda.synchronize()
             assert torch.equal(th.view(torch.uint8), t.view(torch.uint8)), p
             assert torch.equal(ho.data, out.data.cpu()), p
+        if not p["interp"]:
+            # frame-range shards emulated on this GPU: each
+            # rank binds only its window [halo | own | halo] at its global base
+            # and plans from its window's flags; its tuples equal the
+            # single-GPU ones byte for byte
+            world = 2 + p["seed"] % 3
+            L = (p["N"] - 1) // 2
+            try:
+                shards = [sh.shard_of(F, world, rk, L, p["N"] - 1 - L) for rk in range(world)]
+            except ValueError:
+                shards = []
+            for s_ in shards:
+                h.bind_frames(buf.descriptors(range(s_.window_first, s_.window_first + s_.window_count)),
+                              base=s_.window_first)
+                ins, _ = h.plan_range(F, s_.window_first, cut[s_.window_first:s_.window_first + s_.window_count],
+                                      s_.begin, s_.end)
+                assert np.array_equal(ins, runs[s_.begin:s_.end]), p
+                if len(ins) == 0 or p["yuv"]:  # (YUV-native tensors: the plan only)
+                    continue
+                ts = torch.full((len(ins), pstride), float("nan"), dtype=tdt, device=DEV)
+                h.frames_to_tensor_batch(ins, ts.data_ptr(), pstride * ts.element_size())
+                torch.cuda.synchronize()
+                assert torch.equal(ts.view(torch.uint8), t[s_.begin:s_.end].view(torch.uint8)), (p, s_)
+            h.bind_frames(buf.descriptors())
         if p["interp"]:  # the emission schedule (NEXT-1) equals the oracle's
             assert h.schedule_outputs(cut) == E.schedule_outputs(cut, 1, 2, 3, True, True), p
         if p["interp"] and not p["yuv"]:
