@@ -140,6 +140,12 @@ def _check(p):
             torch.cuda.synchronize()
             assert torch.equal(th.view(torch.uint8), t.view(torch.uint8)), p
             assert torch.equal(ho.data, out.data.cpu()), p
+        if not p["yuv"] and len(runs):
+            # the single-tuple call with frame descriptors (duplicates allowed)
+            one = torch.full((pstride,), float("nan"), dtype=tdt, device=DEV)
+            h.frames_to_tensor(buf.descriptors(runs[-1]), one.data_ptr())
+            torch.cuda.synchronize()
+            assert torch.equal(one.view(torch.uint8), t[len(runs) - 1].view(torch.uint8)), p
         if not p["interp"]:
             # frame-range shards emulated on this GPU: each
             # rank binds only its window [halo | own | halo] at its global base
