@@ -146,6 +146,11 @@ def _check(p):
             h.frames_to_tensor(buf.descriptors(runs[-1]), one.data_ptr())
             torch.cuda.synchronize()
             assert torch.equal(one.view(torch.uint8), t[len(runs) - 1].view(torch.uint8)), p
+            # and the single-tuple tensor -> frames call
+            o1 = FrameBuffer(olay, M, device=DEV)
+            h.tensor_to_frames(to[1].data_ptr(), Ho, Wo, o1.descriptors())
+            torch.cuda.synchronize()
+            assert torch.equal(o1.data, out.data[M:2 * M]), p
         if not p["interp"]:
             # frame-range shards emulated on this GPU: each
             # rank binds only its window [halo | own | halo] at its global base
