@@ -21,6 +21,9 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 SRC_PATH = os.path.join(HERE, "nnvisr_oracle.c")
+# tests/test_oracle_mutations.py loads deliberately broken builds of the
+# oracle through this variable to show that the pins go red on them
+_MUTANT = os.environ.get("NNVISR_ORACLE_MUTANT_LIB")
 
 YUV420, YUV444, RGB = 0, 1, 2
 BT601, BT709, BT2020 = 0, 1, 2
@@ -49,8 +52,11 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(LIB_PATH)
+        if _MUTANT:
+            L = C.CDLL(_MUTANT)
+        else:
+            build()
+            L = C.CDLL(LIB_PATH)
         i64p = C.POINTER(C.c_int64)
         L.oracle_plan.restype = C.c_int64
         L.oracle_plan.argtypes = [C.c_int64, C.c_void_p, C.c_int, C.c_int, C.c_int, i64p, i64p, C.c_int64]
