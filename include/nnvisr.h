@@ -45,8 +45,12 @@
  *   - Frames: planar, plane order (Y, U, V) or (R, G, B); 8-bit samples are
  *     uint8, 10/16-bit samples are uint16 holding the value in the low bits.
  *     4:2:0 chroma planes are (width/2) x (height/2).  `pitch` is the byte
- *     distance between rows.  Frames and tensors are in device memory unless
- *     a parameter says "host".
+ *     distance between rows.  Every plane must be readable for rows * pitch
+ *     bytes from its pointer, i.e. including the pitch padding after the
+ *     last row (the TMA paths round copy windows up to 16-byte groups and may
+ *     copy a whole plane as rows * pitch bytes; the padding values are never
+ *     used).  Frames and tensors are in device memory unless a parameter
+ *     says "host".
  *   - Tensors: NCHW, batch 1, fp32 or fp16, rows contiguous.  Input tensor
  *     [1, 3N, Hp, Wp]: tuple slot t -> channels 3t, 3t+1, 3t+2 = R', G', B'
  *     (reading A7), Hp/Wp = height/width rounded up to `align`, padding

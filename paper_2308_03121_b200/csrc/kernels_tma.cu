@@ -542,19 +542,19 @@ __global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
                     }
                     bulk_commit();
                     ++ng;
-                    continue;
-                }
-                for (int c = 0; c < 3; ++c) {
-                    if (whole_rows) {
-                        s2g_ob(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
-                    } else {
-                        for (int rr = 0; rr < rows; ++rr)
-                            s2g_ob(o + c * plane + static_cast<int64_t>(rr) * a.Wp, ob + (c * brows + rr) * sw,
-                                     sw * sizeof(OUT));
+                } else {
+                    for (int c = 0; c < 3; ++c) {
+                        if (whole_rows) {
+                            s2g_ob(o + c * plane, ob + c * brows * sw, rows * sw * sizeof(OUT));
+                        } else {
+                            for (int rr = 0; rr < rows; ++rr)
+                                s2g_ob(o + c * plane + static_cast<int64_t>(rr) * a.Wp, ob + (c * brows + rr) * sw,
+                                       sw * sizeof(OUT));
+                        }
                     }
+                    bulk_commit();
+                    ++ng;
                 }
-                bulk_commit();
-                ++ng;
             }
             NNVISR_TRACE(true, 5, i);
             if (rel && (back == 0 || !a.release_first)) {
@@ -1059,7 +1059,6 @@ __device__ __forceinline__ void t2f_yuv_issue(const T2FArgs &a, int64_t t, uint8
     const uint32_t lb = (x1 - x0) * sizeof(TIN), cb = (SUB ? (x1 - x0) >> 1 : x1 - x0) * sizeof(TIN);
     mbar_arrive_expect_tx(bar, ROWS * lb + 2 * cb);
     TIN *sv = reinterpret_cast<TIN *>(st);
-#pragma unroll
 #ifdef NNVISR_CHECKED
     {  // into this stage, from inside the slot's luma plane / two chroma planes
         const TIN *l0 = reinterpret_cast<const TIN *>(a.src + static_cast<int64_t>(tup) * a.tensor_stride) +
@@ -1073,6 +1072,7 @@ __device__ __forceinline__ void t2f_yuv_issue(const T2FArgs &a, int64_t t, uint8
                                      reinterpret_cast<const char *>(c0 + 2 * cplane));
     }
 #endif
+#pragma unroll
     for (int r = 0; r < ROWS; ++r) bulk_g2s(sv + r * a.segw, ls + r * a.tw, lb, bar);
 #pragma unroll
     for (int p = 0; p < 2; ++p) bulk_g2s(sv + ROWS * a.segw + p * segwc, cs + p * cplane, cb, bar);

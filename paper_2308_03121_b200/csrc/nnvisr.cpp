@@ -1095,11 +1095,16 @@ nnvisr_status nnvisr_scene_detect(nnvisr_handle *h, int64_t first, int64_t count
     nnvisr_status s = ensure_device(h);
     if (s) return s;
     const int vec = h->frames_vec && h->fmt.width % kPx == 0;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // the kernels read the bound frame table: take an upload slot (no upload)
+    // so that its event orders a later nnvisr_bind_frames after them
+    UploadSlot *slot = nullptr;
+    if ((s = acquire_slot(h, &slot, st))) return s;
     cudaError_t e = launch_scene_detect(h->fmt.family, h->fmt.bits, h->fmt.range, h->fmt.width, h->fmt.height,
-                                        h->frames + (first - h->frames_base), (int)count, vec, threshold, sad, cut,
-                                        static_cast<cudaStream_t>(stream));
+                                        h->frames + (first - h->frames_base), (int)count, vec, threshold, sad, cut, st);
+    nnvisr_status s2 = release_slot(slot, st);
     if (e != cudaSuccess) return cuda_fail(e, "scene detection launch");
-    return NNVISR_OK;
+    return s2;
 }
 
 int64_t nnvisr_shared_slot_offset(int32_t n, int32_t b, int32_t region, int32_t k, int32_t j)
@@ -1153,7 +1158,9 @@ nnvisr_status nnvisr_plan_batches(const nnvisr_handle *h, int64_t num_frames, co
                     lanes[nb * b + j] = r;
                     emit[nb * b + j] = real;
                     full = full && real;
-                    all_aligned = all_aligned && consecutive(r) && (j == 0 || ins[r * N] == ins[(r - 1) * N] + n);
+                    // padding lanes (!real) never make a shared batch (full is false);
+                    // skipping them also keeps r - 1 >= 0
+                    all_aligned = all_aligned && (!real || (consecutive(r) && (j == 0 || ins[r * N] == ins[(r - 1) * N] + n)));
                 }
                 const bool sh = extra && full && all_aligned;
                 shared[nb] = sh;

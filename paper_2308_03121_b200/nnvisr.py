@@ -194,6 +194,24 @@ class Handle:
         except Exception:
             pass
 
+    # -- argument checks: the C side reads exactly N / M / count*M descriptors
+    # and N indices per run, so short arrays are rejected here (ctypes would
+    # hand the library whatever lies past their end)
+    def _runs(self, run_inputs) -> tuple[np.ndarray, int]:
+        ri = np.ascontiguousarray(np.asarray(run_inputs, dtype=np.int64))
+        if ri.ndim == 2:
+            if ri.shape[1] != self.N:
+                raise ValueError(f"run_inputs has {ri.shape[1]} columns, the network takes N = {self.N}")
+            return ri, ri.shape[0]
+        if ri.ndim != 1 or ri.size % self.N:
+            raise ValueError(f"run_inputs of shape {ri.shape} is not a whole number of N = {self.N} runs")
+        return ri, ri.size // self.N
+
+    @staticmethod
+    def _need(what: str, have: int, need: int):
+        if have < need:
+            raise ValueError(f"{what}: {have} given, {need} needed")
+
     @property
     def N(self):
         return self.cfg.input_count
@@ -230,12 +248,13 @@ class Handle:
         _check(_lib.nnvisr_bind_frames(self._h, base, arr, len(frames)))
 
     def frames_to_tensor(self, frames: Sequence[Frame], tensor_ptr: int, stream=None):
+        if len(frames) != self.N:
+            raise ValueError(f"{len(frames)} frame descriptors given, the network takes N = {self.N}")
         arr = frame_array(frames)
         _check(_lib.nnvisr_frames_to_tensor(self._h, arr, tensor_ptr, _stream_ptr(stream)))
 
     def frames_to_tensor_batch(self, run_inputs: np.ndarray, tensors_ptr: int, stride: int, stream=None):
-        ri = np.ascontiguousarray(run_inputs, dtype=np.int64)
-        nr = ri.shape[0] if ri.ndim == 2 else ri.size // self.N
+        ri, nr = self._runs(run_inputs)
         _check(_lib.nnvisr_frames_to_tensor_batch(self._h, _i64p(ri), nr, tensors_ptr, stride, _stream_ptr(stream)))
 
     def release_graph_tables(self):
@@ -246,6 +265,7 @@ class Handle:
         _check(_lib.nnvisr_frames_to_store(self._h, first, count, store_ptr, _stream_ptr(stream)))
 
     def tensor_to_frames(self, tensor_ptr: int, t_h: int, t_w: int, out: Sequence[Frame], stream=None):
+        self._need("output frame descriptors", len(out), self.M)
         arr = frame_array(out)
         _check(_lib.nnvisr_tensor_to_frames(self._h, tensor_ptr, t_h, t_w, arr, _stream_ptr(stream)))
 
@@ -283,13 +303,14 @@ class Handle:
 
     def frames_to_tensor_batch_host(self, host_frames: Sequence[Frame], base: int, run_inputs, tensors_ptr: int,
                                     stride: int, stream=None):
-        ri = np.ascontiguousarray(run_inputs, dtype=np.int64)
+        ri, nr = self._runs(run_inputs)
         arr = frame_array(host_frames)
         _check(_lib.nnvisr_frames_to_tensor_batch_host(self._h, arr, base, len(host_frames), _i64p(ri),
-                                                       ri.size // self.N, tensors_ptr, stride, _stream_ptr(stream)))
+                                                       nr, tensors_ptr, stride, _stream_ptr(stream)))
 
     def tensor_to_frames_batch_host(self, tensors_ptr: int, stride: int, t_h: int, t_w: int,
                                     host_out: Sequence[Frame], count: int, stream=None):
+        self._need("host output frame descriptors", len(host_out), count * self.M)
         arr = frame_array(host_out)
         _check(_lib.nnvisr_tensor_to_frames_batch_host(self._h, tensors_ptr, stride, t_h, t_w, arr, count,
                                                        _stream_ptr(stream)))
@@ -298,7 +319,8 @@ class Handle:
         _check(_lib.nnvisr_host_fence(self._h, _stream_ptr(stream)))
 
     def copy_frames(self, src_frames, out: Sequence[Frame], stream=None):
-        sf = np.ascontiguousarray(src_frames, dtype=np.int64)
+        sf = np.ascontiguousarray(src_frames, dtype=np.int64).reshape(-1)
+        self._need("pass-through output descriptors", len(out), sf.size)
         arr = frame_array(out)
         _check(_lib.nnvisr_copy_frames(self._h, _i64p(sf), arr, sf.size, _stream_ptr(stream)))
 
@@ -315,18 +337,19 @@ class Handle:
 
     def frames_to_tensor_yuv_batch(self, run_inputs, luma_ptr: int, luma_stride: int, chroma_ptr: int,
                                    chroma_stride: int, stream=None):
-        ri = np.ascontiguousarray(np.asarray(run_inputs, dtype=np.int64))
-        nr = ri.shape[0] if ri.ndim > 1 else (ri.shape[0] // self.N if ri.size else 0)
+        ri, nr = self._runs(run_inputs)
         _check(_lib.nnvisr_frames_to_tensor_yuv_batch(self._h, _i64p(ri), nr, luma_ptr, luma_stride, chroma_ptr,
                                                       chroma_stride, _stream_ptr(stream)))
 
     def tensor_to_frames_yuv_batch(self, luma_ptr: int, luma_stride: int, chroma_ptr: int, chroma_stride: int,
                                    t_h: int, t_w: int, out: Sequence[Frame], count: int, stream=None):
+        self._need("output frame descriptors", len(out), count * self.M)
         _check(_lib.nnvisr_tensor_to_frames_yuv_batch(self._h, luma_ptr, luma_stride, chroma_ptr, chroma_stride,
                                                       t_h, t_w, frame_array(out), count, _stream_ptr(stream)))
 
     def tensor_to_frames_batch(self, tensors_ptr: int, stride: int, t_h: int, t_w: int, out: Sequence[Frame],
                                count: int, stream=None):
+        self._need("output frame descriptors", len(out), count * self.M)
         arr = frame_array(out)
         _check(_lib.nnvisr_tensor_to_frames_batch(self._h, tensors_ptr, stride, t_h, t_w, arr, count,
                                                   _stream_ptr(stream)))

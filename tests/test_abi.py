@@ -266,3 +266,27 @@ def test_release_graph_tables_without_captures():
     assert nv.lib().nnvisr_release_graph_tables(None) == 2  # INVALID_ARG: null handle
     with nv.open(_cfg()) as h:
         h.release_graph_tables()  # nothing captured: a no-op, no device touched
+
+
+def test_binding_rejects_short_descriptor_and_run_arrays():
+    """the ctypes wrappers check array lengths before the call
+    (the C side reads N / M / count*M descriptors and N indices per run)."""
+    with nv.open(_cfg()) as h:
+        N, M = h.N, h.M
+        f = nv.Frame()
+        with pytest.raises(ValueError):
+            h.frames_to_tensor([f] * (N - 1) if N > 1 else [], 4096)
+        with pytest.raises(ValueError):
+            h.frames_to_tensor_batch(np.zeros((2, N + 1), np.int64), 4096, 1 << 20)
+        with pytest.raises(ValueError):
+            h.frames_to_tensor_batch(np.zeros(2 * N + 1, np.int64), 4096, 1 << 20)
+        with pytest.raises(ValueError):
+            h.tensor_to_frames(4096, 64, 64, [f] * (M - 1))
+        with pytest.raises(ValueError):
+            h.tensor_to_frames_batch(4096, 1 << 20, 64, 64, [f] * (2 * M - 1), 2)
+        with pytest.raises(ValueError):
+            h.tensor_to_frames_batch_host(4096, 1 << 20, 64, 64, [f] * (3 * M - 1), 3)
+        with pytest.raises(ValueError):
+            h.copy_frames([0, 1, 2], [f, f])
+        with pytest.raises(ValueError):
+            h.frames_to_tensor_batch_host([f], 0, np.zeros((1, N + 2), np.int64), 4096, 1 << 20)
