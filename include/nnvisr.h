@@ -77,6 +77,7 @@ typedef enum {
     NNVISR_ERR_UNSUPPORTED = 3,     /* valid request this build does not implement */
     NNVISR_ERR_OUT_OF_MEMORY = 4,   /* scratch allocation failed */
     NNVISR_ERR_CUDA = 5,            /* a CUDA runtime call or kernel launch failed */
+    NNVISR_ERR_NCCL = 6,            /* NCCL missing, or an NCCL call / communicator failed */
     NNVISR_ERR_CAPACITY = 7         /* caller's output array too small */
 } nnvisr_status;
 
@@ -353,6 +354,16 @@ nnvisr_status nnvisr_frames_to_slots(nnvisr_handle *h, const int64_t *slot_frame
  * copy store slot src to slot dst on `stream`. */
 nnvisr_status nnvisr_copy_slot(nnvisr_handle *h, void *store, int64_t src, int64_t dst, void *stream);
 
+/* Region advance of a bounded store ring (store mode S with a ring of
+ * regions; the b = 1 form of PAPER.md P:380-382 "only the
+ * last frame need to be copied ... (6 to 5 in the figure)"): copy `count`
+ * consecutive slots starting at slot src to slot dst of `store` in one
+ * device copy on `stream` (a sliding window of N frames carries its last
+ * N-1 slots into the next region).  The two ranges must not overlap
+ * (NNVISR_ERR_INVALID_ARG). */
+nnvisr_status nnvisr_copy_slots(nnvisr_handle *h, void *store, int64_t src, int64_t dst, int64_t count,
+                                void *stream);
+
 /* Scene-change detection (SPEC.md [MODULE] scenedetect,
  * detect_scene_changes, S:105-113 -- the paper leaves detection to upstream
  * filters, §3.2).  For bound frames first+i, i in
@@ -399,6 +410,105 @@ nnvisr_status nnvisr_peer_import(const nnvisr_peer_handle *in, void **dev_ptr);
 /* Unmap a pointer returned by nnvisr_peer_import (after the work reading it
  * has completed).  NNVISR_ERR_INVALID_ARG for a pointer not imported here. */
 nnvisr_status nnvisr_peer_close(void *dev_ptr);
+
+/* ---- Multi-GPU frame-range shards and the NCCL halo exchange (SURVEY.md
+ * §8(b), §8(e)).  The clip shards by contiguous frame ranges: rank r of W
+ * owns the runs whose fresh frame lies in [r*F/W, (r+1)*F/W).  A sliding
+ * window reads L frames before and R = N-1-L frames after its fresh frame
+ * (reading A8), and whether each of them is used or replaced by a duplicate
+ * depends on its scene-cut flag (§3.2, §3.3).
+ * So a rank keeps a WINDOW of frames [left halo | owned | right halo] and
+ * needs its neighbours' edge frames and flags: one grouped point-to-point
+ * exchange per step, the only data that crosses ranks.  Window rows are
+ * frame records of frame_bytes bytes each (a k-frame halo is one message),
+ * with the flags in a parallel byte array (cut_window[i] = flag of window
+ * frame i, as nnvisr_plan reads it).  The local plan is then
+ * nnvisr_plan_range(total, window_first, cut_window, begin, end), which
+ * equals the whole clip's plan restricted to the shard.
+ *
+ * NCCL (libnccl.so.2) is loaded at the first nnvisr_comm_* call (the copy
+ * the process already loaded is reused, NNVISR_NCCL_LIB overrides); without
+ * it those calls return NNVISR_ERR_NCCL.  nnvisr_shard_of and
+ * nnvisr_halo_plan are pure host functions. */
+
+typedef struct {
+    int64_t begin, end;               /* owned frames [begin, end) = [r*F/W, (r+1)*F/W) */
+    int64_t left, right;              /* halo frames before begin (min(L, begin)) / after end (min(R, F-end)) */
+    int64_t window_first, window_count; /* the window = frames [window_first, window_first+window_count) */
+} nnvisr_shard;
+
+/* Geometry of shard `rank` of `world` over a clip of `total` frames for a
+ * window reaching L frames back and R frames ahead (0 <= L, R <= 15).
+ * NNVISR_ERR_INVALID_ARG if rank is outside [0, world) or (world > 1) a
+ * shard holds fewer than max(L, R, 1) frames (a halo would then span more
+ * than one neighbour). */
+nnvisr_status nnvisr_shard_of(int64_t total, int32_t world, int32_t rank, int32_t L, int32_t R, nnvisr_shard *out);
+
+/* One point-to-point message of a rank's halo exchange: window rows
+ * [first, first+count) are sent to (send = 1) or received from (send = 0)
+ * rank `peer`.  The flags of the same rows travel in a second message of
+ * count bytes. */
+typedef struct {
+    int32_t peer, send;
+    int64_t first, count;
+} nnvisr_halo_msg;
+
+/* The messages of rank `rank` (at most 4, *count set): my first min(R, F-begin)
+ * owned rows to rank-1 and my left halo from it; my last min(L, end) owned
+ * rows to rank+1 and my right halo from it.  Every send matches the
+ * neighbour's receive of the same count. */
+nnvisr_status nnvisr_halo_plan(int64_t total, int32_t world, int32_t rank, int32_t L, int32_t R,
+                               nnvisr_halo_msg msgs[4], int32_t *count);
+
+typedef struct nnvisr_comm nnvisr_comm;
+#define NNVISR_COMM_ID_BYTES 128
+
+/* A new communicator id (ncclGetUniqueId) on rank 0; broadcast its bytes to
+ * the other ranks out of band (e.g. torch.distributed). */
+nnvisr_status nnvisr_comm_unique_id(uint8_t id[NNVISR_COMM_ID_BYTES]);
+
+/* One process per GPU: join communicator `id` as rank `rank` of `world` on
+ * the CUDA device current in this thread (ncclCommInitRank; collective, every
+ * rank must call it).  Free with nnvisr_comm_destroy. */
+nnvisr_status nnvisr_comm_init_rank(const uint8_t id[NNVISR_COMM_ID_BYTES], int32_t world, int32_t rank,
+                                    nnvisr_comm **out);
+
+/* One process driving ndev GPUs: comms[i] is rank i on device devs[i]
+ * (ncclCommInitAll).  Use with nnvisr_halo_exchange_all. */
+nnvisr_status nnvisr_comm_init_all(int32_t ndev, const int32_t *devs, nnvisr_comm **comms);
+
+/* Rank, world size and CUDA device of a communicator (any may be NULL). */
+nnvisr_status nnvisr_comm_info(const nnvisr_comm *comm, int32_t *rank, int32_t *world, int32_t *device);
+
+/* NNVISR_ERR_NCCL if the communicator has an asynchronous error
+ * (ncclCommGetAsyncError: a failed peer or transport); the exchange calls
+ * also check after enqueueing. */
+nnvisr_status nnvisr_comm_check(const nnvisr_comm *comm);
+
+/* The halo exchange of this rank: one ncclGroupStart /
+ * ncclGroupEnd holding the messages of nnvisr_halo_plan(total_frames,
+ * world, rank, L, R), each as one ncclSend / ncclRecv of count*frame_bytes
+ * bytes of `window` (device, [window_count][frame_bytes], owned rows filled)
+ * plus one of count bytes of `cut_window` (device [window_count]), enqueued
+ * on `stream`.  window = NULL exchanges the flags only (frames read in place,
+ * nnvisr_peer_*); cut_window = NULL the frames only.  Every rank must call it
+ * with the same total_frames, L, R.  Returns after enqueueing; the halo rows
+ * are valid once `stream` reaches that point.  World 1: nothing to send. */
+nnvisr_status nnvisr_halo_exchange(nnvisr_comm *comm, int64_t total_frames, int32_t L, int32_t R, void *window,
+                                   int64_t frame_bytes, uint8_t *cut_window, void *stream);
+
+/* Single-process form: the exchange of every rank of an
+ * nnvisr_comm_init_all communicator in one group (windows[i],
+ * cut_windows[i], streams[i] on device i). */
+nnvisr_status nnvisr_halo_exchange_all(nnvisr_comm *const *comms, int32_t ndev, int64_t total_frames, int32_t L,
+                                       int32_t R, void *const *windows, int64_t frame_bytes,
+                                       uint8_t *const *cut_windows, void *const *streams);
+
+/* Free a communicator (ncclCommDestroy; after its work completed).  NULL is OK. */
+nnvisr_status nnvisr_comm_destroy(nnvisr_comm *comm);
+
+/* NCCL version code of the loaded library (e.g. 22809), -1 if NCCL is unavailable. */
+int32_t nnvisr_nccl_version(void);
 
 /* Free the upload tables of every call captured into a CUDA graph so far
  * (see "CUDA graphs" above).  The caller must have destroyed those graphs

@@ -16,7 +16,7 @@ INTERPOLATION, EXTRA_FRAME, DOUBLE_FRAME = 1, 2, 4
 YUV_INPUT, YUV_OUTPUT = 8, 16  # YUV-native network tensors (NEXT-3)
 
 STATUS = {0: "OK", 1: "INVALID_CONFIG", 2: "INVALID_ARG", 3: "UNSUPPORTED", 4: "OUT_OF_MEMORY",
-          5: "CUDA", 7: "CAPACITY"}
+          5: "CUDA", 6: "NCCL", 7: "CAPACITY"}
 
 
 class ClipFormat(C.Structure):

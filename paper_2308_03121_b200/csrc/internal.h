@@ -5,7 +5,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "nnvisr.h"
+
+struct nnvisr_comm;
+
 namespace nnvisr {
+
+// Set the thread's last-error text (nnvisr_last_error) and return s; defined
+// in nnvisr.cpp, used by the other host translation units (comm.cpp).
+nnvisr_status set_error(nnvisr_status s, const char *msg);
 
 constexpr int kYUV420 = 0, kYUV444 = 1, kRGB = 2;
 constexpr int kF32 = 0, kF16 = 1;

@@ -48,6 +48,16 @@ nnvisr_status fail(nnvisr_status s, const char *fmt, ...)
     return s;
 }
 
+}  // namespace
+
+nnvisr_status nnvisr::set_error(nnvisr_status s, const char *msg)
+{
+    g_error = msg ? msg : "";
+    return s;
+}
+
+namespace {
+
 nnvisr_status cuda_fail(cudaError_t e, const char *what)
 {
     return fail(NNVISR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -1218,6 +1228,25 @@ nnvisr_status nnvisr_copy_slot(nnvisr_handle *h, void *store, int64_t src, int64
     cudaError_t e = cudaMemcpyAsync(base + dst * slot_bytes, base + src * slot_bytes, slot_bytes,
                                     cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync (slot copy)");
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_copy_slots(nnvisr_handle *h, void *store, int64_t src, int64_t dst, int64_t count, void *stream)
+{
+    g_error.clear();
+    if (!h || (count > 0 && !store)) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (src < 0 || dst < 0 || count < 0) return fail(NNVISR_ERR_INVALID_ARG, "negative slot or count");
+    if (count == 0 || src == dst) return NNVISR_OK;
+    if (src < dst + count && dst < src + count)
+        return fail(NNVISR_ERR_INVALID_ARG, "slot ranges [%lld, +%lld) and [%lld, +%lld) overlap", (long long)src,
+                    (long long)count, (long long)dst, (long long)count);
+    nnvisr_status s = ensure_device(h);
+    if (s) return s;
+    const int64_t slot_bytes = store_slot_bytes(h);
+    char *base = static_cast<char *>(store);
+    cudaError_t e = cudaMemcpyAsync(base + dst * slot_bytes, base + src * slot_bytes, count * slot_bytes,
+                                    cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync (region advance)");
     return NNVISR_OK;
 }
 

@@ -32,6 +32,20 @@ class NnvisrError(RuntimeError):
         self.message = message
 
 
+class Shard(C.Structure):
+    """nnvisr_shard: owned frames [begin, end), halo sizes and the window."""
+    _fields_ = [("begin", C.c_int64), ("end", C.c_int64), ("left", C.c_int64), ("right", C.c_int64),
+                ("window_first", C.c_int64), ("window_count", C.c_int64)]
+
+
+class HaloMsg(C.Structure):
+    """nnvisr_halo_msg: window rows [first, first+count) sent to / received from `peer`."""
+    _fields_ = [("peer", C.c_int32), ("send", C.c_int32), ("first", C.c_int64), ("count", C.c_int64)]
+
+
+COMM_ID_BYTES = 128
+
+
 class PeerHandle(C.Structure):
     """nnvisr_peer_handle: CUDA IPC handle of an allocation + the pointer's offset in it."""
     _fields_ = [("ipc", C.c_uint8 * 64), ("offset", C.c_int64)]
@@ -65,6 +79,7 @@ def _load():
         "nnvisr_plan_batches": (st, [H, i64, C.c_void_p, C.c_int32, C.c_void_p, i64p, C.c_void_p, i64p, i64, i64p]),
         "nnvisr_frames_to_slots": (st, [H, i64p, i64, C.c_void_p, C.c_void_p]),
         "nnvisr_copy_slot": (st, [H, C.c_void_p, i64, i64, C.c_void_p]),
+        "nnvisr_copy_slots": (st, [H, C.c_void_p, i64, i64, i64, C.c_void_p]),
         "nnvisr_schedule_outputs": (st, [H, i64, C.c_void_p, C.c_void_p, i64p, i64p, i64, i64, i64p, i64p]),
         "nnvisr_copy_frames": (st, [H, i64p, C.POINTER(Frame), i64, C.c_void_p]),
         "nnvisr_frames_to_tensor_batch_host": (st, [H, C.POINTER(Frame), i64, i64, i64p, i64, C.c_void_p, i64,
@@ -79,6 +94,20 @@ def _load():
         "nnvisr_peer_import": (st, [C.POINTER(PeerHandle), C.POINTER(C.c_void_p)]),
         "nnvisr_peer_close": (st, [C.c_void_p]),
         "nnvisr_release_graph_tables": (st, [H]),
+        "nnvisr_shard_of": (st, [i64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(Shard)]),
+        "nnvisr_halo_plan": (st, [i64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(HaloMsg),
+                                  C.POINTER(C.c_int32)]),
+        "nnvisr_comm_unique_id": (st, [C.c_void_p]),
+        "nnvisr_comm_init_rank": (st, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+        "nnvisr_comm_init_all": (st, [C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p)]),
+        "nnvisr_comm_info": (st, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "nnvisr_comm_check": (st, [C.c_void_p]),
+        "nnvisr_halo_exchange": (st, [C.c_void_p, i64, C.c_int32, C.c_int32, C.c_void_p, i64, C.c_void_p,
+                                      C.c_void_p]),
+        "nnvisr_halo_exchange_all": (st, [C.POINTER(C.c_void_p), C.c_int32, i64, C.c_int32, C.c_int32,
+                                          C.POINTER(C.c_void_p), i64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+        "nnvisr_comm_destroy": (st, [C.c_void_p]),
+        "nnvisr_nccl_version": (C.c_int32, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -92,11 +121,14 @@ EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version"
             "nnvisr_tensor_shapes", "nnvisr_plan", "nnvisr_plan_range", "nnvisr_bind_frames",
             "nnvisr_frames_to_tensor", "nnvisr_frames_to_tensor_batch", "nnvisr_frames_to_store",
             "nnvisr_tensor_to_frames", "nnvisr_tensor_to_frames_batch", "nnvisr_scene_detect",
-            "nnvisr_shared_slot_offset", "nnvisr_plan_batches", "nnvisr_frames_to_slots", "nnvisr_copy_slot",
+            "nnvisr_shared_slot_offset", "nnvisr_plan_batches", "nnvisr_frames_to_slots", "nnvisr_copy_slot", "nnvisr_copy_slots",
             "nnvisr_schedule_outputs", "nnvisr_copy_frames", "nnvisr_frames_to_tensor_batch_host",
             "nnvisr_tensor_to_frames_batch_host", "nnvisr_host_fence", "nnvisr_chroma_shapes",
             "nnvisr_frames_to_tensor_yuv_batch", "nnvisr_tensor_to_frames_yuv_batch", "nnvisr_peer_export",
-            "nnvisr_peer_import", "nnvisr_peer_close", "nnvisr_release_graph_tables")
+            "nnvisr_peer_import", "nnvisr_peer_close", "nnvisr_release_graph_tables", "nnvisr_shard_of",
+            "nnvisr_halo_plan", "nnvisr_comm_unique_id", "nnvisr_comm_init_rank", "nnvisr_comm_init_all",
+            "nnvisr_comm_info", "nnvisr_comm_check", "nnvisr_halo_exchange", "nnvisr_halo_exchange_all",
+            "nnvisr_comm_destroy", "nnvisr_nccl_version")
 
 
 def lib():
@@ -148,6 +180,92 @@ def peer_import(handle: bytes) -> int:
 def peer_close(dev_ptr: int) -> None:
     """nnvisr_peer_close: unmap a pointer returned by peer_import."""
     _check(_lib.nnvisr_peer_close(dev_ptr))
+
+
+def shard_of(total: int, world: int, rank: int, L: int, R: int) -> Shard:
+    """nnvisr_shard_of: geometry of shard `rank` of `world` (ValueError if invalid)."""
+    out = Shard()
+    st = _lib.nnvisr_shard_of(total, world, rank, L, R, C.byref(out))
+    if st == 2:
+        raise ValueError(_lib.nnvisr_last_error().decode())
+    _check(st)
+    return out
+
+
+def halo_plan(total: int, world: int, rank: int, L: int, R: int) -> list[tuple[int, bool, int, int]]:
+    """nnvisr_halo_plan: [(peer, send, first window row, count)] of this rank."""
+    msgs = (HaloMsg * 4)()
+    n = C.c_int32()
+    st = _lib.nnvisr_halo_plan(total, world, rank, L, R, msgs, C.byref(n))
+    if st == 2:
+        raise ValueError(_lib.nnvisr_last_error().decode())
+    _check(st)
+    return [(int(m.peer), bool(m.send), int(m.first), int(m.count)) for m in msgs[:n.value]]
+
+
+def nccl_version() -> int:
+    """Version code of the NCCL the library loaded (-1: unavailable)."""
+    return int(_lib.nnvisr_nccl_version())
+
+
+def comm_unique_id() -> bytes:
+    """nnvisr_comm_unique_id (ncclGetUniqueId), to broadcast from rank 0."""
+    buf = (C.c_uint8 * COMM_ID_BYTES)()
+    _check(_lib.nnvisr_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """An NCCL communicator of the library (nnvisr_comm_init_rank ...
+    nnvisr_comm_destroy) carrying the halo exchange."""
+
+    def __init__(self, ptr: int, rank: int, world: int):
+        self._c = C.c_void_p(ptr)
+        self.rank, self.world = rank, world
+
+    @classmethod
+    def init_rank(cls, uid: bytes, world: int, rank: int) -> "Comm":
+        if len(uid) != COMM_ID_BYTES:
+            raise ValueError("communicator id must be %d bytes" % COMM_ID_BYTES)
+        buf = (C.c_uint8 * COMM_ID_BYTES).from_buffer_copy(uid)
+        p = C.c_void_p()
+        _check(_lib.nnvisr_comm_init_rank(buf, world, rank, C.byref(p)))
+        return cls(p.value, rank, world)
+
+    @classmethod
+    def init_all(cls, devs: Sequence[int]) -> list["Comm"]:
+        d = (C.c_int32 * len(devs))(*devs)
+        ps = (C.c_void_p * len(devs))()
+        _check(_lib.nnvisr_comm_init_all(len(devs), d, ps))
+        return [cls(ps[i], i, len(devs)) for i in range(len(devs))]
+
+    def info(self) -> tuple[int, int, int]:
+        r, w, dv = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(_lib.nnvisr_comm_info(self._c, C.byref(r), C.byref(w), C.byref(dv)))
+        return r.value, w.value, dv.value
+
+    def check(self):
+        _check(_lib.nnvisr_comm_check(self._c))
+
+    def halo_exchange(self, total: int, L: int, R: int, window_ptr: int | None, frame_bytes: int,
+                      cut_window_ptr: int | None, stream=None):
+        _check(_lib.nnvisr_halo_exchange(self._c, total, L, R, window_ptr, frame_bytes, cut_window_ptr,
+                                         _stream_ptr(stream)))
+
+    @staticmethod
+    def halo_exchange_all(comms: Sequence["Comm"], total: int, L: int, R: int, window_ptrs, frame_bytes: int,
+                          cut_window_ptrs, streams):
+        n = len(comms)
+        cs = (C.c_void_p * n)(*[c._c.value for c in comms])
+        ws = (C.c_void_p * n)(*window_ptrs)
+        fs = (C.c_void_p * n)(*cut_window_ptrs)
+        ss = (C.c_void_p * n)(*[_stream_ptr(s) for s in streams])
+        _check(_lib.nnvisr_halo_exchange_all(cs, n, total, L, R, ws, frame_bytes, fs, ss))
+
+    def destroy(self):
+        if self._c is not None and self._c.value:
+            _check(_lib.nnvisr_comm_destroy(self._c))
+        self._c = None
 
 
 def frame_array(frames: Sequence[Frame]):
@@ -330,6 +448,10 @@ class Handle:
 
     def copy_slot(self, store_ptr: int, src: int, dst: int, stream=None):
         _check(_lib.nnvisr_copy_slot(self._h, store_ptr, src, dst, _stream_ptr(stream)))
+
+    def copy_slots(self, store_ptr: int, src: int, dst: int, count: int, stream=None):
+        """nnvisr_copy_slots: region advance of a store ring (count slots src.. -> dst..)."""
+        _check(_lib.nnvisr_copy_slots(self._h, store_ptr, src, dst, count, _stream_ptr(stream)))
 
     def scene_detect(self, first: int, count: int, threshold: float, sad_ptr: int, cut_ptr: int, stream=None):
         """nnvisr_scene_detect: sad (uint64) and cut (uint8) device arrays [count]."""

@@ -6,9 +6,14 @@ frames before a_r and N-1-L frames after b_r-1 (the sliding window of
 reading A8), and its duplication rule needs those frames' scene-cut flags
 (§3.2, §3.3).  The only data-path collective is
 therefore one point-to-point exchange with each neighbour: my first R = N-1-L
-frames (+ flags) go to rank-1, my last L frames (+ flags) go to rank+1.  Over
-NCCL these are NVLink P2P transfers between GPUs; over gloo (the CPU tests)
-the same code moves host tensors.
+frames (+ flags) go to rank-1, my last L frames (+ flags) go to rank+1.
+
+The geometry (nnvisr_shard_of) and the message list (nnvisr_halo_plan) come
+from the C library.  On GPUs the exchange itself is the library's NCCL group
+(NcclHalo -> nnvisr_halo_exchange); torch.distributed only broadcasts the
+communicator id.  halo_exchange() runs the same message list over
+torch.distributed point-to-point calls: it is what the gloo (CPU) tests
+execute, so the library's plan is checked end to end without GPUs.
 
 Each rank keeps its frames in one window buffer [left + owned + right]
 [frame_bytes], so received halos land in place and a k-frame halo is one
@@ -21,6 +26,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 import torch.distributed as dist
+
+from . import nnvisr as nv
 
 
 @dataclass(frozen=True)
@@ -60,11 +67,12 @@ class Shard:
 
 
 def shard_of(total: int, world: int, rank: int, L: int, R: int) -> Shard:
-    """Contiguous shard r of W: frames [r*F/W, (r+1)*F/W)."""
-    a, b = rank * total // world, (rank + 1) * total // world
-    if world > 1 and b - a < max(L, R, 1):
-        raise ValueError(f"shard of {b - a} frames is shorter than the halo ({L}, {R})")
-    return Shard(rank, world, total, L, R, a, b)
+    """Contiguous shard r of W: frames [r*F/W, (r+1)*F/W) (nnvisr_shard_of;
+    ValueError when a shard is shorter than the halo)."""
+    g = nv.shard_of(total, world, rank, L, R)
+    s = Shard(rank, world, total, L, R, int(g.begin), int(g.end))
+    assert (s.left, s.right, s.window_first, s.window_count) == (g.left, g.right, g.window_first, g.window_count)
+    return s
 
 
 def halo_exchange(s: Shard, window: torch.Tensor | None, cut_window: torch.Tensor, group=None) -> None:
@@ -73,21 +81,10 @@ def halo_exchange(s: Shard, window: torch.Tensor | None, cut_window: torch.Tenso
     [left, left+owned) must already hold this rank's own frames and flags.
     All sends/receives go out as one batch (one NCCL group).  window = None
     exchanges the flags only (the frames are read in place, PeerHalo)."""
-    own0, own1 = s.left, s.left + s.owned
     ops = []
     bufs = ([window] if window is not None else []) + [cut_window]
-    if s.rank > 0:
-        need = s.neighbour(s.rank - 1).right       # rank-1's right halo = my first frames
-        if need:
-            ops += [dist.P2POp(dist.isend, b[own0:own0 + need], s.rank - 1, group) for b in bufs]
-        if s.left:
-            ops += [dist.P2POp(dist.irecv, b[0:s.left], s.rank - 1, group) for b in bufs]
-    if s.rank < s.world - 1:
-        need = s.neighbour(s.rank + 1).left        # rank+1's left halo = my last frames
-        if need:
-            ops += [dist.P2POp(dist.isend, b[own1 - need:own1], s.rank + 1, group) for b in bufs]
-        if s.right:
-            ops += [dist.P2POp(dist.irecv, b[own1:own1 + s.right], s.rank + 1, group) for b in bufs]
+    for peer, send, first, count in nv.halo_plan(s.total, s.world, s.rank, s.L, s.R):
+        ops += [dist.P2POp(dist.isend if send else dist.irecv, b[first:first + count], peer, group) for b in bufs]
     if ops:
         nvtx = torch.cuda.is_available()  # NVTX range for nsys / ncu --nvtx (SURVEY.md §5)
         if nvtx:
@@ -96,6 +93,34 @@ def halo_exchange(s: Shard, window: torch.Tensor | None, cut_window: torch.Tenso
             req.wait()
         if nvtx:
             torch.cuda.nvtx.range_pop()
+
+
+class NcclHalo:
+    """The product halo exchange: the library's NCCL communicator
+    (nnvisr_comm_init_rank) and nnvisr_halo_exchange, one NCCL group per
+    step enqueued on the caller's stream.  torch.distributed only carries the
+    communicator id from rank 0 (collective constructor)."""
+
+    def __init__(self, s: Shard, group=None):
+        self.s = s
+        uid = [nv.comm_unique_id() if s.rank == 0 else None]
+        if s.world > 1:
+            dist.broadcast_object_list(uid, src=0, group=group)
+        self.comm = nv.Comm.init_rank(uid[0], s.world, s.rank)
+
+    def exchange(self, window: torch.Tensor | None, cut_window: torch.Tensor | None, stream=None) -> None:
+        """Fill the halo rows of window [window_count, frame_bytes] (uint8,
+        device) and cut_window [window_count] on `stream` (None = frames or
+        flags not exchanged)."""
+        s = self.s
+        fb = int(window.shape[1]) if window is not None else 0
+        self.comm.halo_exchange(s.total, s.L, s.R, window.data_ptr() if window is not None else None, fb,
+                                cut_window.data_ptr() if cut_window is not None else None, stream)
+
+    def close(self):
+        if self.comm is not None:
+            self.comm.destroy()
+            self.comm = None
 
 
 def cut_window_of(cut: np.ndarray, s: Shard) -> np.ndarray:
@@ -116,7 +141,6 @@ class PeerHalo:
     written before it are visible to the neighbours' first reads."""
 
     def __init__(self, s: Shard, window: torch.Tensor, group=None):
-        from . import nnvisr as nv
         self._nv = nv
         self.s = s
         self.window = window

@@ -1,0 +1,98 @@
+"""Store mode S as a bounded ring of regions (§3.3
+P:373-382, the region advance "6 to 5" at batch 1; paper_2308_03121_b200/store.py).
+
+Every window of the ring -- across several region advances and scene cuts --
+is compared with the CPU ORACLE's tensor for that tuple (fp16 within 1 ULP,
+fp32 within 1e-6; north_star), and bit-identical to the materialised tuple
+of nnvisr_frames_to_tensor_batch; both advances (paper's N-1-slot copy and
+re-conversion) give identical bytes."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2308_03121_b200 import nnvisr as nv
+from paper_2308_03121_b200 import synth
+from paper_2308_03121_b200.frames import FrameBuffer, FrameLayout
+from paper_2308_03121_b200.store import StoreRing
+
+from .helpers import assert_tensor_close, oracle_f2t
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _clip(lay, F, seed):
+    buf = FrameBuffer(lay, F, device=DEV)
+    host = [synth.random_planes(lay, seed + i, 64 if lay.bits == 10 else 16, 940 if lay.bits == 10 else 235)
+            for i in range(F)]
+    for i, p in enumerate(host):
+        buf.set_planes(i, p)
+    return buf, host
+
+
+@pytest.mark.parametrize("dtype", [nv.F16, nv.F32])
+@pytest.mark.parametrize("N,K,R", [(5, 4, 2), (4, 3, 3), (3, 1, 2)])
+def test_ring_windows_equal_oracle_and_materialised(dtype, N, K, R):
+    W, H, F = 96, 62, 23
+    lay = FrameLayout(W, H, nv.YUV420, 10)
+    cfg = nv.Config(W, H, nv.YUV420, 10, nv.BT709, nv.LIMITED, input_count=N, output_count=1, n=1,
+                    left_context=-1, flags=0, align=16, dtype=dtype)
+    buf, host = _clip(lay, F, 4100 + N)
+    cut = np.zeros(F, np.uint8)
+    cut[[9, 10, 17]] = 1  # a one-frame scene and a cut inside a region
+    with nv.open(cfg) as h:
+        h.bind_frames(buf.descriptors())
+        runs, _ = h.plan(cut)
+        per = int(np.prod(h.in_shape))
+        tdt = torch.float16 if dtype == nv.F16 else torch.float32
+        mat = torch.empty((len(runs), per), dtype=tdt, device=DEV)
+        h.frames_to_tensor_batch(runs, mat.data_ptr(), per * mat.element_size())
+        rings = {adv: StoreRing(h, 0, F, K, R, advance=adv) for adv in ("copy", "convert")}
+        ring = rings["copy"]
+        assert ring.regions >= 4  # >= 3 advances
+        served = []
+        for c in range(ring.regions):
+            for adv, rg in rings.items():
+                info = rg.fill(c)
+                if adv == "copy" and c > 0:
+                    assert info["copied_slots"] == N - 1
+            torch.cuda.synchronize()
+            for r in ring.windows(runs, c):
+                served.append(r)
+                a = int(runs[r][0])
+                win = {}
+                for adv, rg in rings.items():
+                    t = torch.empty(per, dtype=tdt, device=DEV)
+                    nbytes = per * t.element_size()
+                    # copy the window out of the ring (device to device)
+                    view = rg.buf.view(-1)[(rg.window_ptr(a) - rg.buf.data_ptr()) // t.element_size():][:per]
+                    t.copy_(view)
+                    win[adv] = t
+                    assert nbytes == N * rg.slot_bytes
+                assert torch.equal(win["copy"], win["convert"]), (c, r)
+                assert torch.equal(win["copy"], mat[r]), (c, r)
+                ref = oracle_f2t(lay, [host[int(i)] for i in runs[r]], h.in_shape[2], h.in_shape[3], cfg)
+                assert_tensor_close(win["copy"].view(h.in_shape).cpu().numpy(), ref, f"ring window {r}")
+        # every tuple with consecutive inputs is served by exactly one region
+        consecutive = [r for r in range(len(runs)) if np.all(np.diff(runs[r]) == 1)]
+        assert sorted(served) == consecutive
+
+
+def test_ring_rejects_non_resident_and_bad_args():
+    cfg = nv.Config(64, 32, nv.YUV420, 8, nv.BT709, nv.LIMITED, input_count=3, output_count=1, n=1,
+                    left_context=-1, flags=0, align=16, dtype=nv.F16)
+    lay = FrameLayout(64, 32, nv.YUV420, 8)
+    buf, _ = _clip(lay, 12, 7)
+    with nv.open(cfg) as h:
+        h.bind_frames(buf.descriptors())
+        with pytest.raises(ValueError):
+            StoreRing(h, 0, 12, 2, R=1, advance="copy")
+        ring = StoreRing(h, 0, 12, 2, R=2)
+        for c in range(3):
+            ring.fill(c)
+        with pytest.raises(RuntimeError):
+            ring.window_ptr(0)  # region 0 was overwritten by region 2
+        ring.window_ptr(4)
+        with pytest.raises(nv.NnvisrError):
+            h.copy_slots(ring.buf.data_ptr(), 0, 1, 2)  # overlapping ranges
+        torch.cuda.synchronize()
