@@ -1,16 +1,23 @@
 #!/usr/bin/env python3
 """Benchmark of the NNVISR frame<->tensor hot path on B200.
 
-One step = one pass of the whole hot path over the workload's clip (shard):
-halo exchange (N > 1), tuple plan (A1-A2), frames->tensor for every tuple
+One step = one pass of the whole hot path over the workload's clip: halo
+exchange (N > 1 GPUs), tuple plan (A1-A2), frames->tensor for every tuple
 (A3-A7) and tensor->frames for every tuple's network output (B1-B4).  The
 network itself is not part of the build (north_star); t2f reads a ring of
 seeded network-output tensors.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5]
   python bench.py --impl reference ...      # the CPU oracle, timed (reference arm)
 
-Prints ONE JSON line on rank 0 (see DESIGN.md §7 for every key).
+Default workload: c5 (BASELINE.json configs[4], the 4K clip of the 1/2/4/8-GPU
+sweep), STRONG scaling: the 4096-frame clip is split into contiguous frame
+shards over the N ranks, so T(1)/T(N) is north_star's scaling figure.  The
+1080p workload c2 (configs[1]) is measured in the same run, same N, and
+reported under "per_config".  `--gpus N` without torchrun re-launches itself
+under torch.distributed.run with N ranks.
+
+Prints ONE JSON line on rank 0 (DESIGN.md §7 lists every key).
 """
 from __future__ import annotations
 
@@ -18,6 +25,7 @@ import argparse
 import dataclasses
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -31,31 +39,44 @@ sys.path.insert(0, ROOT)
 METRIC = "frames/s per direction at 1080p/4K, 1/2/4/8 B200; HBM GB/s vs peak"
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--per-config", default="auto",
+                   help="comma list of further workloads measured in the same run and reported under "
+                        "per_config ('auto' = c2 when the workload is c5, '' = none)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--chunk", type=int, default=0, help="tuples per launch (0 = auto)")
     p.add_argument("--f2t-mode", default="materialize", choices=["materialize", "store", "batch"],
-                   help="materialize every tuple; store: frame-major store (sliding windows); batch: the paper's "
-                        "Fig. 1 batched shared store (paper grouping, --batch lanes)")
+                   help="materialize every tuple; store: frame-major store ring (sliding windows); batch: the "
+                        "paper's Fig. 1 batched shared store (paper grouping, --batch lanes)")
+    p.add_argument("--store-k", type=int, default=0, help="store ring: new frames per region (0 = auto)")
+    p.add_argument("--store-regions", type=int, default=2, help="store ring: regions")
+    p.add_argument("--store-advance", default="copy", choices=["copy", "convert"],
+                   help="store ring advance: copy the last N-1 slots (the paper's 6 -> 5) or re-convert them")
     p.add_argument("--batch", type=int, default=8, help="lanes per batch for --f2t-mode batch")
     p.add_argument("--emit", action="store_true",
                    help="t2f converts only the outputs the emission schedule presents (NEXT-1; drops e.g. the "
                         "trailing enhanced lookahead of M = 2n+1 networks), pass-through frames are copied")
-    p.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"])
+    p.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                   help="strong (default): the workload's clip split over the ranks; weak: every rank a full "
+                        "clip of its own (global clip N x frames)")
     p.add_argument("--tensors", default="rgb", choices=["rgb", "yuv"],
                    help="network tensor format: RGB (default) or YUV-native luma + chroma tensors (NEXT-3)")
     p.add_argument("--chroma-loc", default="center", choices=["center", "left"],
                    help="4:2:0 chroma siting: centre (default) or LEFT / MPEG-2 (NEXT-3)")
     p.add_argument("--frames", type=int, default=0,
-                   help="clip frames per rank (0 = the workload's; profiling/sweeps only, recorded in config)")
-    p.add_argument("--halo", default="p2p", choices=["p2p", "peer"],
-                   help="N > 1: copy the halo frames each step (NCCL P2P) or read them in place from the "
-                        "neighbours' buffers (nnvisr_peer_import; only the flags travel)")
+                   help="clip frames (0 = the workload's; profiling/sweeps only, recorded in config)")
+    p.add_argument("--halo", default="nccl", choices=["nccl", "peer", "torch"],
+                   help="N > 1: the library's NCCL exchange (nnvisr_halo_exchange, default), peer-mapped frames "
+                        "read in place (nnvisr_peer_import; only the flags travel, over NCCL), or "
+                        "torch.distributed point-to-point calls (comparison baseline)")
+    p.add_argument("--no-overlap", action="store_true",
+                   help="N > 1: run the halo exchange before all tuples instead of overlapping it with the "
+                        "interior tuples")
     p.add_argument("--graph", action="store_true",
                    help="replay the step's launches as one CUDA graph (captured once; re-captured when the "
                         "plan changes); for launch-bound small clips (c1)")
@@ -65,7 +86,28 @@ def parse():
     p.add_argument("--detect-threshold", type=float, default=0.15)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="tuples in the oracle sample (0 = auto)")
-    return p.parse_args()
+    return p.parse_args(argv)
+
+
+# ------------------------------------------------------------- launching
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def torchrun_argv(argv: list[str], gpus: int, port: int) -> list[str]:
+    """The command that re-runs this bench with `gpus` ranks (one per GPU)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def check_world(world: int, gpus: int):
+    if world != gpus:
+        raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}; launch with matching --nproc-per-node "
+                         f"or without torchrun (bench.py --gpus N starts N ranks itself)")
 
 
 def load_peaks():
@@ -77,15 +119,17 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def load_traffic(kernel: str, workload: str):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    capture (profiles/traffic.json), or None."""
+def load_traffic(kernel: str, workload: str, mode: str):
+    """The dominant kernel's ncu DRAM bytes from profiles/traffic.json:
+    {"ncu_bytes", "algorithmic_bytes", "units", "source"} of one captured
+    launch, or None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
         d = json.load(f)
-    return d.get(workload, {}).get(kernel)
+    e = d.get(f"{workload}_{mode}" if mode != "materialize" else workload, {}).get(kernel)
+    return e if isinstance(e, dict) else None
 
 
 class ClockSampler:
@@ -142,6 +186,17 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ oracle
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample(w, count: int, threads: int):
     """Time the CPU oracle (as it stands) on `count` tuples of workload w:
     each unit = the tuple's frames->tensor plus its output tensor->frames.
@@ -187,6 +242,21 @@ def default_cpu_sample(w, cores=None):
     return int(max(2, min(256, round(4 * cores * (1920 * 1080) / px))))
 
 
+def cpu_baseline(w, name: str, sample: int | None):
+    """The oracle on the host cores (all threads, plus one thread on a
+    smaller sample): BASELINE.md's CPU baseline plan."""
+    cores = os.cpu_count() or 1
+    sample = sample or default_cpu_sample(w)
+    v, secs, used = oracle_sample(w, sample, cores)
+    one = max(1, min(sample, 2))
+    v1, secs1, _ = oracle_sample(w, one, 1)
+    return {"value": v, "unit": "frames/s", "cores": used, "kind": "oracle", "cpu_model": cpu_model(),
+            "host_threads": cores,
+            "sample": f"{sample} tuples of {name} (frames->tensor + tensor->frames each) in {secs:.1f} s on "
+                      f"{used} host threads",
+            "single_thread": {"value": v1, "unit": "frames/s", "sample": f"{one} tuples in {secs1:.1f} s"}}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on the box's host cores, per step a
     bounded sample of the workload (rank 0 only under torchrun)."""
@@ -200,6 +270,7 @@ def run_reference(args):
     for _ in range(args.warmup):
         oracle_sample(w, max(1, sample // 4), cores)
     times = []
+    used = cores
     for _ in range(args.steps):
         _, s, used = oracle_sample(w, sample, cores)
         times.append(s)
@@ -208,9 +279,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "description": w.description, "sample_tuples": sample},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": used, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"{sample} tuples of {args.workload} (frames->tensor + tensor->frames each), "
                                    f"{used} host threads"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -219,31 +291,66 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- GPU
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
-    import torch
-    import torch.distributed as dist
+class Ctx:
+    """Process-wide state shared by the workloads of one run."""
 
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.args = args
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        self.comm = None
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+            if args.halo in ("nccl", "peer"):
+                from paper_2308_03121_b200 import nnvisr as nv
+                uid = [nv.comm_unique_id() if self.rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
+                self.comm = nv.Comm.init_rank(uid[0], self.world, self.rank)
+
+    def barrier(self):
+        self.torch.cuda.synchronize(self.dev)
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def max_over_ranks(self, v: float) -> float:
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def min_over_ranks(self, v: float) -> float:
+        return -self.max_over_ranks(-v)
+
+    def close(self):
+        if self.comm is not None:
+            self.comm.destroy()
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def measure(ctx: Ctx, wname: str, primary: bool):
+    """One workload: warm-up, K timed steps, per-kernel statistics, e2e,
+    halo check.  Returns the workload's block of the JSON line (rank 0)."""
+    args, torch = ctx.args, ctx.torch
     from paper_2308_03121_b200 import nnvisr as nv
     from paper_2308_03121_b200 import shard as sh
     from paper_2308_03121_b200 import synth
     from paper_2308_03121_b200.frames import FrameBuffer
+    from paper_2308_03121_b200.store import StoreRing
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    w = synth.WORKLOADS[args.workload]
+    world, rank, dev = ctx.world, ctx.rank, ctx.dev
+    w = synth.WORKLOADS[wname]
     cfg = w.cfg
-    scaling = args.scaling if args.scaling != "auto" else ("strong" if args.workload == "c5" else "weak")
-    total = (args.frames or w.frames) * (world if scaling == "weak" else 1)
+    scaling = args.scaling
+    frames_arg = args.frames if primary else 0
+    total = (frames_arg or w.frames) * (world if scaling == "weak" else 1)
     yuv = args.tensors == "yuv"
     if yuv:
         cfg = dataclasses.replace(cfg, flags=cfg.flags | nv.YUV_INPUT | nv.YUV_OUTPUT)
@@ -251,10 +358,11 @@ def main():
         cfg = dataclasses.replace(cfg, chroma_loc=nv.CHROMA_LEFT)
     h = nv.open(cfg)
     N, M = h.N, h.M
-    L = 0 if cfg.flags else ((N - 1) // 2 if cfg.left_context == -1 else cfg.left_context)
+    L = 0 if cfg.flags & 7 else ((N - 1) // 2 if cfg.left_context == -1 else cfg.left_context)
     R = N - 1 - L
     s = sh.shard_of(total, world, rank, L, R)
     cut_all = synth.cut_flags(w, total)  # each rank only uses its own flags + what the halo brings
+    mode = args.f2t_mode if primary else "materialize"
 
     # window buffer: [left halo | owned frames | right halo]
     lay = w.layout()
@@ -262,6 +370,7 @@ def main():
     synth.generate_clip(w, device=dev, frames=s.owned, first=s.begin, total_frames=total, out=win, out_offset=s.left)
     cut_win = torch.zeros(s.window_count, dtype=torch.uint8, device=dev)
     cut_win[s.left:s.left + s.owned] = torch.from_numpy(cut_all[s.begin:s.end]).to(dev)
+    own_flags = cut_all[s.begin:s.end].copy()  # host flags this rank knows itself
     peer = None
     if world > 1 and args.halo == "peer":
         peer = sh.PeerHalo(s, win.data)
@@ -277,7 +386,6 @@ def main():
     in_elems = int(np.prod(in_shape))
     out_elems = int(np.prod(out_shape))
     # YUV-native tensors: luma [1, N, Hp, Wp] + chroma [1, 2N, Hc, Wc] per tuple
-    # (in_shape / out_shape are the luma tensors), separate buffers
     in_c = int(np.prod(h.in_chroma_shape)) if yuv else 0
     out_c = int(np.prod(h.out_chroma_shape)) if yuv else 0
     in_l, out_l = in_elems, out_elems
@@ -295,17 +403,21 @@ def main():
     tens_in = torch.empty((fchunk, in_elems), dtype=tdt, device=dev)
     tens_out = synth.random_tensor((n_out, out_elems), cfg.dtype, w.seed + 99, device=dev)
     if yuv:
-        if args.f2t_mode != "materialize":
+        if mode != "materialize":
             raise SystemExit("--tensors yuv supports --f2t-mode materialize only")
-        tin_l, tin_c = torch.empty((fchunk, in_l), dtype=tdt, device=dev), torch.empty((fchunk, in_c), dtype=tdt, device=dev)
+        tin_l, tin_c = torch.empty((fchunk, in_l), dtype=tdt, device=dev), torch.empty((fchunk, in_c), dtype=tdt,
+                                                                                          device=dev)
         tout_l = synth.random_tensor((n_out, out_l), cfg.dtype, w.seed + 99, device=dev)
         tout_c = synth.random_tensor((n_out, out_c), cfg.dtype, w.seed + 98, device=dev)
     ofb = FrameBuffer(olay, tchunk * M, device=dev)
     ofb_desc = ofb.descriptors()
-    store = None
-    if args.f2t_mode == "store":
-        store = torch.empty((s.window_count, slot_bytes // esz), dtype=tdt, device=dev)
-    if args.f2t_mode == "batch":
+    ring = None
+    if mode == "store":
+        # store mode S as a bounded ring: R regions of K + N - 1
+        # slots, ~3 GB of conversion traffic per region fill
+        K = args.store_k or max(1, min(256, int(3e9 // (frame_payload + slot_bytes))))
+        ring = StoreRing(h, s.window_first, s.window_count, K, args.store_regions, args.store_advance, device=dev)
+    if mode == "batch":
         # Fig. 1 batches (§3.3): each batch's slots (b*n+1 shared, or
         # b*N plain) in its own region of a chunk store; a launch converts the
         # slots of ~fchunk runs' batches, every distinct frame once
@@ -313,41 +425,155 @@ def main():
         per_launch = max(1, fchunk // args.batch)
         store = torch.empty((per_launch * bmax, slot_bytes // esz), dtype=tdt, device=dev)
     stream = torch.cuda.Stream(device=dev)
+    hstream = torch.cuda.Stream(device=dev)
 
-    # the flags the planner reads: on one GPU without --detect they are host
-    # data (no device round trip per step); otherwise they come from the
-    # device (halo exchange / GPU scene detection) each step
     host_flags = world == 1 and not args.detect
     cut_host = cut_all[s.window_first:s.window_first + s.window_count].copy()
+    overlap = (world > 1 and not args.no_overlap and not args.detect and not args.graph and not args.emit and
+               mode == "materialize")
 
-    def flags_now():
-        return cut_host if host_flags else cut_win.cpu().numpy()
+    def flags_now(st=None):
+        """The window's flags as the planner sees them: host data on one GPU
+        without --detect, else the device flags (halo / detection), read on
+        the stream that produced them."""
+        if host_flags:
+            return cut_host
+        with torch.cuda.stream(st or stream):
+            return cut_win.cpu().numpy()
 
-    def plan_local():
-        return h.plan_range(total, s.window_first, flags_now(), s.begin, s.end)
+    def plan_local(flags=None):
+        return h.plan_range(total, s.window_first, flags_now() if flags is None else flags, s.begin, s.end)
 
     # per launch: (start event, end event, units, algorithmic bytes)
-    ev_pairs = {"f2t": [], "t2f": [], "detect": []}
+    ev_pairs = {"f2t": [], "t2f": [], "detect": [], "halo": [], "advance": []}
     if args.detect:
         sad_d = torch.zeros(s.window_count, dtype=torch.int64, device=dev)
         cut_d = torch.zeros(s.window_count, dtype=torch.uint8, device=dev)
-        luma_bytes = lay.plane_dims()[0][0] * lay.plane_dims()[0][1] * lay.sample_bytes * (3 if cfg.family == nv.RGB else 1)
+        luma_bytes = (lay.plane_dims()[0][0] * lay.plane_dims()[0][1] * lay.sample_bytes *
+                      (3 if cfg.family == nv.RGB else 1))
+    halo_rows = sum(c for _, snd, _, c in nv.halo_plan(total, world, rank, L, R)) if world > 1 else 0
+    halo_bytes = halo_rows * ((0 if peer else frame_payload) + 1)
 
-    def timed(kind, record, units, nbytes, fn):
+    def timed(kind, record, units, nbytes, fn, st=None):
+        st = st or stream
         if not record:
             fn()
             return
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        a.record(st)
         fn()
-        b.record(stream)
+        b.record(st)
         ev_pairs[kind].append((a, b, units, nbytes))
 
-    def step(record: bool, planned=None):
-        if world > 1:
-            with torch.cuda.stream(stream):
+    def exchange(st):
+        if ctx.comm is not None:
+            # the library's NCCL group: frames (unless read in place) + flags
+            ctx.comm.halo_exchange(total, L, R, None if peer else win.data.data_ptr(), win.frame_bytes,
+                                   cut_win.data_ptr(), st)
+        else:
+            with torch.cuda.stream(st):
                 sh.halo_exchange(s, None if peer else win.data, cut_win)
+
+    def f2t_runs(runs, record):
+        for c0 in range(0, len(runs), fchunk):
+            sel = runs[c0:c0 + fchunk]
+            nbytes = len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz
+            if yuv:
+                timed("f2t", record, len(sel), nbytes,
+                      lambda sel=sel: h.frames_to_tensor_yuv_batch(sel, tin_l.data_ptr(), in_l * esz,
+                                                                   tin_c.data_ptr(), in_c * esz, stream))
+            else:
+                timed("f2t", record, len(sel), nbytes,
+                      lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
+
+    def f2t_store(runs, record):
+        # each window frame converted once into the ring's current region;
+        # tuples with consecutive indices are windows of it, the ones with
+        # duplicated indices (scene edges) are materialised
+        cons = np.all(np.diff(runs, axis=1) == 1, axis=1) if N > 1 else np.ones(len(runs), bool)
+        served_per_region = np.bincount((runs[cons, 0] - ring.first) // ring.K, minlength=ring.regions)
+        for c in range(ring.regions):
+            g0, g1 = ring.region_frames(c)
+            carry = min(N - 1, g1 - g0) if (ring.advance == "copy" and c > 0) else 0
+            if carry:
+                timed("advance", record, 0, 2 * carry * slot_bytes,
+                      lambda c=c, carry=carry: h.copy_slots(ring.buf.data_ptr(), ((c - 1) % ring.R) * ring.span +
+                                                            ring.K, (c % ring.R) * ring.span, carry, stream))
+            nconv = g1 - g0 - carry
+            timed("f2t", record, int(served_per_region[c]), nconv * (frame_payload + slot_bytes),
+                  lambda g0=g0, carry=carry, nconv=nconv, c=c: h.frames_to_store(
+                      g0 + carry, nconv, ring.slot_ptr(c, carry), stream))
+            ring._filled = c
+        dup = np.flatnonzero(~cons)
+        for c0 in range(0, len(dup), fchunk):
+            sel = runs[dup[c0:c0 + fchunk]]
+            timed("f2t", record, len(sel), len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz,
+                  lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
+
+    def f2t_batch(record):
+        batches = h.plan_batches(flags_now(), args.batch)
+        for c0 in range(0, len(batches), per_launch):
+            grp = batches[c0:c0 + per_launch]
+            sf = np.full(len(grp) * bmax, -1, np.int64)
+            for i, x in enumerate(grp):
+                sf[i * bmax:i * bmax + len(x["slots"])] = x["slots"]
+            nslots = int((sf >= 0).sum())
+            nruns = sum(sum(x["emit"]) for x in grp)
+            nbytes = len(np.unique(sf[sf >= 0])) * frame_payload + nslots * slot_bytes
+            timed("f2t", record, nruns, nbytes, lambda sf=sf: h.frames_to_slots(sf, store.data_ptr(), stream))
+
+    def t2f_all(runs, record, flags):
+        sched = h.schedule_outputs(flags)[s.begin - s.window_first:] if args.emit else None
+        for c0 in range(0, len(runs), tchunk):
+            nb = min(tchunk, len(runs) - c0)
+            o0 = (c0 // tchunk * tchunk) % n_out
+            if o0 + nb > n_out:
+                o0 = 0
+            desc, nconv, copies = ofb_desc[:nb * M], nb * M, []
+            if args.emit:
+                # presented outputs only; pass-through frames copied
+                desc, nconv = [nv.Frame() for _ in range(nb * M)], 0
+                for j in range(nb):
+                    for src, pres in sched[c0 + j]:
+                        if src >= 0:
+                            desc[j * M + src] = ofb_desc[j * M + src]
+                            nconv += 1
+                        else:
+                            copies.append((int(runs[c0 + j][-src - 1]), ofb_desc[j * M]))
+            nbytes = nconv * (out_elems // M * esz + olay.payload_bytes())
+            if yuv:
+                timed("t2f", record, nb, nbytes,
+                      lambda o0=o0, nb=nb, desc=desc: h.tensor_to_frames_yuv_batch(
+                          tout_l[o0].data_ptr(), out_l * esz, tout_c[o0].data_ptr(), out_c * esz, Ho, Wo, desc,
+                          nb, stream))
+            else:
+                timed("t2f", record, nb, nbytes,
+                      lambda o0=o0, nb=nb, desc=desc: h.tensor_to_frames_batch(
+                          tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo, desc, nb, stream))
+            if copies:
+                h.copy_frames([c[0] for c in copies], [c[1] for c in copies], stream)
+
+    def step(record: bool, planned=None):
+        if overlap:
+            # halo exchange on a side stream; the interior tuples (whose
+            # windows and flags lie inside the owned frames) and every t2f
+            # start at once; the boundary tuples wait for the halo
+            hstream.wait_stream(stream)
+            timed("halo", record, 0, halo_bytes, lambda: exchange(hstream), st=hstream)
+            i0, i1 = s.begin + s.left, max(s.begin + s.left, s.end - s.right)
+            if i1 > i0:
+                f2t_runs(h.plan_range(total, s.begin, own_flags, i0, i1)[0], record)
+            t2f_all(np.zeros((s.owned, N), np.int64), record, None)
+            flags = flags_now(hstream)  # waits for the exchange (host)
+            edge = [h.plan_range(total, s.window_first, flags, a, b)[0] for a, b in ((s.begin, i0), (i1, s.end))
+                    if b > a]
+            stream.wait_stream(hstream)
+            for e in edge:
+                f2t_runs(e, record)
+            return s.owned
+        if world > 1:
+            timed("halo", record, 0, halo_bytes, lambda: exchange(stream))
         if args.detect:
             # the flags the plan consumes come from the frames themselves
             with torch.cuda.stream(stream):
@@ -355,97 +581,33 @@ def main():
                       lambda: h.scene_detect(s.window_first, s.window_count, args.detect_threshold, sad_d.data_ptr(),
                                              cut_d.data_ptr(), stream))
                 cut_win.copy_(cut_d)
-        runs = plan_local()[0] if planned is None else planned
-        with torch.cuda.stream(stream):
-            if args.f2t_mode == "store":
-                # each window frame converted once into the frame-major store;
-                # tuples with consecutive indices are windows of it, the ones
-                # with duplicated indices (scene edges) are materialised
-                timed("f2t", record, s.owned, s.window_count * (frame_payload + slot_bytes),
-                      lambda: h.frames_to_store(s.window_first, s.window_count, store.data_ptr(), stream))
-                dup = [r for r in range(len(runs)) if np.any(np.diff(runs[r]) != 1)]
-                for c0 in range(0, len(dup), fchunk):
-                    sel = runs[dup[c0:c0 + fchunk]]
-                    timed("f2t", record, 0, len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz,
-                          lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
-            elif args.f2t_mode == "batch":
-                batches = h.plan_batches(flags_now(), args.batch)
-                for c0 in range(0, len(batches), per_launch):
-                    grp = batches[c0:c0 + per_launch]
-                    sf = np.full(len(grp) * bmax, -1, np.int64)
-                    for i, x in enumerate(grp):
-                        sf[i * bmax:i * bmax + len(x["slots"])] = x["slots"]
-                    nslots = int((sf >= 0).sum())
-                    nruns = sum(sum(x["emit"]) for x in grp)
-                    nbytes = len(np.unique(sf[sf >= 0])) * frame_payload + nslots * slot_bytes
-                    timed("f2t", record, nruns, nbytes,
-                          lambda sf=sf: h.frames_to_slots(sf, store.data_ptr(), stream))
-            else:
-                for c0 in range(0, len(runs), fchunk):
-                    sel = runs[c0:c0 + fchunk]
-                    nbytes = len(np.unique(sel)) * frame_payload + len(sel) * in_elems * esz
-                    if yuv:
-                        timed("f2t", record, len(sel), nbytes,
-                              lambda sel=sel: h.frames_to_tensor_yuv_batch(sel, tin_l.data_ptr(), in_l * esz,
-                                                                           tin_c.data_ptr(), in_c * esz, stream))
-                    else:
-                        timed("f2t", record, len(sel), nbytes,
-                              lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz,
-                                                                       stream))
-            sched = h.schedule_outputs(flags_now())[s.begin - s.window_first:] if args.emit else None
-            for c0 in range(0, len(runs), tchunk):
-                nb = min(tchunk, len(runs) - c0)
-                o0 = (c0 // tchunk * tchunk) % n_out
-                if o0 + nb > n_out:
-                    o0 = 0
-                desc, nconv, copies = ofb_desc[:nb * M], nb * M, []
-                if args.emit:
-                    # presented outputs only; pass-through frames copied
-                    desc, nconv = [nv.Frame() for _ in range(nb * M)], 0
-                    for j in range(nb):
-                        for src, pres in sched[c0 + j]:
-                            if src >= 0:
-                                desc[j * M + src] = ofb_desc[j * M + src]
-                                nconv += 1
-                            else:
-                                copies.append((int(runs[c0 + j][-src - 1]), ofb_desc[j * M]))
-                nbytes = nconv * (out_elems // M * esz + olay.payload_bytes())
-                if yuv:
-                    timed("t2f", record, nb, nbytes,
-                          lambda o0=o0, nb=nb, desc=desc: h.tensor_to_frames_yuv_batch(
-                              tout_l[o0].data_ptr(), out_l * esz, tout_c[o0].data_ptr(), out_c * esz, Ho, Wo, desc,
-                              nb, stream))
-                else:
-                    timed("t2f", record, nb, nbytes,
-                          lambda o0=o0, nb=nb, desc=desc: h.tensor_to_frames_batch(
-                              tens_out[o0].data_ptr(), out_elems * esz, Ho, Wo, desc, nb, stream))
-                if copies:
-                    h.copy_frames([c[0] for c in copies], [c[1] for c in copies], stream)
+        flags = flags_now()
+        runs = plan_local(flags)[0] if planned is None else planned
+        if mode == "store":
+            f2t_store(runs, record)
+        elif mode == "batch":
+            f2t_batch(record)
+        else:
+            f2t_runs(runs, record)
+        t2f_all(runs, record, flags)
         return len(runs)
-
-    def barrier():
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
 
     # warm-up
     for _ in range(args.warmup):
         step(False)
-    barrier()
+    ctx.barrier()
 
     # --graph: the step's device work captured once as a CUDA graph (the
     # library records its launches with upload tables of their own); every
     # timed step still plans on the host and replays the graph when the plan
     # is the captured one (else runs eagerly).  Per-kernel times come from one
-    # eager recorded step before the timed region (graph replays are timed as
-    # a whole).
+    # eager recorded step before the timed region.
     graph = None
-    if args.graph:
-        if world > 1 or args.detect or args.emit or yuv or args.f2t_mode != "materialize":
+    if args.graph and primary:
+        if world > 1 or args.detect or args.emit or yuv or mode != "materialize":
             raise SystemExit("--graph supports one GPU, materialised RGB tuples, no --emit / --detect")
         step(True)
-        barrier()
+        ctx.barrier()
         runs_cap = plan_local()[0]
         graph = torch.cuda.CUDAGraph()
         lc0 = nv.launch_count()
@@ -453,7 +615,7 @@ def main():
             step(False, runs_cap)
         graph_launches = nv.launch_count() - lc0
         graph.replay()
-        barrier()
+        ctx.barrier()
 
     def timed_step():
         if graph is None:
@@ -467,27 +629,20 @@ def main():
 
     # ---- timed region: K steps, device time via CUDA events on `stream`
     launches0 = nv.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(ctx.local) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
-        tuples = 0
         for _ in range(args.steps):
-            tuples += timed_step()
+            timed_step()
         t_end.record(stream)
-        barrier()
+        ctx.barrier()
     launches = nv.launch_count() - launches0
     if graph is not None:  # replays do not pass through the library's launch counter
         launches += graph_launches * args.steps
-    ms_total = t_start.elapsed_time(t_end)
-    ms_t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_total = float(ms_t.item())
+    ms_total = ctx.max_over_ranks(t_start.elapsed_time(t_end))
     ms_step = ms_total / args.steps
-    frames_all = s.owned * world if scaling == "weak" else total  # every rank owns a contiguous share
-    if scaling == "strong":
-        frames_all = total
+    frames_all = total  # strong: the whole clip; weak: world x the workload's clip
     value = frames_all * args.steps / (ms_total / 1000.0)
 
     # per-kernel durations and algorithmic bytes
@@ -500,80 +655,98 @@ def main():
         bytes_ = np.array([q for _, _, _, q in ev], dtype=np.float64)
         return {"launches": len(ev), "seconds": float(durs.sum()), "units": float(units.sum()),
                 "bytes": float(bytes_.sum()), "avg_launch_s": float(durs.mean()),
-                "avg_launch_bytes": float(bytes_.mean())}
+                "avg_launch_bytes": float(bytes_.mean()), "avg_launch_units": float(units.mean())}
 
-    ks = {k: kstats(k) for k in ("f2t", "t2f", "detect")}
+    ks = {k: kstats(k) for k in ev_pairs}
     peak, peak_src = load_peaks()
     per_dir = {}
     for k, v in ks.items():
         if v:
             gbs = v["bytes"] / v["seconds"] / 1e9
-            per_dir[k] = {"fps": v["units"] / v["seconds"] * (world if scaling == "weak" else 1),
-                          "achieved_gbs": gbs, "frac_of_measured_peak": gbs / peak, "frac_of_8tbs": gbs / 8000.0,
+            per_dir[k] = {"achieved_gbs": gbs, "frac_of_measured_peak": gbs / peak, "frac_of_8tbs": gbs / 8000.0,
                           "launches_per_step": v["launches"] / args.steps,
-                          "bytes_per_launch": v["avg_launch_bytes"], "avg_launch_ms": 1000 * v["avg_launch_s"]}
-    dom = max((k for k in ks if ks[k]), key=lambda k: ks[k]["seconds"])
+                          "bytes_per_launch": v["avg_launch_bytes"], "avg_launch_ms": 1000 * v["avg_launch_s"],
+                          "ms_per_step": 1000 * v["seconds"] / args.steps}
+            if k in ("f2t", "t2f"):
+                # frames/s of this direction over all ranks (every rank's units / its kernel time)
+                per_dir[k]["fps"] = v["units"] / v["seconds"] * world
+    conv = [k for k in ("f2t", "t2f") if ks[k]]
+    dom = max(conv, key=lambda k: ks[k]["seconds"])
     dv = ks[dom]
     achieved = dv["avg_launch_bytes"] / dv["avg_launch_s"] / 1e9
-    traffic = load_traffic(dom, args.workload)
+    tr = load_traffic(dom, wname, mode)
+    traffic = None
+    if tr:
+        # ncu bytes of the captured launch, scaled per unit to this run's
+        # average launch; ratio against the captured launch's own algorithmic bytes
+        traffic = {"bytes_per_launch": tr["ncu_bytes"] / tr["units"] * dv["avg_launch_units"],
+                   "ncu_over_algorithmic": tr["ncu_bytes"] / tr["algorithmic_bytes"],
+                   "captured_launch": {k: tr[k] for k in ("ncu_bytes", "algorithmic_bytes", "units", "source")}}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": dv["avg_launch_bytes"]}
+                "frac": achieved / peak, "traffic": traffic["bytes_per_launch"] if traffic else None,
+                "traffic_detail": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dv["avg_launch_bytes"],
+                "units_per_launch": dv["avg_launch_units"]}
+
+    # ---- halo check: the received halo frames and flags equal the clip's own
+    halo_check = None
+    if world > 1:
+        ok = 1.0
+        for a, b in ((0, s.left), (s.left + s.owned, s.window_count)):
+            if b > a:
+                ref = synth.generate_clip(w, device=dev, frames=b - a, first=s.window_first + a, total_frames=total)
+                if not peer:
+                    ok = min(ok, float(torch.equal(win.data[a:b], ref.data)))
+                flags = cut_win[a:b].cpu().numpy()
+                ok = min(ok, float(np.array_equal(flags, cut_all[s.window_first + a:s.window_first + b])))
+        ok = ctx.min_over_ranks(ok)
+        halo_check = {"ok": ok == 1.0, "what": ("halo flags (frames read in place)" if peer else
+                                                "halo frames (regenerated from the seed) and flags, every rank")}
 
     # ---- e2e: host (pinned) frames in, host frames out, through the C ABI
     e2e = None
-    if not args.no_e2e and not yuv:
-        e2e = run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, min(8, fchunk, tchunk), in_elems,
-                      out_elems, esz, stream, dev, world, plan_local, scaling, frames_all)
+    if not args.no_e2e and not yuv and mode == "materialize":
+        e2e = run_e2e(ctx, h, s, win, tens_out, n_out, ofb, min(8, fchunk, tchunk), in_elems, out_elems, esz,
+                      stream, plan_local, frames_all, tens_in)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sample = args.cpu_sample or default_cpu_sample(w)
-        v, secs, used = oracle_sample(w, sample, os.cpu_count() or 1)
-        cpu = {"value": v, "unit": "frames/s", "cores": used, "kind": "oracle",
-               "sample": f"{sample} tuples of {args.workload} (frames->tensor + tensor->frames each) in "
-                         f"{secs:.1f} s on {used} host threads"}
+        cpu = cpu_baseline(w, wname, args.cpu_sample if primary else 0)
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": "f64" if cfg.bits == 16 else "f32", "data": "synthetic",
-            "config": {"workload": args.workload, "description": w.description, "frames_per_step": frames_all,
-                       "clip_frames_per_rank": s.owned, "input_tensor": list(in_shape),
-                       "output_tensor": list(out_shape), "tensor_dtype": "f16" if cfg.dtype == nv.F16 else "f32",
-                       "tuples_per_launch": {"f2t": fchunk, "t2f": tchunk}, "f2t_mode": args.f2t_mode,
-                       "tensors": ("YUV-native: luma %s + chroma %s per tuple" % (list(in_shape), list(h.in_chroma_shape))
-                                   if yuv else "RGB"),
-                       "chroma_loc": args.chroma_loc,
-                       "t2f_outputs": "emitted only (NEXT-1 schedule)" if args.emit else "all M slots per tuple",
-                       "scene_flags": ("detected on the GPU each step (threshold %g)" % args.detect_threshold
-                                       if args.detect else "given (synthetic cut pattern)"),
-                       "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB, t2f input ring "
-                                    f"{n_out} x {out_elems * esz / 1e6:.0f} MB >= 4 x L2 ({l2 / 1e6:.0f} MB)",
-                       "parallelism": f"frame-range shards x{world}, halo " + ("peer-mapped" if peer else "P2P"),
-                       "launch": ("CUDA graph replay per step (host plan each step; kernel times from an eager step)"
-                                  if graph is not None else "eager launches")},
-            "unit_definition": "1 frame = one tuple through frames->tensor plus its network output through "
-                               "tensor->frames (n = 1: one tuple per clip frame)",
-            "per_direction": per_dir,
-            "roofline": roofline,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "seed": w.seed,
-        }
-        print(json.dumps(line), flush=True)
+    block = {
+        "value": value, "ms_per_step": ms_step, "frames_per_step": frames_all,
+        "config": {"workload": wname, "description": w.description, "frames_per_step": frames_all,
+                   "clip_frames_per_rank": s.owned, "input_tensor": list(in_shape), "output_tensor": list(out_shape),
+                   "tensor_dtype": "f16" if cfg.dtype == nv.F16 else "f32",
+                   "tuples_per_launch": {"f2t": fchunk, "t2f": tchunk}, "f2t_mode": mode,
+                   "store_ring": ({"new_frames_per_region": ring.K, "regions": ring.R, "slots_per_region": ring.span,
+                                   "advance": ring.advance, "ring_gb": ring.buf.numel() * esz / 1e9}
+                                  if ring else None),
+                   "tensors": ("YUV-native: luma %s + chroma %s per tuple" % (list(in_shape), list(h.in_chroma_shape))
+                               if yuv else "RGB"),
+                   "chroma_loc": args.chroma_loc,
+                   "t2f_outputs": "emitted only (NEXT-1 schedule)" if args.emit else "all M slots per tuple",
+                   "scene_flags": ("detected on the GPU each step (threshold %g)" % args.detect_threshold
+                                   if args.detect else "given (synthetic cut pattern)"),
+                   "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB per rank, t2f input "
+                                f"ring {n_out} x {out_elems * esz / 1e6:.0f} MB >= 4 x L2 ({l2 / 1e6:.0f} MB)",
+                   "parallelism": (f"{scaling} scaling, contiguous frame shards x{world}" +
+                                   (f", halo {args.halo}" + (" overlapped with interior tuples" if overlap else "")
+                                    if world > 1 else "")),
+                   "launch": ("CUDA graph replay per step (host plan each step; kernel times from an eager step)"
+                              if graph is not None else "eager launches")},
+        "per_direction": per_dir, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clk.summary(), "seed": w.seed, "halo_check": halo_check,
+        "dtype": "f64" if cfg.bits == 16 else "f32",
+    }
     if peer:
         peer.close()
     h.close()
-    if world > 1:
-        dist.destroy_process_group()
+    return block
 
 
-def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, in_elems, out_elems, esz, stream,
-            dev, world, plan_local, scaling, frames_all):
+def run_e2e(ctx, h, s, win, tens_out, n_out, ofb, chunk, in_elems, out_elems, esz, stream, plan_local, frames_all,
+            tens_in):
     """Same metric with the frames in pinned HOST memory, through the C ABI's
     host-buffer calls: nnvisr_frames_to_tensor_batch_host uploads each
     chunk's frames (library staging + copy stream) and converts them,
@@ -581,9 +754,7 @@ def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, i
     downloads every output frame to pinned host memory; uploads, kernels and
     downloads of consecutive chunks overlap.  Timed with CUDA events on the
     working stream after nnvisr_host_fence (the downloads are complete)."""
-    import torch
-    import torch.distributed as dist
-
+    torch = ctx.torch
     from paper_2308_03121_b200.frames import FrameBuffer
 
     # pinned host copy of the shard's frames, capped at 256 frames (a 4K clip
@@ -596,7 +767,8 @@ def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, i
     Ho, Wo = h.out_shape[2], h.out_shape[3]
     host_out = [FrameBuffer(ofb.layout, chunk * M, device="cpu", pin=True) for _ in range(2)]
     host_out_desc = [b.descriptors() for b in host_out]
-    runs, _ = plan_local()
+    with torch.cuda.stream(stream):
+        runs, _ = plan_local()
     frame_payload = win.layout.payload_bytes()
     out_payload = ofb.layout.payload_bytes()
 
@@ -618,23 +790,20 @@ def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, i
         h.host_fence(stream)
         return h2d, d2h
 
-    for _ in range(2):
+    # big clips (c5: 4096 8K output frames = 407 GB of downloads per step) get fewer e2e steps
+    big = len(runs) * M * out_payload > 50e9
+    for _ in range(1 if big else 2):
         e2e_step()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    steps = max(1, min(args.steps, 5))
+    ctx.barrier()
+    steps = max(1, min(ctx.args.steps, 2 if big else 5))
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(steps):
         h2d, d2h = e2e_step()
     t1.record(stream)
-    torch.cuda.synchronize(dev)
-    ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    torch.cuda.synchronize(ctx.dev)
+    ms = ctx.max_over_ranks(t0.elapsed_time(t1))
     return {"value": frames_all * steps / (ms / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": ms / steps, "steps": steps,
             "path": "pinned host frames -> nnvisr_frames_to_tensor_batch_host -> network-output tensors -> "
@@ -642,5 +811,44 @@ def run_e2e(args, h, s, w, win, cut_win, tens_in, tens_out, n_out, ofb, chunk, i
                     "uploads/kernels/downloads of consecutive chunks overlapped)"}
 
 
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.impl == "reference":
+        run_reference(args)
+        return 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-run this command under torch.distributed.run
+        return subprocess.call(torchrun_argv(argv, args.gpus, free_port()))
+    check_world(int(os.environ.get("WORLD_SIZE", "1")), args.gpus)
+    ctx = Ctx(args)
+    extra = ([] if args.per_config == "" else
+             (["c2"] if args.workload == "c5" else []) if args.per_config == "auto" else
+             [x for x in args.per_config.split(",") if x and x != args.workload])
+    prim = measure(ctx, args.workload, primary=True)
+    per_config = {}
+    for wl in extra:
+        import gc
+        gc.collect()
+        ctx.torch.cuda.empty_cache()  # the previous workload's clip and rings
+        per_config[wl] = measure(ctx, wl, primary=False)
+    if ctx.rank == 0:
+        line = {
+            "metric": METRIC, "value": prim["value"], "unit": "frames/s", "n_gpus": ctx.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": prim["ms_per_step"], "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": prim["dtype"], "data": "synthetic",
+            "config": prim["config"],
+            "unit_definition": "1 frame = one tuple through frames->tensor plus its network output through "
+                               "tensor->frames (n = 1: one tuple per clip frame)",
+            "per_direction": prim["per_direction"], "roofline": prim["roofline"],
+            "cpu_baseline": prim["cpu_baseline"], "e2e": prim["e2e"], "gpu_launches": prim["gpu_launches"],
+            "clocks": prim["clocks"], "seed": prim["seed"], "halo_check": prim["halo_check"],
+            "per_config": per_config,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
 if __name__ == "__main__":
-    main()
+    sys.exit(main())
