@@ -3,7 +3,7 @@ NVCC    ?= nvcc
 ARCH    ?= -gencode arch=compute_100a,code=sm_100a
 NVFLAGS ?= -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC,-Wall -Iinclude -Xptxas -v $(EXTRA)
 PKG      = paper_2308_03121_b200
-SRC      = $(PKG)/csrc/nnvisr.cpp $(PKG)/csrc/comm.cpp $(PKG)/csrc/kernels.cu $(PKG)/csrc/kernels_tma.cu $(PKG)/csrc/kernels_yuv.cu $(PKG)/csrc/scene.cu
+SRC      = $(PKG)/csrc/nnvisr.cpp $(PKG)/csrc/comm.cpp $(PKG)/csrc/kernels.cu $(PKG)/csrc/kernels_tma.cu $(PKG)/csrc/kernels_yuv.cu $(PKG)/csrc/scene.cu $(PKG)/csrc/kernels_strip.cu
 HDR      = include/nnvisr.h $(PKG)/csrc/internal.h $(PKG)/csrc/common.cuh
 LIB      = $(PKG)/libnnvisr.so
 ORACLE   = oracle/liboracle.so
@@ -18,7 +18,7 @@ $(PKG)/build/%.o: $(PKG)/csrc/%.cpp $(HDR)
 	@mkdir -p $(PKG)/build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIB): $(PKG)/build/nnvisr.o $(PKG)/build/comm.o $(PKG)/build/kernels.o $(PKG)/build/kernels_tma.o $(PKG)/build/kernels_yuv.o $(PKG)/build/scene.o
+$(LIB): $(PKG)/build/nnvisr.o $(PKG)/build/comm.o $(PKG)/build/kernels.o $(PKG)/build/kernels_tma.o $(PKG)/build/kernels_yuv.o $(PKG)/build/scene.o $(PKG)/build/kernels_strip.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -ldl
 
 $(ORACLE): oracle/nnvisr_oracle.c
@@ -37,7 +37,7 @@ $(PKG)/build_checked/%.o: $(PKG)/csrc/%.cpp $(HDR)
 	@mkdir -p $(PKG)/build_checked
 	$(NVCC) $(NVFLAGS) -DNNVISR_CHECKED -c $< -o $@
 
-$(CHK): $(PKG)/build_checked/nnvisr.o $(PKG)/build_checked/comm.o $(PKG)/build_checked/kernels.o $(PKG)/build_checked/kernels_tma.o $(PKG)/build_checked/kernels_yuv.o $(PKG)/build_checked/scene.o
+$(CHK): $(PKG)/build_checked/nnvisr.o $(PKG)/build_checked/comm.o $(PKG)/build_checked/kernels.o $(PKG)/build_checked/kernels_tma.o $(PKG)/build_checked/kernels_yuv.o $(PKG)/build_checked/scene.o $(PKG)/build_checked/kernels_strip.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -ldl
 
 clean:

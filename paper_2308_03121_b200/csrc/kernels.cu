@@ -14,6 +14,7 @@
 // and a scalar path that clamps every coordinate elsewhere.  Frames of the
 // common layouts go to the TMA-pipelined kernels instead (kernels_tma.cu).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -221,7 +222,17 @@ cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, cudaSt
 {
     count_launch();
     if (a.yuv) return launch_f2t_yuv(family, bits, dtype, a, s);
-    if (a.tma_ok) return launch_f2t_tma(family, bits, dtype, a, s);
+    if (a.tma_ok) {
+        // low fan-out 4:2:0 launches (every converted frame written to <= 2
+        // slots: store mode, Fig. 1 slots, 2-frame windows) are bound by the
+        // conversion, not HBM: the lean row-marching kernel (kernels_strip.cu);
+        // NNVISR_F2T_STRIP = 0 / 1 forces the choice (A/B experiments)
+        const char *e = std::getenv("NNVISR_F2T_STRIP");
+        const int force = e && *e ? std::atoi(e) : -1;
+        const bool low = a.dests <= 2 * a.jobs;
+        if (family == kYUV420 && (force == 1 || (force < 0 && low))) return launch_f2t_strip(bits, dtype, a, s);
+        return launch_f2t_tma(family, bits, dtype, a, s);
+    }
     switch (family) {
     case kYUV420: return f2t_dispatch<kYUV420>(bits, dtype, a, s);
     case kYUV444: return f2t_dispatch<kYUV444>(bits, dtype, a, s);

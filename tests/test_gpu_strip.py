@@ -1,0 +1,105 @@
+"""The row-marching low fan-out f2t kernel (csrc/kernels_strip.cu) against
+the CPU oracle and bit-identical to the TMA pipeline (csrc/kernels_tma.cu)
+on the same launch: every depth, tensor dtype, both sitings, ragged widths
+(a last 8-column group partly outside the frame), alignment padding rows
+and columns, bands that start and end anywhere relative to the clip's
+height, cuts (duplicated slots), fan-out 1 and 2.  NNVISR_F2T_STRIP=1 / 0
+forces the kernel choice (read at each launch)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2308_03121_b200 import nnvisr as nv
+from paper_2308_03121_b200 import synth
+from paper_2308_03121_b200.frames import FrameBuffer, FrameLayout
+
+from .helpers import assert_tensor_close, oracle_f2t
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _run(h, runs, per, tdt, strip, band_rows=None):
+    os.environ["NNVISR_F2T_STRIP"] = "1" if strip else "0"
+    if band_rows:
+        os.environ["NNVISR_F2T_STRIP_ROWS"] = str(band_rows)
+    try:
+        out = torch.full((len(runs), per), float("nan"), dtype=tdt, device=DEV)
+        h.frames_to_tensor_batch(runs, out.data_ptr(), per * out.element_size())
+        torch.cuda.synchronize()
+        return out
+    finally:
+        os.environ.pop("NNVISR_F2T_STRIP", None)
+        os.environ.pop("NNVISR_F2T_STRIP_ROWS", None)
+
+
+CASES = [
+    # W, H, bits, dtype, siting, N, align, band rows
+    (96, 62, 10, nv.F16, nv.CHROMA_CENTER, 2, 16, 32),
+    (100, 38, 8, nv.F16, nv.CHROMA_CENTER, 1, 16, 6),     # ragged width, padding rows + columns
+    (1920, 40, 10, nv.F16, nv.CHROMA_CENTER, 2, 16, 32),  # 240 groups: 8 idle lanes
+    (2080, 20, 10, nv.F16, nv.CHROMA_LEFT, 1, 1, 8),      # two strips
+    (64, 64, 8, nv.F32, nv.CHROMA_CENTER, 2, 16, 32),     # c1-like fp32
+    (130, 22, 16, nv.F16, nv.CHROMA_LEFT, 2, 8, 4),
+    (48, 10, 16, nv.F32, nv.CHROMA_CENTER, 1, 64, 2),     # Hp = 64 >> H: padding-only bands
+]
+
+
+@pytest.mark.parametrize("W,H,bits,dtype,siting,N,align,band", CASES)
+def test_strip_equals_tma_and_oracle(W, H, bits, dtype, siting, N, align, band):
+    lay = FrameLayout(W, H, nv.YUV420, bits)
+    F = 6
+    buf = FrameBuffer(lay, F, device=DEV)
+    lo, hi = (0, (1 << bits) - 1)
+    host = [synth.random_planes(lay, 900 + 7 * W + i + bits, lo, hi) for i in range(F)]
+    for i, p in enumerate(host):
+        buf.set_planes(i, p)
+    cfg = nv.Config(W, H, nv.YUV420, bits, nv.BT2020 if bits == 10 else nv.BT709,
+                    nv.FULL if bits == 16 else nv.LIMITED, input_count=N, output_count=1, n=1, left_context=0,
+                    flags=0, align=align, dtype=dtype, chroma_loc=siting)
+    cut = np.zeros(F, np.uint8)
+    cut[3] = 1
+    tdt = torch.float16 if dtype == nv.F16 else torch.float32
+    with nv.open(cfg) as h:
+        h.bind_frames(buf.descriptors())
+        runs, _ = h.plan(cut)
+        per = int(np.prod(h.in_shape))
+        a = _run(h, runs, per, tdt, True, band)
+        b = _run(h, runs, per, tdt, False)
+        assert torch.equal(a.view(torch.int16 if dtype == nv.F16 else torch.int32),
+                           b.view(torch.int16 if dtype == nv.F16 else torch.int32))
+        for r in (0, len(runs) - 1, 2):
+            ref = oracle_f2t(lay, [host[int(i)] for i in runs[r]], h.in_shape[2], h.in_shape[3], cfg) \
+                if siting == nv.CHROMA_CENTER else None
+            if ref is None:
+                from oracle import oracle as O
+                ref = O.f2t([host[int(i)] for i in runs[r]], W, H, cfg.family, bits, cfg.matrix, cfg.range,
+                            h.in_shape[2], h.in_shape[3], O.F16 if dtype == nv.F16 else O.F32, siting=O.CHROMA_LEFT)
+            assert_tensor_close(a[r].view(h.in_shape).cpu().numpy(), ref, f"strip run {r}")
+
+
+def test_strip_store_mode_full_size_c2_frames():
+    """c2 geometry (1920x1080 -> 1088 rows, 10-bit, fp16) in store mode,
+    which auto-selects the strip kernel: equal to the TMA kernel, and the
+    padding rows replicate row H-1."""
+    w = synth.WORKLOADS["c2"]
+    buf = synth.generate_clip(w, device=DEV, frames=3)
+    with nv.open(w.cfg) as h:
+        h.bind_frames(buf.descriptors())
+        slot = 3 * h.in_shape[2] * h.in_shape[3]
+        st = {}
+        for strip in (1, 0):
+            os.environ["NNVISR_F2T_STRIP"] = str(strip)
+            try:
+                s = torch.empty((3, slot), dtype=torch.float16, device=DEV)
+                h.frames_to_store(0, 3, s.data_ptr())
+                torch.cuda.synchronize()
+                st[strip] = s
+            finally:
+                os.environ.pop("NNVISR_F2T_STRIP", None)
+        assert torch.equal(st[1].view(torch.int16), st[0].view(torch.int16))
+        t = st[1].view(3, 3, h.in_shape[2], h.in_shape[3])
+        assert torch.equal(t[:, :, 1080:].view(torch.int16),
+                           t[:, :, 1079:1080].expand(-1, -1, 8, -1).reshape(t[:, :, 1080:].shape).view(torch.int16))
