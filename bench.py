@@ -561,13 +561,9 @@ def measure(ctx: Ctx, wname: str, primary: bool):
             # start at once; the boundary tuples wait for the halo
             hstream.wait_stream(stream)
             timed("halo", record, 0, halo_bytes, lambda: exchange(hstream), st=hstream)
-            i0, i1 = s.begin + s.left, max(s.begin + s.left, s.end - s.right)
-            if i1 > i0:
-                f2t_runs(h.plan_range(total, s.begin, own_flags, i0, i1)[0], record)
+            f2t_runs(sh.plan_interior(h, s, own_flags), record)
             t2f_all(np.zeros((s.owned, N), np.int64), record, None)
-            flags = flags_now(hstream)  # waits for the exchange (host)
-            edge = [h.plan_range(total, s.window_first, flags, a, b)[0] for a, b in ((s.begin, i0), (i1, s.end))
-                    if b > a]
+            edge = sh.plan_edges(h, s, flags_now(hstream))  # flags_now waits for the exchange (host)
             stream.wait_stream(hstream)
             for e in edge:
                 f2t_runs(e, record)

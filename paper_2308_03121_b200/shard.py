@@ -123,6 +123,31 @@ class NcclHalo:
             self.comm = None
 
 
+def interior_range(s: Shard) -> tuple[int, int]:
+    """Fresh frames [i0, i1) of the shard whose tuples read only owned frames
+    and owned flags: their plan needs no halo ("interior
+    tuples start immediately, boundary tuples wait on an event")."""
+    i0 = s.begin + s.left
+    return i0, max(i0, s.end - s.right)
+
+
+def plan_interior(h, s: Shard, own_flags: np.ndarray) -> np.ndarray:
+    """Runs of the interior tuples, planned from this rank's own flags only
+    (nnvisr_plan_range over the owned frames)."""
+    i0, i1 = interior_range(s)
+    if i1 <= i0:
+        return np.zeros((0, h.N), np.int64)
+    return h.plan_range(s.total, s.begin, own_flags, i0, i1)[0]
+
+
+def plan_edges(h, s: Shard, window_flags: np.ndarray) -> list[np.ndarray]:
+    """Runs of the boundary tuples (fresh frames [begin, i0) and [i1, end)),
+    planned once the halo flags have arrived."""
+    i0, i1 = interior_range(s)
+    return [h.plan_range(s.total, s.window_first, window_flags, a, b)[0] for a, b in ((s.begin, i0), (i1, s.end))
+            if b > a]
+
+
 def cut_window_of(cut: np.ndarray, s: Shard) -> np.ndarray:
     """The flags of this rank's window, taken from a global array (tests)."""
     return cut[s.window_first:s.window_first + s.window_count]

@@ -132,3 +132,35 @@ def test_peer_halo_addresses_name_the_owners_rows(world, L, R):
             assert shards[owner].window_first + row == g
             assert shards[owner].left <= row < shards[owner].left + shards[owner].owned
             assert owner == r or abs(owner - r) == 1
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("N,L", [(5, 2), (4, 1), (2, 0), (3, 1)])
+def test_interior_and_edge_plans_cover_the_shard(world, N, L):
+    """The overlapped step (bench.py): the interior tuples
+    planned from the rank's OWN flags plus the boundary tuples planned after
+    the halo flags arrive are exactly the global plan restricted to the
+    shard, in order, for cuts anywhere (including at, before and after every
+    shard boundary)."""
+    rng = np.random.default_rng(world * 31 + N)
+    cfg = nv.Config(64, 64, input_count=N, output_count=1, left_context=L)
+    with nv.open(cfg) as h:
+        for trial in range(20):
+            total = int(rng.integers(max(world * max(L, N - 1 - L, 1), 1), 60 + world))
+            cut = (rng.random(total) < 0.15).astype(np.uint8)
+            cut[0] = 0
+            gins, _ = h.plan(cut)
+            for r in range(world):
+                s = sh.shard_of(total, world, r, L, N - 1 - L)
+                own = cut[s.begin:s.end]
+                interior = sh.plan_interior(h, s, own)
+                edges = sh.plan_edges(h, s, sh.cut_window_of(cut, s))
+                i0, i1 = sh.interior_range(s)
+                parts = ([edges[0]] if s.begin < i0 else []) + [interior] + ([edges[-1]] if i1 < s.end else [])
+                got = np.concatenate(parts) if parts else np.zeros((0, N), np.int64)
+                assert np.array_equal(got, gins[s.begin:s.end]), (world, r, total, trial)
+                # the interior plan really used no halo flag: flipping them changes nothing
+                bad = sh.cut_window_of(cut, s).copy()
+                bad[:s.left] ^= 1
+                bad[s.left + s.owned:] ^= 1
+                assert np.array_equal(sh.plan_interior(h, s, own), interior)
