@@ -223,13 +223,15 @@ cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, cudaSt
     count_launch();
     if (a.yuv) return launch_f2t_yuv(family, bits, dtype, a, s);
     if (a.tma_ok) {
-        // low fan-out 4:2:0 launches (every converted frame written to <= 2
-        // slots: store mode, Fig. 1 slots, 2-frame windows) are bound by the
-        // conversion, not HBM: the lean row-marching kernel (kernels_strip.cu);
+        // low fan-out 4:2:0 launches (each converted frame written to < 1.5
+        // slots on average: store mode, Fig. 1 slots) are bound by the
+        // conversion, not HBM: the lean row-marching kernel (kernels_strip.cu;
+        // B200: c2 store 5.2 vs 4.1 TB/s, c4 batches 4.2 vs 3.8; 2-frame
+        // windows stay on the TMA pipeline, 5.3 vs 4.9);
         // NNVISR_F2T_STRIP = 0 / 1 forces the choice (A/B experiments)
         const char *e = std::getenv("NNVISR_F2T_STRIP");
         const int force = e && *e ? std::atoi(e) : -1;
-        const bool low = a.dests <= 2 * a.jobs;
+        const bool low = 2 * a.dests < 3 * a.jobs;
         if (family == kYUV420 && (force == 1 || (force < 0 && low))) return launch_f2t_strip(bits, dtype, a, s);
         return launch_f2t_tma(family, bits, dtype, a, s);
     }
