@@ -12,10 +12,16 @@ seeded network-output tensors.
 
 Default workload: c5 (BASELINE.json configs[4], the 4K clip of the 1/2/4/8-GPU
 sweep), STRONG scaling: the 4096-frame clip is split into contiguous frame
-shards over the N ranks, so T(1)/T(N) is north_star's scaling figure.  The
-1080p workload c2 (configs[1]) is measured in the same run, same N, and
-reported under "per_config".  `--gpus N` without torchrun re-launches itself
-under torch.distributed.run with N ranks.
+shards over the N ranks, so T(1)/T(N) is north_star's scaling figure.  f2t
+runs in store mode S by default for sliding-window workloads (each frame
+converted once into a bounded ring of frame-major regions, every tuple a
+contiguous window of it, tuples with duplicated frames materialised: the
+paper's Fig. 1 principle at batch 1, §3.3); the
+materialised mode (every tuple's tensor written separately) is measured in
+the same run and reported under "per_mode".  The 1080p workload c2
+(configs[1]) is measured in the same run, same N, under "per_config".
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+with N ranks.
 
 Prints ONE JSON line on rank 0 (DESIGN.md §7 lists every key).
 """
@@ -50,9 +56,13 @@ def parse(argv=None):
                         "per_config ('auto' = c2 when the workload is c5, '' = none)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--chunk", type=int, default=0, help="tuples per launch (0 = auto)")
-    p.add_argument("--f2t-mode", default="materialize", choices=["materialize", "store", "batch"],
-                   help="materialize every tuple; store: frame-major store ring (sliding windows); batch: the "
-                        "paper's Fig. 1 batched shared store (paper grouping, --batch lanes)")
+    p.add_argument("--f2t-mode", default="auto", choices=["auto", "materialize", "store", "batch"],
+                   help="materialize every tuple; store: frame-major store ring (sliding windows: the paper's "
+                        "Fig. 1 principle at batch 1, each frame converted once, every tuple a contiguous window); "
+                        "batch: the paper's Fig. 1 batched shared store (paper grouping, --batch lanes); auto = "
+                        "store for sliding-window workloads (c2, c3, c5), materialize otherwise")
+    p.add_argument("--no-compare-modes", action="store_true",
+                   help="skip the second f2t mode of the main workload (reported under per_mode)")
     p.add_argument("--store-k", type=int, default=0, help="store ring: new frames per region (0 = auto)")
     p.add_argument("--store-regions", type=int, default=2, help="store ring: regions")
     p.add_argument("--store-advance", default="copy", choices=["copy", "convert"],
@@ -335,7 +345,14 @@ class Ctx:
             self.dist.destroy_process_group()
 
 
-def measure(ctx: Ctx, wname: str, primary: bool):
+def default_mode(args, wname: str) -> str:
+    from paper_2308_03121_b200 import synth
+    if args.f2t_mode != "auto":
+        return args.f2t_mode
+    return "materialize" if synth.WORKLOADS[wname].cfg.flags & 7 else "store"
+
+
+def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
     """One workload: warm-up, K timed steps, per-kernel statistics, e2e,
     halo check.  Returns the workload's block of the JSON line (rank 0)."""
     args, torch = ctx.args, ctx.torch
@@ -362,7 +379,6 @@ def measure(ctx: Ctx, wname: str, primary: bool):
     R = N - 1 - L
     s = sh.shard_of(total, world, rank, L, R)
     cut_all = synth.cut_flags(w, total)  # each rank only uses its own flags + what the halo brings
-    mode = args.f2t_mode if primary else "materialize"
 
     # window buffer: [left halo | owned frames | right halo]
     lay = w.layout()
@@ -701,12 +717,12 @@ def measure(ctx: Ctx, wname: str, primary: bool):
 
     # ---- e2e: host (pinned) frames in, host frames out, through the C ABI
     e2e = None
-    if not args.no_e2e and not yuv and mode == "materialize":
+    if full and not args.no_e2e and not yuv:
         e2e = run_e2e(ctx, h, s, win, tens_out, n_out, ofb, min(8, fchunk, tchunk), in_elems, out_elems, esz,
                       stream, plan_local, frames_all, tens_in)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if full and rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, wname, args.cpu_sample if primary else 0)
 
     block = {
@@ -802,9 +818,15 @@ def run_e2e(ctx, h, s, win, tens_out, n_out, ofb, chunk, in_elems, out_elems, es
     ms = ctx.max_over_ranks(t0.elapsed_time(t1))
     return {"value": frames_all * steps / (ms / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": ms / steps, "steps": steps,
-            "path": "pinned host frames -> nnvisr_frames_to_tensor_batch_host -> network-output tensors -> "
+            "path": "pinned host frames -> nnvisr_frames_to_tensor_batch_host (materialised tuples) -> "
+                    "network-output tensors -> "
                     "nnvisr_tensor_to_frames_batch_host -> pinned host frames (library staging + copy streams, "
                     "uploads/kernels/downloads of consecutive chunks overlapped)"}
+
+
+def synth_flags(wname: str) -> int:
+    from paper_2308_03121_b200 import synth
+    return synth.WORKLOADS[wname].cfg.flags
 
 
 def main(argv=None):
@@ -821,13 +843,26 @@ def main(argv=None):
     extra = ([] if args.per_config == "" else
              (["c2"] if args.workload == "c5" else []) if args.per_config == "auto" else
              [x for x in args.per_config.split(",") if x and x != args.workload])
-    prim = measure(ctx, args.workload, primary=True)
+    import gc
+
+    def fresh():
+        gc.collect()
+        ctx.torch.cuda.empty_cache()  # the previous measurement's clip and rings
+
+    mode = default_mode(args, args.workload)
+    prim = measure(ctx, args.workload, True, mode)
+    per_mode = {}
+    if not args.no_compare_modes and mode in ("store", "materialize") and args.tensors == "rgb":
+        other = "materialize" if mode == "store" else "store"
+        if other == "materialize" or not (synth_flags(args.workload) & 7):
+            fresh()
+            b = measure(ctx, args.workload, True, other, full=False)
+            per_mode[other] = {k: b[k] for k in ("value", "ms_per_step", "per_direction", "roofline", "gpu_launches",
+                                                 "clocks")}
     per_config = {}
     for wl in extra:
-        import gc
-        gc.collect()
-        ctx.torch.cuda.empty_cache()  # the previous workload's clip and rings
-        per_config[wl] = measure(ctx, wl, primary=False)
+        fresh()
+        per_config[wl] = measure(ctx, wl, False, default_mode(args, wl))
     if ctx.rank == 0:
         line = {
             "metric": METRIC, "value": prim["value"], "unit": "frames/s", "n_gpus": ctx.world, "steps": args.steps,
@@ -839,7 +874,7 @@ def main(argv=None):
             "per_direction": prim["per_direction"], "roofline": prim["roofline"],
             "cpu_baseline": prim["cpu_baseline"], "e2e": prim["e2e"], "gpu_launches": prim["gpu_launches"],
             "clocks": prim["clocks"], "seed": prim["seed"], "halo_check": prim["halo_check"],
-            "per_config": per_config,
+            "per_mode": per_mode, "per_config": per_config,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
