@@ -244,19 +244,20 @@ def oracle_sample(w, count: int, threads: int):
     return count / dt_s, dt_s, threads
 
 
-def default_cpu_sample(w, cores=None):
-    """Tuples in the oracle sample: ~4 per host thread at 1080p (10-30 s of
-    CPU work on the GPU box), scaled by frame area."""
+def default_cpu_sample(w, cores=None, per_thread=10):
+    """Tuples in the oracle sample: ~per_thread per host thread at 1080p
+    (10-30 s of CPU work on the GPU box: c5 ~10 s, c2 ~25 s on 16 threads),
+    scaled by frame area."""
     cores = cores or os.cpu_count() or 1
     px = w.cfg.width * w.cfg.height
-    return int(max(2, min(256, round(4 * cores * (1920 * 1080) / px))))
+    return int(max(2, min(256, round(per_thread * cores * (1920 * 1080) / px))))
 
 
-def cpu_baseline(w, name: str, sample: int | None):
+def cpu_baseline(w, name: str, sample: int | None, per_thread: int = 10):
     """The oracle on the host cores (all threads, plus one thread on a
     smaller sample): BASELINE.md's CPU baseline plan."""
     cores = os.cpu_count() or 1
-    sample = sample or default_cpu_sample(w)
+    sample = sample or default_cpu_sample(w, per_thread=per_thread)
     v, secs, used = oracle_sample(w, sample, cores)
     one = max(1, min(sample, 2))
     v1, secs1, _ = oracle_sample(w, one, 1)
@@ -276,7 +277,7 @@ def run_reference(args):
     from paper_2308_03121_b200 import synth
     w = synth.WORKLOADS[args.workload]
     cores = os.cpu_count() or 1
-    sample = args.cpu_sample or default_cpu_sample(w)
+    sample = args.cpu_sample or default_cpu_sample(w, per_thread=4)
     for _ in range(args.warmup):
         oracle_sample(w, max(1, sample // 4), cores)
     times = []
@@ -723,7 +724,7 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
 
     cpu = None
     if full and rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(w, wname, args.cpu_sample if primary else 0)
+        cpu = cpu_baseline(w, wname, args.cpu_sample if primary else 0, 10 if primary else 3)
 
     block = {
         "value": value, "ms_per_step": ms_step, "frames_per_step": frames_all,
