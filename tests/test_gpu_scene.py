@@ -63,3 +63,46 @@ def test_scene_detect_workload_c4():
     osad, ocut = O.scene_detect(host, w.cfg.width, w.cfg.height, w.cfg.family, w.cfg.bits, w.cfg.matrix,
                                 w.cfg.range, 0.15)
     assert np.array_equal(sad, osad) and np.array_equal(cut, ocut)
+
+
+def test_plan_follows_each_steps_detected_flags():
+    """flags detected on a non-blocking stream and read
+    back for the plan (bench.read_flags) are the CURRENT step's flags.  Two
+    clips with different cut structure are detected alternately (each
+    detection queued behind a long busy kernel on the same stream, so a read
+    on another stream would see the previous step's flags); the plan each
+    step equals the oracle's plan of that clip's oracle-detected flags."""
+    import bench
+    W, H, F, bits = 256, 128, 24, 8
+    lay = FrameLayout(W, H, nv.YUV420, bits)
+    clips, oflags = [], []
+    for c, period in enumerate((5, 7)):
+        buf = FrameBuffer(lay, F, device="cuda")
+        host = []
+        for i in range(F):
+            base = synth.random_planes(lay, 50 * c + i // period)
+            host.append(base)
+            buf.set_planes(i, base)
+        clips.append(buf)
+        oflags.append(O.scene_detect(host, W, H, nv.YUV420, bits, nv.BT709, nv.LIMITED, 0.15)[1])
+    assert not np.array_equal(oflags[0], oflags[1])
+    cfg = nv.Config(W, H, nv.YUV420, bits, nv.BT709, nv.LIMITED, input_count=5, output_count=1, left_context=-1)
+    st = torch.cuda.Stream()  # non-blocking, as bench.py's
+    sad = torch.zeros(F, dtype=torch.int64, device="cuda")
+    cut_d = torch.zeros(F, dtype=torch.uint8, device="cuda")
+    cut_win = torch.zeros(F, dtype=torch.uint8, device="cuda")
+    busy = torch.randn(4096, 4096, device="cuda")
+    with nv.open(cfg) as h:
+        for step in range(6):
+            c = step % 2
+            h.bind_frames(clips[c].descriptors())
+            with torch.cuda.stream(st):
+                for _ in range(8):
+                    busy = busy @ busy * 1e-3  # keep the stream busy before the detection
+                h.scene_detect(0, F, 0.15, sad.data_ptr(), cut_d.data_ptr(), st)
+                cut_win.copy_(cut_d)
+            flags = bench.read_flags(cut_win, st)
+            assert np.array_equal(flags, oflags[c]), step
+            runs, _ = h.plan(flags)
+            oruns, _ = O.plan_window(oflags[c], 5, 2)
+            assert np.array_equal(runs, oruns), step
