@@ -525,8 +525,8 @@ cudaError_t launch(F2TArgs a, cudaStream_t s)
     // columns: strips of 8 x threads (threads = the row's 8-column groups,
     // whole warps, <= 256); rows: bands of a.band luma rows (even)
     const int groups = a.Wp / kPx;
-    const int threads = std::min(kStripThreads, (groups + 31) / 32 * 32);
-    a.nseg = (groups + threads - 1) / threads;
+    a.nseg = (groups + kStripThreads - 1) / kStripThreads;
+    const int threads = ((groups + a.nseg - 1) / a.nseg + 31) / 32 * 32;  // equal strips, whole warps
     // bands: ~8 tiles per SM per launch (each tile start waits one memory
     // latency before its ring fills), at least 32 rows
     const char *e = std::getenv("NNVISR_F2T_STRIP_ROWS");
