@@ -279,6 +279,10 @@ template <typename OUT, int ND> struct DstRows {
     char *q[ND];
     int64_t plane_b;
     int64_t row_b;
+#ifdef NNVISR_CHECKED
+    const char *lo[ND];  // checked builds: every store lands inside its (run, slot)
+    int64_t slot_b;
+#endif
     __device__ __forceinline__ void init(const F2TArgs &a, const DstList &dl, int x, int y)
     {
         plane_b = static_cast<int64_t>(a.Hp) * a.Wp * sizeof(OUT);
@@ -288,6 +292,10 @@ template <typename OUT, int ND> struct DstRows {
             const int cd = dl.code[d];
             q[d] = a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride + static_cast<int64_t>(cd & 31) * a.slot_bytes +
                    (static_cast<int64_t>(y) * a.Wp + x) * static_cast<int64_t>(sizeof(OUT));
+#ifdef NNVISR_CHECKED
+            lo[d] = a.dst + static_cast<int64_t>(cd >> 5) * a.run_stride + static_cast<int64_t>(cd & 31) * a.slot_bytes;
+            slot_b = a.slot_bytes;
+#endif
         }
     }
     __device__ __forceinline__ void put(const Row8<OUT> (&o)[3], bool pred)
@@ -295,7 +303,13 @@ template <typename OUT, int ND> struct DstRows {
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) stg_row_if(reinterpret_cast<OUT *>(q[d] + c * plane_b), o[c], pred);
+            for (int c = 0; c < 3; ++c) {
+#ifdef NNVISR_CHECKED
+                NNVISR_CHECK(!pred || (q[d] + c * plane_b >= lo[d] &&
+                                       q[d] + c * plane_b + kPx * sizeof(OUT) <= lo[d] + slot_b));
+#endif
+                stg_row_if(reinterpret_cast<OUT *>(q[d] + c * plane_b), o[c], pred);
+            }
             q[d] += row_b;
         }
     }
@@ -408,6 +422,21 @@ __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x
             const bool in = rd && ri <= steps;
             const int jc = min(max(jn, 0), ch - 1);
             const char *un = ub + static_cast<int64_t>(jc) * up, *vn = vb + static_cast<int64_t>(jc) * vp;
+#ifdef NNVISR_CHECKED
+            {  // every copy lands in this stage and reads inside its plane
+                const uint32_t e = st + SB;
+                NNVISR_CHECK(st + ol0 + S::LB <= e && st + ol1 + S::LB <= e && st + ou + S::CB <= e && st + ov + S::CB <= e &&
+                             st + oh_mine + 8 <= e && sbase + kStages * SB <= sbase + (uint32_t)(kStages * SB));
+                auto inside = [&](const char *p, int n, int pl, int rows) {
+                    const char *b = static_cast<const char *>(f.plane[pl]);
+                    return p >= b && p + n <= b + rows * f.pitch[pl];
+                };
+                NNVISR_CHECK(!(in && ri >= 2) || inside(la, S::LB, 0, a.H));
+                NNVISR_CHECK(!(in && ri >= 1 && ri < steps) || inside(lb, S::LB, 0, a.H));
+                NNVISR_CHECK(!in || (inside(un, S::CB, 1, ch) && inside(vn, S::CB, 2, ch)));
+                NNVISR_CHECK(!(in && hv) || (inside(un + hoff, 4, 1, ch) && inside(vn + hoff, 4, 2, ch)));
+            }
+#endif
             cp_async<S::LB>(st + ol0, la, in && ri >= 2);
             cp_async<S::LB>(st + ol1, lb, in && ri >= 1 && ri < steps);
             cp_async<S::CB>(st + ou, un, in);
