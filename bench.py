@@ -96,6 +96,10 @@ def parse(argv=None):
     p.add_argument("--detect-threshold", type=float, default=0.15)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="tuples in the oracle sample (0 = auto)")
+    p.add_argument("--emulate-shard", default="",
+                   help="TESTS ONLY ('W,r'): one process runs rank r's shard of W with the N > 1 code path "
+                        "(overlapped halo, device flags, halo check), the halo frames written from the seed "
+                        "instead of received; the numbers are not a measurement")
     return p.parse_args(argv)
 
 
@@ -316,6 +320,9 @@ class Ctx:
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         self.comm = None
+        self.emu = tuple(int(v) for v in args.emulate_shard.split(",")) if args.emulate_shard else None
+        if self.emu and (self.world != 1 or len(self.emu) != 2 or not 0 <= self.emu[1] < self.emu[0]):
+            raise SystemExit("--emulate-shard W,r needs one process and 0 <= r < W")
         if self.world > 1:
             dist.init_process_group("nccl", device_id=self.dev)
             if args.halo in ("nccl", "peer"):
@@ -373,6 +380,10 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
     from paper_2308_03121_b200.store import StoreRing
 
     world, rank, dev = ctx.world, ctx.rank, ctx.dev
+    if ctx.emu:  # tests only: this process plays rank r of W (shard geometry and the N > 1 code path)
+        world, rank = ctx.emu
+        if args.halo == "peer":
+            raise SystemExit("--emulate-shard runs the copy exchange only")
     w = synth.WORKLOADS[wname]
     cfg = w.cfg
     scaling = args.scaling
@@ -489,6 +500,16 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
         ev_pairs[kind].append((a, b, units, nbytes))
 
     def exchange(st):
+        if ctx.emu:
+            # tests only: deliver what the neighbours would send (frames from the
+            # seed, flags of the global pattern) on the exchange's stream
+            with torch.cuda.stream(st):
+                for a0, b0 in ((0, s.left), (s.left + s.owned, s.window_count)):
+                    if b0 > a0:
+                        synth.generate_clip(w, device=dev, frames=b0 - a0, first=s.window_first + a0,
+                                            total_frames=total, out=win, out_offset=a0)
+                        cut_win[a0:b0].copy_(torch.from_numpy(cut_all[s.window_first + a0:s.window_first + b0]).to(dev))
+            return
         if ctx.comm is not None:
             # the library's NCCL group: frames (unless read in place) + flags
             ctx.comm.halo_exchange(total, L, R, None if peer else win.data.data_ptr(), win.frame_bytes,
@@ -748,7 +769,8 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
                                    if args.detect else "given (synthetic cut pattern)"),
                    "l2_policy": f"inputs larger than L2: clip {win.data.numel() / 1e9:.2f} GB per rank, t2f input "
                                 f"ring {n_out} x {out_elems * esz / 1e6:.0f} MB >= 4 x L2 ({l2 / 1e6:.0f} MB)",
-                   "parallelism": (f"{scaling} scaling, contiguous frame shards x{world}" +
+                   "parallelism": (("EMULATED (tests only) " if ctx.emu else "") +
+                                   f"{scaling} scaling, contiguous frame shards x{world}" +
                                    (f", halo {args.halo}" + (" overlapped with interior tuples" if overlap else "")
                                     if world > 1 else "")),
                    "launch": ("CUDA graph replay per step (host plan each step; kernel times from an eager step)"

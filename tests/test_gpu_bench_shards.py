@@ -1,0 +1,36 @@
+"""bench.py's N > 1 code path on the one GPU of this pool (tests only, not a
+measurement): --emulate-shard W,r runs rank r's shard of a W-rank clip --
+shard window, halo exchange on a side stream overlapped with the interior
+tuples (materialised mode) or before the store ring fills (store mode),
+device flags read back on the exchange's stream, boundary tuples planned
+from them, and the halo check -- with the halo frames written from the seed
+instead of received over NCCL (NCCL refuses two ranks on one GPU).  The
+library's multi-rank message plan itself is checked on CPU
+(tests/test_comm_abi.py, tests/test_shard_gloo.py)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("W,r,mode", [(3, 1, "materialize"), (4, 0, "store"), (4, 3, "materialize"),
+                                      (2, 1, "store")])
+def test_emulated_rank_runs_the_multi_gpu_path(W, r, mode):
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "c2", "--frames", "64", "--steps", "2",
+           "--warmup", "1", "--no-cpu-baseline", "--per-config", "", "--no-compare-modes", "--f2t-mode", mode,
+           "--emulate-shard", f"{W},{r}"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    assert d["halo_check"]["ok"] is True
+    assert "EMULATED" in d["config"]["parallelism"]
+    if mode == "materialize":
+        assert "overlapped" in d["config"]["parallelism"]
+        assert d["per_direction"]["halo"]["launches_per_step"] == 1
+    assert d["per_direction"]["f2t"]["achieved_gbs"] > 0 and d["per_direction"]["t2f"]["achieved_gbs"] > 0
+    assert d["e2e"]["value"] > 0
