@@ -1,13 +1,17 @@
 """GPU tests of the Fig. 1 batched shared frame store (NEXT-2; §3.3
 P:360-382): for every batch of the plan, the batched input of slot k (the b
 lanes at contiguous store offsets) equals the materialised per-run tensors'
-slot k bit for bit, and a ring of R regions advanced by the single slot copy
-('6 to 5') holds exactly the same data as converting every slot afresh."""
+slot k bit for bit and every slot equals the CPU ORACLE's conversion of its
+frame (fp16 within 1 ULP, north_star), and a ring of R regions advanced by the
+single slot copy ('6 to 5') holds exactly the same data as converting every
+slot afresh."""
 import numpy as np
 import pytest
 import torch
 
 from oracle import batch_store as B
+
+from .helpers import assert_tensor_close, oracle_f2t
 from paper_2308_03121_b200 import nnvisr as nv
 from paper_2308_03121_b200 import synth
 from paper_2308_03121_b200.frames import FrameBuffer, FrameLayout
@@ -21,11 +25,13 @@ def _setup(n, dtype=nv.F16, W=96, H=40, F=29, cuts=(13,)):
                     left_context=0, flags=flags, align=16, dtype=dtype)
     lay = FrameLayout(W, H, nv.YUV420, 10)
     buf = FrameBuffer(lay, F, device="cuda")
+    host = [synth.random_planes(lay, 50 + i, 64, 940) for i in range(F)]
     for i in range(F):
-        buf.set_planes(i, synth.random_planes(lay, 50 + i, 64, 940))
+        buf.set_planes(i, host[i])
     cut = np.zeros(F, np.uint8)
     for c in cuts:
         cut[c] = 1
+    _setup.host, _setup.lay = host, lay
     return cfg, buf, cut
 
 
@@ -49,6 +55,11 @@ def test_batched_slots_equal_per_run_tensors(n, b):
             store = torch.full((cnt, slot), float("nan"), dtype=dt, device="cuda")
             h.frames_to_slots(x["slots"], store.data_ptr())
             torch.cuda.synchronize()
+            # every slot against the oracle's conversion of its frame
+            for o, fidx in enumerate(x["slots"]):
+                ref = oracle_f2t(_setup.lay, [_setup.host[fidx]], h.in_shape[2], h.in_shape[3], cfg)
+                assert_tensor_close(store[o].view(1, 3, h.in_shape[2], h.in_shape[3]).cpu().numpy(), ref,
+                                    f"batch slot {o} (frame {fidx})")
             for j, r in enumerate(x["lanes"]):
                 for k in range(N):
                     off = nv.shared_slot_offset(n, b, 0, k, j) if x["shared"] else k * b + j
