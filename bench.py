@@ -479,6 +479,7 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
 
     # per launch: (start event, end event, units, algorithmic bytes)
     ev_pairs = {"f2t": [], "t2f": [], "detect": [], "halo": [], "advance": []}
+    overlap_marks = []  # per overlapped step: (start event, halo index, f2t index ranges)
     if args.detect:
         sad_d = torch.zeros(s.window_count, dtype=torch.int64, device=dev)
         cut_d = torch.zeros(s.window_count, dtype=torch.uint8, device=dev)
@@ -602,14 +603,22 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
             # halo exchange on a side stream; the interior tuples (whose
             # windows and flags lie inside the owned frames) and every t2f
             # start at once; the boundary tuples wait for the halo
+            t0 = None
+            if record:
+                t0 = torch.cuda.Event(enable_timing=True)
+                t0.record(stream)
             hstream.wait_stream(stream)
             timed("halo", record, 0, halo_bytes, lambda: exchange(hstream), st=hstream)
+            i0 = len(ev_pairs["f2t"])
             f2t_runs(sh.plan_interior(h, s, own_flags), record)
+            i1 = len(ev_pairs["f2t"])
             t2f_all(np.zeros((s.owned, N), np.int64), record, None)
             edge = sh.plan_edges(h, s, flags_now(hstream))  # flags_now waits for the exchange (host)
             stream.wait_stream(hstream)
             for e in edge:
                 f2t_runs(e, record)
+            if record:
+                overlap_marks.append((t0, len(ev_pairs["halo"]) - 1, i0, i1, len(ev_pairs["f2t"])))
             return s.owned
         if world > 1:
             timed("halo", record, 0, halo_bytes, lambda: exchange(stream))
@@ -727,6 +736,19 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
                 "algorithmic_bytes_per_launch": dv["avg_launch_bytes"],
                 "units_per_launch": dv["avg_launch_units"]}
 
+    # ---- overlap evidence (N > 1): the last timed step's halo exchange and
+    # its interior / boundary f2t launches on the device timeline, ms from
+    # the step's start (interior f2t starting before the exchange ends = overlap)
+    overlap_ev = None
+    if overlap_marks:
+        t0, hi, i0, i1, i2 = overlap_marks[-1]
+        span = lambda pairs: [t0.elapsed_time(pairs[0][0]), t0.elapsed_time(pairs[-1][1])] if pairs else None
+        hp = ev_pairs["halo"][hi]
+        overlap_ev = {"halo_exchange_ms": [t0.elapsed_time(hp[0]), t0.elapsed_time(hp[1])],
+                      "interior_f2t_ms": span(ev_pairs["f2t"][i0:i1]), "boundary_f2t_ms": span(ev_pairs["f2t"][i1:i2])}
+        overlap_ev["interior_started_before_halo_end"] = bool(
+            overlap_ev["interior_f2t_ms"] and overlap_ev["interior_f2t_ms"][0] < overlap_ev["halo_exchange_ms"][1])
+
     # ---- halo check: the received halo frames and flags equal the clip's own
     halo_check = None
     if world > 1:
@@ -777,6 +799,7 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
                               if graph is not None else "eager launches")},
         "per_direction": per_dir, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clk.summary(), "seed": w.seed, "halo_check": halo_check,
+        "overlap": overlap_ev,
         "dtype": "f64" if cfg.bits == 16 else "f32",
     }
     if peer:
@@ -902,6 +925,7 @@ def main(argv=None):
             "per_direction": prim["per_direction"], "roofline": prim["roofline"],
             "cpu_baseline": prim["cpu_baseline"], "e2e": prim["e2e"], "gpu_launches": prim["gpu_launches"],
             "clocks": prim["clocks"], "seed": prim["seed"], "halo_check": prim["halo_check"],
+            "overlap": prim["overlap"],
             "per_mode": per_mode, "per_config": per_config,
         }
         print(json.dumps(line), flush=True)

@@ -32,5 +32,10 @@ def test_emulated_rank_runs_the_multi_gpu_path(W, r, mode):
     if mode == "materialize":
         assert "overlapped" in d["config"]["parallelism"]
         assert d["per_direction"]["halo"]["launches_per_step"] == 1
+        ov = d["overlap"]
+        assert ov["halo_exchange_ms"][0] < ov["halo_exchange_ms"][1]
+        # the boundary tuples start only after the exchange has delivered their frames
+        if ov["boundary_f2t_ms"]:
+            assert ov["boundary_f2t_ms"][0] >= ov["halo_exchange_ms"][1]
     assert d["per_direction"]["f2t"]["achieved_gbs"] > 0 and d["per_direction"]["t2f"]["achieved_gbs"] > 0
     assert d["e2e"]["value"] > 0
