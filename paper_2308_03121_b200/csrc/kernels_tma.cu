@@ -368,8 +368,13 @@ __device__ __forceinline__ void f2t_issue(const F2TArgs &a, int64_t t, uint8_t *
 // (acquire) instead of decoding the tile index themselves.
 // Output buffer layout: [channel][B*ROWS rows][sw]: with a single segment a
 // channel's band rows are contiguous in the tensor too, one bulk store each.
-template <int FAMILY, typename IN, typename OUT, bool LOADER, bool YUVN>
-__global__ void __launch_bounds__(kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2) f2t_tma(const F2TArgs a)
+// NARROW: a two-CTA launch with at most kNarrowCT converting threads (rows
+// up to 1536 columns, e.g. 720p: 160): its register budget (2 x 256 threads)
+// holds the consumer without spills, which the 320-thread bound does not.
+constexpr int kNarrowCT = 192;
+template <int FAMILY, typename IN, typename OUT, bool LOADER, bool YUVN, bool NARROW = false>
+__global__ void __launch_bounds__(NARROW ? kNarrowCT + 64 : kThreads + (LOADER ? 96 : 64), LOADER ? 1 : 2)
+    f2t_tma(const F2TArgs a)
 {
     using S = F2TStage<FAMILY, IN>;
     using V8 = typename Pack<IN>::V8;
@@ -1344,7 +1349,9 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     if (a.debug & 16) a.ob_elems -= 8;  // negative control: buffers too short (the checked build must trap)
 #endif
     int loader = env_int("NNVISR_F2T_LOADER", fits2 ? 0 : 1);
-    auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true, YUVN> : f2t_tma<FAMILY, IN, OUT, false, YUVN>;
+    const bool narrow = !loader && a.cthreads <= kNarrowCT;
+    auto kernel = loader ? f2t_tma<FAMILY, IN, OUT, true, YUVN>
+                         : narrow ? f2t_tma<FAMILY, IN, OUT, false, YUVN, true> : f2t_tma<FAMILY, IN, OUT, false, YUVN>;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
