@@ -607,10 +607,17 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
             if record:
                 t0 = torch.cuda.Event(enable_timing=True)
                 t0.record(stream)
-            hstream.wait_stream(stream)
-            timed("halo", record, 0, halo_bytes, lambda: exchange(hstream), st=hstream)
+            # the first interior launch goes out before the exchange is even
+            # enqueued (the exchange's host cost -- an NCCL group call, or the
+            # emulation's kernels -- then overlaps device work), the rest after
+            interior = sh.plan_interior(h, s, own_flags)
+            ready = torch.cuda.Event()
+            ready.record(stream)  # this step's frames are in place (the exchange orders after this point only)
             i0 = len(ev_pairs["f2t"])
-            f2t_runs(sh.plan_interior(h, s, own_flags), record)
+            f2t_runs(interior[:fchunk], record)
+            hstream.wait_event(ready)
+            timed("halo", record, 0, halo_bytes, lambda: exchange(hstream), st=hstream)
+            f2t_runs(interior[fchunk:], record)
             i1 = len(ev_pairs["f2t"])
             t2f_all(np.zeros((s.owned, N), np.int64), record, None)
             edge = sh.plan_edges(h, s, flags_now(hstream))  # flags_now waits for the exchange (host)
