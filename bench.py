@@ -357,6 +357,8 @@ def default_mode(args, wname: str) -> str:
     from paper_2308_03121_b200 import synth
     if args.f2t_mode != "auto":
         return args.f2t_mode
+    if args.tensors == "yuv" or args.graph:  # YUV-native tensors and graph capture: materialised tuples
+        return "materialize"
     return "materialize" if synth.WORKLOADS[wname].cfg.flags & 7 else "store"
 
 
