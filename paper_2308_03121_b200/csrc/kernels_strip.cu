@@ -495,12 +495,12 @@ __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x
     if (y1 > a.H) {
         const HRow pu = chroma_row_direct<IN, LEFT>(ub, up, ch - 1, rd, lane0, lane31, has_l, has_r, coff);
         const HRow pv = chroma_row_direct<IN, LEFT>(vb, vp, ch - 1, rd, lane0, lane31, has_l, has_r, coff);
-        if (fast) {
-            const LV l = *reinterpret_cast<const LV *>(lbase + static_cast<int64_t>(a.H - 1) * lp);
-            Row8<OUT> o[3];
-            convert_row<IN, OUT>(a.col, l, pu, pu, pv, pv, o);
-            for (int y = max(y0, a.H); y < y1; ++y) dst.put(o, live);
-        }
+        // every lane converts (lanes outside the frame convert zeros; ragged
+        // ones are redone by the scalar path), live lanes store
+        const LV l = rd ? *reinterpret_cast<const LV *>(lbase + static_cast<int64_t>(a.H - 1) * lp) : LV{};
+        Row8<OUT> o[3];
+        convert_row<IN, OUT>(a.col, l, pu, pu, pv, pv, o);
+        for (int y = max(y0, a.H); y < y1; ++y) dst.put(o, live);
     }
 }
 
