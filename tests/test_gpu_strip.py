@@ -103,3 +103,37 @@ def test_strip_store_mode_full_size_c2_frames():
         t = st[1].view(3, 3, h.in_shape[2], h.in_shape[3])
         assert torch.equal(t[:, :, 1080:].view(torch.int16),
                            t[:, :, 1079:1080].expand(-1, -1, 8, -1).reshape(t[:, :, 1080:].shape).view(torch.int16))
+
+
+@pytest.mark.parametrize("W,H,bits", [(7680, 4320, 10), (3840, 2160, 8)])
+def test_strip_full_size_frames(W, H, bits):
+    """Maximum sizes: 8K (4 strips of 240 threads) and 4K 8-bit store-mode
+    slots equal the TMA kernel's bit for bit; sampled rows against the oracle."""
+    lay = FrameLayout(W, H, nv.YUV420, bits)
+    buf = FrameBuffer(lay, 2, device=DEV)
+    host = [synth.random_planes(lay, 77 + i + bits, 0, (1 << bits) - 1) for i in range(2)]
+    for i, p in enumerate(host):
+        buf.set_planes(i, p)
+    cfg = nv.Config(W, H, nv.YUV420, bits, nv.BT2020, nv.LIMITED, input_count=3, output_count=1, n=1,
+                    left_context=-1, flags=0, align=16, dtype=nv.F16)
+    with nv.open(cfg) as h:
+        h.bind_frames(buf.descriptors())
+        slot = 3 * h.in_shape[2] * h.in_shape[3]
+        out = {}
+        for strip in (1, 0):
+            os.environ["NNVISR_F2T_STRIP"] = str(strip)
+            try:
+                s = torch.empty((2, slot), dtype=torch.float16, device=DEV)
+                h.frames_to_store(0, 2, s.data_ptr())
+                torch.cuda.synchronize()
+                out[strip] = s
+            finally:
+                os.environ.pop("NNVISR_F2T_STRIP", None)
+        assert torch.equal(out[1].view(torch.int16), out[0].view(torch.int16))
+        # oracle on a 64-row band at the bottom edge of frame 1 (crop the planes: rows H-64 .. H-1)
+        y0 = H - 64
+        crop = (host[1][0][y0:], host[1][1][y0 // 2:], host[1][2][y0 // 2:])
+        ref = oracle_f2t(FrameLayout(W, 64, nv.YUV420, bits), [crop], 64, W, cfg)
+        got = out[1][1].view(3, h.in_shape[2], h.in_shape[3])[:, y0:H].cpu().numpy()[None]
+        # the crop's first luma row takes its far chroma row from inside the crop (clamped): skip it
+        assert_tensor_close(got[:, :, 1:], ref[:, :, 1:], "8K bottom band")
