@@ -461,7 +461,8 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
         # b*N plain) in its own region of a chunk store; a launch converts the
         # slots of ~fchunk runs' batches, every distinct frame once
         bmax = args.batch * N
-        per_launch = max(1, fchunk // args.batch)
+        # ~3 GB of conversion traffic per launch, as the other modes
+        per_launch = max(1, int(3e9 // (bmax * (frame_payload + slot_bytes))))
         store = torch.empty((per_launch * bmax, slot_bytes // esz), dtype=tdt, device=dev)
     stream = torch.cuda.Stream(device=dev)
     hstream = torch.cuda.Stream(device=dev)

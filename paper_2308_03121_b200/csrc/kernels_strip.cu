@@ -511,9 +511,21 @@ template <typename IN, typename OUT, bool LEFT>
 __global__ void __launch_bounds__(kStripThreads, 2) f2t_strip420(const F2TArgs a)
 {
     extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ int64_t next_tile;
     const int bands = (a.Hp + a.band - 1) / a.band;
     const int64_t per_job = static_cast<int64_t>(bands) * a.nseg;
-    for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+    // persistent CTAs, dynamic tiles: each CTA takes the launch's next tile
+    // from the zeroed per-launch counter, so fast SMs take more tiles and no
+    // SM idles through a long static share (r02 ncu: SMs active 86% of the
+    // kernel with static striding)
+    for (int64_t iter = 0;; ++iter) {
+        if (threadIdx.x == 0)  // (no counter: static tiles b, b + G, ...)
+            next_tile = a.tile_counter ? static_cast<int64_t>(atomicAdd(a.tile_counter, 1ull))
+                                       : blockIdx.x + iter * gridDim.x;
+        __syncthreads();
+        const int64_t t = next_tile;
+        __syncthreads();
+        if (t >= a.tiles) break;
         const int job = static_cast<int>(t / per_job);
         const int rem = static_cast<int>(t - job * per_job);
         const int band = rem / a.nseg, strip = rem - band * a.nseg;
@@ -556,15 +568,6 @@ cudaError_t launch(F2TArgs a, cudaStream_t s)
     const int groups = a.Wp / kPx;
     a.nseg = (groups + kStripThreads - 1) / kStripThreads;
     const int threads = ((groups + a.nseg - 1) / a.nseg + 31) / 32 * 32;  // equal strips, whole warps
-    // bands: ~8 tiles per SM per launch (each tile start waits one memory
-    // latency before its ring fills), at least 32 rows
-    const char *e = std::getenv("NNVISR_F2T_STRIP_ROWS");
-    const int64_t rows_all = static_cast<int64_t>(a.Hp) * a.jobs * a.nseg;
-    const int64_t auto_band = std::max<int64_t>(32, std::min<int64_t>(a.Hp, rows_all / (8LL * sms)));
-    a.band = e && *e ? std::max(2, std::atoi(e) & ~1) : static_cast<int>(auto_band + 1) & ~1;
-    const int bands = (a.Hp + a.band - 1) / a.band;
-    a.tiles = a.jobs * bands * a.nseg;
-    if (a.tiles <= 0) return cudaSuccess;
     auto kernel = f2t_strip420<IN, OUT, LEFT>;
     const int smem = kStages * Stage<IN>::bytes(threads);
     cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -572,7 +575,20 @@ cudaError_t launch(F2TArgs a, cudaStream_t s)
     int per_sm = 0;
     err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     if (err != cudaSuccess) return err;
-    const int64_t grid = std::min<int64_t>(a.tiles, static_cast<int64_t>(sms) * std::max(per_sm, 1) * 4);
+    const int64_t slots = static_cast<int64_t>(sms) * std::max(per_sm, 1);
+    // bands: ~NNVISR_F2T_STRIP_TPC (default 12) tiles per resident CTA, so
+    // the dynamic schedule's tail is short, and at least 32 rows (each tile
+    // start waits one memory latency before its ring fills)
+    const char *e = std::getenv("NNVISR_F2T_STRIP_ROWS");
+    const char *tpc_e = std::getenv("NNVISR_F2T_STRIP_TPC");
+    const int64_t tpc = tpc_e && *tpc_e ? std::max(1, std::atoi(tpc_e)) : 12;
+    const int64_t rows_all = static_cast<int64_t>(a.Hp) * a.jobs * a.nseg;
+    const int64_t auto_band = std::max<int64_t>(32, std::min<int64_t>(a.Hp, rows_all / (tpc * slots)));
+    a.band = e && *e ? std::max(2, std::atoi(e) & ~1) : static_cast<int>(auto_band + 1) & ~1;
+    const int bands = (a.Hp + a.band - 1) / a.band;
+    a.tiles = a.jobs * bands * a.nseg;
+    if (a.tiles <= 0) return cudaSuccess;
+    const int64_t grid = std::min<int64_t>(a.tiles, slots);
     kernel<<<static_cast<int>(grid), threads, smem, s>>>(a);
     return cudaGetLastError();
 }
