@@ -663,21 +663,45 @@ __device__ __forceinline__ void t2f_row(const T2FConst<AR> &c, const T2FColour &
         if constexpr (sizeof(AR) == 4) {
             // fp32: pixels 2m, 2m+1 in packed f32x2 (FADD2 / FFMA2: the same
             // per-lane rounding as the scalar FADD / FFMA, half the instructions)
+            // pairs A = (0,2), C = (1,3), B = (4,6), D = (5,7): the 4:2:0 column
+            // sums BY[2m] + BY[2m+1] of m = 0,1 are then A + C, of m = 2,3 B + D
             const float2 kr2 = make_float2(c.kr, c.kr), kb2 = make_float2(c.kb, c.kb);
+            constexpr int P0[4] = {0, 1, 4, 5}, P1[4] = {2, 3, 6, 7};
+            float2 by2[4], ry2[4];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const float2 r2 = make_float2(R[2 * m], R[2 * m + 1]), g2 = make_float2(G[2 * m], G[2 * m + 1]),
-                             b2 = make_float2(B[2 * m], B[2 * m + 1]);
+            for (int q = 0; q < 4; ++q) {
+                const int i0 = P0[q], i1 = P1[q];
+                const float2 r2 = make_float2(R[i0], R[i1]), g2 = make_float2(G[i0], G[i1]),
+                             b2 = make_float2(B[i0], B[i1]);
                 const float2 ng = make_float2(-g2.x, -g2.y);
                 const float2 Y2 = __ffma2_rn(kb2, __fadd2_rn(b2, ng), __ffma2_rn(kr2, __fadd2_rn(r2, ng), g2));
                 const float2 nY = make_float2(-Y2.x, -Y2.y);
-                const float2 by = __fadd2_rn(b2, nY), ry = __fadd2_rn(r2, nY);
-                BY[2 * m] = by.x;
-                BY[2 * m + 1] = by.y;
-                RY[2 * m] = ry.x;
-                RY[2 * m + 1] = ry.y;
-                qy[2 * m] = quant(Y2.x, c.ys, c.yo, c.maxc);
-                qy[2 * m + 1] = quant(Y2.y, c.ys, c.yo, c.maxc);
+                by2[q] = __fadd2_rn(b2, nY);
+                ry2[q] = __fadd2_rn(r2, nY);
+                BY[i0] = by2[q].x;
+                BY[i1] = by2[q].y;
+                RY[i0] = ry2[q].x;
+                RY[i1] = ry2[q].y;
+                qy[i0] = quant(Y2.x, c.ys, c.yo, c.maxc);
+                qy[i1] = quant(Y2.y, c.ys, c.yo, c.maxc);
+            }
+            if constexpr (FAMILY == kYUV420 && !LEFT) {
+                // 4:2:0 centre: ((a+b) + (c+d)) with the row sums (a+b) as A + C, B + D
+                const float2 pb01 = __fadd2_rn(by2[0], by2[1]), pb23 = __fadd2_rn(by2[2], by2[3]);
+                const float2 pr01 = __fadd2_rn(ry2[0], ry2[1]), pr23 = __fadd2_rn(ry2[2], ry2[3]);
+                if (r == 0) {
+                    sb[0] = pb01.x; sb[1] = pb01.y; sb[2] = pb23.x; sb[3] = pb23.y;
+                    sr[0] = pr01.x; sr[1] = pr01.y; sr[2] = pr23.x; sr[3] = pr23.y;
+                } else {
+                    const float2 b01 = __fadd2_rn(make_float2(sb[0], sb[1]), pb01), b23 = __fadd2_rn(make_float2(sb[2], sb[3]), pb23);
+                    const float2 r01 = __fadd2_rn(make_float2(sr[0], sr[1]), pr01), r23 = __fadd2_rn(make_float2(sr[2], sr[3]), pr23);
+                    sb[0] = b01.x; sb[1] = b01.y; sb[2] = b23.x; sb[3] = b23.y;
+                    sr[0] = r01.x; sr[1] = r01.y; sr[2] = r23.x; sr[3] = r23.y;
+                }
+                OS *out = row_ptr_w<OS>(f, 0, y) + x0;
+                if (vec_store) store_samples8(out, qy);
+                else store_samples_n(out, qy, nvalid);
+                return;
             }
         } else {
 #pragma unroll
@@ -738,10 +762,28 @@ __device__ __forceinline__ void t2f_chroma420(const T2FConst<AR> &c, const DevFr
     constexpr float kW = LEFT ? 8.0f : 4.0f;
     const AR db4 = c.db * AR(kW), dr4 = c.dr * AR(kW), idb4 = c.idb * AR(1.0f / kW), idr4 = c.idr * AR(1.0f / kW);
     uint32_t qb[4], qr[4];
+    if constexpr (sizeof(AR) == 4) {
+        // packed f32x2 divide (reciprocal product + one FMA correction, as divide())
+        auto div2 = [](float2 S, float d, float id) {
+            const float2 q0 = __fmul2_rn(S, make_float2(id, id));
+            const float2 rr = __ffma2_rn(make_float2(-q0.x, -q0.y), make_float2(d, d), S);
+            return __ffma2_rn(rr, make_float2(id, id), q0);
+        };
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        qb[m] = quant(divide(sb[m], db4, idb4), c.cs, c.co, c.maxc);
-        qr[m] = quant(divide(sr[m], dr4, idr4), c.cs, c.co, c.maxc);
+        for (int m = 0; m < 4; m += 2) {
+            const float2 b2 = div2(make_float2(sb[m], sb[m + 1]), db4, idb4);
+            const float2 r2 = div2(make_float2(sr[m], sr[m + 1]), dr4, idr4);
+            qb[m] = quant(b2.x, c.cs, c.co, c.maxc);
+            qb[m + 1] = quant(b2.y, c.cs, c.co, c.maxc);
+            qr[m] = quant(r2.x, c.cs, c.co, c.maxc);
+            qr[m + 1] = quant(r2.y, c.cs, c.co, c.maxc);
+        }
+    } else {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            qb[m] = quant(divide(sb[m], db4, idb4), c.cs, c.co, c.maxc);
+            qr[m] = quant(divide(sr[m], dr4, idr4), c.cs, c.co, c.maxc);
+        }
     }
     OS *ob = row_ptr_w<OS>(f, 1, y0 >> 1) + (x0 >> 1), *orr = row_ptr_w<OS>(f, 2, y0 >> 1) + (x0 >> 1);
     if (vec_store) {
