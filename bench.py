@@ -241,10 +241,18 @@ def oracle_sample(w, count: int, threads: int):
             O.t2f(outs[i % len(outs)], M, olay.width, olay.height, cfg.family, cfg.bits, cfg.matrix, cfg.range)
 
     threads = max(1, min(threads, len(jobs)))
-    t0 = time.perf_counter()
+    # the two directions timed one after the other (tuples/s for
+    # f2t, output frames/s for t2f), the unit rate over both
+    per_dir = {}
+    dt_s = 0.0
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(run, jobs))
-    dt_s = time.perf_counter() - t0
+        for kind in ("f2t", "t2f"):
+            t0 = time.perf_counter()
+            list(ex.map(run, [j for j in jobs if j[0] == kind]))
+            d = time.perf_counter() - t0
+            dt_s += d
+            per_dir[kind] = (count * (M if kind == "t2f" else 1)) / d
+    oracle_sample.last_per_direction = per_dir
     return count / dt_s, dt_s, threads
 
 
@@ -263,12 +271,14 @@ def cpu_baseline(w, name: str, sample: int | None, per_thread: int = 10):
     cores = os.cpu_count() or 1
     sample = sample or default_cpu_sample(w, per_thread=per_thread)
     v, secs, used = oracle_sample(w, sample, cores)
+    per_dir = dict(oracle_sample.last_per_direction)
     one = max(1, min(sample, 2))
     v1, secs1, _ = oracle_sample(w, one, 1)
     return {"value": v, "unit": "frames/s", "cores": used, "kind": "oracle", "cpu_model": cpu_model(),
             "host_threads": cores,
             "sample": f"{sample} tuples of {name} (frames->tensor + tensor->frames each) in {secs:.1f} s on "
                       f"{used} host threads",
+            "per_direction": {"f2t_tuples_per_s": per_dir["f2t"], "t2f_output_frames_per_s": per_dir["t2f"]},
             "single_thread": {"value": v1, "unit": "frames/s", "sample": f"{one} tuples in {secs1:.1f} s"}}
 
 
