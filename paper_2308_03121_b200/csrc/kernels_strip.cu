@@ -392,9 +392,9 @@ __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x
     using S = Stage<IN>;
     const int n = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int cw = a.W >> 1, ch = a.H >> 1, i0 = x >> 1;
-    // fast: all 8 columns inside the frame; rd: loads inside the rows (x < W;
-    // padding columns read nothing); live: a tensor column (stores)
-    const bool fast = x + kPx <= a.W, rd = x < a.W, live = x < a.Wp;
+    // rd: loads inside the rows (x < W; padding columns read nothing);
+    // live: a tensor column (stores)
+    const bool rd = x < a.W, live = x < a.Wp;
     const bool has_l = i0 > 0, has_r = i0 + 4 < cw, lane0 = lane == 0, lane31 = lane == 31;
     const float coff = kMagic + static_cast<float>(a.col.c_off >> 4);
     const int64_t lp = f.pitch[0], up = f.pitch[1], vp = f.pitch[2];

@@ -115,6 +115,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // NNVISR_F2T_DEBUG=8): SM clock of event `ev` of tile i, CTAs 0 and 1, first
 // 128 tiles (see f2t_tma_launch).  Compiled out otherwise.
 constexpr int kTraceTiles = 128, kTraceEvents = 8, kTraceCtas = 1024;
+#ifdef NNVISR_F2T_TRACE
 __device__ __forceinline__ uint64_t gtimer()
 {
     uint64_t t;
@@ -127,6 +128,7 @@ __device__ __forceinline__ uint32_t smid()
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
     return r;
 }
+#endif
 #ifdef NNVISR_F2T_TRACE
 #define NNVISR_TRACE(cond, ev, i)                                                                 \
     do {                                                                                          \
@@ -1369,8 +1371,11 @@ cudaError_t f2t_tma_launch(F2TArgs a, cudaStream_t s)
     }
     kernel<<<grid, block, smem, s>>>(a);
     static int traced_launch = 0;  // NNVISR_F2T_TRACE_LAUNCH = k: dump only the k-th traced launch
-    const bool dump = (a.debug & 8) && std::getenv("NNVISR_F2T_TRACE") &&
-                      traced_launch++ == env_int("NNVISR_F2T_TRACE_LAUNCH", traced_launch - 1);
+    bool dump = false;
+    if ((a.debug & 8) && std::getenv("NNVISR_F2T_TRACE")) {
+        const int k = traced_launch++;
+        dump = k == env_int("NNVISR_F2T_TRACE_LAUNCH", k);
+    }
     if (dump) {  // dump the launch's timeline (experiments only)
         std::vector<uint64_t> h(kTraceBytes / sizeof(uint64_t));
         cudaMemcpyAsync(h.data(), trace_buf, kTraceBytes, cudaMemcpyDeviceToHost, s);
