@@ -131,6 +131,7 @@ cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, cudaSt
 cudaError_t launch_t2f(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s);
 cudaError_t launch_f2t_tma(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s);
 cudaError_t launch_f2t_strip(int bits, int dtype, const F2TArgs &a, cudaStream_t s);
+bool f2t_strip_ok(int dtype, const F2TArgs &a);
 cudaError_t launch_t2f_tma(int family, int bits, int dtype, const T2FArgs &a, cudaStream_t s);
 cudaError_t launch_f2t_yuv(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s);
 cudaError_t launch_f2t_yuv_tma(int family, int bits, int dtype, const F2TArgs &a, cudaStream_t s);

@@ -232,7 +232,8 @@ cudaError_t launch_f2t(int family, int bits, int dtype, const F2TArgs &a, cudaSt
         const char *e = std::getenv("NNVISR_F2T_STRIP");
         const int force = e && *e ? std::atoi(e) : -1;
         const bool low = 2 * a.dests < 3 * a.jobs;
-        if (family == kYUV420 && (force == 1 || (force < 0 && low))) return launch_f2t_strip(bits, dtype, a, s);
+        if (family == kYUV420 && f2t_strip_ok(dtype, a) && (force == 1 || (force < 0 && low)))
+            return launch_f2t_strip(bits, dtype, a, s);
         return launch_f2t_tma(family, bits, dtype, a, s);
     }
     switch (family) {

@@ -15,17 +15,31 @@
 //     k+1) and 2k+2 (3 x row k+1 + row k) (reading A5, clamped), so every
 //     chroma row is loaded and upsampled once per band, not three times per
 //     row pair;
-//   * loads are per-thread asynchronous copies (cp.async) kStages steps ahead
-//     into shared memory (each thread reads back only its own bytes: no
-//     barriers); the chroma halo samples come from the neighbouring lanes by
-//     shuffles, at warp edges from a 4-byte copy;
-//   * all float work runs on packed f32x2 pairs of pixels {0,2}, {4,6},
-//     {1,3}, {5,7}, the pair layout in which the horizontal taps 3*c[m+1] +
-//     c[m] / + c[m+2] of adjacent output columns are register pairs, so no
-//     operand is shuffled between registers;
-//   * stores are 128-bit STGs straight into every destination slot;
-//   * the fp16 near-zero test (f2t_fix_tiny) is one vote per 8 pixels, the
-//     fp64 recompute only inside that rare branch.
+//   * loads are per-thread asynchronous copies (cp.async) into a ring of
+//     shared-memory stages laid out at compile time; each lane reads its
+//     own luma and chroma bytes and its neighbouring lanes' outer chroma
+//     samples (one warp barrier per step), the warp's outer halo words are
+//     copied by lanes 0 and 31 into pads around the warp's block;
+//   * all float work runs on packed f32x2 pairs of pixels {0,7}, {1,2},
+//     {3,4}, {5,6}: the centre horizontal taps of {1,2} and {5,6} are
+//     3 x (a natural sample pair) + that pair swapped (an operand swizzle,
+//     no register moves), {0,7} and {3,4} two scalar FMAs each;
+//   * 16-bit samples become magic floats with one LOP3 / LEA.HI each;
+//   * stores are 128-bit STGs straight into every destination slot,
+//     addressed with 32-bit plane / row offsets;
+//   * the fp16 near-zero test (f2t_fix_tiny) is one vote per 8 pixels on the
+//     packed row; the rare branch recomputes the row from its inputs (nothing
+//     but the packed row stays live across the test);
+//   * persistent CTAs take tiles from a per-launch counter, the next index
+//     fetched while the current tile runs.
+//
+// r02 B200 measurements (tools/ab_r02s.sh, tools/ab_cfg.sh): the rewrite
+// executes 13% fewer instructions (ncu 243 M vs 280 M per c5
+// region fill) at the same time (c2 / c5 store 5.3 / 5.45 TB/s, c4 8-bit
+// Fig. 1 batches 4.7 vs 5.0): the kernel is bound by the memory-level
+// parallelism of 16 warps per SM (128 registers) on a 1-read : 2-write mix,
+// not by issue (a 1:2 streaming probe reaches 5.8 TB/s at 32 warps per SM,
+// 6.25 at 64; tools/hbm_probe.cu).
 //
 // The arithmetic is the TMA fast path's operation for operation (magic-number
 // integer->float, exact integer chroma sums -- the horizontal pass first here,
@@ -41,7 +55,17 @@ namespace {
 using namespace dev;
 
 constexpr int kStripThreads = 256;
-constexpr int kStages = 4;  // march steps in flight per thread (cp.async)
+#ifndef NNVISR_STRIP_MINB
+#define NNVISR_STRIP_MINB 2  // resident CTAs per SM the register budget is cut for
+#endif
+#ifndef NNVISR_STRIP_LAYOUT_THREADS
+#define NNVISR_STRIP_LAYOUT_THREADS kStripThreads
+#endif
+#ifndef NNVISR_STRIP_STAGES
+#define NNVISR_STRIP_STAGES 4
+#endif
+// ring entries per thread (cp.async): kStages - 2 steps ahead at each wait
+constexpr int kStages = NNVISR_STRIP_STAGES;
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
@@ -94,27 +118,39 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// One pipeline stage = one march step of every thread of the CTA, structure
-// of arrays (conflict-free vector reads): luma rows 2k+1, 2k+2 (8 samples
-// each), chroma row k+1 of both planes (4 samples each), and per warp the
-// 4-byte words holding the warp's outer halo samples (lane 0: i0-1, lane 31:
-// i0+4) of both planes.
+// One pipeline stage = one march step of every thread of the CTA, laid out
+// for kStripThreads threads at compile time (constant offsets: no address
+// arithmetic from blockDim per step): luma rows 2k+1, 2k+2 (8 samples per
+// thread each, thread-major), then chroma row k+1 of U and of V in per-warp
+// blocks [pad | 32 lanes x 4 samples | pad].  Lane l reads its neighbours'
+// outer samples (the word before its own samples, the word after) from the
+// block after a __syncwarp; the pads hold the warp's outer halo words,
+// copied by lanes 0 and 31 (i0-1 in the pad's last word, i0+4 in the right
+// pad's first word), so every lane reads the same way.
 template <typename IN> struct Stage {
     static constexpr int LB = 8 * sizeof(IN), CB = 4 * sizeof(IN);  // luma / chroma bytes per thread
-    __host__ __device__ static constexpr int bytes(int n) { return (n * (2 * LB + 2 * CB) + (n / 32) * 16 + 15) / 16 * 16; }
-    // byte offsets inside a stage for thread t of n
-    __device__ static int l0(int t) { return t * LB; }
-    __device__ static int l1(int t, int n) { return (n + t) * LB; }
-    __device__ static int u(int t, int n) { return 2 * n * LB + t * CB; }
-    __device__ static int v(int t, int n) { return 2 * n * LB + (n + t) * CB; }
-    __device__ static int halo(int w, int n) { return 2 * n * (LB + CB) + 16 * w; }  // [uL, vL, uR, vR]
+    static constexpr int HB = CB;                                   // pad per side (own samples stay CB-aligned)
+    static constexpr int WB = 32 * CB + 2 * HB;                     // chroma bytes per warp block
+    static constexpr int kT = NNVISR_STRIP_LAYOUT_THREADS;  // threads the layout is cut for
+    static constexpr int kWarps = kT / 32;
+    static constexpr int kL0 = 0, kL1 = kT * LB;
+    static constexpr int kU = 2 * kT * LB, kV = kU + kWarps * WB;
+    static constexpr int kBytes = (kV + kWarps * WB + 127) / 128 * 128;
+    __device__ static int own_c(int t) { return (t >> 5) * WB + HB + (t & 31) * CB; }
 };
 
 // magic float (2^23 + code) of sample i of packed raw words
+// 16-bit sample h (0 low, 1 high) of a word as a magic float: one LOP3 / LEA.HI
+__device__ __forceinline__ float mag16(uint32_t x, int h)
+{
+    if (h) return __uint_as_float((x >> 16) | kMagicBits);
+    uint32_t r;  // (x & 0xffff) | magic in one LOP3 (the magic in a register)
+    asm("lop3.b32 %0, %1, 0xffff, %2, 0xEA;" : "=r"(r) : "r"(x), "r"(kMagicBits));
+    return __uint_as_float(r);
+}
 __device__ __forceinline__ float magc(uint2 w, int i)  // 16-bit, 4 samples
 {
-    const uint32_t x = (i < 2) ? w.x : w.y;
-    return __uint_as_float(__byte_perm(x, kMagicBits, (i & 1) ? 0x7632 : 0x7610));
+    return mag16(i < 2 ? w.x : w.y, i & 1);
 }
 __device__ __forceinline__ float magc(uint32_t w, int i)  // 8-bit, 4 samples
 {
@@ -125,8 +161,7 @@ template <> struct Luma<uint16_t> {  // 8 samples in a uint4
     using V = uint4;
     __device__ static float get(V w, int i)
     {
-        const uint32_t x = i < 2 ? w.x : i < 4 ? w.y : i < 6 ? w.z : w.w;
-        return __uint_as_float(__byte_perm(x, kMagicBits, (i & 1) ? 0x7632 : 0x7610));
+        return mag16(i < 2 ? w.x : i < 4 ? w.y : i < 6 ? w.z : w.w, i & 1);
     }
 };
 template <> struct Luma<uint8_t> {  // 8 samples in a uint2
@@ -145,44 +180,50 @@ template <typename IN> __device__ __forceinline__ float halo_r(uint32_t w)
 }
 
 // A horizontally upsampled chroma row of the thread's 8 columns, 4x scale
-// minus the offset, in the pixel-pair layout A = {0,2}, B = {4,6},
-// C = {1,3}, D = {5,7}.
+// minus the offset, in the pixel-pair layout A = {0,7}, B = {1,2},
+// C = {3,4}, D = {5,6}: B and D are 3 x (a natural sample pair) + the same
+// pair swapped, so the centre taps need no operand moved between registers.
 struct HRow {
     float2 A, B, C, D;
 };
+// pair p of a row holds pixels (kP0[p], kP1[p])
+__device__ constexpr int kP0[4] = {0, 1, 3, 5}, kP1[4] = {7, 2, 4, 6};
 
-// Chroma row from its 4 own raw samples (halos by shuffles / edge words,
-// clamped at the plane edges): centre siting 3*c[m+1] + c[m] (even column
-// 2m) / + c[m+2] (odd 2m+1); LEFT (MPEG-2) 4*c[m+1] / 2*(c[m+1] + c[m+2])
-// (reading A5).  Every lane of the warp calls it (shuffles).
-template <typename IN, bool LEFT>
-__device__ __forceinline__ HRow chroma_row(typename Pack<IN>::V4 own, uint32_t hl, uint32_t hr, bool lane0,
-                                           bool lane31, bool has_l, bool has_r, float coff)
+// Horizontal taps of one chroma row from samples c0 .. c5 (magic floats;
+// c0 = i0-1, c5 = i0+4, already clamped): centre siting 3*c[m+1] + c[m]
+// (even column 2m) / + c[m+2] (odd 2m+1); LEFT (MPEG-2) 4*c[m+1] /
+// 2*(c[m+1] + c[m+2]) (reading A5).  Exact integers throughout.
+template <bool LEFT>
+__device__ __forceinline__ HRow chroma_taps(float c0, float c1, float c2, float c3, float c4, float c5, float coff)
 {
-    const float c1 = magc(own, 0), c2 = magc(own, 1), c3 = magc(own, 2), c4 = magc(own, 3);
-    const float up = __shfl_up_sync(0xffffffffu, c4, 1), dn = __shfl_down_sync(0xffffffffu, c1, 1);
-    float c0 = lane0 ? halo_l<IN>(hl) : up;
-    float c5 = lane31 ? halo_r<IN>(hr) : dn;
-    c0 = has_l ? c0 : c1;
-    c5 = has_r ? c5 : c4;
     const float2 o2 = f2(-coff, -coff);
-    const float2 E01 = fadd2(f2(c0, c1), o2), E23 = fadd2(f2(c2, c3), o2), E45 = fadd2(f2(c4, c5), o2);
-    const float2 O12 = f2(E01.y, E23.x), O34 = f2(E23.y, E45.x);
+    const float2 P = fadd2(f2(c1, c2), o2), Q = fadd2(f2(c3, c4), o2), H = fadd2(f2(c0, c5), o2);
     HRow h;
     if constexpr (!LEFT) {
         const float2 k3 = f2(3.0f, 3.0f);
-        h.A = ffma2(k3, O12, E01);  // pixels 0, 2: 3c1 + c0, 3c2 + c1
-        h.B = ffma2(k3, O34, E23);  // 4, 6: 3c3 + c2, 3c4 + c3
-        h.C = ffma2(k3, O12, E23);  // 1, 3: 3c1 + c2, 3c2 + c3
-        h.D = ffma2(k3, O34, E45);  // 5, 7: 3c3 + c4, 3c4 + c5
+        h.A = f2(fmaf(3.0f, P.x, H.x), fmaf(3.0f, Q.y, H.y));  // pixels 0, 7: 3c1 + c0, 3c4 + c5
+        h.B = ffma2(k3, P, f2(P.y, P.x));                       // 1, 2: 3c1 + c2, 3c2 + c1
+        h.C = f2(fmaf(3.0f, P.y, Q.x), fmaf(3.0f, Q.x, P.y));  // 3, 4: 3c2 + c3, 3c3 + c2
+        h.D = ffma2(k3, Q, f2(Q.y, Q.x));                       // 5, 6: 3c3 + c4, 3c4 + c3
     } else {
-        const float2 k4 = f2(4.0f, 4.0f), k2 = f2(2.0f, 2.0f);
-        h.A = fmul2(k4, O12);
-        h.B = fmul2(k4, O34);
-        h.C = fmul2(k2, fadd2(O12, E23));
-        h.D = fmul2(k2, fadd2(O34, E45));
+        h.A = f2(4.0f * P.x, 2.0f * (Q.y + H.y));  // 0: 4c1, 7: 2(c4 + c5)
+        h.B = f2(2.0f * (P.x + P.y), 4.0f * P.y);  // 1: 2(c1 + c2), 2: 4c2
+        h.C = f2(2.0f * (P.y + Q.x), 4.0f * Q.x);  // 3: 2(c2 + c3), 4: 4c3
+        h.D = f2(2.0f * (Q.x + Q.y), 4.0f * Q.y);  // 5: 2(c3 + c4), 6: 4c4
     }
     return h;
+}
+
+// Chroma row from its 4 own raw samples and the words before / after them
+// (hl ends at sample i0-1, hr starts at i0+4), clamped at the plane edges.
+template <typename IN, bool LEFT>
+__device__ __forceinline__ HRow chroma_row(typename Pack<IN>::V4 own, uint32_t hl, uint32_t hr, bool has_l, bool has_r,
+                                           float coff)
+{
+    const float c1 = magc(own, 0), c2 = magc(own, 1), c3 = magc(own, 2), c4 = magc(own, 3);
+    const float c0 = has_l ? halo_l<IN>(hl) : c1;
+    const float c5 = has_r ? halo_r<IN>(hr) : c4;
+    return chroma_taps<LEFT>(c0, c1, c2, c3, c4, c5, coff);
 }
 
 // fp16 near-zero values of a row recomputed in fp64 (f2t_fix_tiny).  (Out
@@ -198,15 +239,17 @@ __device__ __forceinline__ void fix_tiny_row(const F2TColour &col, const float2 
     }
 }
 
-// One luma row of 8 pixels: chroma 3*near + far (16x scale minus the
-// offset, exact), Y' = (code - y_off/16) * 16 y_scale (one rounding), one
-// FMA per channel; fp16 near-zero values recomputed in fp64 (rare branch).
-template <typename IN, typename OUT>
-__device__ __forceinline__ void convert_row(const F2TColour &col, typename Luma<IN>::V lraw, const HRow &nu,
-                                            const HRow &fu, const HRow &nv, const HRow &fv, Row8<OUT> (&o)[3])
+// R', G', B' of one luma row of 8 pixels in the pair layout: chroma
+// 3*near + far (16x scale minus the offset, exact), Y' = (code - y_off/16) *
+// 16 y_scale (one rounding: yoff = 2^23 + y_off/16, ys16 = 16 y_scale), one
+// FMA per channel.
+template <typename IN>
+__device__ __forceinline__ void rgb_row(const F2TColour &col, float yoff, float ys16, typename Luma<IN>::V lraw,
+                                        const HRow &nu, const HRow &fu, const HRow &nv, const HRow &fv,
+                                        float2 (&dy)[4], float2 (&du)[4], float2 (&dv)[4], float2 (&R)[4],
+                                        float2 (&G)[4], float2 (&B)[4])
 {
     const float2 k3 = f2(3.0f, 3.0f);
-    float2 du[4], dv[4], dy[4], Y[4];
     du[0] = ffma2(k3, nu.A, fu.A);
     du[1] = ffma2(k3, nu.B, fu.B);
     du[2] = ffma2(k3, nu.C, fu.C);
@@ -215,46 +258,91 @@ __device__ __forceinline__ void convert_row(const F2TColour &col, typename Luma<
     dv[1] = ffma2(k3, nv.B, fv.B);
     dv[2] = ffma2(k3, nv.C, fv.C);
     dv[3] = ffma2(k3, nv.D, fv.D);
-    const float yoff = kMagic + static_cast<float>(col.y_off >> 4);
-    const float ys16 = 16.0f * col.y_scale;
     const float2 yo2 = f2(-yoff, -yoff), ys2 = f2(ys16, ys16);
-    // pair p holds pixels (P0[p], P1[p]): A = {0,2}, B = {4,6}, C = {1,3}, D = {5,7}
-    constexpr int P0[4] = {0, 4, 1, 5}, P1[4] = {2, 6, 3, 7};
+    float2 Y[4];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-        dy[p] = fadd2(f2(Luma<IN>::get(lraw, P0[p]), Luma<IN>::get(lraw, P1[p])), yo2);
+        dy[p] = fadd2(f2(Luma<IN>::get(lraw, kP0[p]), Luma<IN>::get(lraw, kP1[p])), yo2);
         Y[p] = fmul2(dy[p], ys2);
     }
     const float2 rv2 = f2(col.r_v, col.r_v), bu2 = f2(col.b_u, col.b_u);
     const float2 gu2 = f2(-col.g_u, -col.g_u), gv2 = f2(-col.g_v, -col.g_v);
-    float2 R[4], G[4], B[4];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         R[p] = ffma2(rv2, dv[p], Y[p]);
         B[p] = ffma2(bu2, du[p], Y[p]);
         G[p] = ffma2(gv2, dv[p], ffma2(gu2, du[p], Y[p]));
     }
+}
+
+// pixels (0,1) = (A.x, B.x), (2,3) = (B.y, C.x), (4,5) = (C.y, D.x), (6,7) = (D.y, A.y)
+__device__ __forceinline__ void pack_row(const float2 (&R)[4], const float2 (&G)[4], const float2 (&B)[4],
+                                         Row8<__half> (&o)[3])
+{
+    const float2(*ch[3])[4] = {&R, &G, &B};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float2(&v)[4] = *ch[c];
+        o[c].v = make_uint4(pack_half2(v[0].x, v[1].x), pack_half2(v[1].y, v[2].x), pack_half2(v[2].y, v[3].x),
+                            pack_half2(v[3].y, v[0].y));
+    }
+}
+__device__ __forceinline__ void pack_row(const float2 (&R)[4], const float2 (&G)[4], const float2 (&B)[4],
+                                         Row8<float> (&o)[3])
+{
+    const float2(*ch[3])[4] = {&R, &G, &B};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float2(&v)[4] = *ch[c];
+        o[c].a = make_float4(v[0].x, v[1].x, v[1].y, v[2].x);
+        o[c].b = make_float4(v[2].y, v[3].x, v[3].y, v[0].y);
+    }
+}
+
+// register barriers: the rare branch below recomputes from these copies
+// instead of the compiler keeping every row's intermediates live across it
+__device__ __forceinline__ void opaque(HRow &h)
+{
+    asm volatile("" : "+f"(h.A.x), "+f"(h.A.y), "+f"(h.B.x), "+f"(h.B.y), "+f"(h.C.x), "+f"(h.C.y), "+f"(h.D.x),
+                 "+f"(h.D.y));
+}
+__device__ __forceinline__ void opaque(uint4 &v) { asm volatile("" : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)); }
+__device__ __forceinline__ void opaque(uint2 &v) { asm volatile("" : "+r"(v.x), "+r"(v.y)); }
+
+// The row again with its fp16 near-zero values recomputed in fp64 (rare:
+// some value of the 8 pixels below 2^-11).
+template <typename IN>
+__device__ __forceinline__ void convert_row_tiny(const F2TColour &col, float yoff, float ys16, typename Luma<IN>::V lraw,
+                                                 HRow nu, HRow fu, HRow nv, HRow fv, Row8<__half> (&o)[3])
+{
+    opaque(lraw);
+    opaque(nu);
+    opaque(fu);
+    opaque(nv);
+    opaque(fv);
+    float2 dy[4], du[4], dv[4], R[4], G[4], B[4];
+    rgb_row<IN>(col, yoff, ys16, lraw, nu, fu, nv, fv, dy, du, dv, R, G, B);
+    fix_tiny_row(col, dy, du, dv, R, G, B);
+    pack_row(R, G, B, o);
+}
+
+// One luma row of 8 pixels converted and packed; fp16 near-zero values
+// recomputed in fp64 (rare branch).
+template <typename IN, typename OUT>
+__device__ __forceinline__ void convert_row(const F2TColour &col, float yoff, float ys16, typename Luma<IN>::V lraw,
+                                            const HRow &nu, const HRow &fu, const HRow &nv, const HRow &fv,
+                                            Row8<OUT> (&o)[3])
+{
+    float2 dy[4], du[4], dv[4], R[4], G[4], B[4];
+    rgb_row<IN>(col, yoff, ys16, lraw, nu, fu, nv, fv, dy, du, dv, R, G, B);
+    pack_row(R, G, B, o);
     if constexpr (sizeof(OUT) == 2) {
         float mn = 1.0f;
 #pragma unroll
         for (int p = 0; p < 4; ++p)
             mn = fminf(mn, fminf(fminf(fminf(fabsf(R[p].x), fabsf(R[p].y)), fminf(fabsf(G[p].x), fabsf(G[p].y))),
                                  fminf(fabsf(B[p].x), fabsf(B[p].y))));
-        if (mn < kF16Tiny) fix_tiny_row(col, dy, du, dv, R, G, B);  // rare: the fp64 near-zero recompute
-        // pixels (0,1) = (A.x, C.x), (2,3) = (A.y, C.y), (4,5) = (B.x, D.x), (6,7) = (B.y, D.y)
-        o[0].v = make_uint4(pack_half2(R[0].x, R[2].x), pack_half2(R[0].y, R[2].y), pack_half2(R[1].x, R[3].x),
-                            pack_half2(R[1].y, R[3].y));
-        o[1].v = make_uint4(pack_half2(G[0].x, G[2].x), pack_half2(G[0].y, G[2].y), pack_half2(G[1].x, G[3].x),
-                            pack_half2(G[1].y, G[3].y));
-        o[2].v = make_uint4(pack_half2(B[0].x, B[2].x), pack_half2(B[0].y, B[2].y), pack_half2(B[1].x, B[3].x),
-                            pack_half2(B[1].y, B[3].y));
-    } else {
-        o[0].a = make_float4(R[0].x, R[2].x, R[0].y, R[2].y);
-        o[0].b = make_float4(R[1].x, R[3].x, R[1].y, R[3].y);
-        o[1].a = make_float4(G[0].x, G[2].x, G[0].y, G[2].y);
-        o[1].b = make_float4(G[1].x, G[3].x, G[1].y, G[3].y);
-        o[2].a = make_float4(B[0].x, B[2].x, B[0].y, B[2].y);
-        o[2].b = make_float4(B[1].x, B[3].x, B[1].y, B[3].y);
+        if (mn < kF16Tiny) convert_row_tiny<IN>(col, yoff, ys16, lraw, nu, fu, nv, fv, o);
     }
 }
 
@@ -273,20 +361,29 @@ __device__ __forceinline__ void store_row(const F2TArgs &a, const DstList &dl, c
     }
 }
 
+// p + off for a 32-bit unsigned offset: one IMAD.WIDE.U32 instead of an
+// IADD3 / IADD3.X pair
+__device__ __forceinline__ char *addw(char *p, uint32_t off)
+{
+    char *r;
+    asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(r) : "r"(off), "l"(p));
+    return r;
+}
+
 // Destination rows of one tile, walked row by row: ND = 1 or 2 slots held as
-// pointers (one add per row and slot), ND = 0 any number (through dl).
+// pointers (one add per row and slot), ND = 0 any number (through dl).  The
+// launch guarantees 2 x plane bytes < 2^32 (f2t_strip_ok).
 template <typename OUT, int ND> struct DstRows {
     char *q[ND];
-    int64_t plane_b;
-    int64_t row_b;
+    uint32_t plane_b, row_b;
 #ifdef NNVISR_CHECKED
     const char *lo[ND];  // checked builds: every store lands inside its (run, slot)
     int64_t slot_b;
 #endif
     __device__ __forceinline__ void init(const F2TArgs &a, const DstList &dl, int x, int y)
     {
-        plane_b = static_cast<int64_t>(a.Hp) * a.Wp * sizeof(OUT);
-        row_b = static_cast<int64_t>(a.Wp) * sizeof(OUT);
+        plane_b = static_cast<uint32_t>(static_cast<int64_t>(a.Hp) * a.Wp * sizeof(OUT));
+        row_b = static_cast<uint32_t>(a.Wp * sizeof(OUT));
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
             const int cd = dl.code[d];
@@ -302,21 +399,21 @@ template <typename OUT, int ND> struct DstRows {
     {
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
+            char *const qc[3] = {q[d], addw(q[d], plane_b), addw(q[d], 2 * plane_b)};
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
 #ifdef NNVISR_CHECKED
-                NNVISR_CHECK(!pred || (q[d] + c * plane_b >= lo[d] &&
-                                       q[d] + c * plane_b + kPx * sizeof(OUT) <= lo[d] + slot_b));
+                NNVISR_CHECK(!pred || (qc[c] >= lo[d] && qc[c] + kPx * sizeof(OUT) <= lo[d] + slot_b));
 #endif
-                stg_row_if(reinterpret_cast<OUT *>(q[d] + c * plane_b), o[c], pred);
+                stg_row_if(reinterpret_cast<OUT *>(qc[c]), o[c], pred);
             }
-            q[d] += row_b;
+            q[d] = addw(q[d], row_b);
         }
     }
     __device__ __forceinline__ void skip()
     {
 #pragma unroll
-        for (int d = 0; d < ND; ++d) q[d] += row_b;
+        for (int d = 0; d < ND; ++d) q[d] = addw(q[d], row_b);
     }
 };
 template <typename OUT> struct DstRows<OUT, 0> {
@@ -362,27 +459,30 @@ __device__ __forceinline__ void slow_row(const F2TArgs &a, const DstList &dl, co
     }
 }
 
-// Chroma row j of this thread read directly (band prologue, padding rows).
+// Chroma row j of this thread read directly, halos included (band
+// prologue, padding rows).
 template <typename IN, bool LEFT>
-__device__ __forceinline__ HRow chroma_row_direct(const char *ub, int64_t pitch, int j, bool live, bool lane0,
-                                                  bool lane31, bool has_l, bool has_r, float coff)
+__device__ __forceinline__ HRow chroma_row_direct(const char *ub, int64_t pitch, int j, bool live, bool has_l,
+                                                  bool has_r, float coff)
 {
     using V4 = typename Pack<IN>::V4;
     const IN *u = reinterpret_cast<const IN *>(ub + j * pitch);
     const V4 r = live ? *reinterpret_cast<const V4 *>(u) : V4{};
     const uint32_t sh = sizeof(IN) == 2 ? 16 : 24;
-    const uint32_t hl = (lane0 && has_l && live) ? static_cast<uint32_t>(load1(u - 1)) << sh : 0u;
-    const uint32_t hr = (lane31 && has_r && live) ? static_cast<uint32_t>(load1(u + 4)) : 0u;
-    return chroma_row<IN, LEFT>(r, hl, hr, lane0, lane31, has_l, has_r, coff);
+    const uint32_t hl = (has_l && live) ? static_cast<uint32_t>(load1(u - 1)) << sh : 0u;
+    const uint32_t hr = (has_r && live) ? static_cast<uint32_t>(load1(u + 4)) : 0u;
+    return chroma_row<IN, LEFT>(r, hl, hr, has_l, has_r, coff);
 }
 
 // Rows [y0, y1) of a band for the 8 columns at x of every thread of the CTA
-// (a strip of 8 x blockDim.x columns).  Step s (s = 0 .. steps-1) brings
-// chroma row y0/2 + s and luma rows y0 + 2s - 1 (s >= 1), y0 + 2s (< the
-// band's last real row) through the cp.async ring; padding rows (y >= H)
-// replicate row H-1.  Lanes whose columns are not all inside the frame run
-// along on dummy data (their shuffles are needed) and are converted by the
-// scalar path afterwards; lanes past the padded width store nothing.
+// (a strip of 8 x blockDim.x columns).  Ring entry r (r = 0 .. steps) holds
+// chroma row y0/2 - 1 + r (clamped to the plane) and luma rows y0 + 2r - 3
+// (r >= 2) and y0 + 2r - 2 (1 <= r < steps); step s = 0 .. steps-1 emits
+// luma rows y0 + 2s - 1 (s >= 1) and y0 + 2s (< the band's last real row)
+// from entries s and s + 1; padding rows (y >= H) replicate row H-1.  Lanes
+// whose columns are not all inside the frame run along on dummy data (their
+// samples are their neighbours' halos) and are converted by the scalar path
+// afterwards; lanes past the padded width store nothing.
 template <typename IN, typename OUT, bool LEFT, class Dst>
 __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x, int y0, int y1, Dst &dst,
                                       uint8_t *smem)
@@ -390,43 +490,44 @@ __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x
     using V4 = typename Pack<IN>::V4;
     using LV = typename Luma<IN>::V;
     using S = Stage<IN>;
-    const int n = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x, lane = t & 31;
     const int cw = a.W >> 1, ch = a.H >> 1, i0 = x >> 1;
     // rd: loads inside the rows (x < W; padding columns read nothing);
     // live: a tensor column (stores)
     const bool rd = x < a.W, live = x < a.Wp;
-    const bool has_l = i0 > 0, has_r = i0 + 4 < cw, lane0 = lane == 0, lane31 = lane == 31;
+    const bool has_l = i0 > 0, has_r = i0 + 4 < cw;
     const float coff = kMagic + static_cast<float>(a.col.c_off >> 4);
+    const float yoff = kMagic + static_cast<float>(a.col.y_off >> 4), ys16 = 16.0f * a.col.y_scale;
     const int64_t lp = f.pitch[0], up = f.pitch[1], vp = f.pitch[2];
     const char *lbase = static_cast<const char *>(f.plane[0]) + x * sizeof(IN);
     const char *ub = static_cast<const char *>(f.plane[1]) + i0 * sizeof(IN);
     const char *vb = static_cast<const char *>(f.plane[2]) + i0 * sizeof(IN);
-    const int SB = S::bytes(n);
     const uint32_t sbase = smem_addr(smem);
+    const int ol = t * S::LB, oc = S::own_c(t);  // this thread's luma / chroma bytes in a stage
     const int yr1 = min(y1, a.H);
     const int steps = yr1 > y0 ? (yr1 - y0) / 2 + 1 : 0;
     if (steps > 0) {
-        // ring entry r: r = 0 the band's first far chroma row y0/2 - 1
-        // (clamped), r = s + 1 step s; running source pointers of the next
-        // entry to issue
-        const char *la = lbase + static_cast<int64_t>(y0 - 3) * lp;  // luma row y0 + 2s - 1 (entry r: y0 + 2r - 3)
-        const char *lb = lbase + static_cast<int64_t>(y0 - 2) * lp;  // luma row y0 + 2s
-        int jn = y0 / 2 - 1;                                         // chroma row of the next entry (unclamped)
-        const int hoff = lane0 ? -4 : 4 * static_cast<int>(sizeof(IN));  // aligned halo words (lanes 0 / 31)
-        const bool hv = rd && (lane0 ? has_l : has_r) && (lane0 || lane31);
-        const uint32_t ol0 = S::l0(t), ol1 = S::l1(t, n), ou = S::u(t, n), ov = S::v(t, n), oh = S::halo(w, n);
-        const uint32_t oh_mine = oh + (lane31 ? 8 : 0);
-        int ri = 0;  // next ring entry to issue
+        // running sources of the next entry to issue: luma rows y0 + 2r - 3 /
+        // y0 + 2r - 2 (not read while out of the band), chroma row jn
+        // clamped (advanced only inside [0, ch-1])
+        const char *la = lbase + static_cast<int64_t>(y0 - 3) * lp;
+        const char *lb = lbase + static_cast<int64_t>(y0 - 2) * lp;
+        int jn = y0 / 2 - 1;
+        const char *un = ub + static_cast<int64_t>(max(jn, 0)) * up, *vn = vb + static_cast<int64_t>(max(jn, 0)) * vp;
+        // the warp's outer halo words: lane 0 the word ending at sample i0-1,
+        // lane 31 the word starting at i0+4 (into the block's pads)
+        const bool hv = rd && ((lane == 0 && has_l) || (lane == 31 && has_r));
+        const int hsrc = lane == 0 ? -4 : S::CB, hdst = oc + hsrc;
+        int ri = 0;        // next ring entry to issue
+        uint32_t wofs = 0;  // its stage offset, (ri % kStages) * kBytes
+        uint32_t rofs = 0;  // stage offset of the next entry to read
         auto issue = [&]() {
-            const uint32_t st = sbase + (ri & (kStages - 1)) * SB;
+            const uint32_t st = sbase + wofs;
             const bool in = rd && ri <= steps;
-            const int jc = min(max(jn, 0), ch - 1);
-            const char *un = ub + static_cast<int64_t>(jc) * up, *vn = vb + static_cast<int64_t>(jc) * vp;
 #ifdef NNVISR_CHECKED
-            {  // every copy lands in this stage and reads inside its plane
-                const uint32_t e = st + SB;
-                NNVISR_CHECK(st + ol0 + S::LB <= e && st + ol1 + S::LB <= e && st + ou + S::CB <= e && st + ov + S::CB <= e &&
-                             st + oh_mine + 8 <= e && sbase + kStages * SB <= sbase + (uint32_t)(kStages * SB));
+            {  // every copy lands in its stage and reads inside its plane
+                NNVISR_CHECK(static_cast<int>(blockDim.x) <= kStripThreads && ol + S::LB <= S::kL1 && S::kV + oc + S::CB <= S::kBytes &&
+                             S::kU + hdst >= S::kU && S::kV + hdst + 4 <= S::kBytes);
                 auto inside = [&](const char *p, int n, int pl, int rows) {
                     const char *b = static_cast<const char *>(f.plane[pl]);
                     return p >= b && p + n <= b + rows * f.pitch[pl];
@@ -434,72 +535,88 @@ __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x
                 NNVISR_CHECK(!(in && ri >= 2) || inside(la, S::LB, 0, a.H));
                 NNVISR_CHECK(!(in && ri >= 1 && ri < steps) || inside(lb, S::LB, 0, a.H));
                 NNVISR_CHECK(!in || (inside(un, S::CB, 1, ch) && inside(vn, S::CB, 2, ch)));
-                NNVISR_CHECK(!(in && hv) || (inside(un + hoff, 4, 1, ch) && inside(vn + hoff, 4, 2, ch)));
+                NNVISR_CHECK(!(in && hv) || (inside(un + hsrc, 4, 1, ch) && inside(vn + hsrc, 4, 2, ch)));
             }
 #endif
-            cp_async<S::LB>(st + ol0, la, in && ri >= 2);
-            cp_async<S::LB>(st + ol1, lb, in && ri >= 1 && ri < steps);
-            cp_async<S::CB>(st + ou, un, in);
-            cp_async<S::CB>(st + ov, vn, in);
-            cp_async_if<4>(st + oh_mine, un + hoff, in && hv);
-            cp_async_if<4>(st + oh_mine + 4, vn + hoff, in && hv);
+            cp_async<S::LB>(st + S::kL0 + ol, la, in && ri >= 2);
+            cp_async<S::LB>(st + S::kL1 + ol, lb, in && ri >= 1 && ri < steps);
+            cp_async<S::CB>(st + S::kU + oc, un, in);
+            cp_async<S::CB>(st + S::kV + oc, vn, in);
+            cp_async_if<4>(st + S::kU + hdst, un + hsrc, in && hv);
+            cp_async_if<4>(st + S::kV + hdst, vn + hsrc, in && hv);
             cp_commit();
             la += 2 * lp;
             lb += 2 * lp;
+            if (static_cast<unsigned>(jn) < static_cast<unsigned>(ch - 1)) {
+                un += up;
+                vn += vp;
+            }
             ++jn;
             ++ri;
+            wofs = wofs + S::kBytes == kStages * S::kBytes ? 0 : wofs + S::kBytes;
         };
 #pragma unroll
         for (int k = 0; k < kStages - 1; ++k) issue();
-        // entry 0: chroma row y0/2 - 1 (clamped), the far row of the band's first luma row
-        auto chroma_entry = [&](int r, HRow &wu, HRow &wv) {
-            const uint8_t *st = smem + (r & (kStages - 1)) * SB;
-            const uint32_t *hw = reinterpret_cast<const uint32_t *>(st + oh);
-            wu = chroma_row<IN, LEFT>(*reinterpret_cast<const V4 *>(st + ou), hw[0], hw[2], lane0, lane31, has_l,
-                                      has_r, coff);
-            wv = chroma_row<IN, LEFT>(*reinterpret_cast<const V4 *>(st + ov), hw[1], hw[3], lane0, lane31, has_l,
-                                      has_r, coff);
+        // chroma rows of entry r: own samples and the neighbours' words
+        // (visible to this lane after the wait and the warp barrier)
+        auto chroma_entry = [&](HRow &wu, HRow &wv) {
+            const uint8_t *st = smem + rofs;
+            rofs = rofs + S::kBytes == kStages * S::kBytes ? 0 : rofs + S::kBytes;
+            const uint8_t *cu = st + S::kU + oc, *cv = st + S::kV + oc;
+            wu = chroma_row<IN, LEFT>(*reinterpret_cast<const V4 *>(cu), *reinterpret_cast<const uint32_t *>(cu - 4),
+                                      *reinterpret_cast<const uint32_t *>(cu + S::CB), has_l, has_r, coff);
+            wv = chroma_row<IN, LEFT>(*reinterpret_cast<const V4 *>(cv), *reinterpret_cast<const uint32_t *>(cv - 4),
+                                      *reinterpret_cast<const uint32_t *>(cv + S::CB), has_l, has_r, coff);
             return st;
         };
+        // Entry r is read at step r - 1 (entry 0 before the first step).  Each
+        // step waits for its entry (this lane's copies), then one warp
+        // barrier makes every lane's copies of it visible AND orders the
+        // neighbours' reads of the previous step before this step's issue,
+        // which reuses the stage of the entry read one step ago.
         HRow bu, bv;
+        cp_wait<kStages - 2>();
+        __syncwarp();
         issue();
-        cp_wait<kStages - 1>();
-        chroma_entry(0, bu, bv);
+        chroma_entry(bu, bv);
         HRow cu, cv;
         // step s: chroma row y0/2 + s arrives in (wu, wv); rows y0 + 2s - 1
         // (near = previous row p, far = w; not at s = 0) and y0 + 2s (near w,
         // far p; not at the last step)
         auto step = [&](int s, HRow &pu, HRow &pv, HRow &wu, HRow &wv, bool first_row, bool second_row) {
+            cp_wait<kStages - 2>();
+            __syncwarp();
             issue();
-            cp_wait<kStages - 1>();
-            const uint8_t *st = chroma_entry(s + 1, wu, wv);
+            const uint8_t *st = chroma_entry(wu, wv);  // entry s + 1
             Row8<OUT> o[3];
             if (first_row) {
-                convert_row<IN, OUT>(a.col, *reinterpret_cast<const LV *>(st + ol0), pu, wu, pv, wv, o);
+                convert_row<IN, OUT>(a.col, yoff, ys16, *reinterpret_cast<const LV *>(st + S::kL0 + ol), pu, wu, pv,
+                                     wv, o);
                 dst.put(o, live);
             }
             if (second_row) {
-                convert_row<IN, OUT>(a.col, *reinterpret_cast<const LV *>(st + ol1), wu, pu, wv, pv, o);
+                convert_row<IN, OUT>(a.col, yoff, ys16, *reinterpret_cast<const LV *>(st + S::kL1 + ol), wu, pu, wv,
+                                     pv, o);
                 dst.put(o, live);
             }
         };
-        // steps >= 2; even steps hold (p, w) = (b, c), odd ones (c, b)
+        // even steps hold (p, w) = (b, c), odd ones (c, b)
         for (int s = 0; s < steps; s += 2) {
             step(s, bu, bv, cu, cv, s >= 1, s + 1 < steps);
             if (s + 1 >= steps) break;
             step(s + 1, cu, cv, bu, bv, true, s + 2 < steps);
         }
-        cp_wait<0>();
+        cp_wait<0>();  // (the tile loop's barrier orders the reads before the next tile's copies)
     }
     // padding rows (y >= H, reading A6): row H-1 (near = far = chroma row ch-1)
     if (y1 > a.H) {
-        const HRow pu = chroma_row_direct<IN, LEFT>(ub, up, ch - 1, rd, lane0, lane31, has_l, has_r, coff);
-        const HRow pv = chroma_row_direct<IN, LEFT>(vb, vp, ch - 1, rd, lane0, lane31, has_l, has_r, coff);
+        const HRow pu = chroma_row_direct<IN, LEFT>(ub, up, ch - 1, rd, has_l, has_r, coff);
+        const HRow pv = chroma_row_direct<IN, LEFT>(vb, vp, ch - 1, rd, has_l, has_r, coff);
         // every lane converts (lanes outside the frame convert zeros; ragged
         // ones are redone by the scalar path), live lanes store
         const LV l = rd ? *reinterpret_cast<const LV *>(lbase + static_cast<int64_t>(a.H - 1) * lp) : LV{};
         Row8<OUT> o[3];
-        convert_row<IN, OUT>(a.col, l, pu, pu, pv, pv, o);
+        convert_row<IN, OUT>(a.col, yoff, ys16, l, pu, pu, pv, pv, o);
         for (int y = max(y0, a.H); y < y1; ++y) dst.put(o, live);
     }
 }
@@ -508,24 +625,28 @@ __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x
 // Every thread of a CTA walks the same tiles (warp-uniform loops: the march
 // shuffles chroma halos between lanes).
 template <typename IN, typename OUT, bool LEFT>
-__global__ void __launch_bounds__(kStripThreads, 2) f2t_strip420(const F2TArgs a)
+__global__ void __launch_bounds__(kStripThreads, NNVISR_STRIP_MINB) f2t_strip420(const F2TArgs a)
 {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ int64_t next_tile;
+    __shared__ int64_t tile_slot[2];
     const int bands = (a.Hp + a.band - 1) / a.band;
     const int64_t per_job = static_cast<int64_t>(bands) * a.nseg;
     // persistent CTAs, dynamic tiles: each CTA takes the launch's next tile
     // from the zeroed per-launch counter, so fast SMs take more tiles and no
     // SM idles through a long static share (r02 ncu: SMs active 86% of the
-    // kernel with static striding)
+    // kernel with static striding).  The next tile's index is fetched when a
+    // tile starts and published when it ends, so the atomic's latency hides
+    // behind the tile (one barrier per tile, double-buffered slot).
+    auto fetch = [&](int64_t i) -> int64_t {  // (no counter: static tiles b, b + G, ...)
+        return a.tile_counter ? static_cast<int64_t>(atomicAdd(a.tile_counter, 1ull)) : blockIdx.x + i * gridDim.x;
+    };
+    if (threadIdx.x == 0) tile_slot[0] = fetch(0);
+    __syncthreads();
     for (int64_t iter = 0;; ++iter) {
-        if (threadIdx.x == 0)  // (no counter: static tiles b, b + G, ...)
-            next_tile = a.tile_counter ? static_cast<int64_t>(atomicAdd(a.tile_counter, 1ull))
-                                       : blockIdx.x + iter * gridDim.x;
-        __syncthreads();
-        const int64_t t = next_tile;
-        __syncthreads();
+        const int64_t t = tile_slot[iter & 1];
         if (t >= a.tiles) break;
+        int64_t nxt = 0;
+        if (threadIdx.x == 0) nxt = fetch(iter + 1);
         const int job = static_cast<int>(t / per_job);
         const int rem = static_cast<int>(t - job * per_job);
         const int band = rem / a.nseg, strip = rem - band * a.nseg;
@@ -550,7 +671,8 @@ __global__ void __launch_bounds__(kStripThreads, 2) f2t_strip420(const F2TArgs a
         if (x < a.Wp && x + kPx > a.W) {  // ragged right edge / padding columns: scalar path
             for (int y = y0; y < y1; ++y) slow_row<IN, OUT>(a, dl, f, x, y);
         }
-        __syncwarp();
+        if (threadIdx.x == 0) tile_slot[(iter + 1) & 1] = nxt;
+        __syncthreads();  // also orders this tile's ring reads before the next tile's copies
     }
 }
 
@@ -569,19 +691,19 @@ cudaError_t launch(F2TArgs a, cudaStream_t s)
     a.nseg = (groups + kStripThreads - 1) / kStripThreads;
     const int threads = ((groups + a.nseg - 1) / a.nseg + 31) / 32 * 32;  // equal strips, whole warps
     auto kernel = f2t_strip420<IN, OUT, LEFT>;
-    const int smem = kStages * Stage<IN>::bytes(threads);
+    const int smem = kStages * Stage<IN>::kBytes;
     cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
     int per_sm = 0;
     err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     if (err != cudaSuccess) return err;
     const int64_t slots = static_cast<int64_t>(sms) * std::max(per_sm, 1);
-    // bands: ~NNVISR_F2T_STRIP_TPC (default 12) tiles per resident CTA, so
+    // bands: ~NNVISR_F2T_STRIP_TPC (default 20) tiles per resident CTA, so
     // the dynamic schedule's tail is short, and at least 32 rows (each tile
     // start waits one memory latency before its ring fills)
     const char *e = std::getenv("NNVISR_F2T_STRIP_ROWS");
     const char *tpc_e = std::getenv("NNVISR_F2T_STRIP_TPC");
-    const int64_t tpc = tpc_e && *tpc_e ? std::max(1, std::atoi(tpc_e)) : 12;
+    const int64_t tpc = tpc_e && *tpc_e ? std::max(1, std::atoi(tpc_e)) : 20;
     const int64_t rows_all = static_cast<int64_t>(a.Hp) * a.jobs * a.nseg;
     const int64_t auto_band = std::max<int64_t>(32, std::min<int64_t>(a.Hp, rows_all / (tpc * slots)));
     a.band = e && *e ? std::max(2, std::atoi(e) & ~1) : static_cast<int>(auto_band + 1) & ~1;
@@ -600,6 +722,13 @@ cudaError_t launch_sited(const F2TArgs &a, cudaStream_t s)
 }
 
 }  // namespace
+
+// The strip kernel addresses a slot's channel planes with 32-bit offsets.
+bool f2t_strip_ok(int dtype, const F2TArgs &a)
+{
+    const int64_t plane = static_cast<int64_t>(a.Hp) * a.Wp * (dtype == kF16 ? 2 : 4);
+    return 2 * plane < (static_cast<int64_t>(1) << 32);
+}
 
 // 4:2:0 RGB tensors with 16-byte aligned planes, pitches and tensor rows
 // (the caller checked a.tma_ok).

@@ -78,6 +78,66 @@ __global__ void fanout_tma(const uint4 *__restrict__ in, uint4 *__restrict__ out
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// 1 read : W writes with U independent 16-byte loads in flight per thread
+// (chunks of U x blockDim vectors; each written to W destinations)
+template <int W, int U>
+__global__ void fanout_ilp(const uint4 *__restrict__ in, uint4 *__restrict__ out, long m)
+{
+    const long chunk = (long)blockDim.x * U;
+    for (long base = (long)blockIdx.x * chunk; base < m; base += (long)gridDim.x * chunk) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long i = base + u * blockDim.x + threadIdx.x;
+            v[u] = i < m ? __ldcs(in + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long i = base + u * blockDim.x + threadIdx.x;
+                if (i < m) out[(long)k * m + i] = v[u];
+            }
+    }
+}
+
+// 1 read : W writes at strip-kernel occupancy: every warp moves 512-byte
+// rows; STG (BULK = false) or per-warp bulk stores of 512 B from a
+// double-buffered staging area (BULK = true)
+template <int W, bool BULK>
+__global__ void __launch_bounds__(256, 2) warp_rows(const uint4 *__restrict__ in, uint4 *__restrict__ out, long m)
+{
+    __shared__ __align__(128) uint4 stage[8][2][W][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long warps = (long)gridDim.x * 8;
+    int b = 0;
+    for (long r = (long)blockIdx.x * 8 + w; r * 32 < m; r += warps) {
+        const long i = r * 32 + lane;
+        const uint4 v = __ldcs(in + i);
+        if (!BULK) {
+#pragma unroll
+            for (int k = 0; k < W; ++k) out[(long)k * m + i] = v;
+        } else {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < W; ++k) stage[w][b][k][lane] = v;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;" ::"l"(out + (long)k * m + r * 32),
+                                 "r"((unsigned)__cvta_generic_to_shared(&stage[w][b][k][0]))
+                                 : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            b ^= 1;
+        }
+    }
+    if (BULK && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void readonly(const uint4 *__restrict__ in, long n, unsigned *sink)
 {
     const long stride = (long)gridDim.x * blockDim.x;
@@ -133,6 +193,20 @@ int main()
     run("1r_6w_tma_8KB_3cta", [&] { fanout_tma<6, 2><<<3 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
     run("1r_6w_tma_16KB_3cta", [&] { fanout_tma<6, 4><<<3 * 148, block, 64 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
     run("1r_6w_tma_8KB_6cta", [&] { fanout_tma<6, 2><<<6 * 148, block, 32 * 1024>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    run("copy_ilp4", [&] { fanout_ilp<1, 4><<<grid, block>>>(a, b, n); }, 2.0 * bytes);
+    run("copy_ilp8", [&] { fanout_ilp<1, 8><<<grid, block>>>(a, b, n); }, 2.0 * bytes);
+    run("1r_2w_ilp4", [&] { fanout_ilp<2, 4><<<grid, block>>>(a, b, n / 2); }, 1.5 * bytes);
+    run("1r_2w_ilp8", [&] { fanout_ilp<2, 8><<<grid, block>>>(a, b, n / 2); }, 1.5 * bytes);
+    run("1r_2w_ilp8_2x", [&] { fanout_ilp<2, 8><<<2 * grid, block>>>(a, b, n / 2); }, 1.5 * bytes);
+    cudaFuncSetAttribute(fanout_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(fanout_tma<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    run("1r_2w_tma_2cta", [&] { fanout_tma<2><<<2 * 148, block, 64 * 1024>>>(a, b, n / 2); }, 1.5 * bytes);
+    run("1r_2w_tma_3cta", [&] { fanout_tma<2><<<3 * 148, block, 64 * 1024>>>(a, b, n / 2); }, 1.5 * bytes);
+    run("1r_2w_tma_16KB_3cta", [&] { fanout_tma<2, 4><<<3 * 148, block, 64 * 1024>>>(a, b, n / 2); }, 1.5 * bytes);
+    run("1r_2w_warp_stg_16w", [&] { warp_rows<2, false><<<2 * 148, block>>>(a, b, n / 2); }, 1.5 * bytes);
+    run("1r_2w_warp_bulk_16w", [&] { warp_rows<2, true><<<2 * 148, block>>>(a, b, n / 2); }, 1.5 * bytes);
+    run("1r_6w_warp_stg_16w", [&] { warp_rows<6, false><<<2 * 148, block>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
+    run("1r_6w_warp_bulk_16w", [&] { warp_rows<6, true><<<2 * 148, block>>>(a, b, n / 6); }, (double)bytes * 7 / 6);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
     return 0;
