@@ -463,8 +463,10 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
     ring = None
     if mode == "store":
         # store mode S as a bounded ring: R regions of K + N - 1
-        # slots, ~3 GB of conversion traffic per region fill
-        K = args.store_k or max(1, min(256, int(3e9 // (frame_payload + slot_bytes))))
+        # slots, ~6 GB of conversion traffic per region fill (B200, c5 1024
+        # frames: K = 40 / 80 / 160 / 320 -> 16.75k / 17.08k / 17.10k / 17.13k
+        # frames/s, f2t 5.48 / 5.63 / 5.53 / 5.50 TB/s; profiles/r02/storek)
+        K = args.store_k or max(1, min(256, int(6e9 // (frame_payload + slot_bytes))))
         ring = StoreRing(h, s.window_first, s.window_count, K, args.store_regions, args.store_advance, device=dev)
     if mode == "batch":
         # Fig. 1 batches (§3.3): each batch's slots (b*n+1 shared, or
