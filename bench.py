@@ -56,6 +56,7 @@ def parse(argv=None):
                         "per_config ('auto' = c2 when the workload is c5, '' = none)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--chunk", type=int, default=0, help="tuples per launch (0 = auto)")
+    p.add_argument("--t2f-chunk", type=int, default=0, help="tuples per t2f launch (0 = --chunk or auto)")
     p.add_argument("--f2t-mode", default="auto", choices=["auto", "materialize", "store", "batch"],
                    help="materialize every tuple; store: frame-major store ring (sliding windows: the paper's "
                         "Fig. 1 principle at batch 1, each frame converted once, every tuple a contiguous window); "
@@ -444,10 +445,12 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
     t2f_bytes = out_elems * esz + M * olay.payload_bytes()
     frame_payload = lay.payload_bytes()
     slot_bytes = 3 * in_shape[2] * in_shape[3] * esz
-    # tuples per launch: ~3 GB of algorithmic traffic per f2t launch, ~4 GB per
-    # t2f launch (launch ramp/tail < 2%); rings sized so nothing is re-read from L2
+    # tuples per launch: ~3 GB of algorithmic traffic per f2t launch, ~16 GB per
+    # t2f launch (launch ramp/tail ~1%: B200 c5 t2f 13 / 26 / 52 tuples per
+    # launch -> 6.96 / 7.00 / 7.07 TB/s, profiles/r02/t2fchunk); rings sized so
+    # nothing is re-read from L2
     fchunk = args.chunk or max(1, min(64, int(3e9 // (frame_payload + in_elems * esz))))
-    tchunk = args.chunk or max(1, min(64, int(4e9 // t2f_bytes)))
+    tchunk = args.t2f_chunk or args.chunk or max(1, min(64, int(16e9 // t2f_bytes)))
     n_out = max(tchunk, -(-4 * l2 // (out_elems * esz)))
     tens_in = torch.empty((fchunk, in_elems), dtype=tdt, device=dev)
     tens_out = synth.random_tensor((n_out, out_elems), cfg.dtype, w.seed + 99, device=dev)
