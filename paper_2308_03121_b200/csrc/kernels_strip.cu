@@ -494,7 +494,11 @@ __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x
     const int cw = a.W >> 1, ch = a.H >> 1, i0 = x >> 1;
     // rd: loads inside the rows (x < W; padding columns read nothing);
     // live: a tensor column (stores)
+#ifdef NNVISR_STRIP_NOSTORE  // decomposition experiments only (tools/ab_decomp.sh): stores off (a.debug is 0)
+    const bool rd = x < a.W, live = x < a.Wp && a.debug == 0x5eed;
+#else
     const bool rd = x < a.W, live = x < a.Wp;
+#endif
     const bool has_l = i0 > 0, has_r = i0 + 4 < cw;
     const float coff = kMagic + static_cast<float>(a.col.c_off >> 4);
     const float yoff = kMagic + static_cast<float>(a.col.y_off >> 4), ys16 = 16.0f * a.col.y_scale;
@@ -523,7 +527,11 @@ __device__ __forceinline__ void march(const F2TArgs &a, const DevFrame &f, int x
         uint32_t rofs = 0;  // stage offset of the next entry to read
         auto issue = [&]() {
             const uint32_t st = sbase + wofs;
+#ifdef NNVISR_STRIP_NOLOAD  // decomposition experiments only (tools/ab_decomp.sh): copies off (a.debug is 0)
+            const bool in = rd && ri <= steps && a.debug == 0x5eed;
+#else
             const bool in = rd && ri <= steps;
+#endif
 #ifdef NNVISR_CHECKED
             {  // every copy lands in its stage and reads inside its plane
                 NNVISR_CHECK(static_cast<int>(blockDim.x) <= kStripThreads && ol + S::LB <= S::kL1 && S::kV + oc + S::CB <= S::kBytes &&
