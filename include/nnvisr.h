@@ -196,12 +196,40 @@ nnvisr_status nnvisr_plan(const nnvisr_handle *h, int64_t num_frames, const uint
  * [count], cut[i] is the flag of frame first+i.  Requires the window to
  * cover [max(0, fresh_begin-L), min(num_frames, fresh_end+N-1-L)).  For the
  * paper's n > 1 grouping the window must be the whole clip (otherwise
- * NNVISR_ERR_UNSUPPORTED).  The result equals nnvisr_plan of the whole clip
- * restricted to those runs. */
+ * NNVISR_ERR_UNSUPPORTED; a shard window uses nnvisr_plan_range_anchored).
+ * The result equals nnvisr_plan of the whole clip restricted to those runs. */
 nnvisr_status nnvisr_plan_range(const nnvisr_handle *h, int64_t num_frames, int64_t first,
                                 int64_t count, const uint8_t *cut, int64_t fresh_begin,
                                 int64_t fresh_end, int64_t *run_inputs, int64_t *run_fresh,
                                 int64_t cap, int64_t *num_runs);
+
+/* Halo a shard's window needs for this handle's plan: a run reads frames
+ * base-L .. base-L+N-1 (clamped to its scene) with base <= its first fresh
+ * frame lo, and under the paper's grouping with n > 1 the last run of a
+ * scene recycles up to n-1 frames before lo (base = max(s, e-n), PAPER.md
+ * §3.3).  So *left = L + (paper grouping ? n-1 : 0) frames before
+ * the shard and *right = N-1-L after it (the L, R of nnvisr_shard_of /
+ * nnvisr_halo_exchange).  Host only. */
+nnvisr_status nnvisr_halo_extent(const nnvisr_handle *h, int32_t *left, int32_t *right);
+
+/* nnvisr_plan_range for the paper's grouping with n > 1 on a shard window
+ * (SURVEY.md §8(e) "Limitation"): a run's phase lo = s + k*n is counted from
+ * its scene start s (§3.3), which may lie many shards to
+ * the left, so the window's flags alone do not fix the plan.  scene_start is
+ * the start of the scene containing frame fresh_begin (the last k <=
+ * fresh_begin with cut[k] = 1, k > 0, else 0; from nnvisr_cut_allgather +
+ * nnvisr_scene_start_scan across ranks).  The window [first, first+count)
+ * with its flags cut (host [count]) must cover [max(scene_start,
+ * fresh_begin-left), min(num_frames, fresh_end+right)) for the handle's
+ * nnvisr_halo_extent.  Returns the runs whose first fresh frame lies in
+ * [fresh_begin, fresh_end) (the whole clip's plan restricted to them, as
+ * nnvisr_plan_range).  NNVISR_ERR_INVALID_ARG if scene_start contradicts
+ * the window's flags or the window is too small.  For sliding windows and
+ * n = 1 scene_start is ignored and this is nnvisr_plan_range. */
+nnvisr_status nnvisr_plan_range_anchored(const nnvisr_handle *h, int64_t num_frames, int64_t first, int64_t count,
+                                         const uint8_t *cut, int64_t scene_start, int64_t fresh_begin,
+                                         int64_t fresh_end, int64_t *run_inputs, int64_t *run_fresh, int64_t cap,
+                                         int64_t *num_runs);
 
 /* Bind the device-resident frames that batched calls refer to: frames[i]
  * (host array of descriptors) is frame number base+i.  The descriptors are
@@ -503,6 +531,26 @@ nnvisr_status nnvisr_halo_exchange(nnvisr_comm *comm, int64_t total_frames, int3
 nnvisr_status nnvisr_halo_exchange_all(nnvisr_comm *const *comms, int32_t ndev, int64_t total_frames, int32_t L,
                                        int32_t R, void *const *windows, int64_t frame_bytes,
                                        uint8_t *const *cut_windows, void *const *streams);
+
+/* The scene-start scan of the paper's n > 1 grouping across ranks
+ * (SURVEY.md §8(e) "Limitation": an exclusive scan of the last cut
+ * position).  last_cuts: device int64 [world]; on entry element `rank`
+ * holds this rank's last cut in its owned frames (nnvisr_last_cut, -1 if
+ * none); one in-place ncclAllGather on `stream` fills every element (valid
+ * once `stream` reaches that point). */
+nnvisr_status nnvisr_cut_allgather(nnvisr_comm *comm, int64_t *last_cuts, void *stream);
+
+/* Host helpers of the scan.  nnvisr_last_cut: the last frame first+i with
+ * cut[i] = 1 and first+i > 0 of a host flag array cut [count] (-1 if none;
+ * cut[0] of the clip is ignored, reading A9).  nnvisr_scene_start_scan: the
+ * start of the scene containing frame `begin` (= this rank's first owned
+ * frame) from the gathered last cuts of ranks 0 .. rank-1 (host [world]) and
+ * begin's own flag cut_begin: begin if it starts a scene, else the largest
+ * lower-rank cut, else 0.  NNVISR_ERR_INVALID_ARG if a lower rank's cut lies
+ * at or after begin. */
+nnvisr_status nnvisr_last_cut(const uint8_t *cut, int64_t first, int64_t count, int64_t *last_cut);
+nnvisr_status nnvisr_scene_start_scan(int32_t world, int32_t rank, const int64_t *last_cuts, int64_t begin,
+                                      uint8_t cut_begin, int64_t *scene_start);
 
 /* Free a communicator (ncclCommDestroy; after its work completed).  NULL is OK. */
 nnvisr_status nnvisr_comm_destroy(nnvisr_comm *comm);

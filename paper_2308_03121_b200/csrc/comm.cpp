@@ -47,6 +47,7 @@ struct NcclApi {
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *);
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
     ncclResult_t (*GroupStart)();
     ncclResult_t (*GroupEnd)();
     const char *(*GetErrorString)(ncclResult_t);
@@ -84,6 +85,7 @@ void load_nccl()
     NNVISR_SYM(CommGetAsyncError)
     NNVISR_SYM(Send)
     NNVISR_SYM(Recv)
+    NNVISR_SYM(AllGather)
     NNVISR_SYM(GroupStart)
     NNVISR_SYM(GroupEnd)
     NNVISR_SYM(GetErrorString)
@@ -312,6 +314,46 @@ nnvisr_status nnvisr_halo_exchange_all(nnvisr_comm *const *comms, int32_t ndev, 
     }
     for (int i = 0; i < ndev; ++i)
         if ((s = check_async(comms[i]))) return s;
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_cut_allgather(nnvisr_comm *comm, int64_t *last_cuts, void *stream)
+{
+    if (!comm || !last_cuts) return arg_fail("nnvisr_cut_allgather: NULL argument");
+    nnvisr_status s = need_nccl();
+    if (s) return s;
+    // in place: this rank's element is the send buffer (world 1: a no-op copy)
+    ncclResult_t r = g_nccl.AllGather(last_cuts + comm->rank, last_cuts, 1, ncclInt64, comm->comm,
+                                      static_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather (last scene cuts)");
+    return check_async(comm);
+}
+
+nnvisr_status nnvisr_last_cut(const uint8_t *cut, int64_t first, int64_t count, int64_t *last_cut)
+{
+    if (!last_cut || (count > 0 && !cut) || first < 0 || count < 0) return arg_fail("nnvisr_last_cut: bad argument");
+    *last_cut = -1;
+    for (int64_t i = count - 1; i >= 0; --i)
+        if (cut[i] && first + i > 0) {  // cut[0] of the clip is ignored (reading A9)
+            *last_cut = first + i;
+            break;
+        }
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_scene_start_scan(int32_t world, int32_t rank, const int64_t *last_cuts, int64_t begin,
+                                      uint8_t cut_begin, int64_t *scene_start)
+{
+    if (!last_cuts || !scene_start || world < 1 || rank < 0 || rank >= world || begin < 0)
+        return arg_fail("nnvisr_scene_start_scan: bad argument");
+    // exclusive prefix max of the ranks' last cuts (every frame of ranks
+    // j < rank lies before `begin`), unless `begin` itself starts a scene
+    int64_t sc = 0;
+    for (int32_t j = 0; j < rank; ++j) {
+        if (last_cuts[j] >= begin) return arg_fail("nnvisr_scene_start_scan: a lower rank's cut lies at or after begin");
+        sc = last_cuts[j] > sc ? last_cuts[j] : sc;
+    }
+    *scene_start = (cut_begin && begin > 0) ? begin : sc;
     return NNVISR_OK;
 }
 

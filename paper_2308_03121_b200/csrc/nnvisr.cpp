@@ -467,6 +467,84 @@ nnvisr_status nnvisr_plan_range(const nnvisr_handle *h, int64_t num_frames, int6
     return NNVISR_OK;
 }
 
+nnvisr_status nnvisr_halo_extent(const nnvisr_handle *h, int32_t *left, int32_t *right)
+{
+    g_error.clear();
+    if (!h || !left || !right) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    // inputs of a run: base - L + j (j < N), clamped to its scene; base >= lo
+    // - (n-1) (the recycled last run of a scene) and base <= lo
+    *left = h->L + (h->paper ? h->n - 1 : 0);
+    *right = h->N - 1 - h->L;
+    return NNVISR_OK;
+}
+
+nnvisr_status nnvisr_plan_range_anchored(const nnvisr_handle *h, int64_t num_frames, int64_t first, int64_t count,
+                                         const uint8_t *cut, int64_t scene_start, int64_t fresh_begin,
+                                         int64_t fresh_end, int64_t *run_inputs, int64_t *run_fresh, int64_t cap,
+                                         int64_t *num_runs)
+{
+    NvtxRange nvtx_("nnvisr_plan_range_anchored");
+    g_error.clear();
+    if (!h || !num_runs) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (!h->paper || h->n == 1)  // sliding windows and n = 1: the window alone fixes the plan
+        return nnvisr_plan_range(h, num_frames, first, count, cut, fresh_begin, fresh_end, run_inputs, run_fresh,
+                                 cap, num_runs);
+    if (num_frames < 0 || first < 0 || count < 0 || first + count > num_frames)
+        return fail(NNVISR_ERR_INVALID_ARG, "window [%lld, %lld) outside the clip of %lld frames",
+                    (long long)first, (long long)(first + count), (long long)num_frames);
+    if (fresh_begin < 0 || fresh_end > num_frames || fresh_begin > fresh_end)
+        return fail(NNVISR_ERR_INVALID_ARG, "bad fresh range [%lld, %lld)", (long long)fresh_begin,
+                    (long long)fresh_end);
+    if (count > 0 && !cut) return fail(NNVISR_ERR_INVALID_ARG, "null cut array");
+    if (cap > 0 && (!run_inputs || !run_fresh)) return fail(NNVISR_ERR_INVALID_ARG, "null output arrays");
+    PlanSink sink{run_inputs, run_fresh, std::max<int64_t>(cap, 0), 0, h->N};
+    if (fresh_begin == fresh_end) { *num_runs = 0; return NNVISR_OK; }
+    if (scene_start < 0 || scene_start > fresh_begin)
+        return fail(NNVISR_ERR_INVALID_ARG, "scene_start %lld outside [0, fresh_begin %lld]", (long long)scene_start,
+                    (long long)fresh_begin);
+    const int32_t lh = h->L + h->n - 1, rh = h->N - 1 - h->L;
+    const int64_t need_lo = std::max<int64_t>(scene_start, fresh_begin - lh);
+    const int64_t need_hi = std::min<int64_t>(num_frames, fresh_end + rh);
+    const int64_t end = first + count;
+    if (first > need_lo || end < need_hi)
+        return fail(NNVISR_ERR_INVALID_ARG, "window [%lld, %lld) does not cover [%lld, %lld)", (long long)first,
+                    (long long)end, (long long)need_lo, (long long)need_hi);
+    auto cut_at = [&](int64_t k) { return k > 0 && cut[k - first] != 0; };
+    // the anchor must agree with the window's own flags: no cut in
+    // (scene_start, fresh_begin], a cut at scene_start if the window sees it
+    for (int64_t k = std::max(scene_start + 1, first); k <= fresh_begin; ++k)
+        if (cut_at(k))
+            return fail(NNVISR_ERR_INVALID_ARG, "scene_start %lld contradicts the cut at frame %lld",
+                        (long long)scene_start, (long long)k);
+    if (scene_start > 0 && scene_start >= first && !cut_at(scene_start))
+        return fail(NNVISR_ERR_INVALID_ARG, "scene_start %lld is not a cut in the window", (long long)scene_start);
+    // Scenes from the anchor on: each ends at the next cut the window shows,
+    // else at the window's end, which binds no run whose fresh frame lies in
+    // [fresh_begin, fresh_end) (their inputs end before it).  A run's phase is
+    // counted from its scene start (§3.3): lo = s + k n.
+    const int64_t n = h->n;
+    int64_t sc = scene_start;
+    while (sc < fresh_end) {
+        int64_t e = std::max(sc, fresh_begin) + 1;
+        while (e < end && !cut_at(e)) ++e;
+        const int64_t m = e - sc, K = (m + n - 1) / n;
+        const int64_t k0 = fresh_begin > sc ? (fresh_begin - sc + n - 1) / n : 0;
+        int64_t in[16];
+        for (int64_t k = k0; k < K; ++k) {
+            const int64_t lo = sc + k * n, hi = std::min(sc + (k + 1) * n, e);
+            if (lo >= fresh_end) break;
+            const int64_t base = std::min(lo, std::max(sc, e - n));
+            for (int j = 0; j < h->N; ++j) in[j] = std::min(std::max(base - h->L + j, sc), e - 1);
+            sink.emit(in, lo, hi);
+        }
+        sc = e;
+    }
+    *num_runs = sink.count;
+    if (sink.count > cap) return fail(NNVISR_ERR_CAPACITY, "plan needs %lld runs, capacity %lld",
+                                      (long long)sink.count, (long long)cap);
+    return NNVISR_OK;
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------ device side

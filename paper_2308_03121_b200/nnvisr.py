@@ -68,6 +68,8 @@ def _load():
         "nnvisr_tensor_shapes": (st, [H, i64p, i64p]),
         "nnvisr_plan": (st, [H, i64, C.c_void_p, i64p, i64p, i64, i64p]),
         "nnvisr_plan_range": (st, [H, i64, i64, i64, C.c_void_p, i64, i64, i64p, i64p, i64, i64p]),
+        "nnvisr_plan_range_anchored": (st, [H, i64, i64, i64, C.c_void_p, i64, i64, i64, i64p, i64p, i64, i64p]),
+        "nnvisr_halo_extent": (st, [H, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         "nnvisr_bind_frames": (st, [H, i64, C.POINTER(Frame), i64]),
         "nnvisr_frames_to_tensor": (st, [H, C.POINTER(Frame), C.c_void_p, C.c_void_p]),
         "nnvisr_frames_to_tensor_batch": (st, [H, i64p, i64, C.c_void_p, i64, C.c_void_p]),
@@ -107,6 +109,9 @@ def _load():
         "nnvisr_halo_exchange_all": (st, [C.POINTER(C.c_void_p), C.c_int32, i64, C.c_int32, C.c_int32,
                                           C.POINTER(C.c_void_p), i64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
         "nnvisr_comm_destroy": (st, [C.c_void_p]),
+        "nnvisr_cut_allgather": (st, [C.c_void_p, C.c_void_p, C.c_void_p]),
+        "nnvisr_last_cut": (st, [C.c_void_p, i64, i64, i64p]),
+        "nnvisr_scene_start_scan": (st, [C.c_int32, C.c_int32, i64p, i64, C.c_uint8, i64p]),
         "nnvisr_nccl_version": (C.c_int32, []),
     }
     for name, (res, args) in sig.items():
@@ -128,7 +133,8 @@ EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version"
             "nnvisr_peer_import", "nnvisr_peer_close", "nnvisr_release_graph_tables", "nnvisr_shard_of",
             "nnvisr_halo_plan", "nnvisr_comm_unique_id", "nnvisr_comm_init_rank", "nnvisr_comm_init_all",
             "nnvisr_comm_info", "nnvisr_comm_check", "nnvisr_halo_exchange", "nnvisr_halo_exchange_all",
-            "nnvisr_comm_destroy", "nnvisr_nccl_version")
+            "nnvisr_comm_destroy", "nnvisr_nccl_version", "nnvisr_plan_range_anchored", "nnvisr_halo_extent",
+            "nnvisr_cut_allgather", "nnvisr_last_cut", "nnvisr_scene_start_scan")
 
 
 def lib():
@@ -203,6 +209,28 @@ def halo_plan(total: int, world: int, rank: int, L: int, R: int) -> list[tuple[i
     return [(int(m.peer), bool(m.send), int(m.first), int(m.count)) for m in msgs[:n.value]]
 
 
+def last_cut(cut, first: int) -> int:
+    """nnvisr_last_cut: the last frame first+i > 0 with cut[i] set (-1: none)."""
+    c = np.ascontiguousarray(np.asarray(cut, dtype=np.uint8))
+    out = C.c_int64()
+    _check(_lib.nnvisr_last_cut(c.ctypes.data if c.shape[0] else None, first, c.shape[0], C.byref(out)))
+    return out.value
+
+
+def scene_start_scan(world: int, rank: int, last_cuts, begin: int, cut_begin: int) -> int:
+    """nnvisr_scene_start_scan: start of the scene containing frame `begin`
+    from the gathered last cuts of every rank (ValueError if inconsistent)."""
+    lc = np.ascontiguousarray(np.asarray(last_cuts, dtype=np.int64))
+    if lc.shape[0] != world:
+        raise ValueError(f"last_cuts has {lc.shape[0]} entries, world is {world}")
+    out = C.c_int64()
+    st = _lib.nnvisr_scene_start_scan(world, rank, _i64p(lc), begin, int(bool(cut_begin)), C.byref(out))
+    if st == 2:
+        raise ValueError(_lib.nnvisr_last_error().decode())
+    _check(st)
+    return out.value
+
+
 def nccl_version() -> int:
     """Version code of the NCCL the library loaded (-1: unavailable)."""
     return int(_lib.nnvisr_nccl_version())
@@ -261,6 +289,11 @@ class Comm:
         fs = (C.c_void_p * n)(*cut_window_ptrs)
         ss = (C.c_void_p * n)(*[_stream_ptr(s) for s in streams])
         _check(_lib.nnvisr_halo_exchange_all(cs, n, total, L, R, ws, frame_bytes, fs, ss))
+
+    def cut_allgather(self, last_cuts_ptr: int, stream=None):
+        """nnvisr_cut_allgather: device int64 [world], element `rank` in,
+        every element out (in place, on `stream`)."""
+        _check(_lib.nnvisr_cut_allgather(self._c, last_cuts_ptr, _stream_ptr(stream)))
 
     def destroy(self):
         if self._c is not None and self._c.value:
@@ -359,6 +392,25 @@ class Handle:
                                       cut.ctypes.data if cut.shape[0] else None, fresh_begin, fresh_end,
                                       _i64p(ins), _i64p(fresh), cap, C.byref(nr)))
         return ins[:nr.value].copy(), fresh[:nr.value].copy()
+
+    def plan_range_anchored(self, num_frames, first, cut_window, scene_start, fresh_begin, fresh_end):
+        """nnvisr_plan_range_anchored: the shard's runs under the paper's
+        n > 1 grouping, given the start of the scene containing fresh_begin."""
+        cut = np.ascontiguousarray(np.asarray(cut_window, dtype=np.uint8))
+        cap = max(fresh_end - fresh_begin, 1)
+        ins = np.zeros((cap, self.N), np.int64)
+        fresh = np.zeros((cap, 2), np.int64)
+        nr = C.c_int64()
+        _check(_lib.nnvisr_plan_range_anchored(self._h, num_frames, first, cut.shape[0],
+                                               cut.ctypes.data if cut.shape[0] else None, scene_start, fresh_begin,
+                                               fresh_end, _i64p(ins), _i64p(fresh), cap, C.byref(nr)))
+        return ins[:nr.value].copy(), fresh[:nr.value].copy()
+
+    def halo_extent(self) -> tuple[int, int]:
+        """nnvisr_halo_extent: (left, right) halo frames of a shard window."""
+        a, b = C.c_int32(), C.c_int32()
+        _check(_lib.nnvisr_halo_extent(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     # -- device work
     def bind_frames(self, frames: Sequence[Frame], base: int = 0):

@@ -117,6 +117,20 @@ class NcclHalo:
         self.comm.halo_exchange(s.total, s.L, s.R, window.data_ptr() if window is not None else None, fb,
                                 cut_window.data_ptr() if cut_window is not None else None, stream)
 
+    def scene_start(self, own_flags: np.ndarray, device, stream=None) -> int:
+        """The scene-start scan over the library's communicator: this rank's
+        last cut into a device int64 [world], nnvisr_cut_allgather on
+        `stream`, then nnvisr_scene_start_scan on the host."""
+        s = self.s
+        buf = torch.full((s.world,), -1, dtype=torch.int64, device=device)
+        buf[s.rank] = nv.last_cut(own_flags, s.begin)
+        if stream is not None:
+            stream.wait_stream(torch.cuda.current_stream(device))
+        self.comm.cut_allgather(buf.data_ptr(), stream)
+        if stream is not None:
+            stream.synchronize()
+        return scene_start(s, own_flags, buf.cpu().numpy())
+
     def close(self):
         if self.comm is not None:
             self.comm.destroy()
@@ -146,6 +160,44 @@ def plan_edges(h, s: Shard, window_flags: np.ndarray) -> list[np.ndarray]:
     i0, i1 = interior_range(s)
     return [h.plan_range(s.total, s.window_first, window_flags, a, b)[0] for a, b in ((s.begin, i0), (i1, s.end))
             if b > a]
+
+
+# ---- the paper's n > 1 grouping across shards (SURVEY.md §8(e) "Limitation")
+# A run's phase lo = s + k*n counts from its scene start s (§3.3
+# P:347-358), which may lie many shards to the left.  Each rank contributes
+# the last cut of its owned frames; the start of the scene containing its
+# first owned frame is the exclusive prefix maximum of those (or its own
+# first frame when that starts a scene).  The library's form is one in-place
+# ncclAllGather of one int64 per rank (nnvisr_cut_allgather, NcclHalo.
+# scene_start); gather_last_cuts runs the same exchange over torch.distributed
+# (what the gloo tests execute).
+
+def shard_for(h, total: int, world: int, rank: int) -> Shard:
+    """The shard of rank r with the halo this handle's plan reads
+    (nnvisr_halo_extent: L + n-1 frames back under the paper's grouping)."""
+    left, right = h.halo_extent()
+    return shard_of(total, world, rank, left, right)
+
+
+def gather_last_cuts(s: Shard, own_flags: np.ndarray, group=None) -> np.ndarray:
+    """Every rank's last cut (torch.distributed all_gather; -1 = none)."""
+    mine = torch.tensor([nv.last_cut(own_flags, s.begin)], dtype=torch.int64)
+    if s.world == 1:
+        return mine.numpy()
+    out = [torch.zeros(1, dtype=torch.int64) for _ in range(s.world)]
+    dist.all_gather(out, mine, group=group)
+    return torch.cat(out).numpy()
+
+
+def scene_start(s: Shard, own_flags: np.ndarray, last_cuts: np.ndarray) -> int:
+    """Start of the scene containing this rank's first owned frame."""
+    return nv.scene_start_scan(s.world, s.rank, last_cuts, s.begin, int(own_flags[0]) if s.owned else 0)
+
+
+def plan_shard(h, s: Shard, window_flags: np.ndarray, start: int) -> np.ndarray:
+    """Runs whose first fresh frame this rank owns (any grouping; the anchor
+    matters for the paper's n > 1 grouping only)."""
+    return h.plan_range_anchored(s.total, s.window_first, window_flags, start, s.begin, s.end)
 
 
 def cut_window_of(cut: np.ndarray, s: Shard) -> np.ndarray:

@@ -82,6 +82,10 @@ def test_comm_argument_checks():
     assert L.nnvisr_halo_exchange_all(None, 0, 10, 1, 1, None, 16, None, None) == 2
     assert L.nnvisr_halo_plan(10, 2, 0, 1, 1, None, None) == 2
     assert L.nnvisr_shard_of(10, 2, 0, 1, 1, None) == 2
+    assert L.nnvisr_cut_allgather(None, 4096, None) == 2  # the n > 1 scene-start scan
+    assert L.nnvisr_last_cut(None, 0, 3, None) == 2
+    assert L.nnvisr_scene_start_scan(2, 2, None, 0, 0, None) == 2
+    assert L.nnvisr_halo_extent(None, None, None) == 2
     with pytest.raises(ValueError):
         nv.halo_plan(5, 4, 1, 2, 2)  # a 1-frame shard is shorter than the halo
 

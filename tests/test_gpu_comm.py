@@ -69,3 +69,37 @@ def test_ncclhalo_world_one_via_torch_distributed():
         h.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_cut_allgather_world_one_and_anchored_plan():
+    """nnvisr_cut_allgather (one in-place ncclAllGather) at world 1, then
+    the scene-start scan and the anchored plan of the paper's n > 1
+    grouping (multi-rank: tests/test_shard_paper.py over gloo)."""
+    import numpy as np
+    from oracle import oracle as O
+    torch.cuda.set_device(0)
+    c = nv.Comm.init_rank(nv.comm_unique_id(), 1, 0)
+    try:
+        cut = np.zeros(50, np.uint8)
+        cut[[7, 30]] = 1
+        buf = torch.full((1,), -5, dtype=torch.int64, device="cuda")
+        buf[0] = nv.last_cut(cut, 0)
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        c.cut_allgather(buf.data_ptr(), st)
+        st.synchronize()
+        assert buf.item() == 30
+        with pytest.raises(nv.NnvisrError):
+            c.cut_allgather(None, st)
+        cfg = nv.Config(64, 64, input_count=4, output_count=3, n=3, left_context=0, flags=nv.EXTRA_FRAME)
+        with nv.open(cfg) as h:
+            s = sh.shard_for(h, 50, 1, 0)
+            halo = sh.NcclHalo.__new__(sh.NcclHalo)  # the library communicator above, rank 0 of 1
+            halo.s, halo.comm = s, c
+            start = halo.scene_start(cut[s.begin:s.end], "cuda", st)
+            assert start == 0
+            ins, fresh = sh.plan_shard(h, s, cut, start)
+            gins, gfresh = O.plan(cut, 3, 4, 0)
+            assert np.array_equal(ins, gins) and np.array_equal(fresh, gfresh)
+    finally:
+        c.destroy()
