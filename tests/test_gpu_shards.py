@@ -69,3 +69,46 @@ def test_shards_equal_single_gpu(name, world):
             got_o.append(o.data)
         assert torch.equal(torch.cat(got_t).view(torch.uint8), ref_t.view(torch.uint8))
         assert torch.equal(torch.cat(got_o), ref_o.data)
+
+
+@pytest.mark.parametrize("n,extra,world", [(3, 1, 3), (4, 0, 2), (2, 1, 4)])
+def test_paper_n_gt_1_shards_equal_single_gpu(n, extra, world):
+    """The paper's n > 1 grouping sharded (SURVEY.md §8(e) "Limitation"):
+    each emulated rank anchors its run phase with the last-cut scan
+    (nnvisr_last_cut / nnvisr_scene_start_scan -- the values
+    nnvisr_cut_allgather gathers), binds its window with the n-1 recycled
+    frames on the left (nnvisr_halo_extent), plans with
+    nnvisr_plan_range_anchored and converts; the concatenated tensors equal
+    the single-GPU run byte for byte."""
+    w = synth.WORKLOADS["c1"]
+    N = n + extra
+    cfg = nv.Config(w.cfg.width, w.cfg.height, w.cfg.family, w.cfg.bits, w.cfg.matrix, w.cfg.range,
+                    input_count=N, output_count=n, n=n, left_context=0, flags=nv.EXTRA_FRAME if extra else 0,
+                    dtype=w.cfg.dtype)
+    total = 41
+    clip = synth.generate_clip(w, device=DEV, frames=total)
+    cut = np.zeros(total, np.uint8)
+    cut[[3, 17]] = 1  # scenes spanning shard boundaries: later ranks' phase comes from far left
+    lay = w.layout()
+    with nv.open(cfg) as h:
+        per = int(np.prod(h.in_shape))
+        dt = torch.float16 if cfg.dtype == nv.F16 else torch.float32
+        runs, fresh_all = h.plan(cut)
+        ref_t = torch.empty((len(runs), per), dtype=dt, device=DEV)
+        h.bind_frames(clip.descriptors())
+        h.frames_to_tensor_batch(runs, ref_t.data_ptr(), per * ref_t.element_size())
+        torch.cuda.synchronize()
+        shards = [sh.shard_for(h, total, world, r) for r in range(world)]
+        lasts = [nv.last_cut(cut[s.begin:s.end], s.begin) for s in shards]
+        got = []
+        for s in shards:
+            start = sh.scene_start(s, cut[s.begin:s.end], lasts)
+            win = FrameBuffer(lay, s.window_count, device=DEV)
+            win.data.copy_(clip.data[s.window_first:s.window_first + s.window_count])
+            h.bind_frames(win.descriptors(), base=s.window_first)
+            ins, fresh = sh.plan_shard(h, s, cut[s.window_first:s.window_first + s.window_count], start)
+            t = torch.empty((len(ins), per), dtype=dt, device=DEV)
+            h.frames_to_tensor_batch(ins, t.data_ptr(), per * t.element_size())
+            torch.cuda.synchronize()
+            got.append(t)
+        assert torch.equal(torch.cat(got).view(torch.uint8), ref_t.view(torch.uint8))
