@@ -149,7 +149,75 @@ __global__ void readonly(const uint4 *__restrict__ in, long n, unsigned *sink)
     if (acc == 0x12345678u) *sink = acc;
 }
 
-int main()
+// 2 reads : 1 write as t2f moves it: inputs staged by TMA bulk copies into a
+// ring of S stages (completion on mbarriers, one elected thread issues), the
+// result written either by every thread with STG.128 (BULK = false, t2f's
+// code stores) or staged in shared memory and written by one thread with TMA
+// bulk stores (BULK = true).  Chunk = 256 threads x U vectors per input.
+__device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+template <bool BULK, int U = 2, int S = 3>
+__global__ void __launch_bounds__(256) r2w1_tma(const uint4 *__restrict__ in, uint4 *__restrict__ out, long m)
+{
+    extern __shared__ __align__(128) uint4 sm[];
+    __shared__ __align__(8) unsigned long long full[S];
+    constexpr int C = 256 * U;  // vectors per input chunk
+    uint4 *stage = sm;          // [S][2][C]
+    uint4 *ob = sm + S * 2 * C; // [2][C] (BULK)
+    const long nchunks = m / C;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < S; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[k])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](long c, int k) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[k])), "r"(2 * C * 16) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(stage + (k * 2) * C)),
+                     "l"(in + c * C), "r"(C * 16), "r"(su32(&full[k])) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(stage + (k * 2 + 1) * C)),
+                     "l"(in + m + c * C), "r"(C * 16), "r"(su32(&full[k])) : "memory");
+    };
+    long c0 = blockIdx.x;
+    const long G = gridDim.x;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < S; ++k)
+            if (c0 + k * G < nchunks) issue(c0 + k * G, k);
+    int k = 0;
+    unsigned ph = 0;
+    int ob_i = 0;
+    for (long c = c0; c < nchunks; c += G) {
+        asm volatile("{ .reg .pred P; W: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1; @!P bra W; }" ::"r"(su32(&full[k])), "r"(ph) : "memory");
+        const uint4 *x = stage + (k * 2) * C, *y = stage + (k * 2 + 1) * C;
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint4 a = x[u * 256 + threadIdx.x], b = y[u * 256 + threadIdx.x];
+            r[u] = make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+        }
+        __syncthreads();  // every thread has read stage k
+        if (threadIdx.x == 0 && c + S * G < nchunks) issue(c + S * G, k);
+        if (!BULK) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) out[c * C + u * 256 + threadIdx.x] = r[u];
+        } else {
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncthreads();
+            uint4 *o = ob + ob_i * C;
+#pragma unroll
+            for (int u = 0; u < U; ++u) o[u * 256 + threadIdx.x] = r[u];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + c * C), "r"(su32(o)), "r"(C * 16) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            ob_i ^= 1;
+        }
+        if (++k == S) { k = 0; ph ^= 1; }
+    }
+    if (BULK && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int main(int argc, char **argv)
 {
     const long bytes = 4l << 30;
     const long n = bytes / 16;
@@ -177,6 +245,25 @@ int main()
         }
         printf("{\"probe\": \"%s\", \"gbs\": %.1f}\n", name, moved / (best / 1000) / 1e9);
     };
+    if (argc > 1) {  // t2f-shaped 2R:1W probes only: hbm_probe t2f
+        auto tma = [&](auto kern, const char *name, int U, int S, int per_sm, bool bulk) {
+            const int smem = (S * 2 + (bulk ? 2 : 0)) * 256 * U * 16;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            run(name, [&] { kern<<<per_sm * 148, 256, smem>>>(a, b, n / 2); }, 1.5 * bytes);
+        };
+        run("2r_1w", [&] { r2w1<<<grid, block>>>(a, b, n / 2); }, 1.5 * bytes);
+        tma(r2w1_tma<false, 2, 3>, "2r_1w_tma_stg_U2_S3_x3", 2, 3, 3, false);
+        tma(r2w1_tma<true, 2, 3>, "2r_1w_tma_bulk_U2_S3_x3", 2, 3, 3, true);
+        tma(r2w1_tma<false, 4, 3>, "2r_1w_tma_stg_U4_S3_x2", 4, 3, 2, false);
+        tma(r2w1_tma<true, 4, 3>, "2r_1w_tma_bulk_U4_S3_x2", 4, 3, 2, true);
+        tma(r2w1_tma<false, 2, 4>, "2r_1w_tma_stg_U2_S4_x3", 2, 4, 3, false);
+        tma(r2w1_tma<true, 2, 4>, "2r_1w_tma_bulk_U2_S4_x3", 2, 4, 3, true);
+        tma(r2w1_tma<false, 1, 4>, "2r_1w_tma_stg_U1_S4_x6", 1, 4, 6, false);
+        tma(r2w1_tma<true, 1, 4>, "2r_1w_tma_bulk_U1_S4_x6", 1, 4, 6, true);
+        cudaError_t err = cudaGetLastError();
+        if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
+        return 0;
+    }
     run("read_only", [&] { readonly<<<grid, block>>>(a, n, sink); }, (double)bytes);
     run("write_only", [&] { mix<<<grid, block>>>(a, b, 0, 1, n); }, (double)bytes);
     run("copy_1r_1w", [&] { mix<<<grid, block>>>(a, b, n, 1, n); }, 2.0 * bytes);
