@@ -96,3 +96,43 @@ def test_ring_rejects_non_resident_and_bad_args():
         with pytest.raises(nv.NnvisrError):
             h.copy_slots(ring.buf.data_ptr(), 0, 1, 2)  # overlapping ranges
         torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_ring_full_size_sampled_vs_oracle(name):
+    """The bench's store mode at BASELINE.json's full frame sizes (1080p with
+    its 1088-row padding, 4K) through the strip kernel's full-size launch
+    shape: every window of three regions (two N-1-slot advances, a cut
+    inside a region) byte-identical to the materialised tuple, and two
+    sampled windows, before and after the advances, against the CPU oracle."""
+    w = synth.WORKLOADS[name]
+    F, K = 15, 5
+    clip = synth.generate_clip(w, device=DEV, frames=F)
+    cut = np.zeros(F, np.uint8)
+    cut[7] = 1
+    lay = w.layout()
+    with nv.open(w.cfg) as h:
+        h.bind_frames(clip.descriptors())
+        runs, _ = h.plan(cut)
+        per = int(np.prod(h.in_shape))
+        ring = StoreRing(h, 0, F, K, 2, advance="copy")
+        assert ring.regions == 3
+        sampled = {3, 11}  # a window of the first region and one served after an advance copy
+        seen = []
+        for c in range(ring.regions):
+            ring.fill(c)
+            torch.cuda.synchronize()
+            for r in ring.windows(runs, c):
+                a = int(runs[r][0])
+                t = torch.empty(per, dtype=torch.float16, device=DEV)
+                t.copy_(ring.buf.view(-1)[(ring.window_ptr(a) - ring.buf.data_ptr()) // 2:][:per])
+                m = torch.empty(per, dtype=torch.float16, device=DEV)
+                h.frames_to_tensor_batch(runs[r:r + 1], m.data_ptr(), per * 2)
+                torch.cuda.synchronize()
+                assert torch.equal(t.view(torch.int16), m.view(torch.int16)), (name, c, r)
+                seen.append(r)
+                if r in sampled:
+                    ref = oracle_f2t(lay, [clip.host_planes(int(i)) for i in runs[r]], h.in_shape[2], h.in_shape[3],
+                                     w.cfg)
+                    assert_tensor_close(t.view(h.in_shape).cpu().numpy(), ref, f"{name} ring window {r}")
+        assert sampled <= set(seen)
