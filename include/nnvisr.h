@@ -203,6 +203,28 @@ nnvisr_status nnvisr_plan_range(const nnvisr_handle *h, int64_t num_frames, int6
                                 int64_t fresh_end, int64_t *run_inputs, int64_t *run_fresh,
                                 int64_t cap, int64_t *num_runs);
 
+/* Scene-padded store layout for store mode S (§3.3
+ * each frame converted once into a frame-major store whose
+ * contiguous slot runs are the tuples -- extended to the tuples with
+ * duplicated inputs at scene edges, P:352-358 / reading A8): the position
+ * sequence Q concatenates, for each scene [s, e) met by the owned fresh
+ * frames, L copies of s, s .. e-1 and R = N-1-L copies of e-1 (only the
+ * entries the owned tuples read), so that EVERY tuple k in [fresh_begin,
+ * fresh_end) -- at a scene edge too -- is the contiguous window Q[w_k ..
+ * w_k+N-1] and nothing is materialised.  positions: host int64 [cap]
+ * receives Q (absolute frame indices; convert with nnvisr_frames_to_slots,
+ * which reads a repeated frame once); *num_positions = |Q| (NNVISR_ERR_CAPACITY
+ * if cap is short, *num_positions then holds the size needed, at most
+ * (fresh_end - fresh_begin) + scenes * (N-1)); window_start: host int64
+ * [fresh_end - fresh_begin], w_k at [k - fresh_begin].  The window [first,
+ * first+count) and its flags cut (host [count], as nnvisr_plan_range) must
+ * cover [max(0, fresh_begin-L), min(num_frames, fresh_end+R)).  One fresh
+ * frame per tuple (n = 1: sliding windows, or the paper's grouping with
+ * n = 1); else NNVISR_ERR_UNSUPPORTED. */
+nnvisr_status nnvisr_plan_store(const nnvisr_handle *h, int64_t num_frames, int64_t first, int64_t count,
+                                const uint8_t *cut, int64_t fresh_begin, int64_t fresh_end, int64_t *positions,
+                                int64_t cap, int64_t *num_positions, int64_t *window_start);
+
 /* Halo a shard's window needs for this handle's plan: a run reads frames
  * base-L .. base-L+N-1 (clamped to its scene) with base <= its first fresh
  * frame lo, and under the paper's grouping with n > 1 the last run of a

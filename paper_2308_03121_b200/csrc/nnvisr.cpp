@@ -467,6 +467,62 @@ nnvisr_status nnvisr_plan_range(const nnvisr_handle *h, int64_t num_frames, int6
     return NNVISR_OK;
 }
 
+nnvisr_status nnvisr_plan_store(const nnvisr_handle *h, int64_t num_frames, int64_t first, int64_t count,
+                                const uint8_t *cut, int64_t fresh_begin, int64_t fresh_end, int64_t *positions,
+                                int64_t cap, int64_t *num_positions, int64_t *window_start)
+{
+    NvtxRange nvtx_("nnvisr_plan_store");
+    g_error.clear();
+    if (!h || !num_positions) return fail(NNVISR_ERR_INVALID_ARG, "null argument");
+    if (h->n != 1) return fail(NNVISR_ERR_UNSUPPORTED, "the padded store needs one fresh frame per tuple (n = 1)");
+    if (num_frames < 0 || first < 0 || count < 0 || first + count > num_frames)
+        return fail(NNVISR_ERR_INVALID_ARG, "window [%lld, %lld) outside the clip of %lld frames",
+                    (long long)first, (long long)(first + count), (long long)num_frames);
+    if (fresh_begin < 0 || fresh_end > num_frames || fresh_begin > fresh_end)
+        return fail(NNVISR_ERR_INVALID_ARG, "bad fresh range [%lld, %lld)", (long long)fresh_begin,
+                    (long long)fresh_end);
+    if (count > 0 && !cut) return fail(NNVISR_ERR_INVALID_ARG, "null cut array");
+    if (fresh_end > fresh_begin && !window_start) return fail(NNVISR_ERR_INVALID_ARG, "null window_start");
+    if (cap > 0 && !positions) return fail(NNVISR_ERR_INVALID_ARG, "null positions");
+    const int64_t L = h->L, R = h->N - 1 - h->L;
+    const int64_t need_lo = std::max<int64_t>(0, fresh_begin - L);
+    const int64_t need_hi = std::min<int64_t>(num_frames, fresh_end + R);
+    const int64_t end = first + count;
+    if (fresh_end > fresh_begin && (first > need_lo || end < need_hi))
+        return fail(NNVISR_ERR_INVALID_ARG, "window [%lld, %lld) does not cover [%lld, %lld)", (long long)first,
+                    (long long)end, (long long)need_lo, (long long)need_hi);
+    auto cut_at = [&](int64_t k) { return k > 0 && cut[k - first] != 0; };
+    // Scenes as seen from the window (bounds beyond it never bind: every
+    // clamp argument of an owned tuple lies inside [need_lo, need_hi)).  A
+    // scene [s, e) padded with L copies of s and R copies of e-1 holds, at
+    // padded index i, frame clamp(s + i - L, s, e - 1), so the window at
+    // padded index k - s is tuple k's inputs clamp(k - L + j, s, e - 1)
+    // (reading A8 at scene edges).  Only the padded indices the owned tuples
+    // read are emitted.
+    int64_t P = 0;
+    int64_t k = fresh_begin;
+    int64_t s = first;
+    for (int64_t q = first + 1; q <= k && q < end; ++q)
+        if (cut_at(q)) s = q;
+    while (k < fresh_end) {
+        if (k > fresh_begin && cut_at(k)) s = k;
+        int64_t e = k + 1;
+        while (e < end && !cut_at(e)) ++e;
+        const int64_t b = std::min(e, fresh_end);  // owned fresh frames of this scene: [k, b)
+        const int64_t p0 = P;
+        for (int64_t i = k - s; i < b - s + h->N - 1; ++i) {
+            if (P < cap) positions[P] = std::min(std::max(s + i - L, s), e - 1);
+            ++P;
+        }
+        for (int64_t kk = k; kk < b; ++kk) window_start[kk - fresh_begin] = p0 + (kk - k);
+        k = b;
+    }
+    *num_positions = P;
+    if (P > cap) return fail(NNVISR_ERR_CAPACITY, "store layout needs %lld positions, capacity %lld", (long long)P,
+                             (long long)cap);
+    return NNVISR_OK;
+}
+
 nnvisr_status nnvisr_halo_extent(const nnvisr_handle *h, int32_t *left, int32_t *right)
 {
     g_error.clear();

@@ -70,6 +70,7 @@ def _load():
         "nnvisr_plan_range": (st, [H, i64, i64, i64, C.c_void_p, i64, i64, i64p, i64p, i64, i64p]),
         "nnvisr_plan_range_anchored": (st, [H, i64, i64, i64, C.c_void_p, i64, i64, i64, i64p, i64p, i64, i64p]),
         "nnvisr_halo_extent": (st, [H, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+        "nnvisr_plan_store": (st, [H, i64, i64, i64, C.c_void_p, i64, i64, i64p, i64, i64p, i64p]),
         "nnvisr_bind_frames": (st, [H, i64, C.POINTER(Frame), i64]),
         "nnvisr_frames_to_tensor": (st, [H, C.POINTER(Frame), C.c_void_p, C.c_void_p]),
         "nnvisr_frames_to_tensor_batch": (st, [H, i64p, i64, C.c_void_p, i64, C.c_void_p]),
@@ -134,7 +135,7 @@ EXPORTED = ("nnvisr_open", "nnvisr_close", "nnvisr_last_error", "nnvisr_version"
             "nnvisr_halo_plan", "nnvisr_comm_unique_id", "nnvisr_comm_init_rank", "nnvisr_comm_init_all",
             "nnvisr_comm_info", "nnvisr_comm_check", "nnvisr_halo_exchange", "nnvisr_halo_exchange_all",
             "nnvisr_comm_destroy", "nnvisr_nccl_version", "nnvisr_plan_range_anchored", "nnvisr_halo_extent",
-            "nnvisr_cut_allgather", "nnvisr_last_cut", "nnvisr_scene_start_scan")
+            "nnvisr_cut_allgather", "nnvisr_last_cut", "nnvisr_scene_start_scan", "nnvisr_plan_store")
 
 
 def lib():
@@ -405,6 +406,25 @@ class Handle:
                                                cut.ctypes.data if cut.shape[0] else None, scene_start, fresh_begin,
                                                fresh_end, _i64p(ins), _i64p(fresh), cap, C.byref(nr)))
         return ins[:nr.value].copy(), fresh[:nr.value].copy()
+
+    def plan_store(self, num_frames, first, cut_window, fresh_begin, fresh_end):
+        """nnvisr_plan_store: (positions Q, window_start w) of the scene-padded
+        store -- tuple k is the window Q[w[k - fresh_begin] ...][:N]."""
+        cut = np.ascontiguousarray(np.asarray(cut_window, dtype=np.uint8))
+        nf = fresh_end - fresh_begin
+        ws = np.zeros(max(nf, 1), np.int64)
+        cap = nf + 16 * (self.N - 1) + 16
+        n = C.c_int64()
+        for _ in range(2):  # the size needed comes back with NNVISR_ERR_CAPACITY
+            pos = np.zeros(max(cap, 1), np.int64)
+            st = _lib.nnvisr_plan_store(self._h, num_frames, first, cut.shape[0],
+                                        cut.ctypes.data if cut.shape[0] else None, fresh_begin, fresh_end,
+                                        _i64p(pos), cap, C.byref(n), _i64p(ws))
+            if st != 7 or n.value <= cap:
+                break
+            cap = n.value
+        _check(st)
+        return pos[:n.value].copy(), ws[:nf].copy()
 
     def halo_extent(self) -> tuple[int, int]:
         """nnvisr_halo_extent: (left, right) halo frames of a shard window."""

@@ -103,3 +103,44 @@ class StoreRing:
             if g0 <= a < g0 + self.K and np.all(np.diff(ins) == 1):
                 out.append(r)
         return out
+
+
+class PaddedStoreRing(StoreRing):
+    """Store mode S over the scene-padded layout (nnvisr_plan_store): the ring
+    holds the position sequence Q -- each scene's frames with L copies of its
+    first and N-1-L copies of its last frame -- so EVERY tuple, the ones with
+    duplicated inputs at scene edges too, is a contiguous window and nothing is
+    materialised.  Regions of K new positions + N - 1 carried by one copy, as
+    StoreRing (whose geometry runs over positions here); a region fill converts
+    its new positions with nnvisr_frames_to_slots (a repeated frame is read
+    and converted once, written to each of its slots)."""
+
+    def __init__(self, h, num_frames: int, first: int, cut_window, fresh_begin: int, fresh_end: int, K: int,
+                 R: int = 2, advance: str = "copy", device="cuda"):
+        positions, window_start = h.plan_store(num_frames, first, cut_window, fresh_begin, fresh_end)
+        super().__init__(h, 0, len(positions), K, R, advance, device)
+        self.positions, self.window_start = positions, window_start
+        self.fresh_begin = fresh_begin
+        self.tuple_region = window_start // K
+
+    def fill(self, c: int, stream=None) -> dict:
+        p0, p1 = self.region_frames(c)
+        n = p1 - p0
+        carry = 0
+        if self.advance == "copy" and c > 0 and c - 1 == self._filled and self.N > 1:
+            carry = min(self.N - 1, n)
+            src = ((c - 1) % self.R) * self.span + self.K
+            self.h.copy_slots(self.buf.data_ptr(), src, (c % self.R) * self.span, carry, stream)
+        new = self.positions[p0 + carry:p1]
+        if len(new):
+            self.h.frames_to_slots(new, self.slot_ptr(c, carry), stream)
+        self._filled = c
+        return {"converted": int(len(new)), "distinct_frames": int(len(np.unique(new))), "copied_slots": carry}
+
+    def tuples(self, c: int) -> np.ndarray:
+        """Tuples (index k - fresh_begin) served by region c."""
+        return np.flatnonzero(self.tuple_region == c)
+
+    def tuple_ptr(self, t: int) -> int:
+        """[1, 3N, Hp, Wp] input tensor of tuple t (= fresh frame fresh_begin + t)."""
+        return self.window_ptr(int(self.window_start[t]))

@@ -13,7 +13,7 @@ import torch
 from paper_2308_03121_b200 import nnvisr as nv
 from paper_2308_03121_b200 import synth
 from paper_2308_03121_b200.frames import FrameBuffer, FrameLayout
-from paper_2308_03121_b200.store import StoreRing
+from paper_2308_03121_b200.store import PaddedStoreRing, StoreRing
 
 from .helpers import assert_tensor_close, oracle_f2t
 
@@ -136,3 +136,76 @@ def test_ring_full_size_sampled_vs_oracle(name):
                                      w.cfg)
                     assert_tensor_close(t.view(h.in_shape).cpu().numpy(), ref, f"{name} ring window {r}")
         assert sampled <= set(seen)
+
+
+def _padded_windows_match(h, ring, runs, per, dt, oracle_of=None, sampled=()):
+    """Fill every region; every tuple's window == its materialised tensor
+    (bit for bit); sampled tuples also against the oracle."""
+    seen = []
+    esz = torch.tensor([], dtype=dt).element_size()
+    for c in range(ring.regions):
+        ring.fill(c)
+        torch.cuda.synchronize()
+        for t in ring.tuples(c):
+            t = int(t)
+            k = ring.fresh_begin + t
+            win = torch.empty(per, dtype=dt, device=DEV)
+            win.copy_(ring.buf.view(-1)[(ring.tuple_ptr(t) - ring.buf.data_ptr()) // esz:][:per])
+            mat = torch.empty(per, dtype=dt, device=DEV)
+            h.frames_to_tensor_batch(runs[k:k + 1], mat.data_ptr(), per * esz)
+            torch.cuda.synchronize()
+            iv = torch.int16 if esz == 2 else torch.int32
+            assert torch.equal(win.view(iv), mat.view(iv)), (c, k)
+            if oracle_of is not None and (not sampled or k in sampled):
+                assert_tensor_close(win.view(h.in_shape).cpu().numpy(), oracle_of(runs[k]), f"padded window {k}")
+            seen.append(k)
+    return seen
+
+
+@pytest.mark.parametrize("dtype", [nv.F16, nv.F32])
+@pytest.mark.parametrize("N,K", [(5, 4), (4, 3), (3, 1), (2, 2)])
+def test_padded_ring_every_tuple_is_a_window(dtype, N, K):
+    """The scene-padded store (nnvisr_plan_store): EVERY tuple -- the ones
+    with duplicated inputs at cuts, a one-frame scene and the clip edges too
+    -- is a window of the ring, equal to the materialised tuple and to the
+    oracle."""
+    W, H, F = 96, 62, 23
+    lay = FrameLayout(W, H, nv.YUV420, 10)
+    cfg = nv.Config(W, H, nv.YUV420, 10, nv.BT709, nv.LIMITED, input_count=N, output_count=1, n=1,
+                    left_context=-1, flags=0, align=16, dtype=dtype)
+    buf, host = _clip(lay, F, 5100 + N)
+    cut = np.zeros(F, np.uint8)
+    cut[[9, 10, 17]] = 1
+    with nv.open(cfg) as h:
+        h.bind_frames(buf.descriptors())
+        runs, _ = h.plan(cut)
+        per = int(np.prod(h.in_shape))
+        ring = PaddedStoreRing(h, F, 0, cut, 0, F, K, 2)
+        dt = torch.float16 if dtype == nv.F16 else torch.float32
+        oracle_of = lambda ins: oracle_f2t(lay, [host[int(i)] for i in ins], h.in_shape[2], h.in_shape[3], cfg)
+        seen = _padded_windows_match(h, ring, runs, per, dt, oracle_of)
+        assert sorted(seen) == list(range(F))
+
+
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_padded_ring_full_size(name):
+    """The padded store at the full c2 / c5 frame sizes: every tuple of a
+    clip with two cuts (one of them two frames apart) a window of the ring,
+    byte-identical to the materialised tuple; a scene-edge tuple (duplicated
+    inputs) and an interior one against the oracle."""
+    w = synth.WORKLOADS[name]
+    F, K = 16, 5
+    clip = synth.generate_clip(w, device=DEV, frames=F)
+    cut = np.zeros(F, np.uint8)
+    cut[[6, 8]] = 1
+    lay = w.layout()
+    with nv.open(w.cfg) as h:
+        h.bind_frames(clip.descriptors())
+        runs, _ = h.plan(cut)
+        per = int(np.prod(h.in_shape))
+        ring = PaddedStoreRing(h, F, 0, cut, 0, F, K, 2)
+        oracle_of = lambda ins: oracle_f2t(lay, [clip.host_planes(int(i)) for i in ins], h.in_shape[2],
+                                           h.in_shape[3], w.cfg)
+        assert not np.all(np.diff(runs[7]) == 1)  # tuple 7 sits in the two-frame scene: duplicated inputs
+        seen = _padded_windows_match(h, ring, runs, per, torch.float16, oracle_of, sampled=(7, 12))
+        assert sorted(seen) == list(range(F))
