@@ -66,6 +66,10 @@ def parse(argv=None):
                    help="skip the second f2t mode of the main workload (reported under per_mode)")
     p.add_argument("--store-k", type=int, default=0, help="store ring: new frames per region (0 = auto)")
     p.add_argument("--store-regions", type=int, default=2, help="store ring: regions")
+    p.add_argument("--store-layout", default="padded", choices=["padded", "frames"],
+                   help="store ring layout: padded (nnvisr_plan_store: every scene padded with copies of its edge "
+                        "frames, so every tuple -- scene edges included -- is a window) or frames (one slot per "
+                        "frame; tuples with duplicated inputs materialised)")
     p.add_argument("--store-advance", default="copy", choices=["copy", "convert"],
                    help="store ring advance: copy the last N-1 slots (the paper's 6 -> 5) or re-convert them")
     p.add_argument("--batch", type=int, default=8, help="lanes per batch for --f2t-mode batch")
@@ -390,7 +394,7 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
     from paper_2308_03121_b200 import shard as sh
     from paper_2308_03121_b200 import synth
     from paper_2308_03121_b200.frames import FrameBuffer
-    from paper_2308_03121_b200.store import StoreRing
+    from paper_2308_03121_b200.store import PaddedStoreRing, StoreRing
 
     world, rank, dev = ctx.world, ctx.rank, ctx.dev
     if ctx.emu:  # tests only: this process plays rank r of W (shard geometry and the N > 1 code path)
@@ -470,7 +474,13 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
         # frames: K = 40 / 80 / 160 / 320 -> 16.75k / 17.08k / 17.10k / 17.13k
         # frames/s, f2t 5.48 / 5.63 / 5.53 / 5.50 TB/s; profiles/r02/storek)
         K = args.store_k or max(1, min(256, int(6e9 // (frame_payload + slot_bytes))))
-        ring = StoreRing(h, s.window_first, s.window_count, K, args.store_regions, args.store_advance, device=dev)
+        if args.store_layout == "padded":
+            ring_flags = [cut_all[s.window_first:s.window_first + s.window_count].copy()]
+            ring = PaddedStoreRing(h, total, s.window_first, ring_flags[0], s.begin, s.end, K, args.store_regions,
+                                   args.store_advance, device=dev)
+        else:
+            ring = StoreRing(h, s.window_first, s.window_count, K, args.store_regions, args.store_advance,
+                             device=dev)
     if mode == "batch":
         # Fig. 1 batches (§3.3): each batch's slots (b*n+1 shared, or
         # b*N plain) in its own region of a chunk store; a launch converts the
@@ -548,6 +558,26 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
             else:
                 timed("f2t", record, len(sel), nbytes,
                       lambda sel=sel: h.frames_to_tensor_batch(sel, tens_in.data_ptr(), in_elems * esz, stream))
+
+    def f2t_store_padded(runs, record, flags):
+        # the scene-padded layout: every tuple is a window of some region
+        # (nnvisr_plan_store); a region fill converts its new positions, a
+        # frame repeated at a scene edge read once (nnvisr_frames_to_slots)
+        if not np.array_equal(flags, ring_flags[0]):
+            ring.replan(flags)
+            ring_flags[0] = flags.copy()
+        served = np.bincount(ring.tuple_region, minlength=ring.regions)
+        for c in range(ring.regions):
+            p0, p1 = ring.region_frames(c)
+            carry = min(N - 1, p1 - p0) if (ring.advance == "copy" and c > 0) else 0
+            if carry:
+                timed("advance", record, 0, 2 * carry * slot_bytes,
+                      lambda c=c, carry=carry: h.copy_slots(ring.buf.data_ptr(), ((c - 1) % ring.R) * ring.span +
+                                                            ring.K, (c % ring.R) * ring.span, carry, stream))
+            new = ring.positions[p0 + carry:p1]
+            timed("f2t", record, int(served[c]), len(np.unique(new)) * frame_payload + len(new) * slot_bytes,
+                  lambda new=new, c=c, carry=carry: h.frames_to_slots(new, ring.slot_ptr(c, carry), stream))
+            ring._filled = c
 
     def f2t_store(runs, record):
         # each window frame converted once into the ring's current region;
@@ -656,7 +686,9 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
                 cut_win.copy_(cut_d)
         flags = flags_now()
         runs = plan_local(flags)[0] if planned is None else planned
-        if mode == "store":
+        if mode == "store" and args.store_layout == "padded":
+            f2t_store_padded(runs, record, flags)
+        elif mode == "store":
             f2t_store(runs, record)
         elif mode == "batch":
             f2t_batch(record)
@@ -806,7 +838,10 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
                    "tensor_dtype": "f16" if cfg.dtype == nv.F16 else "f32",
                    "tuples_per_launch": {"f2t": fchunk, "t2f": tchunk}, "f2t_mode": mode,
                    "store_ring": ({"new_frames_per_region": ring.K, "regions": ring.R, "slots_per_region": ring.span,
-                                   "advance": ring.advance, "ring_gb": ring.buf.numel() * esz / 1e9}
+                                   "advance": ring.advance, "ring_gb": ring.buf.numel() * esz / 1e9,
+                                   "layout": args.store_layout,
+                                   "positions": int(ring.count), "tuples_materialised": (
+                                       0 if args.store_layout == "padded" else None)}
                                   if ring else None),
                    "tensors": ("YUV-native: luma %s + chroma %s per tuple" % (list(in_shape), list(h.in_chroma_shape))
                                if yuv else "RGB"),

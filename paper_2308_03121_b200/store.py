@@ -119,9 +119,23 @@ class PaddedStoreRing(StoreRing):
                  R: int = 2, advance: str = "copy", device="cuda"):
         positions, window_start = h.plan_store(num_frames, first, cut_window, fresh_begin, fresh_end)
         super().__init__(h, 0, len(positions), K, R, advance, device)
+        self.num_frames, self.window_first = num_frames, first
+        self.fresh_begin, self.fresh_end = fresh_begin, fresh_end
+        self._set(positions, window_start)
+
+    def _set(self, positions, window_start):
         self.positions, self.window_start = positions, window_start
-        self.fresh_begin = fresh_begin
-        self.tuple_region = window_start // K
+        self.count = len(positions)
+        self.regions = 0 if self.count < self.N else (self.count - self.N) // self.K + 1
+        self.tuple_region = window_start // self.K
+        self._filled = -1
+
+    def replan(self, cut_window):
+        """New flags (scene detection, a halo exchange): re-plan the layout
+        over the same ring buffer (host only; the ring is refilled from
+        region 0)."""
+        self._set(*self.h.plan_store(self.num_frames, self.window_first, cut_window, self.fresh_begin,
+                                     self.fresh_end))
 
     def fill(self, c: int, stream=None) -> dict:
         p0, p1 = self.region_frames(c)
