@@ -1,5 +1,6 @@
 """Seeded random configurations through the C ABI against the oracle (and,
-without interpolation, store mode byte-identical to the materialised tuples; for
+without interpolation, store mode (one slot per frame, and the scene-padded
+layout where every tuple is a window) byte-identical to the materialised tuples; for
 a third of the seeds, the host-buffer calls byte-identical to the device calls;
 scene detection with exact SADs; for interpolation, the Fig. 1 batch store and the
 emission schedule; for sliding windows, 2-4 emulated frame-range shards): clip
@@ -125,6 +126,16 @@ def _check(p):
                     nin = len(run)  # frames per tuple (in_shape[1] is 3 x that)
                     win = st[run[0]:run[0] + nin].reshape(-1)
                     assert torch.equal(win.view(torch.uint8), t[r, :nin * slot].view(torch.uint8)), (p, r)
+            # the scene-padded store layout (nnvisr_plan_store, the bench's
+            # default): EVERY run, scene edges included, is a window of it
+            pos, ws = h.plan_store(F, 0, cut, 0, F)
+            sp = torch.full((len(pos), slot), float("nan"), dtype=tdt, device=DEV)
+            h.frames_to_slots(pos, sp.data_ptr())
+            torch.cuda.synchronize()
+            for r, run in enumerate(runs):
+                nin = len(run)
+                win = sp[ws[r]:ws[r] + nin].reshape(-1)
+                assert torch.equal(win.view(torch.uint8), t[r, :nin * slot].view(torch.uint8)), (p, "padded", r)
         if not p["yuv"] and p["seed"] % 3 == 0:
             # the host-buffer calls (staging, coalesced copies where the host
             # layout allows) give the same bytes as the device calls
