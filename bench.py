@@ -65,7 +65,8 @@ def parse(argv=None):
     p.add_argument("--no-compare-modes", action="store_true",
                    help="skip the second f2t mode of the main workload (reported under per_mode)")
     p.add_argument("--store-k", type=int, default=0, help="store ring: new frames per region (0 = auto)")
-    p.add_argument("--store-regions", type=int, default=2, help="store ring: regions")
+    p.add_argument("--store-regions", type=int, default=3,
+                   help="store ring: regions (padded layout: back to back, an advance copy only at each wrap)")
     p.add_argument("--store-layout", default="padded", choices=["padded", "frames"],
                    help="store ring layout: padded (nnvisr_plan_store: every scene padded with copies of its edge "
                         "frames, so every tuple -- scene edges included -- is a window) or frames (one slot per "
@@ -566,14 +567,16 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
         if not np.array_equal(flags, ring_flags[0]):
             ring.replan(flags)
             ring_flags[0] = flags.copy()
+        # Regions lie back to back: the N-1 carried positions are shared with
+        # the previous region, copied only where the ring wraps
         served = np.bincount(ring.tuple_region, minlength=ring.regions)
         for c in range(ring.regions):
             p0, p1 = ring.region_frames(c)
-            carry = min(N - 1, p1 - p0) if (ring.advance == "copy" and c > 0) else 0
-            if carry:
+            ring._filled = c - 1  # regions are filled in order within a step
+            carry, copy = ring.advance_plan(c)
+            if copy:
                 timed("advance", record, 0, 2 * carry * slot_bytes,
-                      lambda c=c, carry=carry: h.copy_slots(ring.buf.data_ptr(), ((c - 1) % ring.R) * ring.span +
-                                                            ring.K, (c % ring.R) * ring.span, carry, stream))
+                      lambda carry=carry: h.copy_slots(ring.buf.data_ptr(), ring.R * ring.K, 0, carry, stream))
             new = ring.positions[p0 + carry:p1]
             timed("f2t", record, int(served[c]), len(np.unique(new)) * frame_payload + len(new) * slot_bytes,
                   lambda new=new, c=c, carry=carry: h.frames_to_slots(new, ring.slot_ptr(c, carry), stream))

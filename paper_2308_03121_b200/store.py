@@ -110,13 +110,24 @@ class PaddedStoreRing(StoreRing):
     holds the position sequence Q -- each scene's frames with L copies of its
     first and N-1-L copies of its last frame -- so EVERY tuple, the ones with
     duplicated inputs at scene edges too, is a contiguous window and nothing is
-    materialised.  Regions of K new positions + N - 1 carried by one copy, as
-    StoreRing (whose geometry runs over positions here); a region fill converts
-    its new positions with nnvisr_frames_to_slots (a repeated frame is read
-    and converted once, written to each of its slots)."""
+    materialised.  A region fill converts its new positions with
+    nnvisr_frames_to_slots (a repeated frame is read and converted once,
+    written to each of its slots).
+
+    Regions lie back to back in a ring of R*K + N - 1 slots: region c
+    (j = c mod R) occupies slots [jK, jK + K + N - 1), so its first N - 1
+    positions -- the last N - 1 of region c-1 -- are already in place when
+    the regions are adjacent, and the paper's advance copy ("only the last
+    frame need to be copied to the first location of the next batch",
+    PAPER.md P:380-382) is needed only where the ring wraps (j = 0): one
+    (N-1)-slot copy per R regions instead of one per region.  Filling region
+    c overwrites the first N - 1 slots of the region R - 1 before it, so R - 1
+    regions stay whole (R = 2: the region just filled)."""
 
     def __init__(self, h, num_frames: int, first: int, cut_window, fresh_begin: int, fresh_end: int, K: int,
                  R: int = 2, advance: str = "copy", device="cuda"):
+        if R < 2:
+            raise ValueError("the padded ring needs R >= 2 regions")
         positions, window_start = h.plan_store(num_frames, first, cut_window, fresh_begin, fresh_end)
         super().__init__(h, 0, len(positions), K, R, advance, device)
         self.num_frames, self.window_first = num_frames, first
@@ -137,19 +148,39 @@ class PaddedStoreRing(StoreRing):
         self._set(*self.h.plan_store(self.num_frames, self.window_first, cut_window, self.fresh_begin,
                                      self.fresh_end))
 
+    # ---------------------------------------------------------- geometry
+    def slot_ptr(self, c: int, k: int = 0) -> int:
+        return self.buf.data_ptr() + ((c % self.R) * self.K + k) * self.slot_bytes
+
+    def window_ptr(self, a: int) -> int:
+        c = self.region_of(a)
+        if not (self._filled - self.R + 2 <= c <= self._filled):
+            raise RuntimeError(f"region {c} is not whole (last filled {self._filled}, ring of {self.R})")
+        return self.slot_ptr(c, a - c * self.K)
+
+    def advance_plan(self, c: int) -> tuple[int, bool]:
+        """(positions of region c already in place or copied, copy needed) for
+        a fill right after region c-1: the N-1 carried positions are shared
+        with region c-1 unless region c starts the ring (wrap: one copy)."""
+        p0, p1 = self.region_frames(c)
+        if c == 0 or c - 1 != self._filled or self.N == 1:
+            return 0, False
+        carry = min(self.N - 1, p1 - p0)
+        if self.advance != "copy":  # re-convert the carried positions
+            return 0, False
+        return carry, c % self.R == 0
+
     def fill(self, c: int, stream=None) -> dict:
         p0, p1 = self.region_frames(c)
-        n = p1 - p0
-        carry = 0
-        if self.advance == "copy" and c > 0 and c - 1 == self._filled and self.N > 1:
-            carry = min(self.N - 1, n)
-            src = ((c - 1) % self.R) * self.span + self.K
-            self.h.copy_slots(self.buf.data_ptr(), src, (c % self.R) * self.span, carry, stream)
+        carry, copy = self.advance_plan(c)
+        if copy:  # ring wrap: the previous region's last N-1 slots to the ring's head
+            self.h.copy_slots(self.buf.data_ptr(), self.R * self.K, 0, carry, stream)
         new = self.positions[p0 + carry:p1]
         if len(new):
             self.h.frames_to_slots(new, self.slot_ptr(c, carry), stream)
         self._filled = c
-        return {"converted": int(len(new)), "distinct_frames": int(len(np.unique(new))), "copied_slots": carry}
+        return {"converted": int(len(new)), "distinct_frames": int(len(np.unique(new))),
+                "copied_slots": carry if copy else 0}
 
     def tuples(self, c: int) -> np.ndarray:
         """Tuples (index k - fresh_begin) served by region c."""

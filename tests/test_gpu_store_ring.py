@@ -163,8 +163,8 @@ def _padded_windows_match(h, ring, runs, per, dt, oracle_of=None, sampled=()):
 
 
 @pytest.mark.parametrize("dtype", [nv.F16, nv.F32])
-@pytest.mark.parametrize("N,K", [(5, 4), (4, 3), (3, 1), (2, 2)])
-def test_padded_ring_every_tuple_is_a_window(dtype, N, K):
+@pytest.mark.parametrize("N,K,R", [(5, 4, 2), (4, 3, 3), (3, 1, 2), (2, 2, 4)])
+def test_padded_ring_every_tuple_is_a_window(dtype, N, K, R):
     """The scene-padded store (nnvisr_plan_store): EVERY tuple -- the ones
     with duplicated inputs at cuts, a one-frame scene and the clip edges too
     -- is a window of the ring, equal to the materialised tuple and to the
@@ -180,11 +180,23 @@ def test_padded_ring_every_tuple_is_a_window(dtype, N, K):
         h.bind_frames(buf.descriptors())
         runs, _ = h.plan(cut)
         per = int(np.prod(h.in_shape))
-        ring = PaddedStoreRing(h, F, 0, cut, 0, F, K, 2)
+        ring = PaddedStoreRing(h, F, 0, cut, 0, F, K, R)
         dt = torch.float16 if dtype == nv.F16 else torch.float32
         oracle_of = lambda ins: oracle_f2t(lay, [host[int(i)] for i in ins], h.in_shape[2], h.in_shape[3], cfg)
         seen = _padded_windows_match(h, ring, runs, per, dt, oracle_of)
         assert sorted(seen) == list(range(F))
+        # regions back to back: copies only at the ring wraps; R - 1 regions stay whole
+        ring2 = PaddedStoreRing(h, F, 0, cut, 0, F, K, R)
+        copies = [ring2.fill(c)["copied_slots"] > 0 for c in range(ring2.regions)]
+        assert copies == [c > 0 and c % R == 0 and N > 1 for c in range(ring2.regions)]
+        if ring2.regions > R:
+            with pytest.raises(RuntimeError):
+                ring2.window_ptr(int((ring2.regions - R) * K))  # overwritten by the last fill
+        # out of order (not right after the previous region): the whole region is converted
+        last = ring2.regions - 1
+        if last >= 2:
+            info = ring2.fill(last - 2)
+            assert info["copied_slots"] == 0 and info["converted"] == len(ring2.positions[slice(*ring2.region_frames(last - 2))])
 
 
 @pytest.mark.parametrize("name", ["c2", "c5"])
