@@ -61,7 +61,8 @@ def parse(argv=None):
                    help="materialize every tuple; store: frame-major store ring (sliding windows: the paper's "
                         "Fig. 1 principle at batch 1, each frame converted once, every tuple a contiguous window); "
                         "batch: the paper's Fig. 1 batched shared store (paper grouping, --batch lanes); auto = "
-                        "store for sliding-window workloads (c2, c3, c5), materialize otherwise")
+                        "store (scene-padded layout) for the one-fresh-frame workloads c2-c5, materialize for the "
+                        "tiny c1 clip, YUV-native tensors and --graph")
     p.add_argument("--no-compare-modes", action="store_true",
                    help="skip the second f2t mode of the main workload (reported under per_mode)")
     p.add_argument("--store-k", type=int, default=0, help="store ring: new frames per region (0 = auto)")
@@ -149,6 +150,8 @@ def load_traffic(kernel: str, workload: str, mode: str):
     with open(path) as f:
         d = json.load(f)
     e = d.get(f"{workload}_{mode}" if mode != "materialize" else workload, {}).get(kernel)
+    if e is None and kernel == "t2f":  # t2f launches do not depend on the f2t mode
+        e = d.get(workload, {}).get(kernel)
     return e if isinstance(e, dict) else None
 
 
@@ -375,7 +378,14 @@ def default_mode(args, wname: str) -> str:
         return args.f2t_mode
     if args.tensors == "yuv" or args.graph:  # YUV-native tensors and graph capture: materialised tuples
         return "materialize"
-    return "materialize" if synth.WORKLOADS[wname].cfg.flags & 7 else "store"
+    w = synth.WORKLOADS[wname]
+    # store mode on the scene-padded layout for every one-fresh-frame
+    # workload (sliding windows and the paper's grouping with n = 1: c2-c5;
+    # B200 c4 74.9k vs 69.7k materialised, 71.8k Fig. 1 batches,
+    # profiles/r02/padded/ab_c4store.txt); the tiny launch-bound c1 clip
+    # (96 KB) keeps one materialising launch
+    tiny = w.frames * w.layout().payload_bytes() < (64 << 20)
+    return "materialize" if (w.cfg.n != 1 or tiny) else "store"
 
 
 def read_flags(cut_dev, stream) -> np.ndarray:

@@ -10,6 +10,7 @@ run c2_mat --workload c2 --f2t-mode materialize --no-e2e --no-cpu-baseline
 run c3 --workload c3
 run c3_mat --workload c3 --f2t-mode materialize --no-e2e --no-cpu-baseline
 run c4 --workload c4
+run c4_mat --workload c4 --f2t-mode materialize --no-e2e --no-cpu-baseline
 run c4_batch --workload c4 --f2t-mode batch --no-e2e --no-cpu-baseline
 run c4_emit --workload c4 --emit --no-e2e --no-cpu-baseline
 run c1 --workload c1
