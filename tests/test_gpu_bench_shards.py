@@ -18,10 +18,11 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("W,r,mode", [(3, 1, "materialize"), (4, 0, "store"), (4, 3, "materialize"),
-                                      (2, 1, "store")])
-def test_emulated_rank_runs_the_multi_gpu_path(W, r, mode):
-    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "c2", "--frames", "64", "--steps", "2",
+@pytest.mark.parametrize("W,r,mode,wl", [(3, 1, "materialize", "c2"), (4, 0, "store", "c2"),
+                                         (4, 3, "materialize", "c2"), (2, 1, "store", "c2"), (4, 2, "store", "c2"),
+                                         (3, 1, "store", "c4")])
+def test_emulated_rank_runs_the_multi_gpu_path(W, r, mode, wl):
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", wl, "--frames", "64", "--steps", "2",
            "--warmup", "1", "--no-cpu-baseline", "--per-config", "", "--no-compare-modes", "--f2t-mode", mode,
            "--emulate-shard", f"{W},{r}"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
