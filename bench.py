@@ -580,6 +580,8 @@ def measure(ctx: Ctx, wname: str, primary: bool, mode: str, full: bool = True):
         # Regions lie back to back: the N-1 carried positions are shared with
         # the previous region, copied only where the ring wraps
         served = np.bincount(ring.tuple_region, minlength=ring.regions)
+        if served.sum() != len(runs) or len(served) != ring.regions:  # every tuple a window of exactly one region
+            raise SystemExit(f"padded store serves {served.sum()} of {len(runs)} tuples")
         for c in range(ring.regions):
             p0, p1 = ring.region_frames(c)
             ring._filled = c - 1  # regions are filled in order within a step
